@@ -1,0 +1,179 @@
+/*
+ * tilepipe_b200 — C ABI of the B200-native attention-pipeline hot path.
+ *
+ * Every entry point takes plain pointers and sizes; device pointers are
+ * borrowed (the caller owns the memory, e.g. torch tensors), `stream` is a
+ * cudaStream_t passed as void*. Calls are stream-ordered and return an int
+ * status (0 = TP_OK); on failure tp_last_error() describes the cause. Nothing
+ * is allocated per call: the YOLO plan works inside a caller-provided
+ * workspace.
+ *
+ * Reference interfaces each entry point replaces (paths relative to the
+ * reference package root, pkg/src/tilepipe/):
+ *   tp_gather_tiles          detector.py:223-247 (cut_tile), pipeline.py:291-294 (_tile_for)
+ *   tp_yolo_*                detector.py:77-96   (Detector.detect body: YOLO v2-608)
+ *   tp_region_decode         detector.py:86-96 output contract + geometry.py:237-256 (to_global)
+ *   tp_attention_boxes       pipeline.py:313-316 (attention_pass confidence filter + box list)
+ *   tp_select_active         pipeline.py:319-354 (merge_temporal + select_active)
+ *   tp_build_jobs            pipeline.py:366     (final_pass: sorted(active_ids) tile order)
+ *   tp_collect_final         pipeline.py:357-375 (final_pass tagged list, crop-id order)
+ *   tp_postprocess           postprocess.py:54-187 + pipeline.py:378-385
+ *                            (nms_keep_indices, merge_split, postprocess, finish_detections)
+ */
+#ifndef TILEPIPE_B200_H
+#define TILEPIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define TP_API __attribute__((visibility("default")))
+#else
+#define TP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TP_MODEL_SIDE 608
+#define TP_GRID 19
+#define TP_ANCHORS 5
+#define TP_CLASSES 80
+#define TP_HEAD_CH 425 /* 5 * (4 + 1 + 80) */
+
+enum { TP_RESAMPLE_NEAREST = 0, TP_RESAMPLE_BILINEAR = 1 };
+
+/* One 608x608 tile to produce: crop square (x, y, side) of batch frame `frame`. */
+typedef struct tp_tile_job {
+  int32_t frame;   /* index into the device frame batch */
+  int32_t crop_id; /* unified crop id (GridPlan) */
+  int32_t x, y, side;
+  int32_t cell;    /* row * grid_cols + col of the crop in its grid */
+  int32_t pad0, pad1;
+} tp_tile_job_t;
+
+/* Region-layer output record, one per kept (cell, anchor). */
+typedef struct tp_det {
+  float lx, ly, lw, lh;     /* crop-local 608-space rect, clipped to [0,608]^2 */
+  int32_t gx, gy, gw, gh;   /* to_global(local, crop, W, H): integer global rect */
+  float conf;               /* sigmoid(obj) * softmax(cls)[argmax] */
+  int32_t cls;              /* argmax class (COCO-80 index) */
+  int32_t crop_id;
+  int32_t frame;
+} tp_det_t;
+
+/* Postprocess record: global rect in fp64 (the reference Rect arithmetic). */
+typedef struct tp_pdet {
+  double x, y, w, h;
+  double conf;
+  int32_t cls;
+  int32_t cell;    /* grid cell of the crop that produced it */
+  int32_t crop_id;
+  int32_t src;     /* index in the caller's input order */
+} tp_pdet_t;
+
+#define TP_MAX_CLASSES 128
+enum { TP_RULE_NONE = 0, TP_RULE_VERTICAL = 1, TP_RULE_HORIZONTAL = 2, TP_RULE_BOTH = 3 };
+
+typedef struct tp_post_policy {
+  double nms_iou;
+  double gap_px;
+  double tol_px;
+  double min_conf;          /* final confidence filter; < 0 disables */
+  int32_t merge_before_nms;
+  int32_t nms_per_crop;
+  int32_t do_nms;           /* 0: skip NMS (merge_split only) */
+  int32_t do_merge;         /* 0: skip merge (NMS only) */
+  int32_t grid_cols;
+  int32_t n_cells;          /* <= 256 */
+  uint8_t class_rule[TP_MAX_CLASSES];
+} tp_post_policy_t;
+
+TP_API const char* tp_last_error(void);
+TP_API int tp_version(void);
+TP_API int tp_device_sm_count(int* out);
+
+/* K1/K2: crop gather + resample (+ normalise). frames: u8 [n][H][W][3] with
+ * frame_stride bytes between frames. out_u8: optional [n_jobs][608][608][3].
+ * out_act: optional bf16 [n_jobs][610][610][8] (halo must be pre-zeroed; the
+ * interior is written as pixel/255 in channels 0..2, zeros in 3..7).
+ * n_jobs_dev: optional device count overriding n_jobs (n_jobs is then the max). */
+TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
+                    const tp_tile_job_t* jobs, int n_jobs, const int32_t* n_jobs_dev,
+                    int mode, uint8_t* out_u8, void* out_act, void* stream);
+
+/* K3/K4: YOLO v2-608 forward plan (23 tcgen05 implicit-GEMM conv layers,
+ * maxpools, route/reorg). Weights are bf16 [cout_pad][taps*cin] K-major with
+ * BN folded in; biases fp32 [cout_pad]. */
+typedef struct tp_yolo_net tp_yolo_net;
+TP_API size_t tp_yolo_workspace_bytes(int max_tiles);
+TP_API int tp_yolo_create(int max_tiles, const void* const* weights, const float* const* biases,
+                   void* workspace, size_t workspace_bytes, tp_yolo_net** out);
+TP_API void* tp_yolo_input(tp_yolo_net* net);        /* bf16 [max_tiles][610][610][8] */
+TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][21][21][448] */
+TP_API int tp_yolo_head_cstride(void);
+TP_API int tp_yolo_forward(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev, void* stream);
+/* Debug/parity: run layers [first, last] only and expose any layer's output. */
+TP_API int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev,
+                          int first, int last, void* stream);
+TP_API int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res, int* cstride);
+TP_API int tp_yolo_destroy(tp_yolo_net* net);
+
+/* Generic implicit-GEMM conv on padded NHWC bf16 (one layer), for tests. */
+TP_API int tp_conv_bf16(const void* in, int n_img, int res, int cin_stride, const void* weight,
+                 const float* bias, int cout, int cout_pad, int ksize, int leaky,
+                 void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
+                 void* stream);
+
+/* K5: region decode + threshold + sort + project. head: fp32 padded
+ * [n][21][21][cstride]. out: [n][max_per_tile] sorted by (-conf, cell*5+anchor). */
+TP_API int tp_region_decode(const float* head, int head_cstride, int n_tiles, const int32_t* n_tiles_dev,
+                     const tp_tile_job_t* jobs, int frame_w, int frame_h, float thresh,
+                     const float* anchors_host, tp_det_t* out, int max_per_tile,
+                     int32_t* counts, void* stream);
+
+/* Attention boxes per frame: concat over the frame's A attention tiles (crop
+ * order, detector order) of dets with conf >= min_conf. boxes: fp64
+ * [n_frames][max_boxes][4] (x, y, w, h). */
+TP_API int tp_attention_boxes(const tp_det_t* dets, const int32_t* counts, int max_per_tile,
+                       int n_frames, int tiles_per_frame, double min_conf, double* boxes,
+                       int32_t* box_counts, int max_boxes, void* stream);
+
+/* K6: merge_temporal over `window` slots + select_active. boxes/box_counts are
+ * slot-indexed: slot s holds frame (s - (window-1)) of the batch, so slots
+ * 0..window-2 carry history. crops: fp64 [n_crops][4]. Outputs per frame:
+ * active bitmask words [n_frames][mask_words], sorted active crop ids,
+ * counts, and the first-seen-deduplicated merged box list. */
+TP_API int tp_select_active(const double* boxes, const int32_t* box_counts, int max_boxes,
+                     int n_frames, int window, const double* crops, int n_crops,
+                     int crop_id_base, double margin, double frame_w, double frame_h,
+                     uint32_t* active_mask, int mask_words, int32_t* active_ids,
+                     int32_t* active_counts, double* merged, int32_t* merged_counts,
+                     int max_merged, void* stream);
+
+/* Stage-2 job list from per-frame active ids (frame-major, crop-id ascending). */
+TP_API int tp_build_jobs(const int32_t* active_ids, const int32_t* active_counts, int n_frames,
+                  int max_active, const int32_t* crop_table /* [n_crops][4] x,y,side,cell */,
+                  int crop_id_base, tp_tile_job_t* jobs, int32_t* frame_job_start,
+                  int32_t* n_jobs_dev, void* stream);
+
+/* final_pass tagged list per frame: concat over the frame's jobs (in job order)
+ * of their dets, converted to fp64 postprocess records. */
+TP_API int tp_collect_final(const tp_det_t* dets, const int32_t* counts, int max_per_tile,
+                     const tp_tile_job_t* jobs, const int32_t* frame_job_start, int n_frames,
+                     tp_pdet_t* out, int32_t* out_counts, int max_per_frame, void* stream);
+
+/* K7: per-frame postprocess (NMS / merge_split / both / variants + min_conf
+ * filter). keep_idx (optional): NMS keep indices in keep order per frame. */
+TP_API int tp_postprocess(const tp_pdet_t* dets, const int32_t* counts, int n_frames,
+                   int max_per_frame, const tp_post_policy_t* policy, tp_pdet_t* out,
+                   int32_t* out_counts, int32_t* keep_idx, int32_t* keep_counts, void* stream);
+
+/* 2x2/2 max pool on padded NHWC bf16 (exposed for tests). */
+TP_API int tp_maxpool2(const void* in, int n_img, int res, int cstride, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

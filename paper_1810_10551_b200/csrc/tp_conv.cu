@@ -1,0 +1,682 @@
+// K3/K4 — YOLO v2-608 conv stack as tcgen05/TMEM implicit-GEMM kernels.
+//
+// No reference kernel exists (the reference detector is an abstract boundary,
+// pkg/src/tilepipe/detector.py:77-96); the topology is yolov2-608 (Darknet-19 +
+// passthrough head) as cited by PAPER.md:85,120, restated in oracle/yolo_ref.py.
+//
+// Activation layout ("padded flat NHWC"): every feature map of side R lives in a
+// buffer [tile][R+2][R+2][C] bf16 whose 1-pixel halo is zero and never written.
+// A 3x3/1 same conv is then a GEMM over the flat padded pixel index p:
+//     out[p, n] = sum_{tap, c} in[p + dy*(R+2) + dx, c] * W[n, tap, c]
+// so the A operand of tap (dy,dx) for an M tile [m0, m0+128) is a plain 2-D TMA
+// box at row m0 + shift — no im2col buffer, no gather. Rows that land on halo
+// pixels compute garbage that the epilogue never stores; TMA zero-fills the rows
+// outside the tensor. The waste is the halo share ((R+2)^2/R^2: 0.7% at 608,
+// 22% at 19).
+//
+// Kernel: persistent, warp-specialised, one CTA per SM (192 threads):
+//   warp 0      TMA producer (A box + B box per k-block into an S-stage ring)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256,
+//               K=16 per instruction, fp32 accumulate in TMEM, 2 accumulators)
+//   warps 2..5  epilogue: tcgen05.ld -> +bias (BN folded) -> leaky(0.1) -> bf16
+//               -> interior-only store (optionally channel-offset into the route
+//               concat buffer, or space-to-depth "reorg", or fp32 for the head)
+// Operand smem tiles use the 128B (BK=64) or 64B (BK=32) swizzle; layer 0 (3 input
+// channels, padded to 8) uses SWIZZLE_NONE with two 16-byte taps per K=16 step.
+#include <cuda.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <vector>
+
+#include "tp_common.cuh"
+#include "../../include/tilepipe_b200.h"
+
+namespace {
+
+enum ConvMode { MODE_SW128 = 0, MODE_SW64 = 1, MODE_PAIR = 2 };
+
+struct ConvParams {
+  int n_img;
+  const int32_t* n_img_dev;
+  int res, wp, img_px;
+  int ksize;
+  int cin;        // channels per tap used by K (multiple of BK)
+  int cout;       // real output channels
+  int bn;         // N tile
+  int n_blocks_n;
+  int num_kb;     // k-blocks per output tile
+  int kb_per_tap;
+  int stages;
+  uint32_t a_stage_bytes, b_stage_bytes;
+  uint32_t tmem_cols;
+  const float* bias;
+  void* out;
+  int out_cstride, out_coff, out_fp32, leaky, reorg;
+};
+
+__device__ __forceinline__ int tap_shift(int tap, int ksize, int wp) {
+  if (ksize == 1) return 0;
+  if (tap > 8) tap = 8;  // layer-0 pad tap: weights are zero, reuse a valid shift
+  return (tap / 3 - 1) * wp + (tap % 3 - 1);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(192, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const ConvParams p) {
+  constexpr int BK = MODE == MODE_SW128 ? 64 : (MODE == MODE_SW64 ? 32 : 8);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + (size_t)S * p.b_stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+  const uint32_t warp = tp::warp_id();
+  const uint32_t lane = tp::lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tp::tma_prefetch(&tmA);
+    tp::tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      tp::mbar_init(&full[s], 1);
+      tp::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tp::mbar_init(&tfull[a], 1);
+      tp::mbar_init(&tempty[a], 4);
+    }
+    tp::fence_mbar_init();
+  }
+  if (warp == 1) tp::tmem_alloc(tmem_slot, p.tmem_cols);
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
+  const long long total_px = (long long)n_img * p.img_px;
+  const int m_blocks = (int)((total_px + 127) / 128);
+  const int total_tiles = m_blocks * p.n_blocks_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer =================
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t tx_bytes = p.a_stage_bytes + p.b_stage_bytes;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const int m0 = (t / p.n_blocks_n) * 128;
+        const int n0 = (t % p.n_blocks_n) * p.bn;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* a_dst = smA + (size_t)s * p.a_stage_bytes;
+          uint8_t* b_dst = smB + (size_t)s * p.b_stage_bytes;
+          tp::mbar_arrive_expect_tx(&full[s], tx_bytes);
+          if (MODE == MODE_PAIR) {
+            const int t0 = 2 * kb, t1 = 2 * kb + 1;
+            tp::tma_load_2d(a_dst, &tmA, &full[s], 0, m0 + tap_shift(t0, p.ksize, p.wp));
+            tp::tma_load_2d(a_dst + 128 * 16, &tmA, &full[s], 0, m0 + tap_shift(t1, p.ksize, p.wp));
+            tp::tma_load_2d(b_dst, &tmB, &full[s], t0 * 8, n0);
+            tp::tma_load_2d(b_dst + p.bn * 16, &tmB, &full[s], t1 * 8, n0);
+          } else {
+            const int tap = kb / p.kb_per_tap;
+            const int cb = kb - tap * p.kb_per_tap;
+            tp::tma_load_2d(a_dst, &tmA, &full[s], cb * BK, m0 + tap_shift(tap, p.ksize, p.wp));
+            tp::tma_load_2d(b_dst, &tmB, &full[s], tap * p.cin + cb * BK, n0);
+          }
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer (single thread) =================
+      const uint32_t idesc = tp::idesc_bf16(128, p.bn);
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        tp::mbar_wait(&tempty[acc], aph ^ 1);
+        tp::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&full[s], ph);
+          tp::tc_fence_after();
+          const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * p.a_stage_bytes);
+          const uint32_t b_addr = tp::smem_u32(smB + (size_t)s * p.b_stage_bytes);
+          if (MODE == MODE_SW128) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 1024, 2);
+              uint64_t bd = tp::umma_desc(b_addr + k * 32, 16, 1024, 2);
+              tp::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
+          } else if (MODE == MODE_SW64) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 512, 4);
+              uint64_t bd = tp::umma_desc(b_addr + k * 32, 16, 512, 4);
+              tp::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
+          } else {
+            uint64_t ad = tp::umma_desc(a_addr, 128 * 16, 128, 0);
+            uint64_t bd = tp::umma_desc(b_addr, p.bn * 16, 128, 0);
+            tp::mma_bf16(d_tmem, ad, bd, idesc, kb != 0);
+          }
+          tp::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        tp::mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        acc ^= 1;
+        if (acc == 0) aph ^= 1;
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5) =================
+    const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = (int)(q * 32 + lane);
+    int acc = 0;
+    uint32_t aph = 0;
+    const int out_res = p.res >> 1, out_wp = out_res + 2, out_img_px = out_wp * out_wp;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const int m0 = (t / p.n_blocks_n) * 128;
+      const int n0 = (t % p.n_blocks_n) * p.bn;
+      tp::mbar_wait(&tfull[acc], aph);
+      tp::tc_fence_after();
+
+      const long long pix = (long long)m0 + row;
+      bool valid = pix < total_px;
+      long long out_px = 0;
+      int sub = 0;
+      if (valid) {
+        const int img = (int)(pix / p.img_px);
+        const int rem = (int)(pix - (long long)img * p.img_px);
+        const int yp = rem / p.wp, xp = rem - (rem / p.wp) * p.wp;
+        valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
+        if (p.reorg) {
+          const int y = yp - 1, x = xp - 1;
+          sub = (y & 1) * 2 + (x & 1);
+          out_px = (long long)img * out_img_px + (long long)((y >> 1) + 1) * out_wp + ((x >> 1) + 1);
+        } else {
+          out_px = pix;
+        }
+      }
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * p.bn);
+      for (int c = 0; c < p.bn; c += 16) {
+        uint32_t v[16];
+        tp::tmem_ld16(t_row + (uint32_t)c, v);
+        tp::tmem_ld_wait();
+        const int ch0 = n0 + c;
+        if (!valid || ch0 >= p.cout) continue;
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int ch = ch0 + j;
+          float x = __uint_as_float(v[j]) + (ch < p.cout ? __ldg(p.bias + ch) : 0.0f);
+          if (p.leaky) x = x > 0.0f ? x : 0.1f * x;
+          f[j] = x;
+        }
+        if (p.out_fp32) {
+          float* o = reinterpret_cast<float*>(p.out) + out_px * p.out_cstride + p.out_coff + ch0;
+          if (ch0 + 16 <= p.cout) {
+#pragma unroll
+            for (int j = 0; j < 16; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
+          } else {
+            for (int j = 0; j < 16 && ch0 + j < p.cout; ++j) o[j] = f[j];
+          }
+        } else {
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          const int cofs = p.out_coff + (p.reorg ? sub * p.cout : 0) + ch0;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + out_px * p.out_cstride + cofs;
+          *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+      tp::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tp::mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aph ^= 1;
+    }
+  }
+
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  if (warp == 1) tp::tmem_dealloc(tmem_base, p.tmem_cols);
+}
+
+// 2x2/2 max pool, padded NHWC bf16 -> padded NHWC bf16 (interior only), 8 channels/thread.
+__global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
+                                int cstride, __nv_bfloat16* __restrict__ out) {
+  const int ores = res >> 1, iwp = res + 2, owp = ores + 2;
+  const int cg = cstride >> 3;
+  const long long total = (long long)n_img * ores * ores * cg;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % cg);
+    long long r = i / cg;
+    const int x = (int)(r % ores);
+    r /= ores;
+    const int y = (int)(r % ores);
+    const int img = (int)(r / ores);
+    const __nv_bfloat16* src =
+        in + (((long long)img * iwp + (2 * y + 1)) * iwp + (2 * x + 1)) * cstride + g * 8;
+    uint4 a = *reinterpret_cast<const uint4*>(src);
+    uint4 b = *reinterpret_cast<const uint4*>(src + cstride);
+    uint4 c = *reinterpret_cast<const uint4*>(src + (long long)iwp * cstride);
+    uint4 d = *reinterpret_cast<const uint4*>(src + (long long)iwp * cstride + cstride);
+    uint4 m;
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
+    __nv_bfloat162* pm = reinterpret_cast<__nv_bfloat162*>(&m);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pm[j] = __hmax2(__hmax2(pa[j], pb[j]), __hmax2(pc[j], pd[j]));
+    __nv_bfloat16* dst = out + (((long long)img * owp + (y + 1)) * owp + (x + 1)) * cstride + g * 8;
+    *reinterpret_cast<uint4*>(dst) = m;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map over [rows][cols] (cols contiguous), box {box_cols, box_rows}.
+int make_tmap_2d(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                 uint32_t box_rows, CUtensorMapSwizzle swz) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (enc == nullptr) {
+    tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+    return TP_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    tp_set_error("cuTensorMapEncodeTiled failed (%d): cols=%llu rows=%llu box=%u,%u", (int)r,
+                 (unsigned long long)cols, (unsigned long long)rows, box_cols, box_rows);
+    return TP_ERR_CUDA;
+  }
+  return TP_OK;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// A fully prepared layer launch (tensor maps encoded once).
+struct ConvLaunch {
+  int mode;
+  CUtensorMap tmA, tmB;
+  ConvParams p;
+  size_t smem;
+  int max_tiles_total;
+};
+
+int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_stride, int cin_used,
+                 const void* weight, const float* bias, int cout, int cout_pad, int ksize,
+                 int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg) {
+  memset(L, 0, sizeof(*L));
+  int mode;
+  int bk;
+  if (cin_used == 8 && ksize == 3) {
+    mode = MODE_PAIR;
+    bk = 8;
+  } else if (cin_used % 64 == 0) {
+    mode = MODE_SW128;
+    bk = 64;
+  } else if (cin_used == 32) {
+    mode = MODE_SW64;
+    bk = 32;
+  } else {
+    tp_set_error("conv: unsupported cin %d", cin_used);
+    return TP_ERR_UNSUPPORTED;
+  }
+  if (cout_pad % 16 != 0 || cout_pad < 16 || cout > cout_pad) {
+    tp_set_error("conv: bad cout/cout_pad %d/%d", cout, cout_pad);
+    return TP_ERR_ARG;
+  }
+  int bn = cout_pad;
+  if (bn > 256) {
+    bn = 256;
+    while (cout_pad % bn != 0 || bn % 16 != 0) bn -= 16;
+  }
+  if (!out_fp32 && (cout % 16 != 0 || out_cstride % 8 != 0 || out_coff % 8 != 0)) {
+    tp_set_error("conv: bf16 output needs 16-channel multiples");
+    return TP_ERR_ARG;
+  }
+  const int wp = res + 2;
+  const int img_px = wp * wp;
+  const int taps = ksize * ksize;
+  const int ktotal = mode == MODE_PAIR ? 80 : taps * cin_used;
+  CUtensorMapSwizzle swz = mode == MODE_SW128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : mode == MODE_SW64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
+  int rc = make_tmap_2d(&L->tmA, in, (uint64_t)cin_stride, (uint64_t)max_img * img_px, bk, 128, swz);
+  if (rc) return rc;
+  rc = make_tmap_2d(&L->tmB, weight, (uint64_t)ktotal, (uint64_t)cout_pad, bk, bn, swz);
+  if (rc) return rc;
+
+  ConvParams& p = L->p;
+  p.n_img = max_img;
+  p.res = res;
+  p.wp = wp;
+  p.img_px = img_px;
+  p.ksize = ksize;
+  p.cin = cin_used;
+  p.cout = cout;
+  p.bn = bn;
+  p.n_blocks_n = cout_pad / bn;
+  p.kb_per_tap = mode == MODE_PAIR ? 1 : cin_used / bk;
+  p.num_kb = mode == MODE_PAIR ? 5 : taps * p.kb_per_tap;
+  p.a_stage_bytes = mode == MODE_PAIR ? 2 * 128 * 16 : 128 * bk * 2;
+  p.b_stage_bytes = mode == MODE_PAIR ? 2 * bn * 16 : bn * bk * 2;
+  const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
+  int stages = (int)((200 * 1024) / stage_bytes);
+  if (stages > 8) stages = 8;
+  if (stages < 2) {
+    tp_set_error("conv: stage too large");
+    return TP_ERR_UNSUPPORTED;
+  }
+  p.stages = stages;
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(2 * bn)) cols <<= 1;
+  p.tmem_cols = cols;
+  p.bias = bias;
+  p.out = out;
+  p.out_cstride = out_cstride;
+  p.out_coff = out_coff;
+  p.out_fp32 = out_fp32;
+  p.leaky = leaky;
+  p.reorg = reorg;
+  L->mode = mode;
+  L->smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  const long long m_blocks = ((long long)max_img * img_px + 127) / 128;
+  L->max_tiles_total = (int)(m_blocks * p.n_blocks_n);
+  return TP_OK;
+}
+
+template <int MODE>
+int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  ConvParams p = L.p;
+  p.n_img = n_img;
+  p.n_img_dev = n_img_dev;
+  const long long m_blocks = ((long long)n_img * p.img_px + 127) / 128;
+  const long long tiles = m_blocks * p.n_blocks_n;
+  if (tiles == 0) return TP_OK;
+  int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  conv_tc_kernel<MODE><<<grid, 192, L.smem, st>>>(L.tmA, L.tmB, p);
+  TP_LAUNCH_CHECK();
+  return TP_OK;
+}
+
+int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
+  if (n_img > L.p.n_img) {
+    tp_set_error("conv: n_img %d exceeds planned %d", n_img, L.p.n_img);
+    return TP_ERR_CAPACITY;
+  }
+  switch (L.mode) {
+    case MODE_SW128: return launch_mode<MODE_SW128>(L, n_img, n_img_dev, st);
+    case MODE_SW64: return launch_mode<MODE_SW64>(L, n_img, n_img_dev, st);
+    default: return launch_mode<MODE_PAIR>(L, n_img, n_img_dev, st);
+  }
+}
+
+int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st) {
+  const long long total = (long long)n_img * (res / 2) * (res / 2) * (cstride / 8);
+  if (total == 0) return TP_OK;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  maxpool2_kernel<<<(int)blocks, 256, 0, st>>>((const __nv_bfloat16*)in, n_img, res, cstride,
+                                               (__nv_bfloat16*)out);
+  TP_LAUNCH_CHECK();
+  return TP_OK;
+}
+
+// ------------------------------------------------------------------ YOLO v2-608 plan
+// Layer table (darknet layer index, cin, cout, ksize, res). BN is folded into
+// weights+bias by the host; layer 30 is linear (no BN, no leaky).
+struct LayerDef {
+  int idx, cin, cout, k, res;
+};
+const LayerDef kConvs[23] = {
+    {0, 8, 32, 3, 608},      {2, 32, 64, 3, 304},     {4, 64, 128, 3, 152},
+    {5, 128, 64, 1, 152},    {6, 64, 128, 3, 152},    {8, 128, 256, 3, 76},
+    {9, 256, 128, 1, 76},    {10, 128, 256, 3, 76},   {12, 256, 512, 3, 38},
+    {13, 512, 256, 1, 38},   {14, 256, 512, 3, 38},   {15, 512, 256, 1, 38},
+    {16, 256, 512, 3, 38},   {18, 512, 1024, 3, 19},  {19, 1024, 512, 1, 19},
+    {20, 512, 1024, 3, 19},  {21, 1024, 512, 1, 19},  {22, 512, 1024, 3, 19},
+    {23, 1024, 1024, 3, 19}, {24, 1024, 1024, 3, 19}, {26, 512, 64, 1, 38},
+    {29, 1280, 1024, 3, 19}, {30, 1024, 425, 1, 19}};
+
+enum Buf {
+  I608, C608, P304, C304, P152, A152, B152, C152, P76, A76, B76, C76, P38, A38, B38, E38, P19,
+  A19, B19, C19, CAT19, HEAD, NBUF
+};
+struct BufDef {
+  int res, ch, bytes_per;  // bytes per element
+};
+const BufDef kBufs[NBUF] = {{608, 8, 2},   {608, 32, 2},  {304, 32, 2},   {304, 64, 2},
+                            {152, 64, 2},  {152, 128, 2}, {152, 64, 2},   {152, 128, 2},
+                            {76, 128, 2},  {76, 256, 2},  {76, 128, 2},   {76, 256, 2},
+                            {38, 256, 2},  {38, 512, 2},  {38, 256, 2},   {38, 512, 2},
+                            {19, 512, 2},  {19, 1024, 2}, {19, 512, 2},   {19, 1024, 2},
+                            {19, 1280, 2}, {19, 448, 4}};
+constexpr int kHeadCstride = 448;
+
+// Step list: conv (layer slot, in, out, coff, reorg) or pool (in, out).
+struct Step {
+  int is_pool;
+  int conv;  // index into kConvs
+  int in, out, coff, reorg;
+};
+const Step kSteps[] = {
+    {0, 0, I608, C608, 0, 0},   {1, -1, C608, P304, 0, 0},  {0, 1, P304, C304, 0, 0},
+    {1, -1, C304, P152, 0, 0},  {0, 2, P152, A152, 0, 0},   {0, 3, A152, B152, 0, 0},
+    {0, 4, B152, C152, 0, 0},   {1, -1, C152, P76, 0, 0},   {0, 5, P76, A76, 0, 0},
+    {0, 6, A76, B76, 0, 0},     {0, 7, B76, C76, 0, 0},     {1, -1, C76, P38, 0, 0},
+    {0, 8, P38, A38, 0, 0},     {0, 9, A38, B38, 0, 0},     {0, 10, B38, A38, 0, 0},
+    {0, 11, A38, B38, 0, 0},    {0, 12, B38, E38, 0, 0},    {1, -1, E38, P19, 0, 0},
+    {0, 13, P19, A19, 0, 0},    {0, 14, A19, B19, 0, 0},    {0, 15, B19, C19, 0, 0},
+    {0, 16, C19, B19, 0, 0},    {0, 17, B19, A19, 0, 0},    {0, 18, A19, C19, 0, 0},
+    {0, 19, C19, CAT19, 256, 0}, {0, 20, E38, CAT19, 0, 1}, {0, 21, CAT19, A19, 0, 0},
+    {0, 22, A19, HEAD, 0, 0}};
+constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
+
+size_t buf_bytes(int b, int max_tiles) {
+  const size_t wp = kBufs[b].res + 2;
+  return (size_t)max_tiles * wp * wp * kBufs[b].ch * kBufs[b].bytes_per;
+}
+
+}  // namespace
+
+struct tp_yolo_net {
+  int max_tiles;
+  void* bufs[NBUF];
+  ConvLaunch convs[23];
+  int step_of_conv[23];
+};
+
+extern "C" size_t tp_yolo_workspace_bytes(int max_tiles) {
+  size_t total = 0;
+  for (int b = 0; b < NBUF; ++b) total += (buf_bytes(b, max_tiles) + 1023) & ~size_t(1023);
+  return total;
+}
+
+extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
+                              const float* const* biases, void* workspace,
+                              size_t workspace_bytes, tp_yolo_net** out) {
+  if (max_tiles < 1 || weights == nullptr || biases == nullptr || workspace == nullptr ||
+      out == nullptr) {
+    tp_set_error("tp_yolo_create: bad argument");
+    return TP_ERR_ARG;
+  }
+  if (workspace_bytes < tp_yolo_workspace_bytes(max_tiles)) {
+    tp_set_error("tp_yolo_create: workspace too small");
+    return TP_ERR_CAPACITY;
+  }
+  tp_yolo_net* net = new tp_yolo_net();
+  net->max_tiles = max_tiles;
+  uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
+  for (int b = 0; b < NBUF; ++b) {
+    net->bufs[b] = w;
+    w += (buf_bytes(b, max_tiles) + 1023) & ~size_t(1023);
+  }
+  // halos (and every never-written byte) must be zero
+  cudaError_t e = cudaMemset(workspace, 0, tp_yolo_workspace_bytes(max_tiles));
+  if (e != cudaSuccess) {
+    delete net;
+    tp_set_error("tp_yolo_create: memset: %s", cudaGetErrorString(e));
+    return TP_ERR_CUDA;
+  }
+  for (int s = 0; s < kNumSteps; ++s) {
+    const Step& st = kSteps[s];
+    if (st.is_pool) continue;
+    const LayerDef& L = kConvs[st.conv];
+    const int cout_pad = L.cout == 425 ? kHeadCstride : L.cout;
+    const bool head = (st.out == HEAD);
+    int rc = prepare_conv(&net->convs[st.conv], net->bufs[st.in], max_tiles, L.res,
+                          kBufs[st.in].ch, L.cin, weights[st.conv], biases[st.conv], L.cout,
+                          cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], kBufs[st.out].ch,
+                          st.coff, head ? 1 : 0, st.reorg);
+    if (rc) {
+      delete net;
+      return rc;
+    }
+    net->step_of_conv[st.conv] = s;
+  }
+  *out = net;
+  return TP_OK;
+}
+
+extern "C" void* tp_yolo_input(tp_yolo_net* net) { return net ? net->bufs[I608] : nullptr; }
+extern "C" const float* tp_yolo_head(tp_yolo_net* net) {
+  return net ? reinterpret_cast<const float*>(net->bufs[HEAD]) : nullptr;
+}
+extern "C" int tp_yolo_head_cstride(void) { return kHeadCstride; }
+
+extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev,
+                                     int first, int last, void* stream) {
+  if (net == nullptr || n_tiles < 0 || n_tiles > net->max_tiles) {
+    tp_set_error("tp_yolo_forward: bad n_tiles %d", n_tiles);
+    return TP_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int s = first; s <= last && s < kNumSteps; ++s) {
+    const Step& sp = kSteps[s];
+    int rc;
+    if (sp.is_pool) {
+      rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, kBufs[sp.in].ch, net->bufs[sp.out],
+                    st);
+    } else {
+      rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
+    }
+    if (rc) return rc;
+  }
+  return TP_OK;
+}
+
+extern "C" int tp_yolo_forward(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev,
+                               void* stream) {
+  return tp_yolo_forward_range(net, n_tiles, n_tiles_dev, 0, kNumSteps - 1, stream);
+}
+
+// Output buffer of step `layer` (index into the step list).
+extern "C" int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res,
+                                    int* cstride) {
+  if (net == nullptr || layer < 0 || layer >= kNumSteps) {
+    tp_set_error("tp_yolo_layer_output: bad step %d", layer);
+    return TP_ERR_ARG;
+  }
+  const int b = kSteps[layer].out;
+  *ptr = net->bufs[b];
+  *res = kBufs[b].res;
+  *cstride = kBufs[b].ch;
+  return TP_OK;
+}
+
+extern "C" int tp_yolo_destroy(tp_yolo_net* net) {
+  delete net;
+  return TP_OK;
+}
+
+extern "C" int tp_conv_bf16(const void* in, int n_img, int res, int cin_stride, const void* weight,
+                            const float* bias, int cout, int cout_pad, int ksize, int leaky,
+                            void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
+                            void* stream) {
+  if (in == nullptr || weight == nullptr || bias == nullptr || out == nullptr || n_img < 1 ||
+      (ksize != 1 && ksize != 3)) {
+    tp_set_error("tp_conv_bf16: bad argument");
+    return TP_ERR_ARG;
+  }
+  ConvLaunch L;
+  int rc = prepare_conv(&L, in, n_img, res, cin_stride, cin_stride, weight, bias, cout, cout_pad,
+                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg);
+  if (rc) return rc;
+  return run_conv(L, n_img, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int tp_maxpool2(const void* in, int n_img, int res, int cstride, void* out,
+                           void* stream) {
+  if (in == nullptr || out == nullptr || (res & 1) || (cstride & 7)) {
+    tp_set_error("tp_maxpool2: bad argument");
+    return TP_ERR_ARG;
+  }
+  return run_pool(in, n_img, res, cstride, out, (cudaStream_t)stream);
+}

@@ -1,0 +1,132 @@
+// K1/K2 — frame ingest + crop gather: crop square -> 608x608 tile.
+//
+// Replaces the reference tile cutter `cut_tile` (pkg/src/tilepipe/detector.py:223-247),
+// which maps output pixel u to source floor(u*side/608) and zero-fills crop area that
+// lies outside the frame. Mode NEAREST is bit-exact with it. Mode BILINEAR is the
+// north-star downscale: 8-bit fixed-point weights, half-pixel centres, identical
+// integer arithmetic to oracle/resample_ref.py so it is bit-exact as well.
+//
+// One CTA per (tile, output row). Each thread produces whole pixels: 3 bytes of the
+// u8 tile and/or one 16-byte bf16x8 group of the padded layer-0 input
+// ([tile][610][610][8], channels 3..7 zero), so every store is a full, aligned
+// vector store. Source reads are row-local (one or two source rows per CTA), which
+// keeps them L1/L2-resident; the kernel is HBM-bound on the tile writes.
+#include "tp_common.cuh"
+#include "../../include/tilepipe_b200.h"
+
+namespace {
+
+constexpr int S = TP_MODEL_SIDE;
+constexpr int SP = S + 2;  // padded side of the layer-0 activation buffer
+
+struct Tap {
+  int i0, i1, f;  // source offsets (relative to crop origin) and 8-bit weight of i1
+};
+
+__device__ __forceinline__ Tap bilinear_tap(int u, int side) {
+  // source centre = (u + 0.5) * side / 608 - 0.5 ; fixed point with 8 fraction bits
+  int num = (2 * u + 1) * side - S;  // = 1216 * centre
+  if (num < 0) num = 0;
+  int s256 = (int)(((long long)num * 256) / (2 * S));
+  Tap t;
+  t.i0 = s256 >> 8;
+  t.f = s256 & 255;
+  t.i1 = min(t.i0 + 1, side - 1);
+  return t;
+}
+
+__device__ __forceinline__ void load_px(const uint8_t* __restrict__ frame, int H, int W, int gx,
+                                        int gy, int& r, int& g, int& b) {
+  if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+    const uint8_t* p = frame + ((size_t)gy * W + gx) * 3;
+    r = p[0];
+    g = p[1];
+    b = p[2];
+  } else {
+    r = g = b = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ frames,
+                                                     int64_t frame_stride, int H, int W,
+                                                     const tp_tile_job_t* __restrict__ jobs,
+                                                     const int32_t* __restrict__ n_jobs_dev,
+                                                     int mode, uint8_t* __restrict__ out_u8,
+                                                     __nv_bfloat16* __restrict__ out_act) {
+  const int v = blockIdx.x;  // output row
+  const int t = blockIdx.y;  // tile
+  if (n_jobs_dev != nullptr && t >= *n_jobs_dev) return;
+  const tp_tile_job_t job = jobs[t];
+  const uint8_t* frame = frames + (int64_t)job.frame * frame_stride;
+  const int side = job.side;
+
+  int sy0, sy1 = 0, fy = 0;
+  if (mode == TP_RESAMPLE_NEAREST) {
+    sy0 = job.y + (int)(((long long)v * side) / S);
+  } else {
+    Tap ty = bilinear_tap(v, side);
+    sy0 = job.y + ty.i0;
+    sy1 = job.y + ty.i1;
+    fy = ty.f;
+  }
+
+  for (int u = threadIdx.x; u < S; u += blockDim.x) {
+    int r, g, b;
+    if (mode == TP_RESAMPLE_NEAREST) {
+      int sx = job.x + (int)(((long long)u * side) / S);
+      load_px(frame, H, W, sx, sy0, r, g, b);
+    } else {
+      Tap tx = bilinear_tap(u, side);
+      int r00, g00, b00, r01, g01, b01, r10, g10, b10, r11, g11, b11;
+      load_px(frame, H, W, job.x + tx.i0, sy0, r00, g00, b00);
+      load_px(frame, H, W, job.x + tx.i1, sy0, r01, g01, b01);
+      load_px(frame, H, W, job.x + tx.i0, sy1, r10, g10, b10);
+      load_px(frame, H, W, job.x + tx.i1, sy1, r11, g11, b11);
+      const int w00 = (256 - tx.f) * (256 - fy), w01 = tx.f * (256 - fy);
+      const int w10 = (256 - tx.f) * fy, w11 = tx.f * fy;
+      r = (r00 * w00 + r01 * w01 + r10 * w10 + r11 * w11 + 32768) >> 16;
+      g = (g00 * w00 + g01 * w01 + g10 * w10 + g11 * w11 + 32768) >> 16;
+      b = (b00 * w00 + b01 * w01 + b10 * w10 + b11 * w11 + 32768) >> 16;
+    }
+    if (out_u8 != nullptr) {
+      uint8_t* o = out_u8 + (((size_t)t * S + v) * S + u) * 3;
+      o[0] = (uint8_t)r;
+      o[1] = (uint8_t)g;
+      o[2] = (uint8_t)b;
+    }
+    if (out_act != nullptr) {
+      __nv_bfloat162 rg = __floats2bfloat162_rn((float)r / 255.0f, (float)g / 255.0f);
+      __nv_bfloat162 b0 = __floats2bfloat162_rn((float)b / 255.0f, 0.0f);
+      uint4 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&rg);
+      pk.y = *reinterpret_cast<uint32_t*>(&b0);
+      pk.z = 0u;
+      pk.w = 0u;
+      __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 8;
+      *reinterpret_cast<uint4*>(o) = pk;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
+                               const tp_tile_job_t* jobs, int n_jobs, const int32_t* n_jobs_dev,
+                               int mode, uint8_t* out_u8, void* out_act, void* stream) {
+  if (frames == nullptr || jobs == nullptr || H < 1 || W < 1 || n_jobs < 0 ||
+      (mode != TP_RESAMPLE_NEAREST && mode != TP_RESAMPLE_BILINEAR)) {
+    tp_set_error("tp_gather_tiles: bad argument");
+    return TP_ERR_ARG;
+  }
+  if (out_u8 == nullptr && out_act == nullptr) {
+    tp_set_error("tp_gather_tiles: no output requested");
+    return TP_ERR_ARG;
+  }
+  if (n_jobs == 0) return TP_OK;
+  dim3 grid(S, n_jobs);
+  gather_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(frames, frame_stride, H, W, jobs,
+                                                        n_jobs_dev, mode, out_u8,
+                                                        (__nv_bfloat16*)out_act);
+  TP_LAUNCH_CHECK();
+  return TP_OK;
+}

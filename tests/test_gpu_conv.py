@@ -1,0 +1,114 @@
+"""tcgen05 implicit-GEMM conv kernel vs a plain PyTorch fp32 conv of the same op.
+
+Inputs/weights are bf16 (exactly representable in fp32), the reference accumulates
+in fp32 with TF32 off; the kernel accumulates in fp32 in TMEM and rounds the output
+to bf16, so the tolerance is the bf16 output rounding (2^-8 relative) plus
+accumulation-order noise.
+"""
+
+import numpy as np
+import pytest
+
+from paper_1810_10551_b200 import native
+
+pytestmark = pytest.mark.gpu
+
+
+def _padded_input(torch, n, res, c, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = torch.zeros(n, res + 2, res + 2, c, dtype=torch.float32)
+    x[:, 1:-1, 1:-1, :] = torch.randn(n, res, res, c, generator=g)
+    return x.to(torch.bfloat16).cuda()
+
+
+def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reorg=False,
+              out_cstride=None, out_coff=0, seed=1):
+    n = x.shape[0]
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    taps = k * k
+    scale = (2.0 / (cin * taps)) ** 0.5
+    w = torch.randn(cout, taps, cin, generator=g) * scale
+    bias = torch.randn(cout, generator=g) * 0.1
+    pair = cin == 8 and k == 3
+    kdim = 80 if pair else taps * cin
+    wpack = torch.zeros(cout_pad, kdim)
+    wpack[:cout, : taps * cin] = w.reshape(cout, taps * cin)
+    wpack = wpack.to(torch.bfloat16).cuda()
+    bpack = torch.zeros(cout_pad)
+    bpack[:cout] = bias
+    bpack = bpack.cuda()
+    if out_cstride is None:
+        out_cstride = cout_pad if out_fp32 else cout
+    ores = res // 2 if reorg else res
+    out = torch.zeros(n, ores + 2, ores + 2, out_cstride,
+                      dtype=torch.float32 if out_fp32 else torch.bfloat16, device="cuda")
+    native.call("tp_conv_bf16", native.ptr(x), n, res, cin, native.ptr(wpack), native.ptr(bpack),
+                cout, cout_pad, k, int(leaky), native.ptr(out), out_cstride, out_coff,
+                int(out_fp32), int(reorg), native.stream_handle())
+    torch.cuda.synchronize()
+    # reference
+    xin = x[:, 1:-1, 1:-1, :].float().permute(0, 3, 1, 2)
+    wq = wpack[:cout, : taps * cin].float().reshape(cout, k, k, cin).permute(0, 3, 1, 2)
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    ref = torch.nn.functional.conv2d(xin, wq, bias=bpack[:cout], padding=k // 2)
+    if leaky:
+        ref = torch.where(ref > 0, ref, 0.1 * ref)
+    ref = ref.permute(0, 2, 3, 1)  # n, res, res, cout
+    return out, ref
+
+
+def _check(torch, got, ref, rel=2e-2):
+    got = got.float()
+    err = (got - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    assert err <= rel * scale, f"max err {err} vs scale {scale}"
+
+
+@pytest.mark.parametrize(
+    "cin,cout,k,res",
+    [(8, 32, 3, 16), (32, 64, 3, 16), (64, 128, 3, 19), (128, 64, 1, 19), (256, 512, 3, 12),
+     (64, 1024, 1, 7)],
+)
+def test_conv_matches_torch(cuda, cin, cout, k, res):
+    torch = cuda
+    x = _padded_input(torch, 3, res, cin, seed=cin + cout)
+    out, ref = _run_conv(torch, x, res, cin, cout, cout, k, leaky=True)
+    _check(torch, out[:, 1:-1, 1:-1, :], ref)
+    # halo untouched
+    assert out[:, 0, :, :].abs().max().item() == 0
+    assert out[:, :, -1, :].abs().max().item() == 0
+
+
+def test_conv_head_fp32_linear(cuda):
+    torch = cuda
+    x = _padded_input(torch, 2, 19, 64, seed=5)
+    out, ref = _run_conv(torch, x, 19, 64, 425, 448, 1, leaky=False, out_fp32=True)
+    got = out[:, 1:-1, 1:-1, :425]
+    err = (got - ref).abs().max().item()
+    assert err <= 1e-3 * (ref.abs().max().item() + 1e-6)
+
+
+def test_conv_reorg_and_channel_offset(cuda):
+    torch = cuda
+    x = _padded_input(torch, 2, 38, 64, seed=9)
+    out, ref = _run_conv(torch, x, 38, 64, 64, 64, 1, leaky=True, reorg=True, out_cstride=1280,
+                         out_coff=0)
+    # space-to-depth: out(y, x, (dy*2+dx)*64 + c) = in(2y+dy, 2x+dx, c)
+    r = ref.reshape(2, 19, 2, 19, 2, 64).permute(0, 1, 3, 2, 4, 5).reshape(2, 19, 19, 256)
+    _check(torch, out[:, 1:-1, 1:-1, :256], r)
+    assert out[:, :, :, 256:].abs().max().item() == 0
+    out2, ref2 = _run_conv(torch, _padded_input(torch, 2, 19, 128, seed=3), 19, 128, 64, 64, 3,
+                           leaky=True, out_cstride=1280, out_coff=256)
+    _check(torch, out2[:, 1:-1, 1:-1, 256:320], ref2)
+    assert out2[:, :, :, :256].abs().max().item() == 0
+
+
+def test_maxpool(cuda):
+    torch = cuda
+    x = _padded_input(torch, 3, 16, 64, seed=2)
+    out = torch.zeros(3, 10, 10, 64, dtype=torch.bfloat16, device="cuda")
+    native.call("tp_maxpool2", native.ptr(x), 3, 16, 64, native.ptr(out), native.stream_handle())
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.max_pool2d(x[:, 1:-1, 1:-1, :].float().permute(0, 3, 1, 2), 2)
+    assert torch.equal(out[:, 1:-1, 1:-1, :].float(), ref.permute(0, 2, 3, 1))
