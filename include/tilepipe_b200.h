@@ -13,6 +13,7 @@
  *   tp_gather_tiles          detector.py:223-247 (cut_tile), pipeline.py:291-294 (_tile_for)
  *   tp_yolo_*                detector.py:77-96   (Detector.detect body: YOLO v2-608)
  *   tp_region_decode         detector.py:86-96 output contract + geometry.py:237-256 (to_global)
+ *   tp_project_rects         geometry.py:237-256 (to_global, foreign-detector path)
  *   tp_attention_boxes       pipeline.py:313-316 (attention_pass confidence filter + box list)
  *   tp_select_active         pipeline.py:319-354 (merge_temporal + select_active)
  *   tp_build_jobs            pipeline.py:366     (final_pass: sorted(active_ids) tile order)
@@ -132,6 +133,11 @@ TP_API int tp_region_decode(const float* head, int head_cstride, int n_tiles, co
                      const tp_tile_job_t* jobs, int frame_w, int frame_h, float thresh,
                      const float* anchors_host, tp_det_t* out, int max_per_tile,
                      int32_t* counts, void* stream);
+
+/* to_global for rects from a foreign (host) Detector plugin: local fp64 [n][4],
+ * crop_xyside int32 [n][3]; frame_w <= 0 disables the frame clip. out int32 [n][4]. */
+TP_API int tp_project_rects(const double* local, const int32_t* crop_xyside, int n, int frame_w,
+                            int frame_h, int32_t* out, void* stream);
 
 /* Attention boxes per frame: concat over the frame's A attention tiles (crop
  * order, detector order) of dets with conf >= min_conf. boxes: fp64

@@ -270,7 +270,9 @@ __global__ void __launch_bounds__(192, 1)
 
 // 2x2/2 max pool, padded NHWC bf16 -> padded NHWC bf16 (interior only), 8 channels/thread.
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
-                                int cstride, __nv_bfloat16* __restrict__ out) {
+                                int cstride, __nv_bfloat16* __restrict__ out,
+                                const int32_t* __restrict__ n_img_dev) {
+  if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
   const int ores = res >> 1, iwp = res + 2, owp = ores + 2;
   const int cg = cstride >> 3;
   const long long total = (long long)n_img * ores * ores * cg;
@@ -478,13 +480,14 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
   }
 }
 
-int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st) {
+int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st,
+             const int32_t* n_img_dev = nullptr) {
   const long long total = (long long)n_img * (res / 2) * (res / 2) * (cstride / 8);
   if (total == 0) return TP_OK;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   maxpool2_kernel<<<(int)blocks, 256, 0, st>>>((const __nv_bfloat16*)in, n_img, res, cstride,
-                                               (__nv_bfloat16*)out);
+                                               (__nv_bfloat16*)out, n_img_dev);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
@@ -623,7 +626,7 @@ extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_
     int rc;
     if (sp.is_pool) {
       rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, kBufs[sp.in].ch, net->bufs[sp.out],
-                    st);
+                    st, n_tiles_dev);
     } else {
       rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
     }

@@ -238,7 +238,44 @@ __global__ void collect_final_kernel(const tp_det_t* __restrict__ dets,
   if (threadIdx.x == 0) out_counts[f] = n;  // true count; > max_per_frame means truncated
 }
 
+// to_global for detections produced by a foreign (host) detector plugin.
+__global__ void project_kernel(const double* __restrict__ local, const int32_t* __restrict__ crop,
+                               int n, int frame_w, int frame_h, int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double s = __ddiv_rn((double)crop[3 * i + 2], 608.0);
+  const double* r = local + 4 * (long long)i;
+  int x1, x2, y1, y2;
+  if (frame_w > 0) {
+    project_axis((double)crop[3 * i], s, r[0], r[2], (double)frame_w, x1, x2);
+    project_axis((double)crop[3 * i + 1], s, r[1], r[3], (double)frame_h, y1, y2);
+  } else {  // no frame clip (to_global without frame dims)
+    const double gx = crop[3 * i], gy = crop[3 * i + 1];
+    x1 = __double2int_rn(__dadd_rn(gx, __dmul_rn(r[0], s)));
+    y1 = __double2int_rn(__dadd_rn(gy, __dmul_rn(r[1], s)));
+    x2 = max(x1 + 1, __double2int_rn(__dadd_rn(gx, __dmul_rn(__dadd_rn(r[0], r[2]), s))));
+    y2 = max(y1 + 1, __double2int_rn(__dadd_rn(gy, __dmul_rn(__dadd_rn(r[1], r[3]), s))));
+  }
+  out[4 * i] = x1;
+  out[4 * i + 1] = y1;
+  out[4 * i + 2] = x2 - x1;
+  out[4 * i + 3] = y2 - y1;
+}
+
 }  // namespace
+
+extern "C" int tp_project_rects(const double* local, const int32_t* crop_xyside, int n,
+                                int frame_w, int frame_h, int32_t* out, void* stream) {
+  if (local == nullptr || crop_xyside == nullptr || out == nullptr || n < 0) {
+    tp_set_error("tp_project_rects: bad argument");
+    return TP_ERR_ARG;
+  }
+  if (n == 0) return TP_OK;
+  project_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(local, crop_xyside, n, frame_w,
+                                                                     frame_h, out);
+  TP_LAUNCH_CHECK();
+  return TP_OK;
+}
 
 extern "C" int tp_region_decode(const float* head, int head_cstride, int n_tiles,
                                 const int32_t* n_tiles_dev, const tp_tile_job_t* jobs, int frame_w,

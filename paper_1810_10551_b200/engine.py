@@ -1,0 +1,303 @@
+"""Batched, device-resident attention pipeline (the B200-native hot path).
+
+One call processes a batch of N frames already in HBM with no host round trip inside:
+
+  gather A attention tiles/frame (K1) -> YOLO v2 (K3/K4, tcgen05) -> region decode +
+  to_global (K5) -> attention box lists (conf >= min_conf) -> merge_temporal +
+  select_active over the K-frame window (K6) -> stage-2 job list -> gather active
+  crops (K2) -> YOLO v2 on the active tiles (count read on device) -> decode ->
+  final_pass tagged lists -> NMS + merge + min_conf (K7)
+
+Batching frames is semantically free: attention for frame t depends only
+on frame t, selection on frames t-K+1..t, and the final pass never feeds back; the
+attention boxes of the last K-1 frames are carried on the device into the next batch.
+Results equal the reference's run_sequence (pipeline.py:442-457) frame by frame.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import kernels, native
+from .detector import Detection
+from .geometry import Rect
+from .pipeline_types import AttentionModel, FrameResult, GridPlan, PipelineSettings, \
+    StageFailure, TimingProfile
+from .postprocess import LabelTable, MergePolicy, make_policy_struct, ctypes_ref
+from .yolo import COCO_NAMES, YoloNet
+
+MAX_BOXES = 256        # attention boxes per frame (conf >= min_conf)
+MAX_MERGED = 512       # merged window boxes per frame
+MAX_PER_FRAME = 2048   # raw stage-2 detections per frame (postprocess capacity)
+
+
+class AttentionPipelineB200:
+    def __init__(self, settings: PipelineSettings, frame_w: int, frame_h: int, *,
+                 max_frames: int = 8, seed: int = 0, threshold: float = 0.25,
+                 policy: MergePolicy | None = None, resample: str = "nearest",
+                 head: str = "calibrated", net: YoloNet | None = None):
+        torch = native.require_cuda()
+        if resample not in native.RESAMPLE:
+            raise ValueError(f"resample must be one of {tuple(native.RESAMPLE)}")
+        self.torch = torch
+        self.settings = settings
+        self.W, self.H = int(frame_w), int(frame_h)
+        self.plan = GridPlan.build(self.W, self.H, settings)
+        self.policy = policy or MergePolicy()
+        self.threshold = float(threshold)
+        self.resample = resample
+        self.max_frames = int(max_frames)
+        att, fin = self.plan.attention_grid, self.plan.final_grid
+        self.A, self.F = len(att.crops), len(fin.crops)
+        self.K = settings.temporal_window
+        if self.F > 1024 or fin.rows * fin.cols > 256:
+            raise ValueError("final grid too large for the selection/merge kernels")
+        mf = self.max_frames
+        self.max_tiles = mf * max(self.A, self.F)
+        self.net = net if net is not None else YoloNet(self.max_tiles, seed=seed, head=head)
+        if self.net.max_tiles < self.max_tiles:
+            raise ValueError("shared YoloNet too small for this batch size")
+
+        dev = "cuda"
+        self.frames = torch.empty((mf, self.H, self.W, 3), dtype=torch.uint8, device=dev)
+        self.frame_stride = self.H * self.W * 3
+        self.att_jobs = kernels.jobs_tensor(
+            (f, c.crop_id, int(c.global_rect.x), int(c.global_rect.y), int(c.global_rect.w),
+             c.row * att.cols + c.col) for f in range(mf) for c in att.crops)
+        self.fin_rects = torch.tensor(
+            [[c.global_rect.x, c.global_rect.y, c.global_rect.w, c.global_rect.h]
+             for c in fin.crops], dtype=torch.float64, device=dev)
+        self.fin_table = torch.tensor(
+            [[int(c.global_rect.x), int(c.global_rect.y), int(c.global_rect.w),
+              c.row * fin.cols + c.col] for c in fin.crops], dtype=torch.int32, device=dev)
+        self.dets1, self.counts1 = kernels.alloc_dets(mf * self.A)
+        slots = (self.K - 1) + mf
+        self.boxes = torch.zeros((slots, MAX_BOXES, 4), dtype=torch.float64, device=dev)
+        self.box_counts = torch.zeros(slots, dtype=torch.int32, device=dev)
+        self.words = (self.F + 31) // 32
+        self.mask = torch.zeros((mf, self.words), dtype=torch.int32, device=dev)
+        self.active_ids = torch.zeros((mf, self.F), dtype=torch.int32, device=dev)
+        self.active_counts = torch.zeros(mf, dtype=torch.int32, device=dev)
+        self.merged = torch.zeros((mf, MAX_MERGED, 4), dtype=torch.float64, device=dev)
+        self.merged_counts = torch.zeros(mf, dtype=torch.int32, device=dev)
+        self.jobs2 = torch.zeros(mf * self.F * native.JOB_DTYPE.itemsize, dtype=torch.uint8,
+                                 device=dev)
+        self.frame_job_start = torch.zeros(mf + 1, dtype=torch.int32, device=dev)
+        self.n_jobs2 = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.dets2, self.counts2 = kernels.alloc_dets(mf * self.F)
+        rec = native.PDET_DTYPE.itemsize
+        self.pdets = torch.zeros(mf * MAX_PER_FRAME * rec, dtype=torch.uint8, device=dev)
+        self.pcounts = torch.zeros(mf, dtype=torch.int32, device=dev)
+        self.outp = torch.zeros(mf * MAX_PER_FRAME * rec, dtype=torch.uint8, device=dev)
+        self.ocounts = torch.zeros(mf, dtype=torch.int32, device=dev)
+        self.labels = LabelTable(COCO_NAMES)
+        self.post_policy = make_policy_struct(self.policy, self.labels, fin.cols,
+                                              fin.rows * fin.cols,
+                                              min_conf=settings.min_confidence)
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        self.last_timing = TimingProfile()
+        self.last_n_tiles = (0, 0)
+
+    # ------------------------------------------------------------------ state
+    def reset_history(self, history=()):
+        """Seed the K-1 history slots from host AttentionModels (oldest first)."""
+        self.box_counts[: self.K - 1].zero_()
+        hist = list(history)[-(self.K - 1):] if self.K > 1 else []
+        off = (self.K - 1) - len(hist)
+        for i, m in enumerate(hist):
+            n = len(m.boxes)
+            if n > MAX_BOXES:
+                raise ValueError(f"history model has {n} boxes (> {MAX_BOXES})")
+            if n:
+                self.boxes[off + i, :n] = self.torch.tensor(
+                    [[b.x, b.y, b.w, b.h] for b in m.boxes], dtype=self.torch.float64)
+            self.box_counts[off + i] = n
+
+    def upload(self, frames_host, n: int, non_blocking: bool = True):
+        """Host uint8 [n,H,W,3] (ideally pinned) -> the device frame batch."""
+        self.frames[:n].copy_(frames_host[:n], non_blocking=non_blocking)
+
+    # ------------------------------------------------------------------ run
+    def run_device(self, n: int, frames=None, stream=None, timed: bool = False) -> None:
+        """Launch the whole pipeline for frames[0:n] (device). No host synchronisation."""
+        if not (1 <= n <= self.max_frames):
+            raise ValueError(f"batch of {n} frames (max {self.max_frames})")
+        fr = self.frames if frames is None else frames
+        st = native.stream_handle(stream)
+        ev = self.events
+        K1 = self.K - 1
+        try:
+            if timed:
+                ev[0].record(stream)
+            nt1 = n * self.A
+            kernels.gather(fr, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
+                           self.resample, out_act_ptr=self.net.input_ptr, stream=stream)
+            self.net.forward(nt1, stream=stream)
+            kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
+                           self.dets1, self.counts1, stream=stream)
+            native.call("tp_attention_boxes", native.ptr(self.dets1), native.ptr(self.counts1),
+                        kernels.MAX_PER_TILE, n, self.A, float(self.settings.min_confidence),
+                        native.ptr(self.boxes) + K1 * MAX_BOXES * 32,
+                        native.ptr(self.box_counts) + K1 * 4, MAX_BOXES, st)
+        except native.NativeError as exc:
+            raise StageFailure("attention", -1) from exc
+        try:
+            if timed:
+                ev[1].record(stream)
+            native.call("tp_select_active", native.ptr(self.boxes), native.ptr(self.box_counts),
+                        MAX_BOXES, n, self.K, native.ptr(self.fin_rects), self.F, self.A,
+                        float(self.settings.attention_margin_px), float(self.W), float(self.H),
+                        native.ptr(self.mask), self.words, native.ptr(self.active_ids),
+                        native.ptr(self.active_counts), native.ptr(self.merged),
+                        native.ptr(self.merged_counts), MAX_MERGED, st)
+            native.call("tp_build_jobs", native.ptr(self.active_ids),
+                        native.ptr(self.active_counts), n, self.F, native.ptr(self.fin_table),
+                        self.A, native.ptr(self.jobs2), native.ptr(self.frame_job_start),
+                        native.ptr(self.n_jobs2), st)
+        except native.NativeError as exc:
+            raise StageFailure("select", -1) from exc
+        try:
+            if timed:
+                ev[2].record(stream)
+            nt2 = n * self.F  # upper bound; kernels read the real count from n_jobs2
+            kernels.gather(fr, self.frame_stride, self.H, self.W, self.jobs2, nt2, self.resample,
+                           out_act_ptr=self.net.input_ptr, n_jobs_dev=self.n_jobs2, stream=stream)
+            self.net.forward(nt2, n_tiles_dev=self.n_jobs2, stream=stream)
+            kernels.decode(self.net, nt2, self.jobs2, self.W, self.H, self.threshold, self.dets2,
+                           self.counts2, n_tiles_dev=self.n_jobs2, stream=stream)
+            native.call("tp_collect_final", native.ptr(self.dets2), native.ptr(self.counts2),
+                        kernels.MAX_PER_TILE, native.ptr(self.jobs2),
+                        native.ptr(self.frame_job_start), n, native.ptr(self.pdets),
+                        native.ptr(self.pcounts), MAX_PER_FRAME, st)
+        except native.NativeError as exc:
+            raise StageFailure("final", -1) from exc
+        try:
+            if timed:
+                ev[3].record(stream)
+            native.call("tp_postprocess", native.ptr(self.pdets), native.ptr(self.pcounts), n,
+                        MAX_PER_FRAME, ctypes_ref(self.post_policy), native.ptr(self.outp),
+                        native.ptr(self.ocounts), None, None, st)
+            if timed:
+                ev[4].record(stream)
+        except native.NativeError as exc:
+            raise StageFailure("postprocess", -1) from exc
+        # carry the last K-1 frames' attention boxes to the history slots (device copy)
+        if K1 > 0:
+            self.boxes[:K1].copy_(self.boxes[n:n + K1].clone())
+            self.box_counts[:K1].copy_(self.box_counts[n:n + K1].clone())
+        self._n = n
+
+    # ------------------------------------------------------------------ API helpers
+    def _upload_frames(self, frames):
+        torch = self.torch
+        for i, fr in enumerate(frames):
+            if fr.width != self.W or fr.height != self.H:
+                raise ValueError("frame size differs from the engine's")
+            if fr.pixels is None:
+                raise StageFailure("attention", fr.frame_id) from ValueError(
+                    "YoloB200Detector needs frame pixels")
+            self.frames[i].copy_(torch.from_numpy(np.ascontiguousarray(fr.pixels)))
+
+    def evaluate_frames(self, frames, history=()):
+        """Frames (host pixels) -> [(FrameResult, AttentionModel)]. history=None keeps the
+        device-carried attention of the previous call (clip mode)."""
+        n = len(frames)
+        if history is not None:
+            self.reset_history(history)
+        self._upload_frames(frames)
+        self.run_device(n, timed=True)
+        t = [v / n for v in self.stage_times_ms()]
+        timing = TimingProfile(attention_wait_ms=t[0], client_processing_ms=t[1],
+                               final_eval_ms=t[2], postprocess_ms=t[3])
+        return self.results([f.frame_id for f in frames], timing)
+
+    def attention_only(self, frame):
+        """attention_pass for one frame: stage 1 + box extraction, no selection."""
+        self._upload_frames([frame])
+        nt1 = self.A
+        K1 = self.K - 1
+        try:
+            kernels.gather(self.frames, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
+                           self.resample, out_act_ptr=self.net.input_ptr)
+            self.net.forward(nt1)
+            kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
+                           self.dets1, self.counts1)
+            native.call("tp_attention_boxes", native.ptr(self.dets1), native.ptr(self.counts1),
+                        kernels.MAX_PER_TILE, 1, self.A, float(self.settings.min_confidence),
+                        native.ptr(self.boxes) + K1 * MAX_BOXES * 32,
+                        native.ptr(self.box_counts) + K1 * 4, MAX_BOXES, native.stream_handle())
+        except native.NativeError as exc:
+            raise StageFailure("attention", frame.frame_id) from exc
+        (bx,) = self.box_counts_snapshot(1)
+        boxes = tuple(Rect(int(b[0]), int(b[1]), int(b[2]), int(b[3])) for b in bx)
+        return AttentionModel(frame.frame_id, boxes, (frame.frame_id,))
+
+    # ------------------------------------------------------------------ host views
+    def stage_times_ms(self):
+        self.events[4].synchronize()
+        e = self.events
+        return (e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
+                e[3].elapsed_time(e[4]))
+
+    def results(self, frame_ids, timing: TimingProfile | None = None):
+        """Download and convert the last batch to (FrameResult, AttentionModel) pairs."""
+        torch = self.torch
+        n = self._n
+        torch.cuda.current_stream().synchronize()
+        oc = self.ocounts[:n].cpu().numpy()
+        pc = self.pcounts[:n].cpu().numpy()
+        if (pc > MAX_PER_FRAME).any():
+            raise StageFailure("final", int(frame_ids[int(np.argmax(pc))]))
+        ac = self.active_counts[:n].cpu().numpy()
+        rec = self.outp.view(-1)[: n * MAX_PER_FRAME * native.PDET_DTYPE.itemsize].cpu().numpy()
+        rec = rec.view(native.PDET_DTYPE).reshape(n, MAX_PER_FRAME)
+        bc = self.box_counts_snapshot(n)
+        out = []
+        timing = timing or TimingProfile()
+        for f in range(n):
+            dets = tuple(
+                Detection(Rect(int(r["x"]), int(r["y"]), int(r["w"]), int(r["h"])),
+                          self.labels.names[int(r["cls"])], float(r["conf"]))
+                for r in rec[f, : oc[f]])
+            res = FrameResult(int(frame_ids[f]), dets, int(ac[f]), self.F, timing)
+            boxes = tuple(Rect(int(b[0]), int(b[1]), int(b[2]), int(b[3])) for b in bc[f])
+            out.append((res, AttentionModel(int(frame_ids[f]), boxes, (int(frame_ids[f]),))))
+        return out
+
+    def box_counts_snapshot(self, n):
+        """Attention boxes per frame of the last batch (host lists)."""
+        K1 = self.K - 1
+        # after run_device the batch's own slots are K1..K1+n-1 (the history copy only
+        # overwrote slots 0..K1-1)
+        cnt = self.box_counts[K1:K1 + n].cpu().numpy()
+        if (cnt > MAX_BOXES).any():
+            raise StageFailure("attention", -1)
+        bx = self.boxes[K1:K1 + n].cpu().numpy()
+        return [bx[f, : cnt[f]] for f in range(n)]
+
+
+def yolo_tagged(det, frame, crops):
+    """final_pass / downscale body for the YOLO detector: the given crops of one frame are
+    gathered, run and decoded (with to_global) on the GPU; returns the reference's tagged
+    list [(crop_id, Detection)] in crop order, detector order within a crop."""
+    torch = native.require_cuda()
+    net = det.net
+    dev = torch.from_numpy(np.ascontiguousarray(frame.pixels)).cuda()
+    H, W = frame.height, frame.width
+    out = []
+    for s in range(0, len(crops), net.max_tiles):
+        chunk = crops[s:s + net.max_tiles]
+        n = len(chunk)
+        jobs = kernels.jobs_tensor((0, c.crop_id, int(c.global_rect.x), int(c.global_rect.y),
+                                    int(c.global_rect.w), 0) for c in chunk)
+        kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr)
+        net.forward(n)
+        recs, counts = kernels.alloc_dets(n)
+        kernels.decode(net, n, jobs, W, H, det.threshold, recs, counts)
+        rec, cnt = kernels.dets_to_host(recs, counts, n)
+        for i, c in enumerate(chunk):
+            for r in rec[i, : cnt[i]]:
+                out.append((c.crop_id, Detection(
+                    Rect(int(r["gx"]), int(r["gy"]), int(r["gw"]), int(r["gh"])),
+                    COCO_NAMES[int(r["cls"])], float(r["conf"]))))
+    return out

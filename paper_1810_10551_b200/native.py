@@ -86,6 +86,7 @@ SIGNATURES = {
     "tp_yolo_destroy": (_I, [_P]),
     "tp_conv_bf16": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, _P]),
     "tp_region_decode": (_I, [_P, _I, _I, _P, _P, _I, _I, _F, _P, _P, _I, _P, _P]),
+    "tp_project_rects": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "tp_attention_boxes": (_I, [_P, _P, _I, _I, _I, _D, _P, _P, _I, _P]),
     "tp_select_active": (
         _I, [_P, _P, _I, _I, _I, _P, _I, _I, _D, _D, _D, _P, _I, _P, _P, _P, _P, _I, _P]),

@@ -1,0 +1,266 @@
+"""YOLO v2-608 behind the reference Detector boundary (detector.py:77-96), on B200.
+
+* ``LAYERS`` — yolov2-608 conv table (Darknet-19 + passthrough head), the network the
+  paper runs; the reference itself has no network.
+* ``make_weights(seed)`` — deterministic random init shared with the CPU oracle:
+  He-normal conv weights, BatchNorm statistics folded into weight+bias, weights rounded
+  to bf16. The 1x1 head (layer 30) is a committed, deterministic linear probe
+  (tools/calibrate_head.py) so the random backbone emits boxes on the synthetic
+  scenes; without it no score reaches the pipeline's 0.3 threshold.
+* ``YoloNet`` — the device plan (23 tcgen05 conv launches + pools + route/reorg) over
+  a persistent workspace; ``YoloB200Detector`` — the plugin-compatible Detector.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import native
+from .detector import Detection, Detector, DetectorProfile
+from .geometry import MODEL_SIDE
+
+# (darknet index, cin, cout, ksize, input side) — identical to csrc/tp_conv.cu kConvs
+LAYERS = [
+    (0, 3, 32, 3, 608), (2, 32, 64, 3, 304), (4, 64, 128, 3, 152), (5, 128, 64, 1, 152),
+    (6, 64, 128, 3, 152), (8, 128, 256, 3, 76), (9, 256, 128, 1, 76), (10, 128, 256, 3, 76),
+    (12, 256, 512, 3, 38), (13, 512, 256, 1, 38), (14, 256, 512, 3, 38), (15, 512, 256, 1, 38),
+    (16, 256, 512, 3, 38), (18, 512, 1024, 3, 19), (19, 1024, 512, 1, 19),
+    (20, 512, 1024, 3, 19), (21, 1024, 512, 1, 19), (22, 512, 1024, 3, 19),
+    (23, 1024, 1024, 3, 19), (24, 1024, 1024, 3, 19), (26, 512, 64, 1, 38),
+    (29, 1280, 1024, 3, 19), (30, 1024, 425, 1, 19),
+]
+HEAD = 22
+HEAD_CPAD = 448
+ANCHORS = np.array([0.57273, 0.677385, 1.87446, 2.06253, 3.33843, 5.47434, 7.88282, 3.52778,
+                    9.77052, 9.16828], dtype=np.float32)
+GFLOP_PER_TILE = sum(2.0 * (s * s) * cout * cin * k * k for _, cin, cout, k, s in LAYERS) / 1e9
+
+COCO_NAMES = (
+    "person", "bicycle", "car", "motorbike", "aeroplane", "bus", "train", "truck", "boat",
+    "traffic light", "fire hydrant", "stop sign", "parking meter", "bench", "bird", "cat", "dog",
+    "horse", "sheep", "cow", "elephant", "bear", "zebra", "giraffe", "backpack", "umbrella",
+    "handbag", "tie", "suitcase", "frisbee", "skis", "snowboard", "sports ball", "kite",
+    "baseball bat", "baseball glove", "skateboard", "surfboard", "tennis racket", "bottle",
+    "wine glass", "cup", "fork", "knife", "spoon", "bowl", "banana", "apple", "sandwich",
+    "orange", "broccoli", "carrot", "hot dog", "pizza", "donut", "cake", "chair", "sofa",
+    "pottedplant", "bed", "diningtable", "toilet", "tvmonitor", "laptop", "mouse", "remote",
+    "keyboard", "cell phone", "microwave", "oven", "toaster", "sink", "refrigerator", "book",
+    "clock", "vase", "scissors", "teddy bear", "hair drier", "toothbrush",
+)
+assert len(COCO_NAMES) == 80
+
+DATA_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
+
+
+def head_path(seed: int) -> str:
+    return os.path.join(DATA_DIR, f"yolo_head_seed{seed}.npz")
+
+
+def _bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round fp32 -> bf16 (RNE) and back, in numpy (no torch needed)."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32)
+
+
+def pack_weight(li: int, w: np.ndarray) -> np.ndarray:
+    """[cout][cin][k][k] -> packed K-major [cout_pad][K] (bf16-valued fp32)."""
+    _, cin, cout, k, _ = LAYERS[li]
+    cpad = HEAD_CPAD if li == HEAD else cout
+    wt = np.transpose(w, (0, 2, 3, 1))  # cout, ky, kx, cin
+    if li == 0:
+        full = np.zeros((cpad, 10, 8), dtype=np.float32)
+        full[:cout, :9, :cin] = wt.reshape(cout, 9, cin)
+        return _bf16_round(full.reshape(cpad, 80))
+    full = np.zeros((cpad, k * k * cin), dtype=np.float32)
+    full[:cout] = wt.reshape(cout, k * k * cin)
+    return _bf16_round(full)
+
+
+_CACHE: dict = {}
+
+
+def make_weights(seed: int = 0, head: str = "calibrated"):
+    """Deterministic YOLO v2 weights: (packed weights [23], biases [23]) as numpy fp32.
+
+    head="calibrated" uses the committed probe head for this seed when present,
+    head="random" always uses a random head.
+    """
+    key = (seed, head)
+    if key in _CACHE:
+        return _CACHE[key]
+    rng = np.random.default_rng(seed)
+    wpacks, biases = [], []
+    for li, (_, cin, cout, k, _) in enumerate(LAYERS):
+        fan_in = cin * k * k
+        w = rng.standard_normal((cout, cin, k, k), dtype=np.float32)
+        w *= np.float32(np.sqrt(2.0 / (1.01 * fan_in)))
+        if li == HEAD:
+            b = np.zeros(cout, dtype=np.float32)
+            w *= np.float32(0.05)
+        else:
+            gamma = rng.uniform(0.9, 1.1, cout).astype(np.float32)
+            beta = (rng.standard_normal(cout, dtype=np.float32) * 0.05).astype(np.float32)
+            mean = (rng.standard_normal(cout, dtype=np.float32) * 0.05).astype(np.float32)
+            var = rng.uniform(0.8, 1.2, cout).astype(np.float32)
+            scale = gamma / np.sqrt(var + np.float32(1e-5))
+            w = w * scale[:, None, None, None]
+            b = (beta - mean * scale).astype(np.float32)
+        cpad = HEAD_CPAD if li == HEAD else cout
+        bp = np.zeros(cpad, dtype=np.float32)
+        bp[:cout] = b
+        wpacks.append(pack_weight(li, w))
+        biases.append(bp)
+    if head == "calibrated" and os.path.exists(head_path(seed)):
+        z = np.load(head_path(seed))
+        wpacks[HEAD] = pack_weight(HEAD, z["w"].reshape(425, 1024, 1, 1))
+        bp = np.zeros(HEAD_CPAD, dtype=np.float32)
+        bp[:425] = z["b"]
+        biases[HEAD] = bp
+    _CACHE[key] = (wpacks, biases)
+    return wpacks, biases
+
+
+class YoloNet:
+    """Device-resident YOLO v2-608 plan over a persistent workspace (max_tiles tiles)."""
+
+    def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated"):
+        torch = native.require_cuda()
+        lib = native.load()
+        wpacks, biases = weights if weights is not None else make_weights(seed, head)
+        self.max_tiles = int(max_tiles)
+        self.w_dev = [torch.from_numpy(w).to(torch.bfloat16).cuda() for w in wpacks]
+        self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
+        nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        wptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.w_dev])
+        bptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.b_dev])
+        handle = ctypes.c_void_p()
+        native.call("tp_yolo_create", self.max_tiles, wptrs, bptrs, native.ptr(self.workspace),
+                    nbytes, ctypes.byref(handle))
+        self.handle = handle
+        self.input_ptr = int(lib.tp_yolo_input(handle))
+        self.head_ptr = int(lib.tp_yolo_head(handle))
+        self.head_cstride = int(lib.tp_yolo_head_cstride())
+
+    def forward(self, n_tiles: int, n_tiles_dev=None, stream=None) -> None:
+        native.call("tp_yolo_forward", self.handle, int(n_tiles), native.ptr(n_tiles_dev),
+                    native.stream_handle(stream))
+
+    def forward_range(self, n_tiles, first, last, stream=None):
+        native.call("tp_yolo_forward_range", self.handle, int(n_tiles), None, first, last,
+                    native.stream_handle(stream))
+
+    def layer_output(self, step: int):
+        """(device pointer, side, channel stride) of a step's output buffer."""
+        p, r, c = ctypes.c_void_p(), ctypes.c_int(), ctypes.c_int()
+        native.call("tp_yolo_layer_output", self.handle, step, ctypes.byref(p), ctypes.byref(r),
+                    ctypes.byref(c))
+        return int(p.value), r.value, c.value
+
+    def _view(self, addr: int, nbytes: int):
+        off = addr - self.workspace.data_ptr()
+        return self.workspace[off: off + nbytes]
+
+    def head_tensor(self, n_tiles: int):
+        """fp32 head view [n, 21, 21, 448] (padded, channels 425.. are zero)."""
+        import torch
+
+        nb = n_tiles * 21 * 21 * self.head_cstride * 4
+        return self._view(self.head_ptr, nb).view(torch.float32).view(
+            n_tiles, 21, 21, self.head_cstride)
+
+    def input_tensor(self, n_tiles: int):
+        """bf16 layer-0 input view [n, 610, 610, 8]."""
+        import torch
+
+        nb = n_tiles * 610 * 610 * 8 * 2
+        return self._view(self.input_ptr, nb).view(torch.bfloat16).view(n_tiles, 610, 610, 8)
+
+    def step_tensor(self, step: int, n_tiles: int):
+        """bf16 view of a step's output buffer [n, R+2, R+2, C] (padded)."""
+        import torch
+
+        addr, res, cs = self.layer_output(step)
+        if step == len(STEPS) - 1:
+            return self.head_tensor(n_tiles)
+        nb = n_tiles * (res + 2) * (res + 2) * cs * 2
+        return self._view(addr, nb).view(torch.bfloat16).view(n_tiles, res + 2, res + 2, cs)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and native._lib is not None:
+            native._lib.tp_yolo_destroy(h)
+            self.handle = None
+
+
+# step list of csrc/tp_conv.cu kSteps: ("conv", layer slot) or ("pool", None)
+STEPS = [("conv", 0), ("pool", None), ("conv", 1), ("pool", None), ("conv", 2), ("conv", 3),
+         ("conv", 4), ("pool", None), ("conv", 5), ("conv", 6), ("conv", 7), ("pool", None),
+         ("conv", 8), ("conv", 9), ("conv", 10), ("conv", 11), ("conv", 12), ("pool", None),
+         ("conv", 13), ("conv", 14), ("conv", 15), ("conv", 16), ("conv", 17), ("conv", 18),
+         ("conv", 19), ("conv", 20), ("conv", 21), ("conv", 22)]
+
+
+class YoloB200Detector(Detector):
+    """YOLO v2-608 on the B200 behind the reference Detector interface.
+
+    ``detect`` takes one 608x608x3 uint8 tile and returns crop-local detections sorted
+    by descending confidence (ties: cell-major, anchor order). Calls are serialised on
+    the current CUDA stream; the batched pipeline (engine.AttentionPipelineB200) bypasses
+    per-tile calls entirely. The class labels are COCO-80 names.
+    """
+
+    def __init__(self, seed: int = 0, threshold: float = 0.25, max_tiles: int = 32,
+                 head: str = "calibrated"):
+        if not (0.0 <= threshold <= 1.0):
+            raise ValueError("threshold must be in [0, 1]")
+        self.profile = DetectorProfile(input_side=MODEL_SIDE, min_confidence=threshold)
+        self.threshold = float(threshold)
+        self.seed = seed
+        self.head = head
+        self.max_tiles = max_tiles
+        self._net = None
+
+    @property
+    def net(self) -> YoloNet:
+        if self._net is None:
+            self._net = YoloNet(self.max_tiles, seed=self.seed, head=self.head)
+        return self._net
+
+    def detect_tiles(self, tiles_u8) -> list[list[Detection]]:
+        """Batched detect over [n,608,608,3] uint8 tiles (numpy or CUDA tensor)."""
+        from . import kernels
+
+        torch = native.require_cuda()
+        t = tiles_u8 if not isinstance(tiles_u8, np.ndarray) else torch.from_numpy(
+            np.ascontiguousarray(tiles_u8)).cuda()
+        n = int(t.shape[0])
+        out = []
+        for s in range(0, n, self.net.max_tiles):
+            chunk = t[s:s + self.net.max_tiles]
+            recs, counts = kernels.detect_tiles_device(self.net, chunk, self.threshold)
+            for i in range(chunk.shape[0]):
+                rows = recs[i][: counts[i]]
+                out.append([Detection(_local_rect(r), COCO_NAMES[int(r["cls"])], float(r["conf"]))
+                            for r in rows])
+        return out
+
+    def detect(self, frame_id: int, crop_id: int, tile: np.ndarray | None = None
+               ) -> list[Detection]:
+        side = self.profile.input_side
+        if tile is None:
+            raise ValueError("YoloB200Detector needs tile pixels (got None)")
+        if not isinstance(tile, np.ndarray) or tile.shape != (side, side, 3):
+            got = tile.shape if isinstance(tile, np.ndarray) else type(tile)
+            raise ValueError(f"tile must be {side}x{side}x3, got {got}")
+        return self.detect_tiles(tile[None])[0]
+
+
+def _local_rect(r):
+    from .geometry import Rect
+
+    return Rect(float(r["lx"]), float(r["ly"]), float(r["lw"]), float(r["lh"]))
