@@ -1,0 +1,129 @@
+"""CPU-only checks: host value types / validation mirror the reference, the C-ABI
+library loads and exports every symbol include/tilepipe_b200.h declares, and the
+product package never imports the oracle."""
+
+import ast
+import json
+import os
+import re
+
+import pytest
+
+from paper_1810_10551_b200 import native
+from paper_1810_10551_b200.geometry import (CropSettings, Rect, build_grid, crop_side_px,
+                                            intersects, iou, to_global, to_local)
+from paper_1810_10551_b200.pipeline_types import (ActiveSet, FrameResult, GridPlan,
+                                                  PipelineSettings, TimingProfile)
+from paper_1810_10551_b200.postprocess import MergePolicy
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_golden.json")))
+
+
+def test_grid_planning_matches_reference_golden():
+    for g in GOLD["grids"]:
+        grid = build_grid(g["fw"], g["fh"], CropSettings(g["rows"], g["overlap"]))
+        assert (grid.crop_side, grid.cols) == (g["side"], g["cols"])
+        got = [[c.crop_id, c.row, c.col, c.global_rect.x, c.global_rect.y, c.global_rect.w,
+                c.global_rect.h, c.scale] for c in grid.crops]
+        assert got == g["crops"]
+
+
+def test_table_one_golden():
+    for fh, rows, side in [(2160, 1, 2160), (2160, 2, 1098), (2160, 3, 736), (2160, 4, 554),
+                           (2160, 6, 370), (4320, 1, 4320), (4320, 2, 2196), (4320, 3, 1472),
+                           (4320, 4, 1107)]:
+        assert crop_side_px(fh, CropSettings(rows, 20)) == side
+
+
+def test_host_to_global_matches_reference_golden():
+    from paper_1810_10551_b200.geometry import CropSpec
+
+    for c in GOLD["to_global"]:
+        cx, cy, side = c["crop"]
+        crop = CropSpec(0, 0, 0, Rect(cx, cy, side, side), side / 608)
+        r = Rect(*c["local"])
+        out = to_global(r, crop, c["fw"], c["fh"]) if c["clip"] else to_global(r, crop)
+        assert [out.x, out.y, out.w, out.h] == c["out"]
+
+
+def test_rect_semantics():
+    with pytest.raises(ValueError):
+        Rect(0, 0, 0, 5)
+    with pytest.raises(ValueError):
+        Rect(float("nan"), 0, 1, 1)
+    a, b = Rect(0, 0, 10, 10), Rect(10, 0, 5, 5)
+    assert not intersects(a, b) and iou(a, b) == 0.0
+    assert iou(a, a) == 1.0
+    crop = build_grid(1216, 1216, CropSettings(1, 0)).crops[0]
+    loc = to_local(crop.global_rect, crop)
+    assert (loc.x, loc.y, loc.w, loc.h) == (0, 0, 608, 608)
+
+
+def test_pipeline_settings_and_plan():
+    s = PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    assert s.preset_name() == "1 att, 3 fin, 20 over"
+    with pytest.raises(ValueError):
+        PipelineSettings.from_preset("3 rows")
+    with pytest.raises(ValueError):
+        PipelineSettings(CropSettings(3), CropSettings(2))
+    plan = GridPlan.build(3840, 2160, s)
+    assert len(plan.attention_grid.crops) == 2 and len(plan.final_grid.crops) == 18
+    assert plan.downscale_id == 20 and plan.downscale_crop.global_rect == Rect(0, 0, 3840, 3840)
+    with pytest.raises(ValueError):
+        ActiveSet(plan.final_grid, frozenset({999}))
+    with pytest.raises(ValueError):
+        FrameResult(0, (), 5, 2, TimingProfile())
+    with pytest.raises(ValueError):
+        TimingProfile(final_eval_ms=-1.0)
+    with pytest.raises(ValueError):
+        MergePolicy(nms_iou=1.0)
+    with pytest.raises(ValueError):
+        MergePolicy(mergeable_classes={"person": "diagonal"})
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "tilepipe_b200.h")).read()
+    return set(re.findall(r"TP_API\s+[\w\s\*]+?\b(tp_\w+)\s*\(", src))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = native.load()  # loading needs no GPU
+    declared = _header_symbols()
+    assert declared, "no TP_API declarations found"
+    assert declared == set(native.SIGNATURES), declared ^ set(native.SIGNATURES)
+    for name in declared:
+        assert getattr(lib, name) is not None
+    assert lib.tp_version() == 1
+    assert lib.tp_yolo_workspace_bytes(1) > 80_000_000
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1810_10551_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            tree = ast.parse(open(os.path.join(pkg, fn)).read())
+            for node in ast.walk(tree):
+                if isinstance(node, ast.Import):
+                    assert not any(a.name.split(".")[0] == "oracle" for a in node.names), fn
+                if isinstance(node, ast.ImportFrom):
+                    assert (node.module or "").split(".")[0] != "oracle", fn
+
+
+def test_ops_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+
+    from paper_1810_10551_b200.detector import cut_tile
+    from paper_1810_10551_b200.postprocess import nms
+
+    crop = build_grid(608, 608, CropSettings(1, 0)).crops[0]
+    with pytest.raises(native.NativeUnavailable):
+        cut_tile(np.zeros((608, 608, 3), np.uint8), crop)
+    from paper_1810_10551_b200.detector import Detection
+
+    with pytest.raises(native.NativeUnavailable):
+        nms([Detection(Rect(0, 0, 5, 5), "a", 0.5)], 0.45)
