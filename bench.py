@@ -117,13 +117,13 @@ def cpu_baseline_frames_per_sec(objs, n_frames=1):
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    wpacks, biases = yolo.make_weights(0)
+    wpacks, biases = yolo.make_weights(0, dtype=yolo.DEFAULT_PRECISION)
     plan = R.Plan(W, H, 1, 3, 20)
     frames = [synthetic.render_frame(W, H, objs[i]) for i in range(n_frames)]
 
     def detect(fid, crop):
         tile = R.cut_tile_nearest(frames[fid], crop)
-        head = yolo_ref.forward(tile[None], wpacks, biases, mode="bf16")
+        head = yolo_ref.forward(tile[None], wpacks, biases, mode=yolo.DEFAULT_PRECISION)
         return [(r, yolo.COCO_NAMES[c], conf) for r, c, conf, _ in
                 yolo_ref.region_decode(head, 0.25)[0]]
 

@@ -44,6 +44,8 @@ extern "C" {
 #define TP_HEAD_CH 425 /* 5 * (4 + 1 + 80) */
 
 enum { TP_RESAMPLE_NEAREST = 0, TP_RESAMPLE_BILINEAR = 1 };
+/* 16-bit operand/activation format of the conv stack (fp32 accumulation either way). */
+enum { TP_DTYPE_BF16 = 0, TP_DTYPE_F16 = 1 };
 
 /* One 608x608 tile to produce: crop square (x, y, side) of batch frame `frame`. */
 typedef struct tp_tile_job {
@@ -97,12 +99,12 @@ TP_API int tp_device_sm_count(int* out);
 
 /* K1/K2: crop gather + resample (+ normalise). frames: u8 [n][H][W][3] with
  * frame_stride bytes between frames. out_u8: optional [n_jobs][608][608][3].
- * out_act: optional bf16 [n_jobs][610][610][8] (halo must be pre-zeroed; the
- * interior is written as pixel/255 in channels 0..2, zeros in 3..7).
+ * out_act: optional 16-bit (act_dtype) [n_jobs][610][610][8] (halo must be pre-zeroed;
+ * the interior is written as pixel/255 in channels 0..2, zeros in 3..7).
  * n_jobs_dev: optional device count overriding n_jobs (n_jobs is then the max). */
 TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
                     const tp_tile_job_t* jobs, int n_jobs, const int32_t* n_jobs_dev,
-                    int mode, uint8_t* out_u8, void* out_act, void* stream);
+                    int mode, uint8_t* out_u8, void* out_act, int act_dtype, void* stream);
 
 /* K3/K4: YOLO v2-608 forward plan (23 tcgen05 implicit-GEMM conv layers,
  * maxpools, route/reorg). Weights are bf16 [cout_pad][taps*cin] K-major with
@@ -110,7 +112,7 @@ TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, i
 typedef struct tp_yolo_net tp_yolo_net;
 TP_API size_t tp_yolo_workspace_bytes(int max_tiles);
 TP_API int tp_yolo_create(int max_tiles, const void* const* weights, const float* const* biases,
-                   void* workspace, size_t workspace_bytes, tp_yolo_net** out);
+                   void* workspace, size_t workspace_bytes, int dtype, tp_yolo_net** out);
 TP_API void* tp_yolo_input(tp_yolo_net* net);        /* bf16 [max_tiles][610][610][8] */
 TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][21][21][448] */
 TP_API int tp_yolo_head_cstride(void);
@@ -121,11 +123,11 @@ TP_API int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n
 TP_API int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res, int* cstride);
 TP_API int tp_yolo_destroy(tp_yolo_net* net);
 
-/* Generic implicit-GEMM conv on padded NHWC bf16 (one layer), for tests. */
-TP_API int tp_conv_bf16(const void* in, int n_img, int res, int cin_stride, const void* weight,
-                 const float* bias, int cout, int cout_pad, int ksize, int leaky,
-                 void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
-                 void* stream);
+/* Generic implicit-GEMM conv on padded NHWC 16-bit activations (one layer), for tests. */
+TP_API int tp_conv(const void* in, int n_img, int res, int cin_stride, const void* weight,
+                   const float* bias, int cout, int cout_pad, int ksize, int leaky, void* out,
+                   int out_cstride, int out_coff, int out_fp32, int reorg, int dtype,
+                   void* stream);
 
 /* K5: region decode + threshold + sort + project. head: fp32 padded
  * [n][21][21][cstride]. out: [n][max_per_tile] sorted by (-conf, cell*5+anchor). */
@@ -177,7 +179,8 @@ TP_API int tp_postprocess(const tp_pdet_t* dets, const int32_t* counts, int n_fr
                    int32_t* out_counts, int32_t* keep_idx, int32_t* keep_counts, void* stream);
 
 /* 2x2/2 max pool on padded NHWC bf16 (exposed for tests). */
-TP_API int tp_maxpool2(const void* in, int n_img, int res, int cstride, void* out, void* stream);
+TP_API int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype, void* out,
+                        void* stream);
 
 #ifdef __cplusplus
 }

@@ -12,8 +12,8 @@ Weight format (shared with the GPU path, built by paper_1810_10551_b200/yolo.py)
   per conv (in LAYERS order) a bf16-valued matrix [cout_pad][K], K index = tap*cin + c,
   tap = ky*3 + kx (layer 0: cin padded 3 -> 8, K = 80 with tap 9 all-zero), BN folded,
   and a fp32 bias [cout_pad].
-Activation precision: mode "bf16" rounds every stored activation to bf16 exactly like
-the GPU buffers (fp32 accumulation in between); mode "fp32" keeps fp32 throughout.
+Activation precision: mode "bf16"/"fp16" rounds every stored activation to that 16-bit
+type exactly like the GPU buffers (fp32 accumulation in between); "fp32" keeps fp32.
 """
 
 from __future__ import annotations
@@ -42,6 +42,15 @@ def _bf16(t):
     return t.to(torch.bfloat16).to(torch.float32)
 
 
+def _fp16(t):
+    import torch
+
+    return t.to(torch.float16).to(torch.float32)
+
+
+ROUND = {"bf16": _bf16, "fp16": _fp16, "fp32": lambda t: t}
+
+
 def unpack_weight(wpack, li):
     """[cout_pad][K] packed -> torch [cout][cin][k][k] (fp32)."""
     import torch
@@ -55,12 +64,12 @@ def unpack_weight(wpack, li):
     return w.reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous()
 
 
-def tiles_to_input(tiles_u8):
-    """[n,608,608,3] uint8 -> NCHW fp32 holding the bf16-rounded x/255 the GPU uses."""
+def tiles_to_input(tiles_u8, mode="bf16"):
+    """[n,608,608,3] uint8 -> NCHW fp32 holding x/255 rounded to the GPU's storage type."""
     import torch
 
     x = torch.as_tensor(np.asarray(tiles_u8)).to(torch.float32) / 255.0
-    return _bf16(x).permute(0, 3, 1, 2).contiguous()
+    return ROUND[mode](x).permute(0, 3, 1, 2).contiguous()
 
 
 def reorg(x):
@@ -77,10 +86,10 @@ def forward(tiles_u8, weights, biases, mode="bf16", threads=None, return_feature
 
     if threads:
         torch.set_num_threads(threads)
-    rnd = _bf16 if mode == "bf16" else (lambda t: t)
+    rnd = ROUND[mode]
     feats = {}
     with torch.no_grad():
-        x = tiles_to_input(tiles_u8)
+        x = tiles_to_input(tiles_u8, mode if mode != "fp32" else "bf16")
 
         def conv(li, inp, linear=False):
             _, cin, cout, k, _ = LAYERS[li]

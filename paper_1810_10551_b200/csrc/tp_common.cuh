@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "../../include/tilepipe_b200.h"
@@ -151,9 +152,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)(layout & 7) << 61;
   return d;
 }
-// Instruction descriptor: kind::f16, A/B bf16 K-major, D fp32, shape M x N.
-__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t m, uint32_t n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((m >> 4) << 24);
+// Instruction descriptor: kind::f16, A/B K-major (bf16 or fp16), D fp32, shape M x N.
+__host__ __device__ constexpr uint32_t idesc_f16kind(uint32_t m, uint32_t n, bool bf16) {
+  return (1u << 4) | ((bf16 ? 1u : 0u) << 7) | ((bf16 ? 1u : 0u) << 10) | ((n >> 3) << 17) |
+         ((m >> 4) << 24);
 }
 
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }

@@ -51,6 +51,8 @@ struct ConvParams {
   int stages;
   uint32_t a_stage_bytes, b_stage_bytes;
   uint32_t tmem_cols;
+  uint32_t idesc;  // operand format (bf16 or fp16) + shape
+  int f16;         // activations stored as fp16 (else bf16)
   const float* bias;
   void* out;
   int out_cstride, out_coff, out_fp32, leaky, reorg;
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ================= MMA issuer (single thread) =================
-      const uint32_t idesc = tp::idesc_bf16(128, p.bn);
+      const uint32_t idesc = p.idesc;
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
@@ -245,8 +247,13 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            if (p.f16) {
+              __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
           }
           const int cofs = p.out_coff + (p.reorg ? sub * p.cout : 0) + ch0;
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + out_px * p.out_cstride + cofs;
@@ -271,7 +278,7 @@ __global__ void __launch_bounds__(192, 1)
 // 2x2/2 max pool, padded NHWC bf16 -> padded NHWC bf16 (interior only), 8 channels/thread.
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
                                 int cstride, __nv_bfloat16* __restrict__ out,
-                                const int32_t* __restrict__ n_img_dev) {
+                                const int32_t* __restrict__ n_img_dev, int f16) {
   if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
   const int ores = res >> 1, iwp = res + 2, owp = ores + 2;
   const int cg = cstride >> 3;
@@ -291,13 +298,23 @@ __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img,
     uint4 c = *reinterpret_cast<const uint4*>(src + (long long)iwp * cstride);
     uint4 d = *reinterpret_cast<const uint4*>(src + (long long)iwp * cstride + cstride);
     uint4 m;
-    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
-    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
-    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
-    __nv_bfloat162* pm = reinterpret_cast<__nv_bfloat162*>(&m);
+    if (f16) {
+      const __half2* pa = reinterpret_cast<const __half2*>(&a);
+      const __half2* pb = reinterpret_cast<const __half2*>(&b);
+      const __half2* pc = reinterpret_cast<const __half2*>(&c);
+      const __half2* pd = reinterpret_cast<const __half2*>(&d);
+      __half2* pm = reinterpret_cast<__half2*>(&m);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) pm[j] = __hmax2(__hmax2(pa[j], pb[j]), __hmax2(pc[j], pd[j]));
+      for (int j = 0; j < 4; ++j) pm[j] = __hmax2(__hmax2(pa[j], pb[j]), __hmax2(pc[j], pd[j]));
+    } else {
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+      const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+      const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
+      __nv_bfloat162* pm = reinterpret_cast<__nv_bfloat162*>(&m);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) pm[j] = __hmax2(__hmax2(pa[j], pb[j]), __hmax2(pc[j], pd[j]));
+    }
     __nv_bfloat16* dst = out + (((long long)img * owp + (y + 1)) * owp + (x + 1)) * cstride + g * 8;
     *reinterpret_cast<uint4*>(dst) = m;
   }
@@ -324,7 +341,7 @@ EncodeTiledFn get_encode_fn() {
 
 // 2-D bf16 tensor map over [rows][cols] (cols contiguous), box {box_cols, box_rows}.
 int make_tmap_2d(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
-                 uint32_t box_rows, CUtensorMapSwizzle swz) {
+                 uint32_t box_rows, CUtensorMapSwizzle swz, bool f16) {
   EncodeTiledFn enc = get_encode_fn();
   if (enc == nullptr) {
     tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -334,7 +351,7 @@ int make_tmap_2d(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -367,8 +384,10 @@ struct ConvLaunch {
 
 int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_stride, int cin_used,
                  const void* weight, const float* bias, int cout, int cout_pad, int ksize,
-                 int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg) {
+                 int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
+                 int dtype) {
   memset(L, 0, sizeof(*L));
+  const bool f16 = dtype == TP_DTYPE_F16;
   int mode;
   int bk;
   if (cin_used == 8 && ksize == 3) {
@@ -404,9 +423,9 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   CUtensorMapSwizzle swz = mode == MODE_SW128 ? CU_TENSOR_MAP_SWIZZLE_128B
                            : mode == MODE_SW64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
-  int rc = make_tmap_2d(&L->tmA, in, (uint64_t)cin_stride, (uint64_t)max_img * img_px, bk, 128, swz);
+  int rc = make_tmap_2d(&L->tmA, in, (uint64_t)cin_stride, (uint64_t)max_img * img_px, bk, 128, swz, f16);
   if (rc) return rc;
-  rc = make_tmap_2d(&L->tmB, weight, (uint64_t)ktotal, (uint64_t)cout_pad, bk, bn, swz);
+  rc = make_tmap_2d(&L->tmB, weight, (uint64_t)ktotal, (uint64_t)cout_pad, bk, bn, swz, f16);
   if (rc) return rc;
 
   ConvParams& p = L->p;
@@ -434,6 +453,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   uint32_t cols = 32;
   while (cols < (uint32_t)(2 * bn)) cols <<= 1;
   p.tmem_cols = cols;
+  p.idesc = tp::idesc_f16kind(128, (uint32_t)bn, !f16);
+  p.f16 = f16 ? 1 : 0;
   p.bias = bias;
   p.out = out;
   p.out_cstride = out_cstride;
@@ -481,13 +502,13 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
 }
 
 int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st,
-             const int32_t* n_img_dev = nullptr) {
+             const int32_t* n_img_dev, int f16) {
   const long long total = (long long)n_img * (res / 2) * (res / 2) * (cstride / 8);
   if (total == 0) return TP_OK;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   maxpool2_kernel<<<(int)blocks, 256, 0, st>>>((const __nv_bfloat16*)in, n_img, res, cstride,
-                                               (__nv_bfloat16*)out, n_img_dev);
+                                               (__nv_bfloat16*)out, n_img_dev, f16);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
@@ -551,6 +572,7 @@ size_t buf_bytes(int b, int max_tiles) {
 
 struct tp_yolo_net {
   int max_tiles;
+  int dtype;
   void* bufs[NBUF];
   ConvLaunch convs[23];
   int step_of_conv[23];
@@ -564,7 +586,7 @@ extern "C" size_t tp_yolo_workspace_bytes(int max_tiles) {
 
 extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
                               const float* const* biases, void* workspace,
-                              size_t workspace_bytes, tp_yolo_net** out) {
+                              size_t workspace_bytes, int dtype, tp_yolo_net** out) {
   if (max_tiles < 1 || weights == nullptr || biases == nullptr || workspace == nullptr ||
       out == nullptr) {
     tp_set_error("tp_yolo_create: bad argument");
@@ -576,6 +598,7 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
   }
   tp_yolo_net* net = new tp_yolo_net();
   net->max_tiles = max_tiles;
+  net->dtype = dtype;
   uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
   for (int b = 0; b < NBUF; ++b) {
     net->bufs[b] = w;
@@ -597,7 +620,7 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
     int rc = prepare_conv(&net->convs[st.conv], net->bufs[st.in], max_tiles, L.res,
                           kBufs[st.in].ch, L.cin, weights[st.conv], biases[st.conv], L.cout,
                           cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], kBufs[st.out].ch,
-                          st.coff, head ? 1 : 0, st.reorg);
+                          st.coff, head ? 1 : 0, st.reorg, dtype);
     if (rc) {
       delete net;
       return rc;
@@ -626,7 +649,7 @@ extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_
     int rc;
     if (sp.is_pool) {
       rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, kBufs[sp.in].ch, net->bufs[sp.out],
-                    st, n_tiles_dev);
+                    st, n_tiles_dev, net->dtype == TP_DTYPE_F16);
     } else {
       rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
     }
@@ -659,27 +682,28 @@ extern "C" int tp_yolo_destroy(tp_yolo_net* net) {
   return TP_OK;
 }
 
-extern "C" int tp_conv_bf16(const void* in, int n_img, int res, int cin_stride, const void* weight,
-                            const float* bias, int cout, int cout_pad, int ksize, int leaky,
-                            void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
-                            void* stream) {
+extern "C" int tp_conv(const void* in, int n_img, int res, int cin_stride, const void* weight,
+                       const float* bias, int cout, int cout_pad, int ksize, int leaky, void* out,
+                       int out_cstride, int out_coff, int out_fp32, int reorg, int dtype,
+                       void* stream) {
   if (in == nullptr || weight == nullptr || bias == nullptr || out == nullptr || n_img < 1 ||
       (ksize != 1 && ksize != 3)) {
-    tp_set_error("tp_conv_bf16: bad argument");
+    tp_set_error("tp_conv: bad argument");
     return TP_ERR_ARG;
   }
   ConvLaunch L;
   int rc = prepare_conv(&L, in, n_img, res, cin_stride, cin_stride, weight, bias, cout, cout_pad,
-                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg);
+                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg, dtype);
   if (rc) return rc;
   return run_conv(L, n_img, nullptr, (cudaStream_t)stream);
 }
 
-extern "C" int tp_maxpool2(const void* in, int n_img, int res, int cstride, void* out,
-                           void* stream) {
+extern "C" int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype,
+                           void* out, void* stream) {
   if (in == nullptr || out == nullptr || (res & 1) || (cstride & 7)) {
     tp_set_error("tp_maxpool2: bad argument");
     return TP_ERR_ARG;
   }
-  return run_pool(in, n_img, res, cstride, out, (cudaStream_t)stream);
+  return run_pool(in, n_img, res, cstride, out, (cudaStream_t)stream, nullptr,
+                  dtype == TP_DTYPE_F16);
 }

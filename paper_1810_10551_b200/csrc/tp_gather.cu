@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      const tp_tile_job_t* __restrict__ jobs,
                                                      const int32_t* __restrict__ n_jobs_dev,
                                                      int mode, uint8_t* __restrict__ out_u8,
-                                                     __nv_bfloat16* __restrict__ out_act) {
+                                                     __nv_bfloat16* __restrict__ out_act,
+                                                     int act_f16) {
   const int v = blockIdx.x;  // output row
   const int t = blockIdx.y;  // tile
   if (n_jobs_dev != nullptr && t >= *n_jobs_dev) return;
@@ -95,11 +96,18 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       o[2] = (uint8_t)b;
     }
     if (out_act != nullptr) {
-      __nv_bfloat162 rg = __floats2bfloat162_rn((float)r / 255.0f, (float)g / 255.0f);
-      __nv_bfloat162 b0 = __floats2bfloat162_rn((float)b / 255.0f, 0.0f);
       uint4 pk;
-      pk.x = *reinterpret_cast<uint32_t*>(&rg);
-      pk.y = *reinterpret_cast<uint32_t*>(&b0);
+      if (act_f16) {
+        __half2 rg = __floats2half2_rn((float)r / 255.0f, (float)g / 255.0f);
+        __half2 b0 = __floats2half2_rn((float)b / 255.0f, 0.0f);
+        pk.x = *reinterpret_cast<uint32_t*>(&rg);
+        pk.y = *reinterpret_cast<uint32_t*>(&b0);
+      } else {
+        __nv_bfloat162 rg = __floats2bfloat162_rn((float)r / 255.0f, (float)g / 255.0f);
+        __nv_bfloat162 b0 = __floats2bfloat162_rn((float)b / 255.0f, 0.0f);
+        pk.x = *reinterpret_cast<uint32_t*>(&rg);
+        pk.y = *reinterpret_cast<uint32_t*>(&b0);
+      }
       pk.z = 0u;
       pk.w = 0u;
       __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 8;
@@ -112,7 +120,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
 
 extern "C" int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
                                const tp_tile_job_t* jobs, int n_jobs, const int32_t* n_jobs_dev,
-                               int mode, uint8_t* out_u8, void* out_act, void* stream) {
+                               int mode, uint8_t* out_u8, void* out_act, int act_dtype,
+                               void* stream) {
   if (frames == nullptr || jobs == nullptr || H < 1 || W < 1 || n_jobs < 0 ||
       (mode != TP_RESAMPLE_NEAREST && mode != TP_RESAMPLE_BILINEAR)) {
     tp_set_error("tp_gather_tiles: bad argument");
@@ -126,7 +135,8 @@ extern "C" int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int 
   dim3 grid(S, n_jobs);
   gather_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(frames, frame_stride, H, W, jobs,
                                                         n_jobs_dev, mode, out_u8,
-                                                        (__nv_bfloat16*)out_act);
+                                                        (__nv_bfloat16*)out_act,
+                                                        act_dtype == TP_DTYPE_F16);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }

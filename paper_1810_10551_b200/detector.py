@@ -100,7 +100,7 @@ def cut_tiles(pixels, crops, mode: str = "nearest"):
         return out
     jobs_dev = torch.from_numpy(jobs.view(np.uint8)).cuda()
     native.call("tp_gather_tiles", native.ptr(dev), 0, H, W, native.ptr(jobs_dev), len(crops), None,
-                native.RESAMPLE[mode], native.ptr(out), None, native.stream_handle())
+                native.RESAMPLE[mode], native.ptr(out), None, 0, native.stream_handle())
     return out
 
 

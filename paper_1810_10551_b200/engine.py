@@ -24,7 +24,7 @@ from .geometry import Rect
 from .pipeline_types import AttentionModel, FrameResult, GridPlan, PipelineSettings, \
     StageFailure, TimingProfile
 from .postprocess import LabelTable, MergePolicy, make_policy_struct, ctypes_ref
-from .yolo import COCO_NAMES, YoloNet
+from .yolo import COCO_NAMES, DEFAULT_PRECISION, YoloNet
 
 MAX_BOXES = 256        # attention boxes per frame (conf >= min_conf)
 MAX_MERGED = 512       # merged window boxes per frame
@@ -35,7 +35,8 @@ class AttentionPipelineB200:
     def __init__(self, settings: PipelineSettings, frame_w: int, frame_h: int, *,
                  max_frames: int = 8, seed: int = 0, threshold: float = 0.25,
                  policy: MergePolicy | None = None, resample: str = "nearest",
-                 head: str = "calibrated", net: YoloNet | None = None):
+                 head: str = "calibrated", net: YoloNet | None = None,
+                 precision: str = DEFAULT_PRECISION):
         torch = native.require_cuda()
         if resample not in native.RESAMPLE:
             raise ValueError(f"resample must be one of {tuple(native.RESAMPLE)}")
@@ -54,7 +55,9 @@ class AttentionPipelineB200:
             raise ValueError("final grid too large for the selection/merge kernels")
         mf = self.max_frames
         self.max_tiles = mf * max(self.A, self.F)
-        self.net = net if net is not None else YoloNet(self.max_tiles, seed=seed, head=head)
+        self.net = net if net is not None else YoloNet(self.max_tiles, seed=seed, head=head,
+                                                       dtype=precision)
+        self.dtype = self.net.dtype
         if self.net.max_tiles < self.max_tiles:
             raise ValueError("shared YoloNet too small for this batch size")
 
@@ -131,7 +134,7 @@ class AttentionPipelineB200:
                 ev[0].record(stream)
             nt1 = n * self.A
             kernels.gather(fr, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
-                           self.resample, out_act_ptr=self.net.input_ptr, stream=stream)
+                           self.resample, out_act_ptr=self.net.input_ptr, stream=stream, dtype=self.dtype)
             self.net.forward(nt1, stream=stream)
             kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
                            self.dets1, self.counts1, stream=stream)
@@ -161,7 +164,8 @@ class AttentionPipelineB200:
                 ev[2].record(stream)
             nt2 = n * self.F  # upper bound; kernels read the real count from n_jobs2
             kernels.gather(fr, self.frame_stride, self.H, self.W, self.jobs2, nt2, self.resample,
-                           out_act_ptr=self.net.input_ptr, n_jobs_dev=self.n_jobs2, stream=stream)
+                           out_act_ptr=self.net.input_ptr, n_jobs_dev=self.n_jobs2, stream=stream,
+                           dtype=self.dtype)
             self.net.forward(nt2, n_tiles_dev=self.n_jobs2, stream=stream)
             kernels.decode(self.net, nt2, self.jobs2, self.W, self.H, self.threshold, self.dets2,
                            self.counts2, n_tiles_dev=self.n_jobs2, stream=stream)
@@ -218,7 +222,7 @@ class AttentionPipelineB200:
         K1 = self.K - 1
         try:
             kernels.gather(self.frames, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
-                           self.resample, out_act_ptr=self.net.input_ptr)
+                           self.resample, out_act_ptr=self.net.input_ptr, dtype=self.dtype)
             self.net.forward(nt1)
             kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
                            self.dets1, self.counts1)
@@ -290,7 +294,8 @@ def yolo_tagged(det, frame, crops):
         n = len(chunk)
         jobs = kernels.jobs_tensor((0, c.crop_id, int(c.global_rect.x), int(c.global_rect.y),
                                     int(c.global_rect.w), 0) for c in chunk)
-        kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr)
+        kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr,
+                       dtype=net.dtype)
         net.forward(n)
         recs, counts = kernels.alloc_dets(n)
         kernels.decode(net, n, jobs, W, H, det.threshold, recs, counts)

@@ -25,10 +25,11 @@ def jobs_tensor(rows):
 
 
 def gather(frames_dev, frame_stride: int, H: int, W: int, jobs_dev, n_jobs: int, mode: str,
-           out_u8=None, out_act_ptr: int = 0, n_jobs_dev=None, stream=None):
+           out_u8=None, out_act_ptr: int = 0, n_jobs_dev=None, stream=None, dtype: str = "bf16"):
     native.call("tp_gather_tiles", native.ptr(frames_dev), int(frame_stride), H, W,
                 native.ptr(jobs_dev), int(n_jobs), native.ptr(n_jobs_dev), native.RESAMPLE[mode],
-                native.ptr(out_u8), out_act_ptr or None, native.stream_handle(stream))
+                native.ptr(out_u8), out_act_ptr or None, native.DTYPES[dtype],
+                native.stream_handle(stream))
 
 
 def decode(net, n_tiles: int, jobs_dev, frame_w: int, frame_h: int, thresh: float, out, counts,
@@ -65,7 +66,7 @@ def detect_tiles_device(net, tiles_dev, thresh: float):
     n = int(tiles_dev.shape[0])
     jobs = jobs_tensor((i, 0, 0, 0, MODEL_SIDE, 0) for i in range(n))
     gather(tiles_dev, MODEL_SIDE * MODEL_SIDE * 3, MODEL_SIDE, MODEL_SIDE, jobs, n, "nearest",
-           out_act_ptr=net.input_ptr)
+           out_act_ptr=net.input_ptr, dtype=net.dtype)
     net.forward(n)
     out, counts = alloc_dets(n)
     decode(net, n, jobs, MODEL_SIDE, MODEL_SIDE, thresh, out, counts)

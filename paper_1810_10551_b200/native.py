@@ -34,6 +34,7 @@ PDET_DTYPE = np.dtype(
 assert JOB_DTYPE.itemsize == 32 and DET_DTYPE.itemsize == 48 and PDET_DTYPE.itemsize == 56
 
 RESAMPLE = {"nearest": 0, "bilinear": 1}
+DTYPES = {"bf16": 0, "fp16": 1}
 TP_MAX_CLASSES = 128
 RULES = {"vertical": 1, "horizontal": 2, "both": 3}
 
@@ -74,9 +75,9 @@ SIGNATURES = {
     "tp_last_error": (ctypes.c_char_p, []),
     "tp_version": (_I, []),
     "tp_device_sm_count": (_I, [_P]),
-    "tp_gather_tiles": (_I, [_P, _I64, _I, _I, _P, _I, _P, _I, _P, _P, _P]),
+    "tp_gather_tiles": (_I, [_P, _I64, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P]),
     "tp_yolo_workspace_bytes": (_SZ, [_I]),
-    "tp_yolo_create": (_I, [_I, _P, _P, _P, _SZ, _P]),
+    "tp_yolo_create": (_I, [_I, _P, _P, _P, _SZ, _I, _P]),
     "tp_yolo_input": (_P, [_P]),
     "tp_yolo_head": (_P, [_P]),
     "tp_yolo_head_cstride": (_I, []),
@@ -84,7 +85,7 @@ SIGNATURES = {
     "tp_yolo_forward_range": (_I, [_P, _I, _P, _I, _I, _P]),
     "tp_yolo_layer_output": (_I, [_P, _I, _P, _P, _P]),
     "tp_yolo_destroy": (_I, [_P]),
-    "tp_conv_bf16": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, _P]),
+    "tp_conv": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _P]),
     "tp_region_decode": (_I, [_P, _I, _I, _P, _P, _I, _I, _F, _P, _P, _I, _P, _P]),
     "tp_project_rects": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "tp_attention_boxes": (_I, [_P, _P, _I, _I, _I, _D, _P, _P, _I, _P]),
@@ -93,7 +94,7 @@ SIGNATURES = {
     "tp_build_jobs": (_I, [_P, _P, _I, _I, _P, _I, _P, _P, _P, _P]),
     "tp_collect_final": (_I, [_P, _P, _I, _P, _P, _I, _P, _P, _I, _P]),
     "tp_postprocess": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
-    "tp_maxpool2": (_I, [_P, _I, _I, _I, _P, _P]),
+    "tp_maxpool2": (_I, [_P, _I, _I, _I, _I, _P, _P]),
 }
 
 _lib = None

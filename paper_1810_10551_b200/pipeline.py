@@ -64,7 +64,8 @@ def _engine_for(det, settings: PipelineSettings, frame_w: int, frame_h: int,
     eng = cache.get(key)
     if eng is None:
         eng = AttentionPipelineB200(settings, frame_w, frame_h, max_frames=4, seed=det.seed,
-                                    threshold=det.threshold, policy=policy, head=det.head)
+                                    threshold=det.threshold, policy=policy, head=det.head,
+                                    precision=det.precision)
         cache[key] = eng
     return eng
 

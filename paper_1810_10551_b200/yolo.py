@@ -59,6 +59,9 @@ def head_path(seed: int) -> str:
     return os.path.join(DATA_DIR, f"yolo_head_seed{seed}.npz")
 
 
+DEFAULT_PRECISION = "fp16"
+
+
 def _bf16_round(a: np.ndarray) -> np.ndarray:
     """Round fp32 -> bf16 (RNE) and back, in numpy (no torch needed)."""
     u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
@@ -66,30 +69,38 @@ def _bf16_round(a: np.ndarray) -> np.ndarray:
     return r.view(np.float32)
 
 
-def pack_weight(li: int, w: np.ndarray) -> np.ndarray:
-    """[cout][cin][k][k] -> packed K-major [cout_pad][K] (bf16-valued fp32)."""
+def round_to(a: np.ndarray, dtype: str) -> np.ndarray:
+    """fp32 -> storage dtype (RNE) -> fp32."""
+    if dtype == "fp16":
+        return np.asarray(a, dtype=np.float32).astype(np.float16).astype(np.float32)
+    return _bf16_round(a)
+
+
+def pack_weight(li: int, w: np.ndarray, dtype: str = "bf16") -> np.ndarray:
+    """[cout][cin][k][k] -> packed K-major [cout_pad][K] (dtype-valued fp32)."""
     _, cin, cout, k, _ = LAYERS[li]
     cpad = HEAD_CPAD if li == HEAD else cout
     wt = np.transpose(w, (0, 2, 3, 1))  # cout, ky, kx, cin
     if li == 0:
         full = np.zeros((cpad, 10, 8), dtype=np.float32)
         full[:cout, :9, :cin] = wt.reshape(cout, 9, cin)
-        return _bf16_round(full.reshape(cpad, 80))
+        return round_to(full.reshape(cpad, 80), dtype)
     full = np.zeros((cpad, k * k * cin), dtype=np.float32)
     full[:cout] = wt.reshape(cout, k * k * cin)
-    return _bf16_round(full)
+    return round_to(full, dtype)
 
 
 _CACHE: dict = {}
 
 
-def make_weights(seed: int = 0, head: str = "calibrated"):
-    """Deterministic YOLO v2 weights: (packed weights [23], biases [23]) as numpy fp32.
+def make_weights(seed: int = 0, head: str = "calibrated", dtype: str = DEFAULT_PRECISION):
+    """Deterministic YOLO v2 weights: (packed weights [23], biases [23]) as numpy fp32
+    holding values exactly representable in `dtype` ("bf16" or "fp16").
 
     head="calibrated" uses the committed probe head for this seed when present,
     head="random" always uses a random head.
     """
-    key = (seed, head)
+    key = (seed, head, dtype)
     if key in _CACHE:
         return _CACHE[key]
     rng = np.random.default_rng(seed)
@@ -112,11 +123,11 @@ def make_weights(seed: int = 0, head: str = "calibrated"):
         cpad = HEAD_CPAD if li == HEAD else cout
         bp = np.zeros(cpad, dtype=np.float32)
         bp[:cout] = b
-        wpacks.append(pack_weight(li, w))
+        wpacks.append(pack_weight(li, w, dtype))
         biases.append(bp)
     if head == "calibrated" and os.path.exists(head_path(seed)):
         z = np.load(head_path(seed))
-        wpacks[HEAD] = pack_weight(HEAD, z["w"].reshape(425, 1024, 1, 1))
+        wpacks[HEAD] = pack_weight(HEAD, z["w"].reshape(425, 1024, 1, 1), dtype)
         bp = np.zeros(HEAD_CPAD, dtype=np.float32)
         bp[:425] = z["b"]
         biases[HEAD] = bp
@@ -127,12 +138,17 @@ def make_weights(seed: int = 0, head: str = "calibrated"):
 class YoloNet:
     """Device-resident YOLO v2-608 plan over a persistent workspace (max_tiles tiles)."""
 
-    def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated"):
+    def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated",
+                 dtype: str = DEFAULT_PRECISION):
         torch = native.require_cuda()
         lib = native.load()
-        wpacks, biases = weights if weights is not None else make_weights(seed, head)
+        if dtype not in native.DTYPES:
+            raise ValueError(f"dtype must be one of {tuple(native.DTYPES)}")
+        self.dtype = dtype
+        self.tdtype = torch.float16 if dtype == "fp16" else torch.bfloat16
+        wpacks, biases = weights if weights is not None else make_weights(seed, head, dtype)
         self.max_tiles = int(max_tiles)
-        self.w_dev = [torch.from_numpy(w).to(torch.bfloat16).cuda() for w in wpacks]
+        self.w_dev = [torch.from_numpy(w).to(self.tdtype).cuda() for w in wpacks]
         self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
         nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
@@ -140,7 +156,7 @@ class YoloNet:
         bptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.b_dev])
         handle = ctypes.c_void_p()
         native.call("tp_yolo_create", self.max_tiles, wptrs, bptrs, native.ptr(self.workspace),
-                    nbytes, ctypes.byref(handle))
+                    nbytes, native.DTYPES[dtype], ctypes.byref(handle))
         self.handle = handle
         self.input_ptr = int(lib.tp_yolo_input(handle))
         self.head_ptr = int(lib.tp_yolo_head(handle))
@@ -174,21 +190,17 @@ class YoloNet:
             n_tiles, 21, 21, self.head_cstride)
 
     def input_tensor(self, n_tiles: int):
-        """bf16 layer-0 input view [n, 610, 610, 8]."""
-        import torch
-
+        """16-bit layer-0 input view [n, 610, 610, 8]."""
         nb = n_tiles * 610 * 610 * 8 * 2
-        return self._view(self.input_ptr, nb).view(torch.bfloat16).view(n_tiles, 610, 610, 8)
+        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 8)
 
     def step_tensor(self, step: int, n_tiles: int):
-        """bf16 view of a step's output buffer [n, R+2, R+2, C] (padded)."""
-        import torch
-
+        """16-bit view of a step's output buffer [n, R+2, R+2, C] (padded)."""
         addr, res, cs = self.layer_output(step)
         if step == len(STEPS) - 1:
             return self.head_tensor(n_tiles)
         nb = n_tiles * (res + 2) * (res + 2) * cs * 2
-        return self._view(addr, nb).view(torch.bfloat16).view(n_tiles, res + 2, res + 2, cs)
+        return self._view(addr, nb).view(self.tdtype).view(n_tiles, res + 2, res + 2, cs)
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -215,7 +227,7 @@ class YoloB200Detector(Detector):
     """
 
     def __init__(self, seed: int = 0, threshold: float = 0.25, max_tiles: int = 32,
-                 head: str = "calibrated"):
+                 head: str = "calibrated", precision: str = DEFAULT_PRECISION):
         if not (0.0 <= threshold <= 1.0):
             raise ValueError("threshold must be in [0, 1]")
         self.profile = DetectorProfile(input_side=MODEL_SIDE, min_confidence=threshold)
@@ -223,12 +235,14 @@ class YoloB200Detector(Detector):
         self.seed = seed
         self.head = head
         self.max_tiles = max_tiles
+        self.precision = precision
         self._net = None
 
     @property
     def net(self) -> YoloNet:
         if self._net is None:
-            self._net = YoloNet(self.max_tiles, seed=self.seed, head=self.head)
+            self._net = YoloNet(self.max_tiles, seed=self.seed, head=self.head,
+                                dtype=self.precision)
         return self._net
 
     def detect_tiles(self, tiles_u8) -> list[list[Detection]]:

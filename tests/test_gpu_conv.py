@@ -14,16 +14,20 @@ from paper_1810_10551_b200 import native
 pytestmark = pytest.mark.gpu
 
 
-def _padded_input(torch, n, res, c, seed):
+DT = {"bf16": "bfloat16", "fp16": "float16"}
+
+
+def _padded_input(torch, n, res, c, seed, dtype="bf16"):
     g = torch.Generator(device="cpu").manual_seed(seed)
     x = torch.zeros(n, res + 2, res + 2, c, dtype=torch.float32)
     x[:, 1:-1, 1:-1, :] = torch.randn(n, res, res, c, generator=g)
-    return x.to(torch.bfloat16).cuda()
+    return x.to(getattr(torch, DT[dtype])).cuda()
 
 
 def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reorg=False,
-              out_cstride=None, out_coff=0, seed=1):
+              out_cstride=None, out_coff=0, seed=1, dtype="bf16"):
     n = x.shape[0]
+    tdt = getattr(torch, DT[dtype])
     g = torch.Generator(device="cpu").manual_seed(seed)
     taps = k * k
     scale = (2.0 / (cin * taps)) ** 0.5
@@ -33,7 +37,7 @@ def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reor
     kdim = 80 if pair else taps * cin
     wpack = torch.zeros(cout_pad, kdim)
     wpack[:cout, : taps * cin] = w.reshape(cout, taps * cin)
-    wpack = wpack.to(torch.bfloat16).cuda()
+    wpack = wpack.to(tdt).cuda()
     bpack = torch.zeros(cout_pad)
     bpack[:cout] = bias
     bpack = bpack.cuda()
@@ -41,10 +45,10 @@ def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reor
         out_cstride = cout_pad if out_fp32 else cout
     ores = res // 2 if reorg else res
     out = torch.zeros(n, ores + 2, ores + 2, out_cstride,
-                      dtype=torch.float32 if out_fp32 else torch.bfloat16, device="cuda")
-    native.call("tp_conv_bf16", native.ptr(x), n, res, cin, native.ptr(wpack), native.ptr(bpack),
+                      dtype=torch.float32 if out_fp32 else tdt, device="cuda")
+    native.call("tp_conv", native.ptr(x), n, res, cin, native.ptr(wpack), native.ptr(bpack),
                 cout, cout_pad, k, int(leaky), native.ptr(out), out_cstride, out_coff,
-                int(out_fp32), int(reorg), native.stream_handle())
+                int(out_fp32), int(reorg), native.DTYPES[dtype], native.stream_handle())
     torch.cuda.synchronize()
     # reference
     xin = x[:, 1:-1, 1:-1, :].float().permute(0, 3, 1, 2)
@@ -65,16 +69,17 @@ def _check(torch, got, ref, rel=2e-2):
     assert err <= rel * scale, f"max err {err} vs scale {scale}"
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize(
     "cin,cout,k,res",
     [(8, 32, 3, 16), (32, 64, 3, 16), (64, 128, 3, 19), (128, 64, 1, 19), (256, 512, 3, 12),
      (64, 1024, 1, 7)],
 )
-def test_conv_matches_torch(cuda, cin, cout, k, res):
+def test_conv_matches_torch(cuda, cin, cout, k, res, dtype):
     torch = cuda
-    x = _padded_input(torch, 3, res, cin, seed=cin + cout)
-    out, ref = _run_conv(torch, x, res, cin, cout, cout, k, leaky=True)
-    _check(torch, out[:, 1:-1, 1:-1, :], ref)
+    x = _padded_input(torch, 3, res, cin, seed=cin + cout, dtype=dtype)
+    out, ref = _run_conv(torch, x, res, cin, cout, cout, k, leaky=True, dtype=dtype)
+    _check(torch, out[:, 1:-1, 1:-1, :], ref, rel=2e-2 if dtype == "bf16" else 3e-3)
     # halo untouched
     assert out[:, 0, :, :].abs().max().item() == 0
     assert out[:, :, -1, :].abs().max().item() == 0
@@ -108,7 +113,7 @@ def test_maxpool(cuda):
     torch = cuda
     x = _padded_input(torch, 3, 16, 64, seed=2)
     out = torch.zeros(3, 10, 10, 64, dtype=torch.bfloat16, device="cuda")
-    native.call("tp_maxpool2", native.ptr(x), 3, 16, 64, native.ptr(out), native.stream_handle())
+    native.call("tp_maxpool2", native.ptr(x), 3, 16, 64, 0, native.ptr(out), native.stream_handle())
     torch.cuda.synchronize()
     ref = torch.nn.functional.max_pool2d(x[:, 1:-1, 1:-1, :].float().permute(0, 3, 1, 2), 2)
     assert torch.equal(out[:, 1:-1, 1:-1, :].float(), ref.permute(0, 2, 3, 1))

@@ -20,10 +20,14 @@ from paper_1810_10551_b200.engine import MAX_PER_FRAME, AttentionPipelineB200
 
 pytestmark = pytest.mark.gpu
 
-# bf16 activation storage: rounding flips caused by a different fp32 accumulation order
-# propagate through 23 layers; measured max score drift on B200 ~5e-3.
-BOX_REL = 2e-3     # |d coord| / 608 (608-space local rects)
-CONF_ABS = 1e-2    # absolute score difference
+# 16-bit activation storage (default fp16 operands, fp32 accumulation): rounding flips
+# caused by a different fp32 accumulation order propagate through 23 layers.
+BOX_REL = 1e-3     # |d coord| / 608 (608-space local rects)
+# Measured on B200 with fp16 operands: boxes 1.8e-4 (inside the north-star 1e-3), scores
+# up to 4.9e-3 relative for low-confidence detections (sigmoid slope x fp16 activation
+# rounding through 23 layers); the north-star 1e-3 score bar needs fp32 activation storage.
+CONF_REL = 6e-3    # |d score| / score
+CONF_ABS = 2e-3    # a detection this close to the threshold may exist on one side only
 
 
 @pytest.fixture(scope="module")
@@ -107,10 +111,10 @@ def test_boxes_and_scores_match_cpu_oracle(engine, clip):
                      + [R.cut_tile_nearest(fr.pixels, plan.fin[3][k]) for k in (7, 8)])
     det = yolo.YoloB200Detector(max_tiles=4)
     gpu = det.detect_tiles(tiles)
-    wpacks, biases = yolo.make_weights(0)
-    head = yolo_ref.forward(tiles, wpacks, biases, mode="bf16")
+    wpacks, biases = yolo.make_weights(0, dtype=det.precision)
+    head = yolo_ref.forward(tiles, wpacks, biases, mode=det.precision)
     ref = yolo_ref.region_decode(head, det.threshold)
-    n_match = 0
+    n_match, conf_err, box_err = 0, 0.0, 0.0
     for g_list, r_list in zip(gpu, ref):
         r_used = set()
         for g in g_list:
@@ -126,9 +130,12 @@ def test_boxes_and_scores_match_cpu_oracle(engine, clip):
                 assert abs(g.confidence - det.threshold) < CONF_ABS, (g, bd)
                 continue
             r_used.add(best)
-            assert abs(r_list[best][2] - g.confidence) <= CONF_ABS
+            conf_err = max(conf_err, abs(r_list[best][2] - g.confidence) / r_list[best][2])
+            box_err = max(box_err, bd / 608)
             n_match += 1
         for k, (rr, cls, conf, idx) in enumerate(r_list):
             if k not in r_used:
                 assert abs(conf - det.threshold) < CONF_ABS, (rr, conf)
+    print(f"matched {n_match}: max score rel err {conf_err:.2e}, max box err/608 {box_err:.2e}")
     assert n_match > 0
+    assert conf_err <= CONF_REL and box_err <= BOX_REL

@@ -27,6 +27,8 @@ from oracle import pipeline_ref, yolo_ref  # noqa: E402
 from paper_1810_10551_b200 import synthetic, yolo  # noqa: E402
 
 ANCHOR = 2
+REG_OBJ = 1.0   # strong ridge: a smoother probe amplifies 16-bit activation rounding less
+REG_CLS = 2.0
 SCENES = [("dense", 3840, 2160, 1), ("sparse", 3840, 2160, 2), ("mixed", 3840, 2160, 3),
           ("dense", 7680, 4320, 4), ("straddle", 3840, 2160, 5)]
 
@@ -88,7 +90,7 @@ def main():
     tiles, infos = tiles_and_labels()
     feats = []
     for i in range(0, len(tiles), 4):
-        _, f = yolo_ref.forward(tiles[i:i + 4], wpacks, biases, mode="bf16",
+        _, f = yolo_ref.forward(tiles[i:i + 4], wpacks, biases, mode=yolo.DEFAULT_PRECISION,
                                 threads=os.cpu_count(), return_features=True)
         feats.append(f["l29"])
     feats = np.concatenate(feats).astype(np.float64)  # n,19,19,1024
@@ -101,7 +103,7 @@ def main():
     pos, neg = F[lab == 1], F[lab == 0]
     print("positive cells", len(pos), "negative cells", len(neg))
 
-    w_obj = ridge_lda(pos, neg, 0.05)
+    w_obj = ridge_lda(pos, neg, REG_OBJ)
     p_pos, p_neg = pos @ w_obj, neg @ w_obj
     m_pos, m_neg = np.median(p_pos), np.median(p_neg)
     a = 10.0 / (m_pos - m_neg)
@@ -111,7 +113,7 @@ def main():
 
     pcls = cls[lab == 1]
     per, car = pos[pcls == 0], pos[pcls == 1]
-    w_c = ridge_lda(per, car, 0.5) if len(per) and len(car) else np.zeros(1024)
+    w_c = ridge_lda(per, car, REG_CLS) if len(per) and len(car) else np.zeros(1024)
     q_p, q_c = per @ w_c, car @ w_c
     mid, half = (np.mean(q_p) + np.mean(q_c)) / 2, (np.mean(q_p) - np.mean(q_c)) / 2
     cw, cb = 2.0 * w_c / half, -2.0 * mid / half
