@@ -99,8 +99,9 @@ TP_API int tp_device_sm_count(int* out);
 
 /* K1/K2: crop gather + resample (+ normalise). frames: u8 [n][H][W][3] with
  * frame_stride bytes between frames. out_u8: optional [n_jobs][608][608][3].
- * out_act: optional 16-bit (act_dtype) [n_jobs][610][610][8] (halo must be pre-zeroed;
- * the interior is written as pixel/255 in channels 0..2, zeros in 3..7).
+ * out_act: optional 16-bit (act_dtype) [n_jobs][610][610][16] layer-0 input (halo must be
+ * pre-zeroed); interior pixel = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000], p = value/255,
+ * neighbours outside the tile are 0.
  * n_jobs_dev: optional device count overriding n_jobs (n_jobs is then the max). */
 TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
                     const tp_tile_job_t* jobs, int n_jobs, const int32_t* n_jobs_dev,
@@ -113,7 +114,8 @@ typedef struct tp_yolo_net tp_yolo_net;
 TP_API size_t tp_yolo_workspace_bytes(int max_tiles);
 TP_API int tp_yolo_create(int max_tiles, const void* const* weights, const float* const* biases,
                    void* workspace, size_t workspace_bytes, int dtype, tp_yolo_net** out);
-TP_API void* tp_yolo_input(tp_yolo_net* net);        /* bf16 [max_tiles][610][610][8] */
+TP_API void* tp_yolo_input(tp_yolo_net* net);        /* 16-bit [max_tiles][610][610][16] */
+TP_API int tp_yolo_num_steps(void);
 TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][21][21][448] */
 TP_API int tp_yolo_head_cstride(void);
 TP_API int tp_yolo_forward(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev, void* stream);
@@ -123,10 +125,12 @@ TP_API int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n
 TP_API int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res, int* cstride);
 TP_API int tp_yolo_destroy(tp_yolo_net* net);
 
-/* Generic implicit-GEMM conv on padded NHWC 16-bit activations (one layer), for tests. */
+/* Generic implicit-GEMM conv on padded NHWC 16-bit activations (one layer), for tests.
+ * cin_stride == 16 with ksize 3 is the layer-0 expanded-input mode; pool != 0 fuses a
+ * 2x2/2 max pool (out is then the half-resolution padded buffer). */
 TP_API int tp_conv(const void* in, int n_img, int res, int cin_stride, const void* weight,
                    const float* bias, int cout, int cout_pad, int ksize, int leaky, void* out,
-                   int out_cstride, int out_coff, int out_fp32, int reorg, int dtype,
+                   int out_cstride, int out_coff, int out_fp32, int reorg, int dtype, int pool,
                    void* stream);
 
 /* K5: region decode + threshold + sort + project. head: fp32 padded

@@ -10,7 +10,7 @@ pinned by the repo's own golden vectors (seeded weights, rendered synthetic tile
 
 Weight format (shared with the GPU path, built by paper_1810_10551_b200/yolo.py):
   per conv (in LAYERS order) a bf16-valued matrix [cout_pad][K], K index = tap*cin + c,
-  tap = ky*3 + kx (layer 0: cin padded 3 -> 8, K = 80 with tap 9 all-zero), BN folded,
+  tap = ky*3 + kx (layer 0: K = 48 = ky x [kx 0..2, pad] x [rgb, pad]), BN folded,
   and a fp32 bias [cout_pad].
 Activation precision: mode "bf16"/"fp16" rounds every stored activation to that 16-bit
 type exactly like the GPU buffers (fp32 accumulation in between); "fp32" keeps fp32.
@@ -57,8 +57,8 @@ def unpack_weight(wpack, li):
 
     _, cin, cout, k, _ = LAYERS[li]
     w = torch.as_tensor(np.asarray(wpack, dtype=np.float32))
-    if li == 0:
-        w = w[:cout, :72].reshape(cout, 9, 8)[:, :, :cin]
+    if li == 0:  # K = dy(3) x [dx(3)+pad] x [rgb+pad]
+        w = w[:cout, :48].reshape(cout, 3, 4, 4)[:, :, :3, :cin].reshape(cout, 9, cin)
     else:
         w = w[:cout, : k * k * cin].reshape(cout, k * k, cin)
     return w.reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous()

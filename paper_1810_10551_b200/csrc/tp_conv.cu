@@ -4,55 +4,62 @@
 // pkg/src/tilepipe/detector.py:77-96); the topology is yolov2-608 (Darknet-19 +
 // passthrough head) as cited by PAPER.md:85,120, restated in oracle/yolo_ref.py.
 //
-// Activation layout ("padded flat NHWC"): every feature map of side R lives in a
-// buffer [tile][R+2][R+2][C] bf16 whose 1-pixel halo is zero and never written.
-// A 3x3/1 same conv is then a GEMM over the flat padded pixel index p:
-//     out[p, n] = sum_{tap, c} in[p + dy*(R+2) + dx, c] * W[n, tap, c]
-// so the A operand of tap (dy,dx) for an M tile [m0, m0+128) is a plain 2-D TMA
-// box at row m0 + shift — no im2col buffer, no gather. Rows that land on halo
-// pixels compute garbage that the epilogue never stores; TMA zero-fills the rows
-// outside the tensor. The waste is the halo share ((R+2)^2/R^2: 0.7% at 608,
-// 22% at 19).
+// Activation layout ("padded NHWC"): every feature map of side R lives in a buffer
+// [tile][R+2][R+2][C] (fp16 or bf16) whose 1-pixel halo is zero and never written.
+// A 3x3/1 same conv is a GEMM over output pixels, K = taps x C, and the A operand of
+// tap (dy,dx) is a TMA box shifted by (dy,dx) — no im2col buffer:
+//   * FLAT tiles (non-pooled layers): M tile = 128 consecutive padded pixels; the
+//     shifted box is a plain 2-D box at row m0 + dy*(R+2) + dx. Rows on halo pixels
+//     compute garbage the epilogue never stores (waste = (R+2)^2/R^2).
+//   * RECT tiles (layers followed by a 2x2 maxpool): M tile = a 16x8 pixel rectangle
+//     loaded as a 3-D box {C, 16, 8}; the epilogue pools in registers (lane^1 and
+//     lane^16 shuffles) and writes the half-resolution map directly, so the
+//     full-resolution activation never touches HBM and no pool kernel runs.
+//   * Layer 0 (3 channels) reads a horizontally expanded input (gather writes, per
+//     pixel, [p(x-1) rgb0, p(x) rgb0, p(x+1) rgb0, 0000] = 32 bytes): one 32-byte-wide
+//     box per kernel row dy, K = 16 per MMA, 3 MMAs per tile.
 //
-// Kernel: persistent, warp-specialised, one CTA per SM (192 threads):
-//   warp 0      TMA producer (A box + B box per k-block into an S-stage ring)
+// Kernel: persistent, warp-specialised, one CTA per SM (320 threads):
+//   warp 0      TMA producer (A box + B box per k-block into an S-stage smem ring)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256,
-//               K=16 per instruction, fp32 accumulate in TMEM, 2 accumulators)
-//   warps 2..5  epilogue: tcgen05.ld -> +bias (BN folded) -> leaky(0.1) -> bf16
-//               -> interior-only store (optionally channel-offset into the route
-//               concat buffer, or space-to-depth "reorg", or fp32 for the head)
-// Operand smem tiles use the 128B (BK=64) or 64B (BK=32) swizzle; layer 0 (3 input
-// channels, padded to 8) uses SWIZZLE_NONE with two 16-byte taps per K=16 step.
+//               K=16 per instruction, fp32 accumulate in TMEM, double-buffered)
+//   warps 2..9  epilogue, two warps per TMEM lane quadrant splitting the columns:
+//               tcgen05.ld -> +bias (BN folded) -> leaky(0.1) -> [2x2 max] -> 16-bit
+//               -> interior-only store (or channel-offset into the route concat
+//               buffer, space-to-depth "reorg", or fp32 for the head)
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
-
-#include <vector>
 
 #include "tp_common.cuh"
 #include "../../include/tilepipe_b200.h"
 
 namespace {
 
-enum ConvMode { MODE_SW128 = 0, MODE_SW64 = 1, MODE_PAIR = 2 };
+enum ConvMode { MODE_SW128 = 0, MODE_SW64 = 1, MODE_L0X = 2 };
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int RECT_W = 16, RECT_H = 8;
 
 struct ConvParams {
   int n_img;
   const int32_t* n_img_dev;
   int res, wp, img_px;
   int ksize;
-  int cin;        // channels per tap used by K (multiple of BK)
-  int cout;       // real output channels
-  int bn;         // N tile
+  int cin;         // channels per tap used by K (multiple of BK)
+  int cout;        // real output channels
+  int bn;          // N tile
   int n_blocks_n;
-  int num_kb;     // k-blocks per output tile
+  int num_kb;      // k-blocks per output tile
   int kb_per_tap;
   int stages;
   uint32_t a_stage_bytes, b_stage_bytes;
   uint32_t tmem_cols;
   uint32_t idesc;  // operand format (bf16 or fp16) + shape
   int f16;         // activations stored as fp16 (else bf16)
+  int rect;        // RECT tiles + fused 2x2 maxpool
+  int tiles_x, tiles_y;
   const float* bias;
   void* out;
   int out_cstride, out_coff, out_fp32, leaky, reorg;
@@ -60,15 +67,23 @@ struct ConvParams {
 
 __device__ __forceinline__ int tap_shift(int tap, int ksize, int wp) {
   if (ksize == 1) return 0;
-  if (tap > 8) tap = 8;  // layer-0 pad tap: weights are zero, reuse a valid shift
   return (tap / 3 - 1) * wp + (tap % 3 - 1);
 }
 
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar,
+                                            int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(tp::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(tp::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const ConvParams p) {
-  constexpr int BK = MODE == MODE_SW128 ? 64 : (MODE == MODE_SW64 ? 32 : 8);
+  constexpr int BK = MODE == MODE_SW128 ? 64 : (MODE == MODE_SW64 ? 32 : 16);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -94,7 +109,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tp::mbar_init(&tfull[a], 1);
-      tp::mbar_init(&tempty[a], 4);
+      tp::mbar_init(&tempty[a], kEpiWarps);
     }
     tp::fence_mbar_init();
   }
@@ -105,9 +120,10 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
-  const long long total_px = (long long)n_img * p.img_px;
-  const int m_blocks = (int)((total_px + 127) / 128);
+  const int rect_per_img = p.tiles_x * p.tiles_y;
+  const int m_blocks = p.rect ? n_img * rect_per_img : (n_img * p.img_px + 127) / 128;
   const int total_tiles = m_blocks * p.n_blocks_n;
+  const int hp = p.res + 2;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -116,23 +132,39 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t ph = 0;
       const uint32_t tx_bytes = p.a_stage_bytes + p.b_stage_bytes;
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const int m0 = (t / p.n_blocks_n) * 128;
-        const int n0 = (t % p.n_blocks_n) * p.bn;
+        const int mt = t / p.n_blocks_n;
+        const int n0 = (t - mt * p.n_blocks_n) * p.bn;
+        int m0 = 0, rx = 0, ry = 0;
+        if (p.rect) {
+          const int img = mt / rect_per_img;
+          const int r = mt - img * rect_per_img;
+          const int by = r / p.tiles_x;
+          rx = 1 + (r - by * p.tiles_x) * RECT_W;
+          ry = img * hp + 1 + by * RECT_H;
+        } else {
+          m0 = mt * 128;
+        }
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&empty[s], ph ^ 1);
           uint8_t* a_dst = smA + (size_t)s * p.a_stage_bytes;
           uint8_t* b_dst = smB + (size_t)s * p.b_stage_bytes;
           tp::mbar_arrive_expect_tx(&full[s], tx_bytes);
-          if (MODE == MODE_PAIR) {
-            const int t0 = 2 * kb, t1 = 2 * kb + 1;
-            tp::tma_load_2d(a_dst, &tmA, &full[s], 0, m0 + tap_shift(t0, p.ksize, p.wp));
-            tp::tma_load_2d(a_dst + 128 * 16, &tmA, &full[s], 0, m0 + tap_shift(t1, p.ksize, p.wp));
-            tp::tma_load_2d(b_dst, &tmB, &full[s], t0 * 8, n0);
-            tp::tma_load_2d(b_dst + p.bn * 16, &tmB, &full[s], t1 * 8, n0);
+          if (MODE == MODE_L0X) {  // one k-block per kernel row dy
+            if (p.rect)
+              tma_load_3d(a_dst, &tmA, &full[s], 0, rx, ry + kb - 1);
+            else
+              tp::tma_load_2d(a_dst, &tmA, &full[s], 0, m0 + (kb - 1) * p.wp);
+            tp::tma_load_2d(b_dst, &tmB, &full[s], kb * 16, n0);
           } else {
             const int tap = kb / p.kb_per_tap;
             const int cb = kb - tap * p.kb_per_tap;
-            tp::tma_load_2d(a_dst, &tmA, &full[s], cb * BK, m0 + tap_shift(tap, p.ksize, p.wp));
+            if (p.rect) {
+              const int dy = p.ksize == 3 ? tap / 3 - 1 : 0;
+              const int dx = p.ksize == 3 ? tap % 3 - 1 : 0;
+              tma_load_3d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry + dy);
+            } else {
+              tp::tma_load_2d(a_dst, &tmA, &full[s], cb * BK, m0 + tap_shift(tap, p.ksize, p.wp));
+            }
             tp::tma_load_2d(b_dst, &tmB, &full[s], tap * p.cin + cb * BK, n0);
           }
           if (++s == S) {
@@ -174,8 +206,8 @@ __global__ void __launch_bounds__(192, 1)
               tp::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
             }
           } else {
-            uint64_t ad = tp::umma_desc(a_addr, 128 * 16, 128, 0);
-            uint64_t bd = tp::umma_desc(b_addr, p.bn * 16, 128, 0);
+            uint64_t ad = tp::umma_desc(a_addr, 16, 256, 6);
+            uint64_t bd = tp::umma_desc(b_addr, 16, 256, 6);
             tp::mma_bf16(d_tmem, ad, bd, idesc, kb != 0);
           }
           tp::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
@@ -190,58 +222,86 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ================= epilogue (warps 2..5) =================
-    const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
+    // ================= epilogue (warps 2..9) =================
+    const uint32_t q = warp & 3;            // TMEM lane quadrant this warp may access
+    const int half = (int)(warp - 2) >> 2;  // which half of the N tile
     const int row = (int)(q * 32 + lane);
+    const int cols_per = p.bn >> 1;
     int acc = 0;
     uint32_t aph = 0;
-    const int out_res = p.res >> 1, out_wp = out_res + 2, out_img_px = out_wp * out_wp;
+    const int ores = p.res >> 1, owp = ores + 2, oimg = owp * owp;
+    const int total_px = n_img * p.img_px;
     for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const int m0 = (t / p.n_blocks_n) * 128;
-      const int n0 = (t % p.n_blocks_n) * p.bn;
+      const int mt = t / p.n_blocks_n;
+      const int n0 = (t - mt * p.n_blocks_n) * p.bn;
       tp::mbar_wait(&tfull[acc], aph);
       tp::tc_fence_after();
 
-      const long long pix = (long long)m0 + row;
-      bool valid = pix < total_px;
-      long long out_px = 0;
-      int sub = 0;
-      if (valid) {
-        const int img = (int)(pix / p.img_px);
-        const int rem = (int)(pix - (long long)img * p.img_px);
-        const int yp = rem / p.wp, xp = rem - (rem / p.wp) * p.wp;
-        valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
-        if (p.reorg) {
-          const int y = yp - 1, x = xp - 1;
-          sub = (y & 1) * 2 + (x & 1);
-          out_px = (long long)img * out_img_px + (long long)((y >> 1) + 1) * out_wp + ((x >> 1) + 1);
-        } else {
-          out_px = pix;
+      bool valid, writer = true;
+      int out_px = 0, sub = 0;
+      if (p.rect) {
+        const int img = mt / rect_per_img;
+        const int r = mt - img * rect_per_img;
+        const int by = r / p.tiles_x, bx = r - (r / p.tiles_x) * p.tiles_x;
+        const int x = bx * RECT_W + (row & (RECT_W - 1)), y = by * RECT_H + (row >> 4);
+        valid = img < n_img && x < p.res && y < p.res;
+        writer = ((x | y) & 1) == 0;
+        out_px = img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
+      } else {
+        const int pix = mt * 128 + row;
+        valid = pix < total_px;
+        if (valid) {
+          const int img = pix / p.img_px;
+          const int rem = pix - img * p.img_px;
+          const int yp = rem / p.wp, xp = rem - (rem / p.wp) * p.wp;
+          valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
+          if (p.reorg) {
+            const int y = yp - 1, x = xp - 1;
+            sub = (y & 1) * 2 + (x & 1);
+            out_px = img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
+          } else {
+            out_px = pix;
+          }
         }
       }
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * p.bn);
-      for (int c = 0; c < p.bn; c += 16) {
+      for (int c = half * cols_per; c < (half + 1) * cols_per; c += 16) {
         uint32_t v[16];
         tp::tmem_ld16(t_row + (uint32_t)c, v);
         tp::tmem_ld_wait();
         const int ch0 = n0 + c;
-        if (!valid || ch0 >= p.cout) continue;
         float f[16];
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + ch0);  // padded to cout_pad
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int ch = ch0 + j;
-          float x = __uint_as_float(v[j]) + (ch < p.cout ? __ldg(p.bias + ch) : 0.0f);
-          if (p.leaky) x = x > 0.0f ? x : 0.1f * x;
-          f[j] = x;
+        for (int j = 0; j < 4; ++j) {
+          const float4 bb = __ldg(b4 + j);
+          f[4 * j + 0] = __uint_as_float(v[4 * j + 0]) + bb.x;
+          f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + bb.y;
+          f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + bb.z;
+          f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + bb.w;
         }
+        if (p.leaky) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = f[j] > 0.0f ? f[j] : 0.1f * f[j];
+        }
+        if (p.rect) {  // fused 2x2 max pool: x pair = lane^1, y pair = lane^16
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+            f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], RECT_W));
+          }
+        }
+        if (!valid || !writer || ch0 >= p.cout) continue;
         if (p.out_fp32) {
-          float* o = reinterpret_cast<float*>(p.out) + out_px * p.out_cstride + p.out_coff + ch0;
+          float* o = reinterpret_cast<float*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
           if (ch0 + 16 <= p.cout) {
 #pragma unroll
             for (int j = 0; j < 16; j += 4)
               *reinterpret_cast<float4*>(o + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
           } else {
-            for (int j = 0; j < 16 && ch0 + j < p.cout; ++j) o[j] = f[j];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (ch0 + j < p.cout) o[j] = f[j];
           }
         } else {
           uint32_t pk[8];
@@ -256,7 +316,7 @@ __global__ void __launch_bounds__(192, 1)
             }
           }
           const int cofs = p.out_coff + (p.reorg ? sub * p.cout : 0) + ch0;
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + out_px * p.out_cstride + cofs;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride + cofs;
           *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
@@ -275,7 +335,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 1) tp::tmem_dealloc(tmem_base, p.tmem_cols);
 }
 
-// 2x2/2 max pool, padded NHWC bf16 -> padded NHWC bf16 (interior only), 8 channels/thread.
+// 2x2/2 max pool, padded NHWC 16-bit -> padded NHWC (interior only), 8 channels/thread.
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
                                 int cstride, __nv_bfloat16* __restrict__ out,
                                 const int32_t* __restrict__ n_img_dev, int f16) {
@@ -339,24 +399,32 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map over [rows][cols] (cols contiguous), box {box_cols, box_rows}.
-int make_tmap_2d(CUtensorMap* tm, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols,
-                 uint32_t box_rows, CUtensorMapSwizzle swz, bool f16) {
+// rank-2 {cols, rows} or rank-3 {cols, width, rows} 16-bit tensor map, cols contiguous.
+int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
+              const uint32_t* box, CUtensorMapSwizzle swz, bool f16) {
   EncodeTiledFn enc = get_encode_fn();
   if (enc == nullptr) {
     tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
     return TP_ERR_CUDA;
   }
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t gdims[3], strides[2];
+  cuuint32_t gbox[3], estr[3] = {1, 1, 1};
+  uint64_t stride = dims[0] * 2;
+  for (int i = 0; i < rank; ++i) {
+    gdims[i] = dims[i];
+    gbox[i] = box[i];
+    if (i > 0) {
+      strides[i - 1] = stride;
+      stride *= dims[i];
+    }
+  }
+  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   rank, const_cast<void*>(base), gdims, strides, gbox, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    tp_set_error("cuTensorMapEncodeTiled failed (%d): cols=%llu rows=%llu box=%u,%u", (int)r,
-                 (unsigned long long)cols, (unsigned long long)rows, box_cols, box_rows);
+    tp_set_error("cuTensorMapEncodeTiled failed (%d): rank %d dims %llu,%llu box %u,%u", (int)r,
+                 rank, (unsigned long long)dims[0], (unsigned long long)dims[1], box[0], box[1]);
     return TP_ERR_CUDA;
   }
   return TP_OK;
@@ -379,20 +447,21 @@ struct ConvLaunch {
   CUtensorMap tmA, tmB;
   ConvParams p;
   size_t smem;
-  int max_tiles_total;
 };
 
+// cin_used == 16 && ksize == 3 selects the layer-0 expanded-input mode.
+// pool != 0 selects RECT tiles with the 2x2 max pool fused; `out` is then the
+// half-resolution buffer.
 int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_stride, int cin_used,
                  const void* weight, const float* bias, int cout, int cout_pad, int ksize,
                  int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
-                 int dtype) {
+                 int dtype, int pool) {
   memset(L, 0, sizeof(*L));
   const bool f16 = dtype == TP_DTYPE_F16;
-  int mode;
-  int bk;
-  if (cin_used == 8 && ksize == 3) {
-    mode = MODE_PAIR;
-    bk = 8;
+  int mode, bk;
+  if (cin_used == 16 && ksize == 3) {
+    mode = MODE_L0X;
+    bk = 16;
   } else if (cin_used % 64 == 0) {
     mode = MODE_SW128;
     bk = 64;
@@ -403,29 +472,51 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     tp_set_error("conv: unsupported cin %d", cin_used);
     return TP_ERR_UNSUPPORTED;
   }
-  if (cout_pad % 16 != 0 || cout_pad < 16 || cout > cout_pad) {
-    tp_set_error("conv: bad cout/cout_pad %d/%d", cout, cout_pad);
+  if (cout_pad % 32 != 0 || cout > cout_pad) {
+    tp_set_error("conv: bad cout/cout_pad %d/%d (cout_pad must be a multiple of 32)", cout,
+                 cout_pad);
+    return TP_ERR_ARG;
+  }
+  if (pool && (res % 2 != 0 || reorg || out_fp32)) {
+    tp_set_error("conv: fused pool needs an even side and a 16-bit plain output");
     return TP_ERR_ARG;
   }
   int bn = cout_pad;
   if (bn > 256) {
     bn = 256;
-    while (cout_pad % bn != 0 || bn % 16 != 0) bn -= 16;
+    while (cout_pad % bn != 0 || bn % 32 != 0) bn -= 32;
   }
   if (!out_fp32 && (cout % 16 != 0 || out_cstride % 8 != 0 || out_coff % 8 != 0)) {
-    tp_set_error("conv: bf16 output needs 16-channel multiples");
+    tp_set_error("conv: 16-bit output needs 16-channel multiples");
     return TP_ERR_ARG;
   }
   const int wp = res + 2;
   const int img_px = wp * wp;
+  if ((long long)max_img * img_px >= (1ll << 31)) {
+    tp_set_error("conv: %d images of side %d exceed 32-bit pixel indexing", max_img, res);
+    return TP_ERR_CAPACITY;
+  }
   const int taps = ksize * ksize;
-  const int ktotal = mode == MODE_PAIR ? 80 : taps * cin_used;
+  const int ktotal = mode == MODE_L0X ? 48 : taps * cin_used;
   CUtensorMapSwizzle swz = mode == MODE_SW128 ? CU_TENSOR_MAP_SWIZZLE_128B
                            : mode == MODE_SW64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
-  int rc = make_tmap_2d(&L->tmA, in, (uint64_t)cin_stride, (uint64_t)max_img * img_px, bk, 128, swz, f16);
+                                               : CU_TENSOR_MAP_SWIZZLE_32B;
+  int rc;
+  if (pool) {
+    const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
+    const uint32_t box[3] = {(uint32_t)bk, RECT_W, RECT_H};
+    rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16);
+  } else {
+    const uint64_t dims[2] = {(uint64_t)cin_stride, (uint64_t)max_img * img_px};
+    const uint32_t box[2] = {(uint32_t)bk, 128};
+    rc = make_tmap(&L->tmA, in, 2, dims, box, swz, f16);
+  }
   if (rc) return rc;
-  rc = make_tmap_2d(&L->tmB, weight, (uint64_t)ktotal, (uint64_t)cout_pad, bk, bn, swz, f16);
+  {
+    const uint64_t dims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+    const uint32_t box[2] = {(uint32_t)bk, (uint32_t)bn};
+    rc = make_tmap(&L->tmB, weight, 2, dims, box, swz, f16);
+  }
   if (rc) return rc;
 
   ConvParams& p = L->p;
@@ -438,13 +529,13 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.cout = cout;
   p.bn = bn;
   p.n_blocks_n = cout_pad / bn;
-  p.kb_per_tap = mode == MODE_PAIR ? 1 : cin_used / bk;
-  p.num_kb = mode == MODE_PAIR ? 5 : taps * p.kb_per_tap;
-  p.a_stage_bytes = mode == MODE_PAIR ? 2 * 128 * 16 : 128 * bk * 2;
-  p.b_stage_bytes = mode == MODE_PAIR ? 2 * bn * 16 : bn * bk * 2;
+  p.kb_per_tap = mode == MODE_L0X ? 1 : cin_used / bk;
+  p.num_kb = mode == MODE_L0X ? 3 : taps * p.kb_per_tap;
+  p.a_stage_bytes = 128 * bk * 2;
+  p.b_stage_bytes = bn * bk * 2;
   const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
   int stages = (int)((200 * 1024) / stage_bytes);
-  if (stages > 8) stages = 8;
+  if (stages > 12) stages = 12;
   if (stages < 2) {
     tp_set_error("conv: stage too large");
     return TP_ERR_UNSUPPORTED;
@@ -455,6 +546,9 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.tmem_cols = cols;
   p.idesc = tp::idesc_f16kind(128, (uint32_t)bn, !f16);
   p.f16 = f16 ? 1 : 0;
+  p.rect = pool ? 1 : 0;
+  p.tiles_x = (res + RECT_W - 1) / RECT_W;
+  p.tiles_y = (res + RECT_H - 1) / RECT_H;
   p.bias = bias;
   p.out = out;
   p.out_cstride = out_cstride;
@@ -464,8 +558,6 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.reorg = reorg;
   L->mode = mode;
   L->smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
-  const long long m_blocks = ((long long)max_img * img_px + 127) / 128;
-  L->max_tiles_total = (int)(m_blocks * p.n_blocks_n);
   return TP_OK;
 }
 
@@ -480,11 +572,12 @@ int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   ConvParams p = L.p;
   p.n_img = n_img;
   p.n_img_dev = n_img_dev;
-  const long long m_blocks = ((long long)n_img * p.img_px + 127) / 128;
+  const long long m_blocks = p.rect ? (long long)n_img * p.tiles_x * p.tiles_y
+                                    : ((long long)n_img * p.img_px + 127) / 128;
   const long long tiles = m_blocks * p.n_blocks_n;
   if (tiles == 0) return TP_OK;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_tc_kernel<MODE><<<grid, 192, L.smem, st>>>(L.tmA, L.tmB, p);
+  conv_tc_kernel<MODE><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
@@ -497,7 +590,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
   switch (L.mode) {
     case MODE_SW128: return launch_mode<MODE_SW128>(L, n_img, n_img_dev, st);
     case MODE_SW64: return launch_mode<MODE_SW64>(L, n_img, n_img_dev, st);
-    default: return launch_mode<MODE_PAIR>(L, n_img, n_img_dev, st);
+    default: return launch_mode<MODE_L0X>(L, n_img, n_img_dev, st);
   }
 }
 
@@ -515,12 +608,13 @@ int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStr
 
 // ------------------------------------------------------------------ YOLO v2-608 plan
 // Layer table (darknet layer index, cin, cout, ksize, res). BN is folded into
-// weights+bias by the host; layer 30 is linear (no BN, no leaky).
+// weights+bias by the host; layer 30 is linear (no BN, no leaky). Layer 0's cin is the
+// 16-channel expanded input (3 taps x 4 channels + 4 zeros per pixel).
 struct LayerDef {
   int idx, cin, cout, k, res;
 };
 const LayerDef kConvs[23] = {
-    {0, 8, 32, 3, 608},      {2, 32, 64, 3, 304},     {4, 64, 128, 3, 152},
+    {0, 16, 32, 3, 608},     {2, 32, 64, 3, 304},     {4, 64, 128, 3, 152},
     {5, 128, 64, 1, 152},    {6, 64, 128, 3, 152},    {8, 128, 256, 3, 76},
     {9, 256, 128, 1, 76},    {10, 128, 256, 3, 76},   {12, 256, 512, 3, 38},
     {13, 512, 256, 1, 38},   {14, 256, 512, 3, 38},   {15, 512, 256, 1, 38},
@@ -530,37 +624,34 @@ const LayerDef kConvs[23] = {
     {29, 1280, 1024, 3, 19}, {30, 1024, 425, 1, 19}};
 
 enum Buf {
-  I608, C608, P304, C304, P152, A152, B152, C152, P76, A76, B76, C76, P38, A38, B38, E38, P19,
-  A19, B19, C19, CAT19, HEAD, NBUF
+  I608, P304, P152, A152, B152, P76, A76, B76, P38, A38, B38, E38, P19, A19, B19, C19, CAT19,
+  HEAD, NBUF
 };
 struct BufDef {
   int res, ch, bytes_per;  // bytes per element
 };
-const BufDef kBufs[NBUF] = {{608, 8, 2},   {608, 32, 2},  {304, 32, 2},   {304, 64, 2},
-                            {152, 64, 2},  {152, 128, 2}, {152, 64, 2},   {152, 128, 2},
-                            {76, 128, 2},  {76, 256, 2},  {76, 128, 2},   {76, 256, 2},
+const BufDef kBufs[NBUF] = {{608, 16, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
+                            {152, 64, 2},  {76, 128, 2},  {76, 256, 2},   {76, 128, 2},
                             {38, 256, 2},  {38, 512, 2},  {38, 256, 2},   {38, 512, 2},
                             {19, 512, 2},  {19, 1024, 2}, {19, 512, 2},   {19, 1024, 2},
                             {19, 1280, 2}, {19, 448, 4}};
 constexpr int kHeadCstride = 448;
 
-// Step list: conv (layer slot, in, out, coff, reorg) or pool (in, out).
+// Step list: conv (layer slot, in, out, channel offset, reorg, fused pool) or pool (in, out).
 struct Step {
   int is_pool;
   int conv;  // index into kConvs
-  int in, out, coff, reorg;
+  int in, out, coff, reorg, fpool;
 };
 const Step kSteps[] = {
-    {0, 0, I608, C608, 0, 0},   {1, -1, C608, P304, 0, 0},  {0, 1, P304, C304, 0, 0},
-    {1, -1, C304, P152, 0, 0},  {0, 2, P152, A152, 0, 0},   {0, 3, A152, B152, 0, 0},
-    {0, 4, B152, C152, 0, 0},   {1, -1, C152, P76, 0, 0},   {0, 5, P76, A76, 0, 0},
-    {0, 6, A76, B76, 0, 0},     {0, 7, B76, C76, 0, 0},     {1, -1, C76, P38, 0, 0},
-    {0, 8, P38, A38, 0, 0},     {0, 9, A38, B38, 0, 0},     {0, 10, B38, A38, 0, 0},
-    {0, 11, A38, B38, 0, 0},    {0, 12, B38, E38, 0, 0},    {1, -1, E38, P19, 0, 0},
-    {0, 13, P19, A19, 0, 0},    {0, 14, A19, B19, 0, 0},    {0, 15, B19, C19, 0, 0},
-    {0, 16, C19, B19, 0, 0},    {0, 17, B19, A19, 0, 0},    {0, 18, A19, C19, 0, 0},
-    {0, 19, C19, CAT19, 256, 0}, {0, 20, E38, CAT19, 0, 1}, {0, 21, CAT19, A19, 0, 0},
-    {0, 22, A19, HEAD, 0, 0}};
+    {0, 0, I608, P304, 0, 0, 1},  {0, 1, P304, P152, 0, 0, 1},  {0, 2, P152, A152, 0, 0, 0},
+    {0, 3, A152, B152, 0, 0, 0},  {0, 4, B152, P76, 0, 0, 1},   {0, 5, P76, A76, 0, 0, 0},
+    {0, 6, A76, B76, 0, 0, 0},    {0, 7, B76, P38, 0, 0, 1},    {0, 8, P38, A38, 0, 0, 0},
+    {0, 9, A38, B38, 0, 0, 0},    {0, 10, B38, A38, 0, 0, 0},   {0, 11, A38, B38, 0, 0, 0},
+    {0, 12, B38, E38, 0, 0, 0},   {1, -1, E38, P19, 0, 0, 0},   {0, 13, P19, A19, 0, 0, 0},
+    {0, 14, A19, B19, 0, 0, 0},   {0, 15, B19, C19, 0, 0, 0},   {0, 16, C19, B19, 0, 0, 0},
+    {0, 17, B19, A19, 0, 0, 0},   {0, 18, A19, C19, 0, 0, 0},   {0, 19, C19, CAT19, 256, 0, 0},
+    {0, 20, E38, CAT19, 0, 1, 0}, {0, 21, CAT19, A19, 0, 0, 0}, {0, 22, A19, HEAD, 0, 0, 0}};
 constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
 
 size_t buf_bytes(int b, int max_tiles) {
@@ -575,7 +666,6 @@ struct tp_yolo_net {
   int dtype;
   void* bufs[NBUF];
   ConvLaunch convs[23];
-  int step_of_conv[23];
 };
 
 extern "C" size_t tp_yolo_workspace_bytes(int max_tiles) {
@@ -620,12 +710,11 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
     int rc = prepare_conv(&net->convs[st.conv], net->bufs[st.in], max_tiles, L.res,
                           kBufs[st.in].ch, L.cin, weights[st.conv], biases[st.conv], L.cout,
                           cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], kBufs[st.out].ch,
-                          st.coff, head ? 1 : 0, st.reorg, dtype);
+                          st.coff, head ? 1 : 0, st.reorg, dtype, st.fpool);
     if (rc) {
       delete net;
       return rc;
     }
-    net->step_of_conv[st.conv] = s;
   }
   *out = net;
   return TP_OK;
@@ -636,6 +725,7 @@ extern "C" const float* tp_yolo_head(tp_yolo_net* net) {
   return net ? reinterpret_cast<const float*>(net->bufs[HEAD]) : nullptr;
 }
 extern "C" int tp_yolo_head_cstride(void) { return kHeadCstride; }
+extern "C" int tp_yolo_num_steps(void) { return kNumSteps; }
 
 extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev,
                                      int first, int last, void* stream) {
@@ -684,7 +774,7 @@ extern "C" int tp_yolo_destroy(tp_yolo_net* net) {
 
 extern "C" int tp_conv(const void* in, int n_img, int res, int cin_stride, const void* weight,
                        const float* bias, int cout, int cout_pad, int ksize, int leaky, void* out,
-                       int out_cstride, int out_coff, int out_fp32, int reorg, int dtype,
+                       int out_cstride, int out_coff, int out_fp32, int reorg, int dtype, int pool,
                        void* stream) {
   if (in == nullptr || weight == nullptr || bias == nullptr || out == nullptr || n_img < 1 ||
       (ksize != 1 && ksize != 3)) {
@@ -693,7 +783,7 @@ extern "C" int tp_conv(const void* in, int n_img, int res, int cin_stride, const
   }
   ConvLaunch L;
   int rc = prepare_conv(&L, in, n_img, res, cin_stride, cin_stride, weight, bias, cout, cout_pad,
-                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg, dtype);
+                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg, dtype, pool);
   if (rc) return rc;
   return run_conv(L, n_img, nullptr, (cudaStream_t)stream);
 }

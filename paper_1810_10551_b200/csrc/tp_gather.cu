@@ -7,9 +7,9 @@
 // integer arithmetic to oracle/resample_ref.py so it is bit-exact as well.
 //
 // One CTA per (tile, output row). Each thread produces whole pixels: 3 bytes of the
-// u8 tile and/or one 16-byte bf16x8 group of the padded layer-0 input
-// ([tile][610][610][8], channels 3..7 zero), so every store is a full, aligned
-// vector store. Source reads are row-local (one or two source rows per CTA), which
+// u8 tile and/or the 32-byte horizontally expanded layer-0 input pixel
+// ([tile][610][610][16] = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000], fp16/bf16),
+// so every activation store is two full, aligned 16-byte vector stores. Source reads are row-local (one or two source rows per CTA), which
 // keeps them L1/L2-resident; the kernel is HBM-bound on the tile writes.
 #include "tp_common.cuh"
 #include "../../include/tilepipe_b200.h"
@@ -71,10 +71,14 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
     fy = ty.f;
   }
 
-  for (int u = threadIdx.x; u < S; u += blockDim.x) {
-    int r, g, b;
+  // RGB of tile column u on this output row (zero outside [0, 608) and outside the frame)
+  auto sample = [&](int u, int& r, int& g, int& b) {
+    if (u < 0 || u >= S) {
+      r = g = b = 0;
+      return;
+    }
     if (mode == TP_RESAMPLE_NEAREST) {
-      int sx = job.x + (int)(((long long)u * side) / S);
+      const int sx = job.x + (int)(((long long)u * side) / S);
       load_px(frame, H, W, sx, sy0, r, g, b);
     } else {
       Tap tx = bilinear_tap(u, side);
@@ -89,6 +93,19 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       g = (g00 * w00 + g01 * w01 + g10 * w10 + g11 * w11 + 32768) >> 16;
       b = (b00 * w00 + b01 * w01 + b10 * w10 + b11 * w11 + 32768) >> 16;
     }
+  };
+  auto pack = [&](int a, int b) -> uint32_t {
+    if (act_f16) {
+      __half2 h = __floats2half2_rn((float)a / 255.0f, (float)b / 255.0f);
+      return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __nv_bfloat162 h = __floats2bfloat162_rn((float)a / 255.0f, (float)b / 255.0f);
+    return *reinterpret_cast<uint32_t*>(&h);
+  };
+
+  for (int u = threadIdx.x; u < S; u += blockDim.x) {
+    int r, g, b;
+    sample(u, r, g, b);
     if (out_u8 != nullptr) {
       uint8_t* o = out_u8 + (((size_t)t * S + v) * S + u) * 3;
       o[0] = (uint8_t)r;
@@ -96,22 +113,22 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       o[2] = (uint8_t)b;
     }
     if (out_act != nullptr) {
-      uint4 pk;
-      if (act_f16) {
-        __half2 rg = __floats2half2_rn((float)r / 255.0f, (float)g / 255.0f);
-        __half2 b0 = __floats2half2_rn((float)b / 255.0f, 0.0f);
-        pk.x = *reinterpret_cast<uint32_t*>(&rg);
-        pk.y = *reinterpret_cast<uint32_t*>(&b0);
-      } else {
-        __nv_bfloat162 rg = __floats2bfloat162_rn((float)r / 255.0f, (float)g / 255.0f);
-        __nv_bfloat162 b0 = __floats2bfloat162_rn((float)b / 255.0f, 0.0f);
-        pk.x = *reinterpret_cast<uint32_t*>(&rg);
-        pk.y = *reinterpret_cast<uint32_t*>(&b0);
-      }
-      pk.z = 0u;
-      pk.w = 0u;
-      __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 8;
-      *reinterpret_cast<uint4*>(o) = pk;
+      // expanded layer-0 pixel: [p(u-1) rgb0 | p(u) rgb0 | p(u+1) rgb0 | 0 0 0 0]
+      int rl, gl, bl, rr, gr, br;
+      sample(u - 1, rl, gl, bl);
+      sample(u + 1, rr, gr, br);
+      uint4 lo, hi;
+      lo.x = pack(rl, gl);
+      lo.y = pack(bl, 0);
+      lo.z = pack(r, g);
+      lo.w = pack(b, 0);
+      hi.x = pack(rr, gr);
+      hi.y = pack(br, 0);
+      hi.z = 0u;
+      hi.w = 0u;
+      __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 16;
+      *reinterpret_cast<uint4*>(o) = lo;
+      *reinterpret_cast<uint4*>(o + 8) = hi;
     }
   }
 }

@@ -85,7 +85,8 @@ SIGNATURES = {
     "tp_yolo_forward_range": (_I, [_P, _I, _P, _I, _I, _P]),
     "tp_yolo_layer_output": (_I, [_P, _I, _P, _P, _P]),
     "tp_yolo_destroy": (_I, [_P]),
-    "tp_conv": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _P]),
+    "tp_conv": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _P]),
+    "tp_yolo_num_steps": (_I, []),
     "tp_region_decode": (_I, [_P, _I, _I, _P, _P, _I, _I, _F, _P, _P, _I, _P, _P]),
     "tp_project_rects": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "tp_attention_boxes": (_I, [_P, _P, _I, _I, _I, _D, _P, _P, _I, _P]),

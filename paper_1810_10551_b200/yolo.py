@@ -81,10 +81,10 @@ def pack_weight(li: int, w: np.ndarray, dtype: str = "bf16") -> np.ndarray:
     _, cin, cout, k, _ = LAYERS[li]
     cpad = HEAD_CPAD if li == HEAD else cout
     wt = np.transpose(w, (0, 2, 3, 1))  # cout, ky, kx, cin
-    if li == 0:
-        full = np.zeros((cpad, 10, 8), dtype=np.float32)
-        full[:cout, :9, :cin] = wt.reshape(cout, 9, cin)
-        return round_to(full.reshape(cpad, 80), dtype)
+    if li == 0:  # expanded input: K = dy(3) x [dx(3)+pad] x [rgb+pad] = 3 x 4 x 4
+        full = np.zeros((cpad, 3, 4, 4), dtype=np.float32)
+        full[:cout, :, :3, :cin] = wt
+        return round_to(full.reshape(cpad, 48), dtype)
     full = np.zeros((cpad, k * k * cin), dtype=np.float32)
     full[:cout] = wt.reshape(cout, k * k * cin)
     return round_to(full, dtype)
@@ -190,9 +190,9 @@ class YoloNet:
             n_tiles, 21, 21, self.head_cstride)
 
     def input_tensor(self, n_tiles: int):
-        """16-bit layer-0 input view [n, 610, 610, 8]."""
-        nb = n_tiles * 610 * 610 * 8 * 2
-        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 8)
+        """16-bit expanded layer-0 input view [n, 610, 610, 16]."""
+        nb = n_tiles * 610 * 610 * 16 * 2
+        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 16)
 
     def step_tensor(self, step: int, n_tiles: int):
         """16-bit view of a step's output buffer [n, R+2, R+2, C] (padded)."""
@@ -209,12 +209,13 @@ class YoloNet:
             self.handle = None
 
 
-# step list of csrc/tp_conv.cu kSteps: ("conv", layer slot) or ("pool", None)
-STEPS = [("conv", 0), ("pool", None), ("conv", 1), ("pool", None), ("conv", 2), ("conv", 3),
-         ("conv", 4), ("pool", None), ("conv", 5), ("conv", 6), ("conv", 7), ("pool", None),
-         ("conv", 8), ("conv", 9), ("conv", 10), ("conv", 11), ("conv", 12), ("pool", None),
-         ("conv", 13), ("conv", 14), ("conv", 15), ("conv", 16), ("conv", 17), ("conv", 18),
-         ("conv", 19), ("conv", 20), ("conv", 21), ("conv", 22)]
+# step list of csrc/tp_conv.cu kSteps: ("conv", layer slot) or ("pool", None); layers 0, 2,
+# 6 and 10 have the 2x2 max pool fused into their epilogue (POOLED)
+STEPS = [("conv", 0), ("conv", 1), ("conv", 2), ("conv", 3), ("conv", 4), ("conv", 5),
+         ("conv", 6), ("conv", 7), ("conv", 8), ("conv", 9), ("conv", 10), ("conv", 11),
+         ("conv", 12), ("pool", None), ("conv", 13), ("conv", 14), ("conv", 15), ("conv", 16),
+         ("conv", 17), ("conv", 18), ("conv", 19), ("conv", 20), ("conv", 21), ("conv", 22)]
+POOLED = {0, 1, 4, 7}  # layer slots with a fused pool
 
 
 class YoloB200Detector(Detector):

@@ -25,7 +25,7 @@ def _padded_input(torch, n, res, c, seed, dtype="bf16"):
 
 
 def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reorg=False,
-              out_cstride=None, out_coff=0, seed=1, dtype="bf16"):
+              out_cstride=None, out_coff=0, seed=1, dtype="bf16", pool=False):
     n = x.shape[0]
     tdt = getattr(torch, DT[dtype])
     g = torch.Generator(device="cpu").manual_seed(seed)
@@ -33,9 +33,7 @@ def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reor
     scale = (2.0 / (cin * taps)) ** 0.5
     w = torch.randn(cout, taps, cin, generator=g) * scale
     bias = torch.randn(cout, generator=g) * 0.1
-    pair = cin == 8 and k == 3
-    kdim = 80 if pair else taps * cin
-    wpack = torch.zeros(cout_pad, kdim)
+    wpack = torch.zeros(cout_pad, taps * cin)
     wpack[:cout, : taps * cin] = w.reshape(cout, taps * cin)
     wpack = wpack.to(tdt).cuda()
     bpack = torch.zeros(cout_pad)
@@ -43,12 +41,13 @@ def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reor
     bpack = bpack.cuda()
     if out_cstride is None:
         out_cstride = cout_pad if out_fp32 else cout
-    ores = res // 2 if reorg else res
+    ores = res // 2 if (reorg or pool) else res
     out = torch.zeros(n, ores + 2, ores + 2, out_cstride,
                       dtype=torch.float32 if out_fp32 else tdt, device="cuda")
     native.call("tp_conv", native.ptr(x), n, res, cin, native.ptr(wpack), native.ptr(bpack),
                 cout, cout_pad, k, int(leaky), native.ptr(out), out_cstride, out_coff,
-                int(out_fp32), int(reorg), native.DTYPES[dtype], native.stream_handle())
+                int(out_fp32), int(reorg), native.DTYPES[dtype], int(pool),
+                native.stream_handle())
     torch.cuda.synchronize()
     # reference
     xin = x[:, 1:-1, 1:-1, :].float().permute(0, 3, 1, 2)
@@ -58,6 +57,8 @@ def _run_conv(torch, x, res, cin, cout, cout_pad, k, leaky, out_fp32=False, reor
     ref = torch.nn.functional.conv2d(xin, wq, bias=bpack[:cout], padding=k // 2)
     if leaky:
         ref = torch.where(ref > 0, ref, 0.1 * ref)
+    if pool:
+        ref = torch.nn.functional.max_pool2d(ref, 2)
     ref = ref.permute(0, 2, 3, 1)  # n, res, res, cout
     return out, ref
 
@@ -72,7 +73,7 @@ def _check(torch, got, ref, rel=2e-2):
 @pytest.mark.parametrize("dtype", ["bf16", "fp16"])
 @pytest.mark.parametrize(
     "cin,cout,k,res",
-    [(8, 32, 3, 16), (32, 64, 3, 16), (64, 128, 3, 19), (128, 64, 1, 19), (256, 512, 3, 12),
+    [(32, 32, 3, 16), (32, 64, 3, 16), (64, 128, 3, 19), (128, 64, 1, 19), (256, 512, 3, 12),
      (64, 1024, 1, 7)],
 )
 def test_conv_matches_torch(cuda, cin, cout, k, res, dtype):
@@ -107,6 +108,45 @@ def test_conv_reorg_and_channel_offset(cuda):
                            leaky=True, out_cstride=1280, out_coff=256)
     _check(torch, out2[:, 1:-1, 1:-1, 256:320], ref2)
     assert out2[:, :, :, :256].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("cin,cout,res", [(32, 64, 32), (64, 128, 40), (128, 256, 76),
+                                          (64, 128, 152)])
+def test_conv_fused_pool_rect_tiles(cuda, cin, cout, res, dtype):
+    """RECT 16x8 tiles (3-D TMA boxes) + 2x2 max pool in the epilogue, incl. partial tiles."""
+    torch = cuda
+    x = _padded_input(torch, 2, res, cin, seed=res, dtype=dtype)
+    out, ref = _run_conv(torch, x, res, cin, cout, cout, 3, leaky=True, dtype=dtype, pool=True)
+    _check(torch, out[:, 1:-1, 1:-1, :], ref, rel=2e-2 if dtype == "bf16" else 3e-3)
+    assert out[:, 0].abs().max().item() == 0 and out[:, :, -1].abs().max().item() == 0
+
+
+def test_conv_layer0_expanded_input(cuda):
+    """Layer-0 mode: input pixel = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000]."""
+    torch = cuda
+    n, res = 2, 64
+    g = torch.Generator(device="cpu").manual_seed(4)
+    img = torch.rand(n, res, res, 3, generator=g).half().float()
+    ex = torch.zeros(n, res + 2, res + 2, 16)
+    ex[:, 1:-1, 1:-1, 4:7] = img
+    ex[:, 1:-1, 2:-1, 0:3] = img[:, :, :-1]
+    ex[:, 1:-1, 1:-2, 8:11] = img[:, :, 1:]
+    ex = ex.half().cuda()
+    w = torch.randn(32, 3, 3, 3, generator=g) * 0.3  # cout, ky, kx, cin
+    wpack = torch.zeros(32, 3, 4, 4)
+    wpack[:, :, :3, :3] = w
+    wpack = wpack.reshape(32, 48).half().cuda()
+    bias = (torch.randn(32, generator=g) * 0.1).cuda()
+    out = torch.zeros(n, res // 2 + 2, res // 2 + 2, 32, dtype=torch.float16, device="cuda")
+    native.call("tp_conv", native.ptr(ex), n, res, 16, native.ptr(wpack), native.ptr(bias), 32,
+                32, 3, 1, native.ptr(out), 32, 0, 0, 0, native.DTYPES["fp16"], 1,
+                native.stream_handle())
+    torch.cuda.synchronize()
+    wq = wpack.float().reshape(32, 3, 4, 4)[:, :, :3, :3].permute(0, 3, 1, 2)
+    ref = torch.nn.functional.conv2d(img.cuda().permute(0, 3, 1, 2), wq, bias, padding=1)
+    ref = torch.nn.functional.max_pool2d(torch.where(ref > 0, ref, 0.1 * ref), 2)
+    _check(torch, out[:, 1:-1, 1:-1, :], ref.permute(0, 2, 3, 1), rel=3e-3)
 
 
 def test_maxpool(cuda):

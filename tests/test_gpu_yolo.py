@@ -53,10 +53,13 @@ def _run(cuda, net, tiles):
 def test_input_normalisation_matches_oracle(cuda, net, tiles):
     torch = cuda
     n = _run(cuda, net, tiles)
-    got = net.input_tensor(n)[:, 1:-1, 1:-1, :3].float().cpu()
+    x = net.input_tensor(n)[:, 1:-1, 1:-1, :].float().cpu()
     ref = yolo_ref.tiles_to_input(tiles, net.dtype).permute(0, 2, 3, 1)
-    assert torch.equal(got, ref)
-    assert net.input_tensor(n)[:, 1:-1, 1:-1, 3:].abs().max().item() == 0
+    assert torch.equal(x[..., 4:7], ref)                    # p(x)
+    assert torch.equal(x[:, :, 1:, 0:3], ref[:, :, :-1])     # p(x-1)
+    assert torch.equal(x[:, :, :-1, 8:11], ref[:, :, 1:])    # p(x+1)
+    assert x[:, :, 0, 0:3].abs().max().item() == 0 and x[:, :, -1, 8:11].abs().max().item() == 0
+    assert x[..., [3, 7, 11, 12, 13, 14, 15]].abs().max().item() == 0
 
 
 def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
@@ -66,9 +69,9 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
     wpacks, biases = yolo.make_weights(0, dtype=net.dtype)
     # producer step of each conv step's input (-1 = network input); buffers are reused
     # across steps, so each step is run and checked before the next one overwrites them
-    conv_inputs = {0: -1, 2: 1, 4: 3, 5: 4, 6: 5, 8: 7, 9: 8, 10: 9, 12: 11, 13: 12, 14: 13,
-                   15: 14, 16: 15, 18: 17, 19: 18, 20: 19, 21: 20, 22: 21, 23: 22, 24: 23,
-                   25: 16, 26: 24, 27: 26}
+    conv_inputs = {0: -1, 1: 0, 2: 1, 3: 2, 4: 3, 5: 4, 6: 5, 7: 6, 8: 7, 9: 8, 10: 9,
+                   11: 10, 12: 11, 14: 13, 15: 14, 16: 15, 17: 16, 18: 17, 19: 18, 20: 19,
+                   21: 12, 22: 20, 23: 22}
     worst = 0.0
     li = -1
     for step, (kind, _) in enumerate(yolo.STEPS):
@@ -80,7 +83,7 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
         src_step = conv_inputs[step]
         _, cin, cout, k, res = yolo.LAYERS[li]
         if src_step < 0:
-            xin = net.input_tensor(n)[:, 1:-1, 1:-1, :3]
+            xin = net.input_tensor(n)[:, 1:-1, 1:-1, 4:7]
         else:
             xin = net.step_tensor(src_step, n)[:, 1:-1, 1:-1, :]
         xin = xin.float().permute(0, 3, 1, 2)
@@ -89,6 +92,8 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
         ref = torch.nn.functional.conv2d(xin, w, b, padding=k // 2)
         if li != yolo.HEAD:
             ref = torch.where(ref > 0, ref, 0.1 * ref)
+        if li in yolo.POOLED:
+            ref = torch.nn.functional.max_pool2d(ref, 2)
         ref = ref.permute(0, 2, 3, 1)
         out = net.step_tensor(step, n)[:, 1:-1, 1:-1, :].float()
         if li == 20:  # reorg into channels [0,256) of the concat buffer
