@@ -169,7 +169,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1810_10551_b200 import native, pipeline as P, synthetic, yolo
+    from paper_1810_10551_b200 import distributed as D, native, pipeline as P, synthetic, yolo
     from paper_1810_10551_b200.engine import AttentionPipelineB200
 
     torch.cuda.set_device(local)
@@ -188,7 +188,6 @@ def main():
     tiles2 = torch.zeros(n_steps, dtype=torch.int32, device="cuda")
     fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(2 * n_steps)]
-    res_buf = torch.zeros((world, 2 * B), dtype=torch.int32, device="cuda")
 
     # instrument the two YOLO forwards of each step (conv roofline)
     fwd_calls = {"i": 0}
@@ -210,9 +209,9 @@ def main():
         frames = clip[s:s + B]
         eng.run_device(B, frames=frames)
         tiles2[i:i + 1].copy_(eng.n_jobs2)
-        if world > 1:  # result gather: per-frame (active, detections) counts to every rank
-            mine = torch.cat([eng.active_counts[:B], eng.ocounts[:B]])
-            dist.all_gather_into_tensor(res_buf.view(-1), mine)
+        if world > 1:  # result gather (NCCL): per-frame counts + first 64 final records
+            recs = eng.outp.view(B, -1)[:, : 64 * native.PDET_DTYPE.itemsize]
+            D.gather_records(eng.ocounts[:B], recs, [B] * world, to_host=False)
 
     eng.reset_history(())
     for i in range(args.warmup):
