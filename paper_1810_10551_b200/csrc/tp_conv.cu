@@ -23,7 +23,8 @@
 //   warp 0      TMA producer (A box + B box per k-block into an S-stage smem ring)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256,
 //               K=16 per instruction, fp32 accumulate in TMEM, double-buffered)
-//   warps 2..9  epilogue, two warps per TMEM lane quadrant splitting the columns:
+//   warps 2..9  epilogue: two warpgroups working on alternate tiles (one per TMEM
+//               accumulator), each warp covering one TMEM lane quadrant:
 //               tcgen05.ld -> +bias (BN folded) -> leaky(0.1) -> [2x2 max] -> 16-bit
 //               -> interior-only store (or channel-offset into the route concat
 //               buffer, space-to-depth "reorg", or fp32 for the head)
@@ -63,6 +64,11 @@ struct ConvParams {
   const float* bias;
   void* out;
   int out_cstride, out_coff, out_fp32, leaky, reorg;
+  int sub;         // RECT super-tile: SUB stacked 16x8 sub-tiles (halo variant)
+  int halo;        // RECT + weights resident in smem + one {BK,16,10} halo box per (dx, cb)
+  uint32_t bres_bytes, bchunk_bytes;
+  int n_bchunks;
+  int dbg;  // profiling only (TP_CONV_DEBUG): 1 = skip epilogue math/stores, 2 = skip MMAs
 };
 
 __device__ __forceinline__ int tap_shift(int tap, int ksize, int wp) {
@@ -79,26 +85,63 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, ui
       : "memory");
 }
 
-template <int MODE>
+// Epilogue variants, chosen at compile time.
+enum Epi { EPI_PLAIN = 0, EPI_POOL = 1, EPI_REORG = 2, EPI_F32 = 3 };
+constexpr int kMaxBias = 1024;
+
+// Walks a CTA's contiguous tile range: t = mt * n_blocks_n + nb, and for RECT tiles
+// mt = (img * tiles_y + by) * tiles_x + bx. Divisions only at the start.
+struct TileIter {
+  int nb, mt, img, by, bx;
+  __device__ __forceinline__ void init(int t, const ConvParams& p) {
+    mt = t / p.n_blocks_n;
+    nb = t - mt * p.n_blocks_n;
+    const int per = p.tiles_x * p.tiles_y;
+    img = mt / per;
+    const int r = mt - img * per;
+    by = r / p.tiles_x;
+    bx = r - by * p.tiles_x;
+  }
+  __device__ __forceinline__ void next(const ConvParams& p) {
+    if (++nb == p.n_blocks_n) {
+      nb = 0;
+      ++mt;
+      if (++bx == p.tiles_x) {
+        bx = 0;
+        if (++by == p.tiles_y) {
+          by = 0;
+          ++img;
+        }
+      }
+    }
+  }
+};
+
+template <int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const ConvParams p) {
   constexpr int BK = MODE == MODE_SW128 ? 64 : (MODE == MODE_SW64 ? 32 : 16);
+  constexpr bool RECT = EPI == EPI_POOL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int S = p.stages;
   uint8_t* smA = smem;
-  uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + (size_t)S * p.b_stage_bytes);
+  uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;  // B stages, or resident B (halo)
+  uint64_t* bars =
+      reinterpret_cast<uint64_t*>(smB + (size_t)S * p.b_stage_bytes + p.bres_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
   uint64_t* tempty = bars + 2 * S + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  uint64_t* bres_bar = bars + 2 * S + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
 
   const uint32_t warp = tp::warp_id();
   const uint32_t lane = tp::lane_id();
+  const int cout_pad = p.bn * p.n_blocks_n;
 
   if (warp == 0 && lane == 0) {
     tp::tma_prefetch(&tmA);
@@ -109,20 +152,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       tp::mbar_init(&tfull[a], 1);
-      tp::mbar_init(&tempty[a], kEpiWarps);
+      tp::mbar_init(&tempty[a], 4);
     }
+    tp::mbar_init(bres_bar, 1);
     tp::fence_mbar_init();
   }
   if (warp == 1) tp::tmem_alloc(tmem_slot, p.tmem_cols);
+  for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
   tp::tc_fence_before();
   __syncthreads();
   tp::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
-  const int rect_per_img = p.tiles_x * p.tiles_y;
-  const int m_blocks = p.rect ? n_img * rect_per_img : (n_img * p.img_px + 127) / 128;
+  const int m_blocks = RECT ? n_img * p.tiles_x * p.tiles_y : (n_img * p.img_px + 127) / 128;
   const int total_tiles = m_blocks * p.n_blocks_n;
+  // contiguous, balanced tile range per CTA
+  const int per_cta = total_tiles / (int)gridDim.x, extra = total_tiles % (int)gridDim.x;
+  const int t_begin = (int)blockIdx.x * per_cta + min((int)blockIdx.x, extra);
+  const int n_tiles = per_cta + ((int)blockIdx.x < extra ? 1 : 0);
   const int hp = p.res + 2;
 
   if (warp == 0) {
@@ -131,26 +179,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const uint32_t tx_bytes = p.a_stage_bytes + p.b_stage_bytes;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        const int mt = t / p.n_blocks_n;
-        const int n0 = (t - mt * p.n_blocks_n) * p.bn;
-        int m0 = 0, rx = 0, ry = 0;
-        if (p.rect) {
-          const int img = mt / rect_per_img;
-          const int r = mt - img * rect_per_img;
-          const int by = r / p.tiles_x;
-          rx = 1 + (r - by * p.tiles_x) * RECT_W;
-          ry = img * hp + 1 + by * RECT_H;
-        } else {
-          m0 = mt * 128;
-        }
+      TileIter it;
+      it.init(t_begin, p);
+      if (RECT && p.halo && n_tiles > 0) {  // weights resident for the whole kernel
+        tp::mbar_arrive_expect_tx(bres_bar, p.bres_bytes);
+        for (int j = 0; j < p.n_bchunks; ++j)
+          tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, j * BK, 0);
+      }
+      for (int i = 0; i < n_tiles; ++i, it.next(p)) {
+        const int n0 = it.nb * p.bn;
+        const int m0 = it.mt * 128;
+        const int rx = 1 + it.bx * RECT_W, ry = it.img * hp + 1 + it.by * RECT_H * p.sub;
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&empty[s], ph ^ 1);
           uint8_t* a_dst = smA + (size_t)s * p.a_stage_bytes;
           uint8_t* b_dst = smB + (size_t)s * p.b_stage_bytes;
           tp::mbar_arrive_expect_tx(&full[s], tx_bytes);
-          if (MODE == MODE_L0X) {  // one k-block per kernel row dy
-            if (p.rect)
+          if (RECT && p.halo) {  // halo box {BK, 16, 10} for kernel column dx, channel block cb
+            const int dx = MODE == MODE_L0X ? 0 : kb / p.kb_per_tap - 1;
+            const int cb = MODE == MODE_L0X ? 0 : kb % p.kb_per_tap;
+            tma_load_3d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry - 1);
+          } else if (MODE == MODE_L0X) {  // one k-block per kernel row dy
+            if (RECT)
               tma_load_3d(a_dst, &tmA, &full[s], 0, rx, ry + kb - 1);
             else
               tp::tma_load_2d(a_dst, &tmA, &full[s], 0, m0 + (kb - 1) * p.wp);
@@ -158,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             const int tap = kb / p.kb_per_tap;
             const int cb = kb - tap * p.kb_per_tap;
-            if (p.rect) {
+            if (RECT) {
               const int dy = p.ksize == 3 ? tap / 3 - 1 : 0;
               const int dx = p.ksize == 3 ? tap % 3 - 1 : 0;
               tma_load_3d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry + dy);
@@ -180,18 +230,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = p.idesc;
       int s = 0;
       uint32_t ph = 0;
-      int acc = 0;
-      uint32_t aph = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        tp::mbar_wait(&tempty[acc], aph ^ 1);
+      uint32_t aph[2] = {0, 0};
+      if (RECT && p.halo && n_tiles > 0) tp::mbar_wait(bres_bar, 0);
+      const uint32_t bres_addr = tp::smem_u32(smB);
+      for (int i = 0; i < n_tiles; ++i) {
+        const int acc = i & 1;
+        tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        aph[acc] ^= 1;
         tp::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.sub * p.bn);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&full[s], ph);
           tp::tc_fence_after();
           const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * p.a_stage_bytes);
           const uint32_t b_addr = tp::smem_u32(smB + (size_t)s * p.b_stage_bytes);
-          if (MODE == MODE_SW128) {
+          if (p.dbg & 2) {
+            // profiling: no MMA
+          } else if (RECT && p.halo) {
+            // three kernel rows dy = sub-windows of the halo box, 16 pixel rows apart
+            constexpr uint32_t row_bytes = BK * 2;
+            constexpr uint32_t sbo = 8 * row_bytes;
+            constexpr uint32_t lay = MODE == MODE_SW128 ? 2 : (MODE == MODE_SW64 ? 4 : 6);
+            const int dx = MODE == MODE_L0X ? 0 : kb / p.kb_per_tap - 1;
+            const int cb = MODE == MODE_L0X ? 0 : kb % p.kb_per_tap;
+            for (int j = 0; j < p.sub; ++j) {
+#pragma unroll
+              for (int dy = 0; dy < 3; ++dy) {
+                const int chunk = MODE == MODE_L0X ? dy : (dy * 3 + dx + 1) * p.kb_per_tap + cb;
+                const uint32_t aw = a_addr + (j * RECT_H + dy) * RECT_W * row_bytes;
+                const uint32_t bw = bres_addr + chunk * p.bchunk_bytes;
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) {
+                  uint64_t ad = tp::umma_desc(aw + k * 32, 16, sbo, lay);
+                  uint64_t bd = tp::umma_desc(bw + k * 32, 16, sbo, lay);
+                  tp::mma_bf16(d_tmem + j * p.bn, ad, bd, idesc, (kb | dy | k) != 0);
+                }
+              }
+            }
+          } else if (MODE == MODE_SW128) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 1024, 2);
@@ -217,45 +293,54 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tp::mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-        acc ^= 1;
-        if (acc == 0) aph ^= 1;
       }
     }
   } else {
-    // ================= epilogue (warps 2..9) =================
-    const uint32_t q = warp & 3;            // TMEM lane quadrant this warp may access
-    const int half = (int)(warp - 2) >> 2;  // which half of the N tile
+    // ================= epilogue: two warpgroups, one per TMEM accumulator =================
+    // group g takes the CTA's local tiles i with i % 2 == g; its 4 warps cover the 4
+    // TMEM lane quadrants, all BN columns.
+    const int g = (int)(warp - 2) >> 2;
+    const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
-    const int cols_per = p.bn >> 1;
-    int acc = 0;
-    uint32_t aph = 0;
+    const bool f16 = p.f16 != 0;
+    const bool leaky = p.leaky != 0;
     const int ores = p.res >> 1, owp = ores + 2, oimg = owp * owp;
     const int total_px = n_img * p.img_px;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const int mt = t / p.n_blocks_n;
-      const int n0 = (t - mt * p.n_blocks_n) * p.bn;
-      tp::mbar_wait(&tfull[acc], aph);
+    const int nchunks = p.bn >> 4;
+    uint32_t ph = 0;
+    TileIter it;
+    it.init(t_begin, p);
+    for (int i = 0; i < n_tiles; ++i, it.next(p)) {
+      if ((i & 1) != g) continue;
+      const int n0 = it.nb * p.bn;
+      tp::mbar_wait(&tfull[g], ph);
+      ph ^= 1;
       tp::tc_fence_after();
+      if (p.dbg & 1) {
+        tp::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tp::mbar_arrive(&tempty[g]);
+        continue;
+      }
 
+      for (int jt = 0; jt < p.sub; ++jt) {  // stacked 16x8 sub-tiles of a RECT super-tile
       bool valid, writer = true;
       int out_px = 0, sub = 0;
-      if (p.rect) {
-        const int img = mt / rect_per_img;
-        const int r = mt - img * rect_per_img;
-        const int by = r / p.tiles_x, bx = r - (r / p.tiles_x) * p.tiles_x;
-        const int x = bx * RECT_W + (row & (RECT_W - 1)), y = by * RECT_H + (row >> 4);
-        valid = img < n_img && x < p.res && y < p.res;
+      if (RECT) {
+        const int x = it.bx * RECT_W + (row & (RECT_W - 1));
+        const int y = (it.by * p.sub + jt) * RECT_H + (row >> 4);
+        valid = it.img < n_img && x < p.res && y < p.res;
         writer = ((x | y) & 1) == 0;
-        out_px = img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
+        out_px = it.img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
       } else {
-        const int pix = mt * 128 + row;
+        const int pix = it.mt * 128 + row;
         valid = pix < total_px;
         if (valid) {
           const int img = pix / p.img_px;
           const int rem = pix - img * p.img_px;
-          const int yp = rem / p.wp, xp = rem - (rem / p.wp) * p.wp;
+          const int yp = rem / p.wp, xp = rem - yp * p.wp;
           valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
-          if (p.reorg) {
+          if (EPI == EPI_REORG) {
             const int y = yp - 1, x = xp - 1;
             sub = (y & 1) * 2 + (x & 1);
             out_px = img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
@@ -264,35 +349,39 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * p.bn);
-      for (int c = half * cols_per; c < (half + 1) * cols_per; c += 16) {
-        uint32_t v[16];
-        tp::tmem_ld16(t_row + (uint32_t)c, v);
+      const uint32_t t_row =
+          tmem_base + ((q * 32u) << 16) + (uint32_t)((g * p.sub + jt) * p.bn);
+      uint32_t v[16];
+      tp::tmem_ld16(t_row, v);
+      for (int c = 0; c < nchunks; ++c) {
         tp::tmem_ld_wait();
-        const int ch0 = n0 + c;
         float f[16];
-        const float4* b4 = reinterpret_cast<const float4*>(p.bias + ch0);  // padded to cout_pad
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+        if (c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);  // overlap
+        const int ch0 = n0 + c * 16;
+        const float4* b4 = reinterpret_cast<const float4*>(bias_s + ch0);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float4 bb = __ldg(b4 + j);
-          f[4 * j + 0] = __uint_as_float(v[4 * j + 0]) + bb.x;
-          f[4 * j + 1] = __uint_as_float(v[4 * j + 1]) + bb.y;
-          f[4 * j + 2] = __uint_as_float(v[4 * j + 2]) + bb.z;
-          f[4 * j + 3] = __uint_as_float(v[4 * j + 3]) + bb.w;
+          const float4 bb = b4[j];
+          f[4 * j + 0] += bb.x;
+          f[4 * j + 1] += bb.y;
+          f[4 * j + 2] += bb.z;
+          f[4 * j + 3] += bb.w;
         }
-        if (p.leaky) {
+        if (leaky) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) f[j] = f[j] > 0.0f ? f[j] : 0.1f * f[j];
         }
-        if (p.rect) {  // fused 2x2 max pool: x pair = lane^1, y pair = lane^16
+        if (RECT) {  // fused 2x2 max pool: x pair = lane^1, y pair = lane^16
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
             f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], RECT_W));
-          }
         }
         if (!valid || !writer || ch0 >= p.cout) continue;
-        if (p.out_fp32) {
+        if (EPI == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
           if (ch0 + 16 <= p.cout) {
 #pragma unroll
@@ -307,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            if (p.f16) {
+            if (f16) {
               __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
               pk[j] = *reinterpret_cast<uint32_t*>(&h);
             } else {
@@ -315,17 +404,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               pk[j] = *reinterpret_cast<uint32_t*>(&h);
             }
           }
-          const int cofs = p.out_coff + (p.reorg ? sub * p.cout : 0) + ch0;
+          const int cofs = p.out_coff + (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride + cofs;
           *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
+      tp::tmem_ld_wait();
+      }  // sub-tiles
       tp::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tp::mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) aph ^= 1;
+      if (lane == 0) tp::mbar_arrive(&tempty[g]);
     }
   }
 
@@ -501,10 +590,21 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   CUtensorMapSwizzle swz = mode == MODE_SW128 ? CU_TENSOR_MAP_SWIZZLE_128B
                            : mode == MODE_SW64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+  // halo variant: weights (whole K x N) fit next to the A ring -> resident in smem
+  const size_t bres = (size_t)cout_pad * ktotal * 2;
+  const bool halo = pool && cout_pad <= 256 && bres <= 48 * 1024;
+  // super-tile height: SUB x 8 rows per halo box (fewer, larger tiles for the 32/64-channel
+  // layers whose per-tile fixed costs dominate); keep SUB x BN <= 256 TMEM columns
+  int subt = 1;
+  if (halo) {
+    subt = mode == MODE_L0X ? 4 : 2;
+    while (subt > 1 && (subt * cout_pad > 256 || res % (RECT_H * subt) != 0)) subt >>= 1;
+  }
   int rc;
   if (pool) {
     const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
-    const uint32_t box[3] = {(uint32_t)bk, RECT_W, RECT_H};
+    const uint32_t box[3] = {(uint32_t)bk, RECT_W,
+                             halo ? (uint32_t)(RECT_H * subt + 2) : (uint32_t)RECT_H};
     rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16);
   } else {
     const uint64_t dims[2] = {(uint64_t)cin_stride, (uint64_t)max_img * img_px};
@@ -533,22 +633,32 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.num_kb = mode == MODE_L0X ? 3 : taps * p.kb_per_tap;
   p.a_stage_bytes = 128 * bk * 2;
   p.b_stage_bytes = bn * bk * 2;
+  p.halo = halo ? 1 : 0;
+  if (halo) {
+    p.num_kb = mode == MODE_L0X ? 1 : 3 * p.kb_per_tap;  // one stage per (dx, channel block)
+    p.a_stage_bytes = (RECT_H * subt + 2) * RECT_W * bk * 2;
+    p.b_stage_bytes = 0;
+    p.bchunk_bytes = bn * bk * 2;
+    p.n_bchunks = ktotal / bk;
+    p.bres_bytes = (uint32_t)bres;
+  }
   const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
-  int stages = (int)((200 * 1024) / stage_bytes);
+  int stages = (int)((196 * 1024 - p.bres_bytes) / stage_bytes);
   if (stages > 12) stages = 12;
   if (stages < 2) {
     tp_set_error("conv: stage too large");
     return TP_ERR_UNSUPPORTED;
   }
   p.stages = stages;
+  p.sub = subt;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(2 * bn)) cols <<= 1;
+  while (cols < (uint32_t)(2 * subt * bn)) cols <<= 1;
   p.tmem_cols = cols;
   p.idesc = tp::idesc_f16kind(128, (uint32_t)bn, !f16);
   p.f16 = f16 ? 1 : 0;
   p.rect = pool ? 1 : 0;
   p.tiles_x = (res + RECT_W - 1) / RECT_W;
-  p.tiles_y = (res + RECT_H - 1) / RECT_H;
+  p.tiles_y = (res + RECT_H * subt - 1) / (RECT_H * subt);
   p.bias = bias;
   p.out = out;
   p.out_cstride = out_cstride;
@@ -556,16 +666,22 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.out_fp32 = out_fp32;
   p.leaky = leaky;
   p.reorg = reorg;
+  p.dbg = getenv("TP_CONV_DEBUG") ? atoi(getenv("TP_CONV_DEBUG")) : 0;
   L->mode = mode;
-  L->smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 4) * 8 + 16;
+  L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + (2 * stages + 6) * 8 +
+            cout_pad * 4 + 16;
+  if (cout_pad > kMaxBias) {
+    tp_set_error("conv: cout_pad %d exceeds %d", cout_pad, kMaxBias);
+    return TP_ERR_UNSUPPORTED;
+  }
   return TP_OK;
 }
 
-template <int MODE>
+template <int MODE, int EPI>
 int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<MODE>,
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<MODE, EPI>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
@@ -577,7 +693,7 @@ int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   const long long tiles = m_blocks * p.n_blocks_n;
   if (tiles == 0) return TP_OK;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_tc_kernel<MODE><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+  conv_tc_kernel<MODE, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
@@ -587,11 +703,20 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
     tp_set_error("conv: n_img %d exceeds planned %d", n_img, L.p.n_img);
     return TP_ERR_CAPACITY;
   }
-  switch (L.mode) {
-    case MODE_SW128: return launch_mode<MODE_SW128>(L, n_img, n_img_dev, st);
-    case MODE_SW64: return launch_mode<MODE_SW64>(L, n_img, n_img_dev, st);
-    default: return launch_mode<MODE_L0X>(L, n_img, n_img_dev, st);
+  const int epi = L.p.rect ? EPI_POOL : L.p.reorg ? EPI_REORG : L.p.out_fp32 ? EPI_F32 : EPI_PLAIN;
+#define TP_EPI_SWITCH(M)                                                  \
+  switch (epi) {                                                          \
+    case EPI_POOL: return launch_mode<M, EPI_POOL>(L, n_img, n_img_dev, st);   \
+    case EPI_REORG: return launch_mode<M, EPI_REORG>(L, n_img, n_img_dev, st); \
+    case EPI_F32: return launch_mode<M, EPI_F32>(L, n_img, n_img_dev, st);     \
+    default: return launch_mode<M, EPI_PLAIN>(L, n_img, n_img_dev, st);        \
   }
+  switch (L.mode) {
+    case MODE_SW128: TP_EPI_SWITCH(MODE_SW128)
+    case MODE_SW64: TP_EPI_SWITCH(MODE_SW64)
+    default: TP_EPI_SWITCH(MODE_L0X)
+  }
+#undef TP_EPI_SWITCH
 }
 
 int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st,
