@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 
 PRESET = "1 att, 3 fin, 20 over"
 W, H = 3840, 2160
+FRAMES = {"4k": (3840, 2160), "8k": (7680, 4320)}
 CLIP = [("sparse", 100), ("dense", 100), ("mixed", 100)]
 METRIC = "frames/sec, synthetic 4K & 8K video, 1/2/4/8 B200; crops/sec; % roofline"
 
@@ -52,14 +53,27 @@ def parse():
     ap.add_argument("--resample", default="nearest", choices=["nearest", "bilinear"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--frame", default="4k", choices=sorted(FRAMES))
+    ap.add_argument("--preset", default=PRESET)
+    ap.add_argument("--mode", default="pipeline", choices=["pipeline", "allcrops"],
+                    help="allcrops = the run_allcrops_baseline comparator (config 3)")
+    ap.add_argument("--density", type=float, default=None,
+                    help="inject stage-1 boxes activating this fraction of the final grid "
+                         "(config 5 density sweep; stage 1 is skipped)")
+    ap.add_argument("--clip-frames", type=int, default=300)
+    args = ap.parse_args()
+    global W, H
+    W, H = FRAMES[args.frame]
+    return args
 
 
-def clip_objects(rank: int = 0):
+def clip_objects(rank: int = 0, n_frames: int = 300):
     from paper_1810_10551_b200 import synthetic
 
     objs = []
-    for kind, n in CLIP:
+    per = max(1, n_frames // len(CLIP))
+    for kind, _ in CLIP:
+        n = per
         gt = synthetic.generate_scene(synthetic.SceneSpec(kind, W, H, n, seed=rank))
         objs += [gt[i] for i in range(n)]
     return objs
@@ -176,9 +190,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch
-    objs = clip_objects(rank)
+    objs = clip_objects(rank, args.clip_frames)
     n_clip = len(objs)
-    settings = P.PipelineSettings.from_preset(PRESET)
+    settings = P.PipelineSettings.from_preset(args.preset)
     eng = AttentionPipelineB200(settings, W, H, max_frames=B, resample=args.resample)
     clip = torch.empty((n_clip, H, W, 3), dtype=torch.uint8, device="cuda")
     for i in range(0, n_clip, 10):
@@ -207,12 +221,34 @@ def main():
     def step(i):
         s = (i * B) % n_clip
         frames = clip[s:s + B]
-        eng.run_device(B, frames=frames)
+        if args.density is not None:
+            eng.set_attention(injected[i % len(injected)])
+            eng.run_device(B, frames=frames, attention="inject")
+        else:
+            eng.run_device(B, frames=frames, attention=attention)
         tiles2[i:i + 1].copy_(eng.n_jobs2)
         if world > 1:  # result gather (NCCL): per-frame counts + first 64 final records
             recs = eng.outp.view(B, -1)[:, : 64 * native.PDET_DTYPE.itemsize]
             D.gather_records(eng.ocounts[:B], recs, [B] * world, to_host=False)
 
+    attention = "all" if args.mode == "allcrops" else "yolo"
+    injected = []
+    if args.density is not None:  # boxes at the centres of round(d*F) crops per frame
+        import random as _random
+
+        fin = eng.plan.final_grid.crops
+        k = int(round(args.density * len(fin)))
+        rng = _random.Random(1234)
+        from paper_1810_10551_b200.engine import exclusive_boxes
+
+        for _ in range(4):
+            batch = []
+            for _f in range(B):
+                chosen = sorted(rng.sample(range(len(fin)), k))
+                batch.append(exclusive_boxes(eng.plan.final_grid,
+                                             [fin[c].crop_id for c in chosen],
+                                             settings.attention_margin_px))
+            injected.append(batch)
     eng.reset_history(())
     for i in range(args.warmup):
         step(i)
@@ -239,8 +275,11 @@ def main():
     # conv roofline over the timed steps
     t2 = tiles2.cpu().numpy()
     fwd_ms, flops = 0.0, 0.0
+    per_step = 2 if attention == "yolo" and args.density is None else 1
     for i in range(args.warmup, n_steps):
-        for k, nt in ((2 * i, B * eng.A), (2 * i + 1, int(t2[i]))):
+        pairs = ((per_step * i, B * eng.A), (per_step * i + 1, int(t2[i]))) if per_step == 2 \
+            else ((i, int(t2[i])),)
+        for k, nt in pairs:
             fwd_ms += fwd_ev[k][0].elapsed_time(fwd_ev[k][1])
             flops += nt * yolo.GFLOP_PER_TILE * 1e9
     conv_tflops = flops / (fwd_ms / 1e3) / 1e12
@@ -250,13 +289,21 @@ def main():
     except Exception:
         pass
     peak = float(peaks.get("bf16_tflops_sustained", 1391.0))
-    tiles_per_frame = (eng.A * B * args.steps + float(t2[args.warmup:].sum())) / (args.steps * B)
+    stage1 = eng.A * B * args.steps if per_step == 2 else 0
+    tiles_per_frame = (stage1 + float(t2[args.warmup:].sum())) / (args.steps * B)
     launches_per_step = (1 + 24 + 1 + 1) + 2 + (1 + 24 + 1 + 1) + 1
 
     # e2e through the public engine API with pinned host frames
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(eng, clip, B, args, world, dist if world > 1 else None)
+        def launch(i, frames):
+            if args.density is not None:
+                eng.set_attention(injected[i % len(injected)])
+                eng.run_device(B, frames=frames, attention="inject")
+            else:
+                eng.run_device(B, frames=frames, attention=attention)
+
+        e2e = run_e2e(eng, clip, B, args, world, dist if world > 1 else None, launch)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -271,8 +318,11 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": yolo.DEFAULT_PRECISION, "data": "synthetic",
             "precision": "fp16 operands/activations, fp32 accumulation (tcgen05 kind::f16)",
-            "config": {"workload": "4K attention pipeline on a 300-frame synthetic clip "
-                                   "(sparse/dense/mixed, seed=rank), preset '1 att, 3 fin, 20 over', "
+            "config": {"workload": f"{args.frame.upper()} "
+                                   f"{'all-crops baseline' if args.mode == 'allcrops' else 'attention pipeline'}"
+                                   f"{'' if args.density is None else f' (injected stage-1, density {args.density})'}"
+                                   f" on a {n_clip}-frame synthetic clip "
+                                   f"(sparse/dense/mixed, seed=rank), preset '{args.preset}', "
                                    "random-init YOLO v2-608 (seed 0, calibrated head)",
                        "frame": [W, H], "frames_per_step": B, "per_gpu_frames": n_clip,
                        "resample": args.resample, "parallelism": f"frame-dp{world}",
@@ -295,7 +345,7 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(eng, clip, B, args, world, dist):
+def run_e2e(eng, clip, B, args, world, dist, launch):
     """Public engine API with HOST frames: pinned staging, H2D overlapped on a copy
     stream, results read back to the host every step."""
     import torch
@@ -329,7 +379,7 @@ def run_e2e(eng, clip, B, args, world, dist):
         torch.cuda.current_stream().wait_event(done_copy[slot])
         if i + 1 < n_steps:
             issue_copy(i + 1)
-        eng.run_device(B, frames=dev[slot])
+        launch(i, dev[slot])
         done_use[slot].record()
         host_counts[:B].copy_(eng.ocounts[:B], non_blocking=True)
         host_counts[B:].copy_(eng.active_counts[:B], non_blocking=True)

@@ -182,6 +182,14 @@ TP_API int tp_postprocess(const tp_pdet_t* dets, const int32_t* counts, int n_fr
                    int max_per_frame, const tp_post_policy_t* policy, tp_pdet_t* out,
                    int32_t* out_counts, int32_t* keep_idx, int32_t* keep_counts, void* stream);
 
+/* Synthetic frame renderer (input generator): per frame, counts[f] <= 64 rectangles
+ * rects int32 [n][max_obj][4] = (x0, y0, x1, y1) exclusive ends, colours u8 [n][max_obj][3],
+ * painted in order over background bg_rgb (r | g<<8 | b<<16) into u8 [n][H][W][3].
+ * Same bytes as the reference render_frame (synthetic.py:183-196). */
+TP_API int tp_render_frames(const int32_t* rects, const uint8_t* colors, const int32_t* counts,
+                            int n_frames, int max_obj, int H, int W, uint32_t bg_rgb,
+                            uint8_t* out, void* stream);
+
 /* 2x2/2 max pool on padded NHWC bf16 (exposed for tests). */
 TP_API int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype, void* out,
                         void* stream);

@@ -97,6 +97,8 @@ class AttentionPipelineB200:
         self.post_policy = make_policy_struct(self.policy, self.labels, fin.cols,
                                               fin.rows * fin.cols,
                                               min_conf=settings.min_confidence)
+        self.full_box = torch.tensor([0.0, 0.0, float(self.W), float(self.H)],
+                                     dtype=torch.float64, device=dev)
         self.events = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         self.last_timing = TimingProfile()
         self.last_n_tiles = (0, 0)
@@ -121,17 +123,51 @@ class AttentionPipelineB200:
         self.frames[:n].copy_(frames_host[:n], non_blocking=non_blocking)
 
     # ------------------------------------------------------------------ run
-    def run_device(self, n: int, frames=None, stream=None, timed: bool = False) -> None:
-        """Launch the whole pipeline for frames[0:n] (device). No host synchronisation."""
+    def set_attention(self, boxes_per_frame) -> None:
+        """Inject stage-1 attention boxes for the next run_device(..., attention="inject")
+        call: one list of (x, y, w, h) global boxes per batch frame."""
+        torch = self.torch
+        K1 = self.K - 1
+        n = len(boxes_per_frame)
+        if n > self.max_frames:
+            raise ValueError("more frames than the batch holds")
+        arr = np.zeros((n, MAX_BOXES, 4), dtype=np.float64)
+        cnt = np.zeros(n, dtype=np.int32)
+        for f, bl in enumerate(boxes_per_frame):
+            if len(bl) > MAX_BOXES:
+                raise ValueError(f"more than {MAX_BOXES} attention boxes in a frame")
+            cnt[f] = len(bl)
+            for k, b in enumerate(bl):
+                arr[f, k] = b
+        self.boxes[K1:K1 + n].copy_(torch.from_numpy(arr))
+        self.box_counts[K1:K1 + n].copy_(torch.from_numpy(cnt))
+
+    def run_device(self, n: int, frames=None, stream=None, timed: bool = False,
+                   attention: str = "yolo") -> None:
+        """Launch the whole pipeline for frames[0:n] (device). No host synchronisation.
+
+        attention: "yolo" (stage 1 on the attention grid), "inject" (boxes from
+        set_attention), or "all" (every final crop active: run_allcrops_baseline)."""
         if not (1 <= n <= self.max_frames):
             raise ValueError(f"batch of {n} frames (max {self.max_frames})")
+        if attention not in ("yolo", "inject", "all"):
+            raise ValueError("attention must be 'yolo', 'inject' or 'all'")
         fr = self.frames if frames is None else frames
         st = native.stream_handle(stream)
         ev = self.events
         K1 = self.K - 1
+        if timed:
+            ev[0].record(stream)
+        if attention == "all":
+            self.boxes[K1:K1 + n, 0] = self.full_box
+            self.box_counts[K1:K1 + n] = 1
+        elif attention == "yolo":
+            self._stage1(fr, n, stream, st)
+        self._finish(fr, n, stream, st, timed)
+
+    def _stage1(self, fr, n, stream, st):
+        K1 = self.K - 1
         try:
-            if timed:
-                ev[0].record(stream)
             nt1 = n * self.A
             kernels.gather(fr, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
                            self.resample, out_act_ptr=self.net.input_ptr, stream=stream, dtype=self.dtype)
@@ -144,6 +180,10 @@ class AttentionPipelineB200:
                         native.ptr(self.box_counts) + K1 * 4, MAX_BOXES, st)
         except native.NativeError as exc:
             raise StageFailure("attention", -1) from exc
+
+    def _finish(self, fr, n, stream, st, timed):
+        ev = self.events
+        K1 = self.K - 1
         try:
             if timed:
                 ev[1].record(stream)
@@ -278,6 +318,35 @@ class AttentionPipelineB200:
             raise StageFailure("attention", -1)
         bx = self.boxes[K1:K1 + n].cpu().numpy()
         return [bx[f, : cnt[f]] for f in range(n)]
+
+
+def exclusive_boxes(final_grid, crop_ids, margin: int, size: int = 4):
+    """Small attention boxes, one per requested crop, placed at the centre of the part of
+    the crop no other crop covers, so after dilation by `margin` each activates exactly
+    its crop (for forced-density runs)."""
+    crops = final_grid.crops
+    out = []
+    for cid in crop_ids:
+        c = final_grid.crop_by_id(cid)
+        g = c.global_rect
+        lo_x, hi_x, lo_y, hi_y = g.x, g.x2, g.y, g.y2
+        for o in crops:
+            if o.crop_id == cid:
+                continue
+            r = o.global_rect
+            if o.row == c.row and o.col == c.col - 1:
+                lo_x = max(lo_x, r.x2)
+            if o.row == c.row and o.col == c.col + 1:
+                hi_x = min(hi_x, r.x)
+            if o.col == c.col and o.row == c.row - 1:
+                lo_y = max(lo_y, r.y2)
+            if o.col == c.col and o.row == c.row + 1:
+                hi_y = min(hi_y, r.y)
+        if hi_x - lo_x < size + 2 * margin + 2 or hi_y - lo_y < size + 2 * margin + 2:
+            raise ValueError(f"crop {cid} has no exclusive region wide enough")
+        cx, cy = (lo_x + hi_x) // 2, (lo_y + hi_y) // 2
+        out.append((cx - size // 2, cy - size // 2, size, size))
+    return out
 
 
 def yolo_tagged(det, frame, crops):
