@@ -369,16 +369,37 @@ __global__ void __launch_bounds__(kThreads, 1)
           f[4 * j + 2] += bb.z;
           f[4 * j + 3] += bb.w;
         }
-        if (leaky) {
+        if (leaky) {  // leaky(x) = max(x, 0.1x), identical to x > 0 ? x : 0.1x
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = f[j] > 0.0f ? f[j] : 0.1f * f[j];
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
         }
-        if (RECT) {  // fused 2x2 max pool: x pair = lane^1, y pair = lane^16
+        if (RECT) {
+          // fused 2x2 max pool on packed 16-bit pairs (rounding is monotonic, so
+          // max-then-round == round-then-max): x pair = lane^1, y pair = lane^16
+          uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], RECT_W));
+          for (int j = 0; j < 8; ++j) {
+            if (f16) {
+              __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+              __half2 o = __shfl_xor_sync(0xffffffffu, h, 1);
+              h = __hmax2(h, o);
+              o = __shfl_xor_sync(0xffffffffu, h, RECT_W);
+              h = __hmax2(h, o);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+              __nv_bfloat162 o = __shfl_xor_sync(0xffffffffu, h, 1);
+              h = __hmax2(h, o);
+              o = __shfl_xor_sync(0xffffffffu, h, RECT_W);
+              h = __hmax2(h, o);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+          if (!valid || !writer || ch0 >= p.cout) continue;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
+          *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          continue;
         }
         if (!valid || !writer || ch0 >= p.cout) continue;
         if (EPI == EPI_F32) {
