@@ -68,6 +68,7 @@ struct ConvParams {
   int halo;        // RECT + weights resident in smem + one {BK,16,10} halo box per (dx, cb)
   uint32_t bres_bytes, bchunk_bytes;
   int n_bchunks;
+  uint32_t stage_bytes;  // epilogue store staging (TMA-store variants): 8 warps x 2 KB
   int dbg;  // profiling only (TP_CONV_DEBUG): 1 = skip epilogue math/stores, 2 = skip MMAs
 };
 
@@ -83,6 +84,33 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, ui
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(tp::smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(tp::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(tp::smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
 }
 
 // Epilogue variants, chosen at compile time.
@@ -120,17 +148,19 @@ struct TileIter {
 template <int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const ConvParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
   constexpr int BK = MODE == MODE_SW128 ? 64 : (MODE == MODE_SW64 ? 32 : 16);
   constexpr bool RECT = EPI == EPI_POOL;
+  // FLAT plain / fp32 outputs leave through per-warp swizzled smem slabs + TMA stores
+  constexpr bool TSTORE = EPI == EPI_PLAIN || EPI == EPI_F32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int S = p.stages;
   uint8_t* smA = smem;
   uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;  // B stages, or resident B (halo)
-  uint64_t* bars =
-      reinterpret_cast<uint64_t*>(smB + (size_t)S * p.b_stage_bytes + p.bres_bytes);
+  uint8_t* smC = smB + (size_t)S * p.b_stage_bytes + p.bres_bytes;  // 1024-aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smC + p.stage_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
@@ -352,13 +382,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_row =
           tmem_base + ((q * 32u) << 16) + (uint32_t)((g * p.sub + jt) * p.bn);
       uint32_t v[16];
-      tp::tmem_ld16(t_row, v);
+      const bool do_ld = (p.dbg & 8) == 0;
+      if (do_ld) {
+        tp::tmem_ld16(t_row, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0u;
+      }
       for (int c = 0; c < nchunks; ++c) {
-        tp::tmem_ld_wait();
+        if (do_ld) tp::tmem_ld_wait();
         float f[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
-        if (c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);  // overlap
+        if (do_ld && c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);
         const int ch0 = n0 + c * 16;
         const float4* b4 = reinterpret_cast<const float4*>(bias_s + ch0);
 #pragma unroll
@@ -373,35 +409,60 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
         }
-        if (RECT) {
-          // fused 2x2 max pool on packed 16-bit pairs (rounding is monotonic, so
-          // max-then-round == round-then-max): x pair = lane^1, y pair = lane^16
-          uint32_t pk[8];
+        if (RECT) {  // fused 2x2 max pool: x pair = lane^1, y pair = lane^16
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (f16) {
-              __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
-              __half2 o = __shfl_xor_sync(0xffffffffu, h, 1);
-              h = __hmax2(h, o);
-              o = __shfl_xor_sync(0xffffffffu, h, RECT_W);
-              h = __hmax2(h, o);
-              pk[j] = *reinterpret_cast<uint32_t*>(&h);
-            } else {
-              __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-              __nv_bfloat162 o = __shfl_xor_sync(0xffffffffu, h, 1);
-              h = __hmax2(h, o);
-              o = __shfl_xor_sync(0xffffffffu, h, RECT_W);
-              h = __hmax2(h, o);
-              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], RECT_W));
+        }
+        if (TSTORE) {
+          // 64-byte-per-row slabs (2 fp16 chunks or 1 fp32 chunk) staged with the SW64
+          // pattern, then one TMA store of {slab, 32 rows}; halo rows are written as zeros
+          constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
+          const int cs = c % CPS;
+          const uint32_t buf = tp::smem_u32(smC) + (warp - 2) * 2048;
+          if (cs == 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+          const uint32_t rbase = buf + lane * 64;
+          const uint32_t swz = (lane >> 1) & 3;
+          if (EPI == EPI_F32) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float a0 = valid ? f[4 * k] : 0.f, a1 = valid ? f[4 * k + 1] : 0.f;
+              const float a2 = valid ? f[4 * k + 2] : 0.f, a3 = valid ? f[4 * k + 3] : 0.f;
+              st_shared_v4(rbase + ((k ^ swz) << 4), __float_as_uint(a0), __float_as_uint(a1),
+                           __float_as_uint(a2), __float_as_uint(a3));
+            }
+          } else {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (f16) {
+                __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+                pk[j] = valid ? *reinterpret_cast<uint32_t*>(&h) : 0u;
+              } else {
+                __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+                pk[j] = valid ? *reinterpret_cast<uint32_t*>(&h) : 0u;
+              }
+            }
+            st_shared_v4(rbase + (((2 * cs) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
+            st_shared_v4(rbase + (((2 * cs + 1) ^ swz) << 4), pk[4], pk[5], pk[6], pk[7]);
+          }
+          if (cs == CPS - 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && (p.dbg & 4) == 0) {
+              tma_store_2d(&tmC, smC + (warp - 2) * 2048, p.out_coff + ch0 - 16 * cs,
+                           it.mt * 128 + (int)q * 32);
+              bulk_commit();
             }
           }
-          if (!valid || !writer || ch0 >= p.cout) continue;
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
-          *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
           continue;
         }
-        if (!valid || !writer || ch0 >= p.cout) continue;
+        if (!valid || !writer || ch0 >= p.cout || (p.dbg & 4)) continue;
         if (EPI == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
           if (ch0 + 16 <= p.cout) {
@@ -437,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) tp::mbar_arrive(&tempty[g]);
     }
+    if (TSTORE && lane == 0) bulk_wait_all();
   }
 
   tp::tc_fence_before();
@@ -510,8 +572,9 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // rank-2 {cols, rows} or rank-3 {cols, width, rows} 16-bit tensor map, cols contiguous.
+// esize 2 = 16-bit (f16 selects fp16 vs bf16), 4 = fp32
 int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
-              const uint32_t* box, CUtensorMapSwizzle swz, bool f16) {
+              const uint32_t* box, CUtensorMapSwizzle swz, bool f16, int esize = 2) {
   EncodeTiledFn enc = get_encode_fn();
   if (enc == nullptr) {
     tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -519,7 +582,7 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
   }
   cuuint64_t gdims[3], strides[2];
   cuuint32_t gbox[3], estr[3] = {1, 1, 1};
-  uint64_t stride = dims[0] * 2;
+  uint64_t stride = dims[0] * esize;
   for (int i = 0; i < rank; ++i) {
     gdims[i] = dims[i];
     gbox[i] = box[i];
@@ -528,7 +591,10 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
       stride *= dims[i];
     }
   }
-  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+  const CUtensorMapDataType dt = esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : f16       ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = enc(tm, dt,
                    rank, const_cast<void*>(base), gdims, strides, gbox, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -554,7 +620,7 @@ int num_sms() {
 // A fully prepared layer launch (tensor maps encoded once).
 struct ConvLaunch {
   int mode;
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmC;
   ConvParams p;
   size_t smem;
 };
@@ -639,6 +705,15 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     rc = make_tmap(&L->tmB, weight, 2, dims, box, swz, f16);
   }
   if (rc) return rc;
+  const bool tstore = !pool && !reorg;
+  if (tstore) {  // output store tensor map: {cstride, rows}, box {64 B of channels, 32 rows}
+    const uint64_t dims[2] = {(uint64_t)out_cstride, (uint64_t)max_img * img_px};
+    const uint32_t box[2] = {out_fp32 ? 16u : 32u, 32u};
+    rc = make_tmap(&L->tmC, out, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_64B, f16, out_fp32 ? 4 : 2);
+    if (rc) return rc;
+  } else {
+    L->tmC = L->tmA;  // unused
+  }
 
   ConvParams& p = L->p;
   p.n_img = max_img;
@@ -663,8 +738,12 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     p.n_bchunks = ktotal / bk;
     p.bres_bytes = (uint32_t)bres;
   }
+  p.stage_bytes = tstore ? 8 * 2048 : 0;
   const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
-  int stages = (int)((196 * 1024 - p.bres_bytes) / stage_bytes);
+  // everything else in smem: 1 KB alignment slack, bias, barriers (<= 12 stages), TMEM slot
+  const int fixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
+  int stages = (int)((227 * 1024 - fixed - (int)p.bres_bytes - (int)p.stage_bytes) /
+                     (int)stage_bytes);
   if (stages > 12) stages = 12;
   if (stages < 2) {
     tp_set_error("conv: stage too large");
@@ -689,8 +768,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.reorg = reorg;
   p.dbg = getenv("TP_CONV_DEBUG") ? atoi(getenv("TP_CONV_DEBUG")) : 0;
   L->mode = mode;
-  L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + (2 * stages + 6) * 8 +
-            cout_pad * 4 + 16;
+  L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + p.stage_bytes +
+            (2 * stages + 6) * 8 + cout_pad * 4 + 16;
   if (cout_pad > kMaxBias) {
     tp_set_error("conv: cout_pad %d exceeds %d", cout_pad, kMaxBias);
     return TP_ERR_UNSUPPORTED;
@@ -714,7 +793,7 @@ int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   const long long tiles = m_blocks * p.n_blocks_n;
   if (tiles == 0) return TP_OK;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_tc_kernel<MODE, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+  conv_tc_kernel<MODE, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
