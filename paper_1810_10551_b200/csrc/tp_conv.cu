@@ -507,6 +507,286 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tp::tmem_dealloc(tmem_base, p.tmem_cols);
 }
 
+// ------------------------------------------------------------------ CTA-pair variant
+// FLAT SW128 layers (every deep 3x3 / 1x1 conv): a 2-CTA cluster computes a 256-row x BN
+// tile with tcgen05.mma.cta_group::2 (M=256). Each CTA stages its own 128 A rows and HALF
+// of the B tile, so per SM the tensor core reads 4 KB + BN/2*32 B of shared memory per
+// K=16 step instead of 4 KB + BN*32 B — the 1-CTA kernel is shared-memory-bound on B.
+// The leader (rank 0) issues the MMAs; both CTAs' TMA loads complete on the leader's
+// full barrier; MMA commits multicast to both CTAs' empty/tfull barriers; both CTAs'
+// epilogue warps release the accumulator on the leader's tempty barrier.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(const void* local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(tp::smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint32_t leader_bar,
+                                                 int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(tp::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(tp::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_pair_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+  constexpr int BK = 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;
+  uint8_t* smC = smB + (size_t)S * p.b_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smC + p.stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
+
+  const uint32_t warp = tp::warp_id();
+  const uint32_t lane = tp::lane_id();
+  const uint32_t rank = cluster_rank();
+  const int cout_pad = p.bn * p.n_blocks_n;
+  const int half_bn = p.bn >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tp::tma_prefetch(&tmA);
+    tp::tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      tp::mbar_init(&full[s], 1);
+      tp::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tp::mbar_init(&tfull[a], 1);
+      tp::mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    tp::fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tp::smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
+  tp::tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialised + TMEM allocated
+  tp::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
+  const int total_px = n_img * p.img_px;
+  const int m_blocks = (total_px + 255) / 256;
+  const int total_tiles = m_blocks * p.n_blocks_n;
+  const int n_clusters = (int)gridDim.x >> 1, cid = (int)blockIdx.x >> 1;
+  const int per = total_tiles / n_clusters, extra = total_tiles % n_clusters;
+  const int t_begin = cid * per + min(cid, extra);
+  const int n_tiles = per + (cid < extra ? 1 : 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ============ TMA producer (both CTAs; bytes land on the leader's barrier) ============
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int t = t_begin + i;
+        const int mt = t / p.n_blocks_n;
+        const int n0 = (t - mt * p.n_blocks_n) * p.bn;
+        const int m0 = mt * 256 + (int)rank * 128;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0)
+            tp::mbar_arrive_expect_tx(&full[s], 2 * (p.a_stage_bytes + p.b_stage_bytes));
+          const uint32_t lbar = mapa_rank(&full[s], 0);
+          const int tap = kb / p.kb_per_tap;
+          const int cb = kb - tap * p.kb_per_tap;
+          tma_load_2d_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK,
+                           m0 + tap_shift(tap, p.ksize, p.wp));
+          tma_load_2d_pair(smB + (size_t)s * p.b_stage_bytes, &tmB, lbar, tap * p.cin + cb * BK,
+                           n0 + (int)rank * half_bn);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ================= MMA issuer: leader CTA, single thread =================
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t aph[2] = {0, 0};
+      for (int i = 0; i < n_tiles; ++i) {
+        const int acc = i & 1;
+        tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        aph[acc] ^= 1;
+        tp::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&full[s], ph);
+          tp::tc_fence_after();
+          const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * p.a_stage_bytes);
+          const uint32_t b_addr = tp::smem_u32(smB + (size_t)s * p.b_stage_bytes);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 1024, 2);
+            uint64_t bd = tp::umma_desc(b_addr + k * 32, 16, 1024, 2);
+            mma_pair(d_tmem, ad, bd, p.idesc, (kb | k) != 0);
+          }
+          commit_pair_mc(&empty[s]);  // frees the stage in both CTAs
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        commit_pair_mc(&tfull[acc]);  // both CTAs' epilogues may read their halves
+      }
+    }
+  } else {
+    // ============ epilogue: both CTAs, own 128 rows; groups alternate accumulators ============
+    const int g = (int)(warp - 2) >> 2;
+    const uint32_t q = warp & 3;
+    const bool f16 = p.f16 != 0;
+    const bool leaky = p.leaky != 0;
+    const int nchunks = p.bn >> 4;
+    const uint32_t leader_tempty[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
+    uint32_t ph = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      if ((i & 1) != g) continue;
+      const int t = t_begin + i;
+      const int mt = t / p.n_blocks_n;
+      const int n0 = (t - mt * p.n_blocks_n) * p.bn;
+      tp::mbar_wait(&tfull[g], ph);
+      ph ^= 1;
+      tp::tc_fence_after();
+      const int rbase = mt * 256 + (int)rank * 128 + (int)q * 32;
+      const int pix = rbase + (int)lane;
+      bool valid = pix < total_px;
+      if (valid) {
+        const int img = pix / p.img_px;
+        const int rem = pix - img * p.img_px;
+        const int yp = rem / p.wp, xp = rem - yp * p.wp;
+        valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
+      }
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * p.bn);
+      const uint32_t buf = tp::smem_u32(smC) + (warp - 2) * 2048;
+      const uint32_t rowa = buf + lane * 64;
+      const uint32_t swz = (lane >> 1) & 3;
+      uint32_t v[16];
+      tp::tmem_ld16(t_row, v);
+      for (int c = 0; c < nchunks; ++c) {
+        tp::tmem_ld_wait();
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+        if (c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);
+        const int ch0 = n0 + c * 16;
+        const float4* b4 = reinterpret_cast<const float4*>(bias_s + ch0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 bb = b4[j];
+          f[4 * j + 0] += bb.x;
+          f[4 * j + 1] += bb.y;
+          f[4 * j + 2] += bb.z;
+          f[4 * j + 3] += bb.w;
+        }
+        if (leaky) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
+        }
+        constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
+        const int cs = c % CPS;
+        if (cs == 0) {
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        }
+        if (EPI == EPI_F32) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float a0 = valid ? f[4 * k] : 0.f, a1 = valid ? f[4 * k + 1] : 0.f;
+            const float a2 = valid ? f[4 * k + 2] : 0.f, a3 = valid ? f[4 * k + 3] : 0.f;
+            st_shared_v4(rowa + ((k ^ swz) << 4), __float_as_uint(a0), __float_as_uint(a1),
+                         __float_as_uint(a2), __float_as_uint(a3));
+          }
+        } else {
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (f16) {
+              __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = valid ? *reinterpret_cast<uint32_t*>(&h) : 0u;
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = valid ? *reinterpret_cast<uint32_t*>(&h) : 0u;
+            }
+          }
+          st_shared_v4(rowa + (((2 * cs) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
+          st_shared_v4(rowa + (((2 * cs + 1) ^ swz) << 4), pk[4], pk[5], pk[6], pk[7]);
+        }
+        if (cs == CPS - 1) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, smC + (warp - 2) * 2048, p.out_coff + ch0 - 16 * cs, rbase);
+            bulk_commit();
+          }
+        }
+      }
+      tp::tmem_ld_wait();
+      tp::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty[g]);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tp::tc_fence_before();
+  cluster_sync_all();
+  tp::tc_fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols)
+                 : "memory");
+}
+
 // 2x2/2 max pool, padded NHWC 16-bit -> padded NHWC (interior only), 8 channels/thread.
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
                                 int cstride, __nv_bfloat16* __restrict__ out,
@@ -620,6 +900,7 @@ int num_sms() {
 // A fully prepared layer launch (tensor maps encoded once).
 struct ConvLaunch {
   int mode;
+  int pair;  // CTA-pair (cta_group::2) kernel
   CUtensorMap tmA, tmB, tmC;
   ConvParams p;
   size_t smem;
@@ -770,6 +1051,22 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   L->mode = mode;
   L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + p.stage_bytes +
             (2 * stages + 6) * 8 + cout_pad * 4 + 16;
+  // CTA-pair variant for FLAT SW128 layers (TP_PAIR=0 disables it)
+  const char* pe = getenv("TP_PAIR");
+  if (tstore && mode == MODE_SW128 && bn == 256 && (pe == nullptr || atoi(pe) != 0)) {
+    const uint64_t dims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+    const uint32_t box[2] = {(uint32_t)bk, (uint32_t)(bn / 2)};
+    rc = make_tmap(&L->tmB, weight, 2, dims, box, swz, f16);
+    if (rc) return rc;
+    L->pair = 1;
+    p.b_stage_bytes = (bn / 2) * bk * 2;
+    p.idesc = tp::idesc_f16kind(256, (uint32_t)bn, !f16);
+    const uint32_t sb = p.a_stage_bytes + p.b_stage_bytes;
+    int st = (int)((227 * 1024 - fixed - (int)p.stage_bytes) / (int)sb);
+    if (st > 12) st = 12;
+    p.stages = st;
+    L->smem = 1024 + (size_t)st * sb + p.stage_bytes + (2 * st + 6) * 8 + cout_pad * 4 + 16;
+  }
   if (cout_pad > kMaxBias) {
     tp_set_error("conv: cout_pad %d exceeds %d", cout_pad, kMaxBias);
     return TP_ERR_UNSUPPORTED;
@@ -798,11 +1095,45 @@ int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   return TP_OK;
 }
 
+template <int EPI>
+int launch_pair(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_pair_kernel<EPI>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  ConvParams p = L.p;
+  p.n_img = n_img;
+  p.n_img_dev = n_img_dev;
+  const long long tiles = (((long long)n_img * p.img_px + 255) / 256) * p.n_blocks_n;
+  if (tiles == 0) return TP_OK;
+  const int max_clusters = num_sms() / 2;
+  const int clusters = (int)(tiles < max_clusters ? tiles : max_clusters);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_kernel<EPI>, L.tmA, L.tmB, L.tmC, p));
+  return TP_OK;
+}
+
 int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
   if (n_img > L.p.n_img) {
     tp_set_error("conv: n_img %d exceeds planned %d", n_img, L.p.n_img);
     return TP_ERR_CAPACITY;
   }
+  if (L.pair)
+    return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
+                        : launch_pair<EPI_PLAIN>(L, n_img, n_img_dev, st);
   const int epi = L.p.rect ? EPI_POOL : L.p.reorg ? EPI_REORG : L.p.out_fp32 ? EPI_F32 : EPI_PLAIN;
 #define TP_EPI_SWITCH(M)                                                  \
   switch (epi) {                                                          \
