@@ -787,6 +787,193 @@ __global__ void __launch_bounds__(kThreads, 1)
                  : "memory");
 }
 
+// ------------------------------------------------------------------ layer 0, pool-in-M
+// Layer 0 (3x3, 3->32, leaky, 2x2 maxpool) has K = 48 but 608^2 outputs per tile, so it
+// is bound by epilogue instructions, not math. Here each M row is one POOLED output
+// pixel: the four pool positions (py,px) accumulate into four TMEM accumulators, fed by
+// TMA boxes with traversal stride 2 in x and y over the expanded input ({16 ch, 32 x/2,
+// 18 y/2}). Per tile (16x8 pooled = 32x16 conv pixels): 4 boxes (x phase px, y phase f),
+// 12 MMAs (4 pool positions x 3 kernel rows, K=16, N=32); the epilogue reads 4 x 32
+// columns per row and does max + bias + leaky + pack per pooled value — ~4.6x fewer
+// instructions per conv output than pooling by shuffles.
+constexpr int L0_BOX_ROWS = 9;                       // strided rows per box
+constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 32;  // 4608
+constexpr int L0_STAGE = 4 * L0_BOX_BYTES;           // 18432
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_l0_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const ConvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + (size_t)S * L0_STAGE;  // resident weights: 3 chunks x 1 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + 3 * 1024);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint64_t* bres_bar = bars + 2 * S + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
+
+  const uint32_t warp = tp::warp_id();
+  const uint32_t lane = tp::lane_id();
+  if (warp == 0 && lane == 0) {
+    tp::tma_prefetch(&tmA);
+    tp::tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      tp::mbar_init(&full[s], 1);
+      tp::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tp::mbar_init(&tfull[a], 1);
+      tp::mbar_init(&tempty[a], 4);
+    }
+    tp::mbar_init(bres_bar, 1);
+    tp::fence_mbar_init();
+  }
+  if (warp == 1) tp::tmem_alloc(tmem_slot, 256);
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) bias_s[i] = p.bias[i];
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
+  const int ores = p.res >> 1, owp = ores + 2, oimg = owp * owp, hp = p.res + 2;
+  const int txs = ores / 16, tys = ores / 8, per_img = txs * tys;  // 304 = 19*16 = 38*8
+  const int total_tiles = n_img * per_img;
+  const int per_cta = total_tiles / (int)gridDim.x, extra = total_tiles % (int)gridDim.x;
+  const int t_begin = (int)blockIdx.x * per_cta + min((int)blockIdx.x, extra);
+  const int n_tiles = per_cta + ((int)blockIdx.x < extra ? 1 : 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      if (n_tiles > 0) {
+        tp::mbar_arrive_expect_tx(bres_bar, 3 * 1024);
+        for (int j = 0; j < 3; ++j) tp::tma_load_2d(smB + j * 1024, &tmB, bres_bar, j * 16, 0);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int t = t_begin + i;
+        const int img = t / per_img, r = t - img * per_img;
+        const int by = r / txs, bx = r - by * txs;
+        tp::mbar_wait(&empty[s], ph ^ 1);
+        tp::mbar_arrive_expect_tx(&full[s], L0_STAGE);
+        uint8_t* dst = smA + (size_t)s * L0_STAGE;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {  // b = px * 2 + y phase
+          const int px = b >> 1, f = b & 1;
+          tma_load_3d(dst + b * L0_BOX_BYTES, &tmA, &full[s], 0, 1 + 32 * bx + px,
+                      img * hp + 1 + 16 * by + f - 1);
+        }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      tp::mbar_wait(bres_bar, 0);
+      const uint32_t bres = tp::smem_u32(smB);
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t aph[2] = {0, 0};
+      for (int i = 0; i < n_tiles; ++i) {
+        const int acc = i & 1;
+        tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        aph[acc] ^= 1;
+        tp::mbar_wait(&full[s], ph);
+        tp::tc_fence_after();
+        const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * L0_STAGE);
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {  // pool position (py, px)
+          const int py = pp >> 1, px = pp & 1;
+          const uint32_t d = tmem_base + (uint32_t)(acc * 128 + pp * 32);
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+            const int o = py + dy;  // input row offset + 1, in 0..3
+            const int box = px * 2 + (o & 1), start = o >> 1;
+            const uint32_t aw = a_addr + box * L0_BOX_BYTES + start * 16 * 32;
+            uint64_t ad = tp::umma_desc(aw, 16, 256, 6);
+            uint64_t bd = tp::umma_desc(bres + dy * 1024, 16, 256, 6);
+            tp::mma_bf16(d, ad, bd, p.idesc, dy != 0);
+          }
+        }
+        tp::mma_commit(&empty[s]);
+        tp::mma_commit(&tfull[acc]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else {
+    const int g = (int)(warp - 2) >> 2;
+    const uint32_t q = warp & 3;
+    const int row = (int)(q * 32 + lane);
+    const bool f16 = p.f16 != 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      if ((i & 1) != g) continue;
+      const int t = t_begin + i;
+      const int img = t / per_img, r = t - img * per_img;
+      const int by = r / txs, bx = r - by * txs;
+      tp::mbar_wait(&tfull[g], ph);
+      ph ^= 1;
+      tp::tc_fence_after();
+      const int X = bx * 16 + (row & 15), Y = by * 8 + (row >> 4);
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                         (size_t)(img * oimg + (Y + 1) * owp + (X + 1)) * p.out_cstride;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 128);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v0[16], v1[16], v2[16], v3[16];
+        tp::tmem_ld16(t_row + c * 16, v0);
+        tp::tmem_ld16(t_row + 32 + c * 16, v1);
+        tp::tmem_ld16(t_row + 64 + c * 16, v2);
+        tp::tmem_ld16(t_row + 96 + c * 16, v3);
+        tp::tmem_ld_wait();
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float a = fmaxf(fmaxf(__uint_as_float(v0[2 * j]), __uint_as_float(v1[2 * j])),
+                          fmaxf(__uint_as_float(v2[2 * j]), __uint_as_float(v3[2 * j])));
+          float b = fmaxf(fmaxf(__uint_as_float(v0[2 * j + 1]), __uint_as_float(v1[2 * j + 1])),
+                          fmaxf(__uint_as_float(v2[2 * j + 1]), __uint_as_float(v3[2 * j + 1])));
+          // bias + leaky are monotonic, so pooling first gives the same value
+          a += bias_s[c * 16 + 2 * j];
+          b += bias_s[c * 16 + 2 * j + 1];
+          a = fmaxf(a, 0.1f * a);
+          b = fmaxf(b, 0.1f * b);
+          if (f16) {
+            __half2 h = __floats2half2_rn(a, b);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          } else {
+            __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+        }
+        if (img < n_img) {
+          *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+      tp::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tp::mbar_arrive(&tempty[g]);
+    }
+  }
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  if (warp == 1) tp::tmem_dealloc(tmem_base, 256);
+}
+
 // 2x2/2 max pool, padded NHWC 16-bit -> padded NHWC (interior only), 8 channels/thread.
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
                                 int cstride, __nv_bfloat16* __restrict__ out,
@@ -854,7 +1041,8 @@ EncodeTiledFn get_encode_fn() {
 // rank-2 {cols, rows} or rank-3 {cols, width, rows} 16-bit tensor map, cols contiguous.
 // esize 2 = 16-bit (f16 selects fp16 vs bf16), 4 = fp32
 int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
-              const uint32_t* box, CUtensorMapSwizzle swz, bool f16, int esize = 2) {
+              const uint32_t* box, CUtensorMapSwizzle swz, bool f16, int esize = 2,
+              const uint32_t* elem_strides = nullptr) {
   EncodeTiledFn enc = get_encode_fn();
   if (enc == nullptr) {
     tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -866,6 +1054,7 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
   for (int i = 0; i < rank; ++i) {
     gdims[i] = dims[i];
     gbox[i] = box[i];
+    if (elem_strides != nullptr) estr[i] = elem_strides[i];
     if (i > 0) {
       strides[i - 1] = stride;
       stride *= dims[i];
@@ -901,6 +1090,7 @@ int num_sms() {
 struct ConvLaunch {
   int mode;
   int pair;  // CTA-pair (cta_group::2) kernel
+  int l0;    // layer-0 pool-in-M kernel
   CUtensorMap tmA, tmB, tmC;
   ConvParams p;
   size_t smem;
@@ -1051,6 +1241,22 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   L->mode = mode;
   L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + p.stage_bytes +
             (2 * stages + 6) * 8 + cout_pad * 4 + 16;
+  // layer 0: pool-in-M kernel with stride-2 TMA boxes (TP_L0=0 disables it)
+  const char* l0e = getenv("TP_L0");
+  if (mode == MODE_L0X && pool && cout_pad == 32 && res % 32 == 0 && !out_fp32 &&
+      (l0e == nullptr || atoi(l0e) != 0)) {
+    const uint64_t dims[3] = {16, (uint64_t)wp, (uint64_t)max_img * wp};
+    const uint32_t box[3] = {16, 32, 18};
+    const uint32_t estr[3] = {1, 2, 2};
+    rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 2, estr);
+    if (rc) return rc;
+    L->l0 = 1;
+    int st = (int)((227 * 1024 - fixed - 3 * 1024) / L0_STAGE);
+    if (st > 8) st = 8;
+    p.stages = st;
+    p.idesc = tp::idesc_f16kind(128, 32, !f16);
+    L->smem = 1024 + (size_t)st * L0_STAGE + 3 * 1024 + (2 * st + 6) * 8 + 32 * 4 + 16;
+  }
   // CTA-pair variant for FLAT SW128 layers (TP_PAIR=0 disables it)
   const char* pe = getenv("TP_PAIR");
   if (tstore && mode == MODE_SW128 && bn == 256 && (pe == nullptr || atoi(pe) != 0)) {
@@ -1134,6 +1340,23 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
   if (L.pair)
     return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
                         : launch_pair<EPI_PLAIN>(L, n_img, n_img_dev, st);
+  if (L.l0) {
+    static bool configured = false;
+    if (!configured) {
+      TP_CUDA_CHECK(cudaFuncSetAttribute(conv_l0_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      configured = true;
+    }
+    ConvParams p = L.p;
+    p.n_img = n_img;
+    p.n_img_dev = n_img_dev;
+    const long long tiles = (long long)n_img * (p.res / 32) * (p.res / 16);
+    if (tiles == 0) return TP_OK;
+    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    conv_l0_kernel<<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+    TP_LAUNCH_CHECK();
+    return TP_OK;
+  }
   const int epi = L.p.rect ? EPI_POOL : L.p.reorg ? EPI_REORG : L.p.out_fp32 ? EPI_F32 : EPI_PLAIN;
 #define TP_EPI_SWITCH(M)                                                  \
   switch (epi) {                                                          \
