@@ -94,18 +94,31 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       b = (b00 * w00 + b01 * w01 + b10 * w10 + b11 * w11 + 32768) >> 16;
     }
   };
-  auto pack = [&](int a, int b) -> uint32_t {
+  // exact value/255 in the activation type, looked up instead of divided (bit-identical)
+  __shared__ uint16_t lut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     if (act_f16) {
-      __half2 h = __floats2half2_rn((float)a / 255.0f, (float)b / 255.0f);
-      return *reinterpret_cast<uint32_t*>(&h);
+      __half h = __float2half_rn((float)i / 255.0f);
+      lut[i] = *reinterpret_cast<uint16_t*>(&h);
+    } else {
+      __nv_bfloat16 h = __float2bfloat16_rn((float)i / 255.0f);
+      lut[i] = *reinterpret_cast<uint16_t*>(&h);
     }
-    __nv_bfloat162 h = __floats2bfloat162_rn((float)a / 255.0f, (float)b / 255.0f);
-    return *reinterpret_cast<uint32_t*>(&h);
-  };
+  }
+  __syncthreads();
+  auto pk2 = [&](int a, int b) -> uint32_t { return (uint32_t)lut[a] | ((uint32_t)lut[b] << 16); };
 
-  for (int u = threadIdx.x; u < S; u += blockDim.x) {
-    int r, g, b;
-    sample(u, r, g, b);
+  // blockDim = 256 threads, 3 passes cover 608 columns; every warp-lane pair (u, u+-1)
+  // lives in the same warp except at warp edges, where the neighbour is re-sampled.
+  for (int base = 0; base < S; base += blockDim.x) {
+    const int u = base + threadIdx.x;
+    int r = 0, g = 0, b = 0;
+    if (u < S) sample(u, r, g, b);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t me_rg = pk2(r, g), me_b0 = pk2(b, 0);
+    uint32_t l_rg = __shfl_up_sync(0xffffffffu, me_rg, 1), l_b0 = __shfl_up_sync(0xffffffffu, me_b0, 1);
+    uint32_t r_rg = __shfl_down_sync(0xffffffffu, me_rg, 1), r_b0 = __shfl_down_sync(0xffffffffu, me_b0, 1);
+    if (u >= S) continue;
     if (out_u8 != nullptr) {
       uint8_t* o = out_u8 + (((size_t)t * S + v) * S + u) * 3;
       o[0] = (uint8_t)r;
@@ -113,22 +126,23 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       o[2] = (uint8_t)b;
     }
     if (out_act != nullptr) {
+      if (lane == 0) {
+        int rl, gl, bl;
+        sample(u - 1, rl, gl, bl);
+        l_rg = pk2(rl, gl);
+        l_b0 = pk2(bl, 0);
+      }
+      if (lane == 31) {
+        int rr, gr, br;
+        sample(u + 1, rr, gr, br);
+        r_rg = pk2(rr, gr);
+        r_b0 = pk2(br, 0);
+      }
+      if (u == S - 1) r_rg = r_b0 = 0u;  // right neighbour outside the tile
       // expanded layer-0 pixel: [p(u-1) rgb0 | p(u) rgb0 | p(u+1) rgb0 | 0 0 0 0]
-      int rl, gl, bl, rr, gr, br;
-      sample(u - 1, rl, gl, bl);
-      sample(u + 1, rr, gr, br);
-      uint4 lo, hi;
-      lo.x = pack(rl, gl);
-      lo.y = pack(bl, 0);
-      lo.z = pack(r, g);
-      lo.w = pack(b, 0);
-      hi.x = pack(rr, gr);
-      hi.y = pack(br, 0);
-      hi.z = 0u;
-      hi.w = 0u;
       __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 16;
-      *reinterpret_cast<uint4*>(o) = lo;
-      *reinterpret_cast<uint4*>(o + 8) = hi;
+      *reinterpret_cast<uint4*>(o) = make_uint4(l_rg, l_b0, me_rg, me_b0);
+      *reinterpret_cast<uint4*>(o + 8) = make_uint4(r_rg, r_b0, 0u, 0u);
     }
   }
 }

@@ -228,3 +228,20 @@ def test_device_renderer_matches_reference_render(cuda):
             else:  # 8K golden not stored: compare with the host restatement
                 ref = synthetic.render_frame(sc["fw"], sc["fh"], gt[f])
                 assert h == hashlib.sha256(ref.tobytes()).hexdigest()
+
+
+def test_run_stream_equals_run_sequence_and_aborts_with_cursor(cuda, clip):
+    from paper_1810_10551_b200.stream import StreamAborted, run_stream
+
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    det = yolo.YoloB200Detector()
+    seq = list(P.run_sequence(clip, settings, det))
+    streamed = run_stream(clip, settings, batch=2)
+    assert [(r.frame_id, r.detections, r.active_count) for r in streamed] == \
+        [(r.frame_id, r.detections, r.active_count) for r in seq]
+    t = streamed[0].timing
+    assert t.io_ms > 0 and t.final_eval_ms > 0 and t.per_worker[0][0].startswith("cuda:")
+    bad = list(clip[:2]) + [P.Frame(9, 1280, 720, np.zeros((720, 1280, 3), np.uint8))]
+    with pytest.raises(StreamAborted) as ei:
+        run_stream(bad, settings, batch=2)
+    assert ei.value.cursor == 2 and len(ei.value.completed) == 2

@@ -127,3 +127,15 @@ def test_ops_fail_loudly_without_gpu():
 
     with pytest.raises(native.NativeUnavailable):
         nms([Detection(Rect(0, 0, 5, 5), "a", 0.5)], 0.45)
+
+
+def test_result_line_is_byte_identical_to_reference_format():
+    from paper_1810_10551_b200.detector import Detection
+    from paper_1810_10551_b200.stream import result_line
+
+    r = FrameResult(7, (Detection(Rect(10, 20, 30, 40), "person", 0.5),
+                        Detection(Rect(1, 2, 3, 4), 'car "x"', 1.0)), 3, 18, TimingProfile())
+    assert result_line(r) == (
+        '{"active_count":3,"detections":[{"class":"person","confidence":0.500000,"h":40,"w":30,'
+        '"x":10,"y":20},{"class":"car \\"x\\"","confidence":1.000000,"h":4,"w":3,"x":1,"y":2}],'
+        '"frame_id":7,"total_count":18}')
