@@ -41,6 +41,9 @@ namespace {
 enum ConvMode { MODE_SW128 = 0, MODE_SW64 = 1, MODE_L0X = 2 };
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
+// Warp roles: the warp scheduler favours HIGHER warp ids, so the two single-thread roles
+// (TMA producer, MMA issuer) take the top ids and are never starved by epilogue warps.
+constexpr uint32_t kProdWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr int RECT_W = 16, RECT_H = 8;
 
 struct ConvParams {
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = tp::lane_id();
   const int cout_pad = p.bn * p.n_blocks_n;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kProdWarp && lane == 0) {
     tp::tma_prefetch(&tmA);
     tp::tma_prefetch(&tmB);
     for (int s = 0; s < S; ++s) {
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tp::mbar_init(bres_bar, 1);
     tp::fence_mbar_init();
   }
-  if (warp == 1) tp::tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, p.tmem_cols);
   for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
   tp::tc_fence_before();
   __syncthreads();
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_tiles = per_cta + ((int)blockIdx.x < extra ? 1 : 0);
   const int hp = p.res + 2;
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     if (lane == 0) {
       // ================= TMA producer =================
       int s = 0;
@@ -224,6 +227,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tp::mbar_wait(&empty[s], ph ^ 1);
           uint8_t* a_dst = smA + (size_t)s * p.a_stage_bytes;
           uint8_t* b_dst = smB + (size_t)s * p.b_stage_bytes;
+          if (p.dbg & 16) {  // profiling: no TMA, stale operands
+            tp::mbar_arrive(&full[s]);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           tp::mbar_arrive_expect_tx(&full[s], tx_bytes);
           if (RECT && p.halo) {  // halo box {BK, 16, 10} for kernel column dx, channel block cb
             const int dx = MODE == MODE_L0X ? 0 : kb / p.kb_per_tap - 1;
@@ -254,15 +265,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ================= MMA issuer (single thread) =================
+  } else if (warp == kMmaWarp) {
+    {
+      // ================= MMA issuer: the warp runs the loop convergent (descriptors stay
+      // in uniform registers) and one elected lane issues; a divergent lane-0 loop made
+      // the compiler wrap every tcgen05.mma in an ELECT/R2UR waterfall (~2.5x slower).
       const uint32_t idesc = p.idesc;
       int s = 0;
       uint32_t ph = 0;
       uint32_t aph[2] = {0, 0};
       if (RECT && p.halo && n_tiles > 0) tp::mbar_wait(bres_bar, 0);
-      const uint32_t bres_addr = tp::smem_u32(smB);
+      // descriptors are built once; per MMA only the start-address field (addr >> 4, low
+      // bits) moves, so each issue is one 64-bit add — rebuilding them per instruction
+      // made the single issuing thread the bottleneck for N <= 128 (~90+ cycles/MMA).
+      constexpr uint32_t row_bytes = BK * 2;
+      constexpr uint32_t sbo = 8 * row_bytes;
+      constexpr uint32_t lay = MODE == MODE_SW128 ? 2 : (MODE == MODE_SW64 ? 4 : 6);
+      const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, sbo, lay);
+      const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, sbo, lay);
+      const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
+      const uint32_t bch = p.bchunk_bytes >> 4;
       for (int i = 0; i < n_tiles; ++i) {
         const int acc = i & 1;
         tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
@@ -272,64 +294,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&full[s], ph);
           tp::tc_fence_after();
-          const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * p.a_stage_bytes);
-          const uint32_t b_addr = tp::smem_u32(smB + (size_t)s * p.b_stage_bytes);
-          if (p.dbg & 2) {
+          const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
+          const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
+          if (!tp::elect_one()) {
+          } else if (p.dbg & 2) {
             // profiling: no MMA
           } else if (RECT && p.halo) {
             // three kernel rows dy = sub-windows of the halo box, 16 pixel rows apart
-            constexpr uint32_t row_bytes = BK * 2;
-            constexpr uint32_t sbo = 8 * row_bytes;
-            constexpr uint32_t lay = MODE == MODE_SW128 ? 2 : (MODE == MODE_SW64 ? 4 : 6);
+            constexpr uint32_t row16 = RECT_W * row_bytes / 16;  // one pixel row, >> 4
             const int dx = MODE == MODE_L0X ? 0 : kb / p.kb_per_tap - 1;
             const int cb = MODE == MODE_L0X ? 0 : kb % p.kb_per_tap;
             for (int j = 0; j < p.sub; ++j) {
+              const uint64_t aj = ad0 + (uint64_t)(j * RECT_H * row16);
+              const uint32_t dj = d_tmem + j * p.bn;
 #pragma unroll
               for (int dy = 0; dy < 3; ++dy) {
                 const int chunk = MODE == MODE_L0X ? dy : (dy * 3 + dx + 1) * p.kb_per_tap + cb;
-                const uint32_t aw = a_addr + (j * RECT_H + dy) * RECT_W * row_bytes;
-                const uint32_t bw = bres_addr + chunk * p.bchunk_bytes;
+                const uint64_t aw = aj + dy * row16;
+                const uint64_t bw = b_desc0 + (uint64_t)(chunk * bch);
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                  uint64_t ad = tp::umma_desc(aw + k * 32, 16, sbo, lay);
-                  uint64_t bd = tp::umma_desc(bw + k * 32, 16, sbo, lay);
-                  tp::mma_bf16(d_tmem + j * p.bn, ad, bd, idesc, (kb | dy | k) != 0);
-                }
+                for (int k = 0; k < BK / 16; ++k)
+                  tp::mma_bf16(dj, aw + 2 * k, bw + 2 * k, idesc, (kb | dy | k) != 0);
               }
             }
-          } else if (MODE == MODE_SW128) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 1024, 2);
-              uint64_t bd = tp::umma_desc(b_addr + k * 32, 16, 1024, 2);
-              tp::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            }
-          } else if (MODE == MODE_SW64) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 512, 4);
-              uint64_t bd = tp::umma_desc(b_addr + k * 32, 16, 512, 4);
-              tp::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            }
           } else {
-            uint64_t ad = tp::umma_desc(a_addr, 16, 256, 6);
-            uint64_t bd = tp::umma_desc(b_addr, 16, 256, 6);
-            tp::mma_bf16(d_tmem, ad, bd, idesc, kb != 0);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tp::mma_bf16(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, (kb | k) != 0);
           }
-          tp::mma_commit(&empty[s]);  // frees the smem stage when these MMAs retire
+          if (tp::elect_one()) tp::mma_commit(&empty[s]);  // frees the stage when these retire
+          __syncwarp();
           if (++s == S) {
             s = 0;
             ph ^= 1;
           }
         }
-        tp::mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (tp::elect_one()) tp::mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        __syncwarp();
       }
     }
   } else {
     // ================= epilogue: two warpgroups, one per TMEM accumulator =================
     // group g takes the CTA's local tiles i with i % 2 == g; its 4 warps cover the 4
     // TMEM lane quadrants, all BN columns.
-    const int g = (int)(warp - 2) >> 2;
+    const int g = (int)warp >> 2;
     const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pattern, then one TMA store of {slab, 32 rows}; halo rows are written as zeros
           constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
           const int cs = c % CPS;
-          const uint32_t buf = tp::smem_u32(smC) + (warp - 2) * 2048;
+          const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
           if (cs == 0) {
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && (p.dbg & 4) == 0) {
-              tma_store_2d(&tmC, smC + (warp - 2) * 2048, p.out_coff + ch0 - 16 * cs,
+              tma_store_2d(&tmC, smC + warp * 2048, p.out_coff + ch0 - 16 * cs,
                            it.mt * 128 + (int)q * 32);
               bulk_commit();
             }
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tp::tc_fence_before();
   __syncthreads();
   tp::tc_fence_after();
-  if (warp == 1) tp::tmem_dealloc(tmem_base, p.tmem_cols);
+  if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, p.tmem_cols);
 }
 
 // ------------------------------------------------------------------ CTA-pair variant
@@ -585,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cout_pad = p.bn * p.n_blocks_n;
   const int half_bn = p.bn >> 1;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kProdWarp && lane == 0) {
     tp::tma_prefetch(&tmA);
     tp::tma_prefetch(&tmB);
     for (int s = 0; s < S; ++s) {
@@ -598,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tp::fence_mbar_init();
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      tp::smem_u32(tmem_slot)),
                  "r"(p.tmem_cols)
@@ -620,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_begin = cid * per + min(cid, extra);
   const int n_tiles = per + (cid < extra ? 1 : 0);
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     if (lane == 0) {
       // ============ TMA producer (both CTAs; bytes land on the leader's barrier) ============
       int s = 0;
@@ -648,9 +656,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ================= MMA issuer: leader CTA, single thread =================
+  } else if (warp == kMmaWarp) {
+    if (rank == 0) {
+      // ============ MMA issuer: leader CTA, warp-convergent loop, one elected lane ============
+      const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 1024, 2);
+      const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 1024, 2);
+      const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
       int s = 0;
       uint32_t ph = 0;
       uint32_t aph[2] = {0, 0};
@@ -663,26 +674,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&full[s], ph);
           tp::tc_fence_after();
-          const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * p.a_stage_bytes);
-          const uint32_t b_addr = tp::smem_u32(smB + (size_t)s * p.b_stage_bytes);
+          const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
+          const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint64_t ad = tp::umma_desc(a_addr + k * 32, 16, 1024, 2);
-            uint64_t bd = tp::umma_desc(b_addr + k * 32, 16, 1024, 2);
-            mma_pair(d_tmem, ad, bd, p.idesc, (kb | k) != 0);
+          if (tp::elect_one()) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_pair(d_tmem, ad0 + 2 * k, bd0 + 2 * k, p.idesc, (kb | k) != 0);
+            commit_pair_mc(&empty[s]);  // frees the stage in both CTAs
           }
-          commit_pair_mc(&empty[s]);  // frees the stage in both CTAs
+          __syncwarp();
           if (++s == S) {
             s = 0;
             ph ^= 1;
           }
         }
-        commit_pair_mc(&tfull[acc]);  // both CTAs' epilogues may read their halves
+        if (tp::elect_one()) commit_pair_mc(&tfull[acc]);  // both CTAs' epilogues may read
+        __syncwarp();
       }
     }
   } else {
     // ============ epilogue: both CTAs, own 128 rows; groups alternate accumulators ============
-    const int g = (int)(warp - 2) >> 2;
+    const int g = (int)warp >> 2;
     const uint32_t q = warp & 3;
     const bool f16 = p.f16 != 0;
     const bool leaky = p.leaky != 0;
@@ -707,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
       }
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * p.bn);
-      const uint32_t buf = tp::smem_u32(smC) + (warp - 2) * 2048;
+      const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
       const uint32_t rowa = buf + lane * 64;
       const uint32_t swz = (lane >> 1) & 3;
       uint32_t v[16];
@@ -765,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, smC + (warp - 2) * 2048, p.out_coff + ch0 - 16 * cs, rbase);
+            tma_store_2d(&tmC, smC + warp * 2048, p.out_coff + ch0 - 16 * cs, rbase);
             bulk_commit();
           }
         }
@@ -781,7 +794,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tp::tc_fence_before();
   cluster_sync_all();
   tp::tc_fence_after();
-  if (warp == 1)
+  if (warp == kMmaWarp)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(p.tmem_cols)
                  : "memory");
@@ -820,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = tp::warp_id();
   const uint32_t lane = tp::lane_id();
-  if (warp == 0 && lane == 0) {
+  if (warp == kProdWarp && lane == 0) {
     tp::tma_prefetch(&tmA);
     tp::tma_prefetch(&tmB);
     for (int s = 0; s < S; ++s) {
@@ -834,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tp::mbar_init(bres_bar, 1);
     tp::fence_mbar_init();
   }
-  if (warp == 1) tp::tmem_alloc(tmem_slot, 256);
+  if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, 256);
   for (int i = threadIdx.x; i < 32; i += blockDim.x) bias_s[i] = p.bias[i];
   tp::tc_fence_before();
   __syncthreads();
@@ -849,7 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t_begin = (int)blockIdx.x * per_cta + min((int)blockIdx.x, extra);
   const int n_tiles = per_cta + ((int)blockIdx.x < extra ? 1 : 0);
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     if (lane == 0) {
       if (n_tiles > 0) {
         tp::mbar_arrive_expect_tx(bres_bar, 3 * 1024);
@@ -876,10 +889,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
+  } else if (warp == kMmaWarp) {
+    {
       tp::mbar_wait(bres_bar, 0);
-      const uint32_t bres = tp::smem_u32(smB);
+      const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 256, 6);
+      const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 256, 6);
       int s = 0;
       uint32_t ph = 0;
       uint32_t aph[2] = {0, 0};
@@ -889,23 +903,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         aph[acc] ^= 1;
         tp::mbar_wait(&full[s], ph);
         tp::tc_fence_after();
-        const uint32_t a_addr = tp::smem_u32(smA + (size_t)s * L0_STAGE);
+        const uint64_t ad0 = a_desc0 + (uint64_t)(s * (L0_STAGE >> 4));
+        if (tp::elect_one()) {
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {  // pool position (py, px)
-          const int py = pp >> 1, px = pp & 1;
-          const uint32_t d = tmem_base + (uint32_t)(acc * 128 + pp * 32);
+          for (int pp = 0; pp < 4; ++pp) {  // pool position (py, px)
+            const int py = pp >> 1, px = pp & 1;
+            const uint32_t d = tmem_base + (uint32_t)(acc * 128 + pp * 32);
 #pragma unroll
-          for (int dy = 0; dy < 3; ++dy) {
-            const int o = py + dy;  // input row offset + 1, in 0..3
-            const int box = px * 2 + (o & 1), start = o >> 1;
-            const uint32_t aw = a_addr + box * L0_BOX_BYTES + start * 16 * 32;
-            uint64_t ad = tp::umma_desc(aw, 16, 256, 6);
-            uint64_t bd = tp::umma_desc(bres + dy * 1024, 16, 256, 6);
-            tp::mma_bf16(d, ad, bd, p.idesc, dy != 0);
+            for (int dy = 0; dy < 3; ++dy) {
+              const int o = py + dy;  // input row offset + 1, in 0..3
+              const int box = px * 2 + (o & 1), start = o >> 1;
+              const uint32_t off16 = (box * L0_BOX_BYTES + start * 16 * 32) >> 4;
+              tp::mma_bf16(d, ad0 + off16, b_desc0 + dy * 64, p.idesc, dy != 0);
+            }
           }
+          tp::mma_commit(&empty[s]);
+          tp::mma_commit(&tfull[acc]);
         }
-        tp::mma_commit(&empty[s]);
-        tp::mma_commit(&tfull[acc]);
+        __syncwarp();
         if (++s == S) {
           s = 0;
           ph ^= 1;
@@ -913,7 +928,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int g = (int)(warp - 2) >> 2;
+    const int g = (int)warp >> 2;
     const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
@@ -971,7 +986,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tp::tc_fence_before();
   __syncthreads();
   tp::tc_fence_after();
-  if (warp == 1) tp::tmem_dealloc(tmem_base, 256);
+  if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, 256);
 }
 
 // 2x2/2 max pool, padded NHWC 16-bit -> padded NHWC (interior only), 8 channels/thread.
