@@ -191,6 +191,11 @@ TP_API int tp_render_frames(const int32_t* rects, const uint8_t* colors, const i
                             uint8_t* out, void* stream);
 
 /* 2x2/2 max pool on padded NHWC bf16 (exposed for tests). */
+/* Profiling only (TP_CONV_DEBUG bit 32 set in the environment when the net/conv runs):
+ * per-role cycle totals of conv_tc_kernel summed over CTAs — 0 producer, 1 producer
+ * empty-wait, 2 MMA issuer, 3 issuer accumulator-wait, 4 issuer stage-wait, 5 epilogue
+ * warp 0, 6 epilogue accumulator-wait, 7 launches. No reference counterpart. */
+TP_API int tp_debug_conv_counters(uint64_t* out, int n, int reset);
 TP_API int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype, void* out,
                         void* stream);
 

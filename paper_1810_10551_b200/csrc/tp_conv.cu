@@ -116,6 +116,14 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                : "memory");
 }
 
+// Profiling counters (TP_CONV_DEBUG bit 32): per-role cycle totals summed over CTAs.
+//   0 producer total, 1 producer empty-wait, 2 mma total, 3 mma tempty-wait, 4 mma full-wait,
+//   5 epilogue total (warp 0), 6 epilogue tfull-wait (warp 0), 7 launches
+__device__ unsigned long long g_conv_prof[8];
+#define PROF_T0(v) long long v = (p.dbg & 32) ? clock64() : 0
+#define PROF_ADD(acc, t0) \
+  if (p.dbg & 32) acc += clock64() - (t0)
+
 // Epilogue variants, chosen at compile time.
 enum Epi { EPI_PLAIN = 0, EPI_POOL = 1, EPI_REORG = 2, EPI_F32 = 3 };
 constexpr int kMaxBias = 1024;
@@ -211,6 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= TMA producer =================
       int s = 0;
       uint32_t ph = 0;
+      long long pr_wait = 0;
+      PROF_T0(pr_start);
       const uint32_t tx_bytes = p.a_stage_bytes + p.b_stage_bytes;
       TileIter it;
       it.init(t_begin, p);
@@ -224,7 +234,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = it.mt * 128;
         const int rx = 1 + it.bx * RECT_W, ry = it.img * hp + 1 + it.by * RECT_H * p.sub;
         for (int kb = 0; kb < p.num_kb; ++kb) {
-          tp::mbar_wait(&empty[s], ph ^ 1);
+          PROF_T0(tw);
+          if (p.dbg & 64)
+            tp::mbar_wait_backoff(&empty[s], ph ^ 1, 32);
+          else
+            tp::mbar_wait(&empty[s], ph ^ 1);
+          PROF_ADD(pr_wait, tw);
           uint8_t* a_dst = smA + (size_t)s * p.a_stage_bytes;
           uint8_t* b_dst = smB + (size_t)s * p.b_stage_bytes;
           if (p.dbg & 16) {  // profiling: no TMA, stale operands
@@ -264,6 +279,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.dbg & 32) {
+        atomicAdd(&g_conv_prof[0], (unsigned long long)(clock64() - pr_start));
+        atomicAdd(&g_conv_prof[1], (unsigned long long)pr_wait);
+        if (blockIdx.x == 0) atomicAdd(&g_conv_prof[7], 1ull);
+      }
     }
   } else if (warp == kMmaWarp) {
     {
@@ -285,14 +305,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, sbo, lay);
       const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
       const uint32_t bch = p.bchunk_bytes >> 4;
+      long long w_te = 0, w_fu = 0;
+      PROF_T0(m_start);
       for (int i = 0; i < n_tiles; ++i) {
         const int acc = i & 1;
+        PROF_T0(t1);
         tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        PROF_ADD(w_te, t1);
         aph[acc] ^= 1;
         tp::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.sub * p.bn);
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          PROF_T0(t2);
           tp::mbar_wait(&full[s], ph);
+          PROF_ADD(w_fu, t2);
           tp::tc_fence_after();
           const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
           const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
@@ -332,6 +358,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tp::elect_one()) tp::mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
         __syncwarp();
       }
+      if ((p.dbg & 32) && lane == 0) {
+        atomicAdd(&g_conv_prof[2], (unsigned long long)(clock64() - m_start));
+        atomicAdd(&g_conv_prof[3], (unsigned long long)w_te);
+        atomicAdd(&g_conv_prof[4], (unsigned long long)w_fu);
+      }
     }
   } else {
     // ================= epilogue: two warpgroups, one per TMEM accumulator =================
@@ -348,10 +379,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0;
     TileIter it;
     it.init(t_begin, p);
+    long long e_wait = 0;
+    PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i, it.next(p)) {
       if ((i & 1) != g) continue;
       const int n0 = it.nb * p.bn;
-      tp::mbar_wait(&tfull[g], ph);
+      PROF_T0(t3);
+      if (p.dbg & 64)
+        tp::mbar_wait_backoff(&tfull[g], ph, 128);
+      else
+        tp::mbar_wait(&tfull[g], ph);
+      PROF_ADD(e_wait, t3);
       ph ^= 1;
       tp::tc_fence_after();
       if (p.dbg & 1) {
@@ -507,6 +545,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) tp::mbar_arrive(&tempty[g]);
     }
     if (TSTORE && lane == 0) bulk_wait_all();
+    if ((p.dbg & 32) && warp == 0 && lane == 0) {
+      atomicAdd(&g_conv_prof[5], (unsigned long long)(clock64() - e_start));
+      atomicAdd(&g_conv_prof[6], (unsigned long long)e_wait);
+    }
   }
 
   tp::tc_fence_before();
@@ -989,6 +1031,286 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, 256);
 }
 
+// ------------------------------------------------------------------ full-halo box kernel
+// 3x3 convs whose input channels fit one K block (cin = BK = 32 or 64) and whose weights
+// fit in shared memory (L2 32->64, L4/L6 64->128). One TMA box per output tile holds the
+// tile plus its one-pixel halo; all nine taps are descriptor row offsets into that box
+// (tcgen05 swizzle is computed from absolute smem address bits, so a K-major SW64/SW128
+// operand may start on any 128/64-byte row and the 8-row group pitch may be any row
+// count — tools/swz_shift_test.cu checks this numerically). Versus the FLAT path (A re-read
+// once per tap, B once per tile) this cuts L2->SM fill traffic ~6x, which is what bounds
+// these layers (the chip's L2 delivers ~42 B/clk/SM when every SM streams).
+//   BOX_PLAIN / BOX_POOL: output tile 8 x 16 pixels (M = 128, row m = pixel (m%8, m/8)),
+//     box {BK, 10, 18}; tap (dy,dx) starts at box row dy*10+dx, group pitch 10 rows.
+//     BOX_POOL pools 2x2 in the epilogue (x pair lane^1, y pair lane^8).
+//   BOX_POOLM: M rows are POOLED pixels (8 x 16 pooled = 16 x 32 conv pixels); the four
+//     pool positions accumulate into four TMEM accumulators fed by four stride-2 parity
+//     planes {BK, 9, 17}; the epilogue pools with a per-thread max (no shuffles).
+enum BoxEpi { BOX_PLAIN = 0, BOX_POOL = 1, BOX_POOLM = 2 };
+constexpr int BOX_TW = 8, BOX_TH = 16;
+constexpr int PLANE_W = BOX_TW + 1, PLANE_H = BOX_TH + 1;  // 9 x 17 parity-plane rows
+
+template <int BK, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_box_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const ConvParams p) {
+  constexpr uint32_t RB = BK * 2;  // bytes per pixel row in smem (one swizzle row)
+  constexpr uint32_t LAY = BK == 64 ? 2 : 4;
+  constexpr bool PM = EPI == BOX_POOLM;
+  constexpr int NACC = PM ? 4 : 1;  // accumulators per tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;  // resident weights, 9 tap chunks
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + p.bres_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint64_t* bres_bar = bars + 2 * S + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
+
+  const uint32_t warp = tp::warp_id();
+  const uint32_t lane = tp::lane_id();
+  const int N = p.bn;
+  if (warp == kProdWarp && lane == 0) {
+    tp::tma_prefetch(&tmA);
+    tp::tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      tp::mbar_init(&full[s], 1);
+      tp::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tp::mbar_init(&tfull[a], 1);
+      tp::mbar_init(&tempty[a], 4);
+    }
+    tp::mbar_init(bres_bar, 1);
+    tp::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, p.tmem_cols);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) bias_s[i] = p.bias[i];
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
+  const int hp = p.res + 2;
+  const int per_img = p.tiles_x * p.tiles_y;
+  const int total_tiles = n_img * per_img;
+  const int per_cta = total_tiles / (int)gridDim.x, extra = total_tiles % (int)gridDim.x;
+  const int t_begin = (int)blockIdx.x * per_cta + min((int)blockIdx.x, extra);
+  const int n_tiles = per_cta + ((int)blockIdx.x < extra ? 1 : 0);
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      // ================= TMA producer: one box (or 4 parity planes) per tile =================
+      if (n_tiles > 0) {
+        tp::mbar_arrive_expect_tx(bres_bar, p.bres_bytes);
+        for (int j = 0; j < 9; ++j)
+          tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, j * BK, 0);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      int img = t_begin / per_img, r = t_begin - img * per_img;
+      int by = r / p.tiles_x, bx = r - by * p.tiles_x;
+      for (int i = 0; i < n_tiles; ++i) {
+        tp::mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* dst = smA + (size_t)s * p.a_stage_bytes;
+        // exact box bytes (stages / planes are padded to 1 KB in smem)
+        constexpr uint32_t tx = PM ? 4 * PLANE_W * PLANE_H * RB : (BOX_TW + 2) * (BOX_TH + 2) * RB;
+        tp::mbar_arrive_expect_tx(&full[s], tx);
+        if (PM) {
+          // plane (ey, ex) holds padded input (2*X0 + 1 - ex + 2i, 2*Y0 + 1 - ey + 2j)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int ey = b >> 1, ex = b & 1;
+            tma_load_3d(dst + b * (p.a_stage_bytes >> 2), &tmA, &full[s], 0,
+                        2 * BOX_TW * bx + 1 - ex, img * hp + 2 * BOX_TH * by + 1 - ey);
+          }
+        } else {
+          tma_load_3d(dst, &tmA, &full[s], 0, BOX_TW * bx, img * hp + BOX_TH * by);
+        }
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (++bx == p.tiles_x) {
+          bx = 0;
+          if (++by == p.tiles_y) {
+            by = 0;
+            ++img;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ================= MMA issuer (warp-convergent, one elected lane) =================
+    tp::mbar_wait(bres_bar, 0);
+    constexpr uint32_t pitch = (PM ? PLANE_W : BOX_TW + 2) * RB;  // 8-row group pitch
+    const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, pitch, LAY);
+    const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 8 * RB, LAY);
+    const uint32_t a_step = p.a_stage_bytes >> 4, bch = p.bchunk_bytes >> 4;
+    const uint32_t plane16 = (p.a_stage_bytes >> 2) >> 4;
+    const uint32_t idesc = p.idesc;
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t aph[2] = {0, 0};
+    for (int i = 0; i < n_tiles; ++i) {
+      const int acc = i & 1;
+      tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+      aph[acc] ^= 1;
+      tp::mbar_wait(&full[s], ph);
+      tp::tc_fence_after();
+      const uint64_t ad = a_desc0 + (uint64_t)(s * a_step);
+      const uint32_t d0 = tmem_base + (uint32_t)(acc * NACC * N);
+      if (tp::elect_one() && (p.dbg & 2) == 0) {
+#pragma unroll
+        for (int pp = 0; pp < NACC; ++pp) {
+          const uint32_t d = d0 + (uint32_t)(pp * N);
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const int dy = tap / 3, dx = tap % 3;
+            uint32_t off;
+            if (PM) {
+              const int sy = (pp >> 1) + dy, sx = (pp & 1) + dx;
+              const int plane = ((sy + 1) & 1) * 2 + ((sx + 1) & 1);
+              off = plane * plane16 + (((sy >> 1) * PLANE_W + (sx >> 1)) * RB >> 4);
+            } else {
+              off = (dy * (BOX_TW + 2) + dx) * RB >> 4;
+            }
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tp::mma_bf16(d, ad + off + 2 * k, b_desc0 + tap * bch + 2 * k, idesc,
+                           (tap | k) != 0);
+          }
+        }
+      }
+      if (tp::elect_one()) {
+        tp::mma_commit(&empty[s]);
+        tp::mma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+      if (++s == S) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else {
+    // ================= epilogue: two warpgroups alternate accumulators =================
+    const int g = (int)warp >> 2;
+    const uint32_t q = warp & 3;
+    const int row = (int)(q * 32 + lane);
+    const bool f16 = p.f16 != 0;
+    const bool leaky = p.leaky != 0;
+    const int ores = PM || EPI == BOX_POOL ? p.res >> 1 : p.res;
+    const int owp = ores + 2, oimg = owp * owp;
+    const int nchunks = N >> 4;
+    uint32_t ph = 0;
+    int img = t_begin / per_img, r = t_begin - img * per_img;
+    int by = r / p.tiles_x, bx = r - by * p.tiles_x;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int timg = img, tby = by, tbx = bx;
+      if (++bx == p.tiles_x) {
+        bx = 0;
+        if (++by == p.tiles_y) {
+          by = 0;
+          ++img;
+        }
+      }
+      if ((i & 1) != g) continue;
+      tp::mbar_wait(&tfull[g], ph);
+      ph ^= 1;
+      tp::tc_fence_after();
+      if (p.dbg & 1) {
+        tp::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tp::mbar_arrive(&tempty[g]);
+        continue;
+      }
+      // this thread's pixel (conv output, or pooled output for POOLM)
+      const int x = tbx * BOX_TW + (row & 7), y = tby * BOX_TH + (row >> 3);
+      bool store;
+      int opx;
+      if (EPI == BOX_POOL) {
+        store = y < p.res && ((x | y) & 1) == 0;
+        opx = timg * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
+      } else {
+        store = y < ores;
+        opx = timg * oimg + (y + 1) * owp + (x + 1);
+      }
+      __nv_bfloat16* o =
+          reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)opx * p.out_cstride + p.out_coff;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * NACC * N);
+      for (int c = 0; c < nchunks; ++c) {
+        float f[16];
+        if (PM) {
+          uint32_t v0[16], v1[16], v2[16], v3[16];
+          tp::tmem_ld16(t_row + c * 16, v0);
+          tp::tmem_ld16(t_row + N + c * 16, v1);
+          tp::tmem_ld16(t_row + 2 * N + c * 16, v2);
+          tp::tmem_ld16(t_row + 3 * N + c * 16, v3);
+          tp::tmem_ld_wait();
+          // bias + leaky are monotonic, so pooling first gives the same value
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            f[j] = fmaxf(fmaxf(__uint_as_float(v0[j]), __uint_as_float(v1[j])),
+                         fmaxf(__uint_as_float(v2[j]), __uint_as_float(v3[j])));
+        } else {
+          uint32_t v[16];
+          tp::tmem_ld16(t_row + c * 16, v);
+          tp::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+        }
+        const float4* b4 = reinterpret_cast<const float4*>(bias_s + c * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 bb = b4[j];
+          f[4 * j + 0] += bb.x;
+          f[4 * j + 1] += bb.y;
+          f[4 * j + 2] += bb.z;
+          f[4 * j + 3] += bb.w;
+        }
+        if (leaky) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
+        }
+        if (EPI == BOX_POOL) {  // x pair = lane^1, y pair = lane^8
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 8));
+        }
+        if (!store || c * 16 >= p.cout || (p.dbg & 4)) continue;
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (f16) {
+            __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          } else {
+            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+        }
+        *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      tp::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tp::mbar_arrive(&tempty[g]);
+    }
+  }
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, p.tmem_cols);
+}
+
 // 2x2/2 max pool, padded NHWC 16-bit -> padded NHWC (interior only), 8 channels/thread.
 __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img, int res,
                                 int cstride, __nv_bfloat16* __restrict__ out,
@@ -1106,6 +1428,8 @@ struct ConvLaunch {
   int mode;
   int pair;  // CTA-pair (cta_group::2) kernel
   int l0;    // layer-0 pool-in-M kernel
+  int box;   // full-halo box kernel: 0 off, else 1 + BoxEpi
+  int box_bk;
   CUtensorMap tmA, tmB, tmC;
   ConvParams p;
   size_t smem;
@@ -1288,10 +1612,86 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     p.stages = st;
     L->smem = 1024 + (size_t)st * sb + p.stage_bytes + (2 * st + 6) * 8 + cout_pad * 4 + 16;
   }
+  // full-halo box kernel (TP_BOX=0 disables it): 3x3, one K block, resident weights
+  const char* be = getenv("TP_BOX");
+  const bool box_ok = ksize == 3 && (cin_used == 32 || cin_used == 64) && cout_pad <= 256 &&
+                      cout == cout_pad && !reorg && !out_fp32 && res % 8 == 0 &&
+                      bres <= 160 * 1024 && (be == nullptr || atoi(be) != 0);
+  if (box_ok) {
+    // pool-in-M: 4 pool accumulators x 2 buffers must fit TMEM; pooled side in 8-px tiles
+    const bool pm = pool && cout_pad <= 64 && (res / 2) % 8 == 0;
+    const int epi = pm ? BOX_POOLM : pool ? BOX_POOL : BOX_PLAIN;
+    const uint32_t rb = (uint32_t)bk * 2;
+    const uint32_t stage = pm ? 4 * ((PLANE_W * PLANE_H * rb + 1023) & ~1023u)
+                              : ((BOX_TW + 2) * (BOX_TH + 2) * rb + 1023) & ~1023u;
+    const int bfixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
+    int st = (int)((227 * 1024 - bfixed - (int)bres) / (int)stage);
+    if (st > 8) st = 8;
+    const uint32_t need = 2u * (pm ? 4u : 1u) * (uint32_t)cout_pad;
+    uint32_t cols = 32;
+    while (cols < need) cols <<= 1;
+    if (st >= 2 && cols <= 512) {
+      if (pm) {
+        const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
+        const uint32_t box[3] = {(uint32_t)bk, 2 * PLANE_W, 2 * PLANE_H};
+        const uint32_t estr[3] = {1, 2, 2};
+        rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16, 2, estr);
+      } else {
+        const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
+        const uint32_t box[3] = {(uint32_t)bk, BOX_TW + 2, BOX_TH + 2};
+        rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16);
+      }
+      if (rc) return rc;
+      {
+        const uint64_t dims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+        const uint32_t box[2] = {(uint32_t)bk, (uint32_t)cout_pad};
+        rc = make_tmap(&L->tmB, weight, 2, dims, box, swz, f16);
+        if (rc) return rc;
+      }
+      p.bn = cout_pad;
+      p.n_blocks_n = 1;
+      p.a_stage_bytes = stage;
+      p.b_stage_bytes = 0;
+      p.bchunk_bytes = cout_pad * rb;
+      p.n_bchunks = 9;
+      p.bres_bytes = (uint32_t)bres;
+      p.stage_bytes = 0;
+      p.sub = 1;
+      p.rect = 0;
+      p.tiles_x = (pm ? res / 2 : res) / BOX_TW;
+      p.tiles_y = ((pm ? res / 2 : res) + BOX_TH - 1) / BOX_TH;
+      p.idesc = tp::idesc_f16kind(128, (uint32_t)cout_pad, !f16);
+      p.tmem_cols = cols;
+      p.stages = st;
+      L->box = 1 + epi;
+      L->box_bk = bk;
+      L->pair = 0;
+      L->smem = 1024 + (size_t)st * stage + bres + (2 * st + 6) * 8 + cout_pad * 4 + 16;
+    }
+  }
   if (cout_pad > kMaxBias) {
     tp_set_error("conv: cout_pad %d exceeds %d", cout_pad, kMaxBias);
     return TP_ERR_UNSUPPORTED;
   }
+  return TP_OK;
+}
+
+template <int BK, int EPI>
+int launch_box(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_box_kernel<BK, EPI>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  ConvParams p = L.p;
+  p.n_img = n_img;
+  p.n_img_dev = n_img_dev;
+  const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y;
+  if (tiles == 0) return TP_OK;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  conv_box_kernel<BK, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+  TP_LAUNCH_CHECK();
   return TP_OK;
 }
 
@@ -1351,6 +1751,16 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
   if (n_img > L.p.n_img) {
     tp_set_error("conv: n_img %d exceeds planned %d", n_img, L.p.n_img);
     return TP_ERR_CAPACITY;
+  }
+  if (L.box) {
+    const int epi = L.box - 1;
+    if (L.box_bk == 64)
+      return epi == BOX_POOLM ? launch_box<64, BOX_POOLM>(L, n_img, n_img_dev, st)
+             : epi == BOX_POOL ? launch_box<64, BOX_POOL>(L, n_img, n_img_dev, st)
+                               : launch_box<64, BOX_PLAIN>(L, n_img, n_img_dev, st);
+    return epi == BOX_POOLM ? launch_box<32, BOX_POOLM>(L, n_img, n_img_dev, st)
+           : epi == BOX_POOL ? launch_box<32, BOX_POOL>(L, n_img, n_img_dev, st)
+                             : launch_box<32, BOX_PLAIN>(L, n_img, n_img_dev, st);
   }
   if (L.pair)
     return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
@@ -1580,6 +1990,26 @@ extern "C" int tp_conv(const void* in, int n_img, int res, int cin_stride, const
                         ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg, dtype, pool);
   if (rc) return rc;
   return run_conv(L, n_img, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int tp_debug_conv_counters(uint64_t* out, int n, int reset) {
+  unsigned long long h[8] = {0};
+  if (n > 8) n = 8;
+  if (out != nullptr && n > 0) {
+    if (cudaMemcpyFromSymbol(h, g_conv_prof, sizeof(h)) != cudaSuccess) {
+      tp_set_error("tp_debug_conv_counters: copy failed");
+      return -1;
+    }
+    for (int i = 0; i < n; ++i) out[i] = h[i];
+  }
+  if (reset) {
+    unsigned long long z[8] = {0};
+    if (cudaMemcpyToSymbol(g_conv_prof, z, sizeof(z)) != cudaSuccess) {
+      tp_set_error("tp_debug_conv_counters: reset failed");
+      return -1;
+    }
+  }
+  return 0;
 }
 
 extern "C" int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype,

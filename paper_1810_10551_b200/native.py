@@ -96,6 +96,7 @@ SIGNATURES = {
     "tp_collect_final": (_I, [_P, _P, _I, _P, _P, _I, _P, _P, _I, _P]),
     "tp_postprocess": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "tp_maxpool2": (_I, [_P, _I, _I, _I, _I, _P, _P]),
+    "tp_debug_conv_counters": (_I, [_P, _I, _I]),
     "tp_render_frames": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_uint32, _P, _P]),
 }
 

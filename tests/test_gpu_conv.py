@@ -157,3 +157,27 @@ def test_maxpool(cuda):
     torch.cuda.synchronize()
     ref = torch.nn.functional.max_pool2d(x[:, 1:-1, 1:-1, :].float().permute(0, 3, 1, 2), 2)
     assert torch.equal(out[:, 1:-1, 1:-1, :].float(), ref.permute(0, 2, 3, 1))
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize(
+    "cin,cout,res,pool",
+    [(32, 64, 16, False), (64, 128, 24, False), (64, 128, 152, False), (32, 32, 40, False),
+     (64, 128, 48, True), (64, 128, 152, True), (64, 256, 16, True),
+     (32, 64, 32, True), (32, 64, 48, True), (64, 64, 32, True), (32, 64, 304, True)],
+)
+def test_conv_box_kernel(cuda, cin, cout, res, pool, dtype, monkeypatch):
+    """Full-halo box kernel (one TMA box per 8x16 tile, taps as descriptor row offsets):
+    plain, shuffle-pooled and pool-in-M (parity planes) epilogues, several images, partial
+    last tile rows; must agree with torch and with the FLAT / RECT kernels (TP_BOX=0)."""
+    torch = cuda
+    n = 1 if res >= 152 else 3
+    x = _padded_input(torch, n, res, cin, seed=res + cin, dtype=dtype)
+    out, ref = _run_conv(torch, x, res, cin, cout, cout, 3, leaky=True, dtype=dtype, pool=pool)
+    _check(torch, out[:, 1:-1, 1:-1, :], ref, rel=2e-2 if dtype == "bf16" else 3e-3)
+    assert out[:, 0].abs().max().item() == 0 and out[:, :, -1].abs().max().item() == 0
+    assert out[:, -1].abs().max().item() == 0 and out[:, :, 0].abs().max().item() == 0
+    monkeypatch.setenv("TP_BOX", "0")
+    out0, _ = _run_conv(torch, x, res, cin, cout, cout, 3, leaky=True, dtype=dtype, pool=pool)
+    # same fp32 accumulation order is not guaranteed across kernels: compare loosely
+    _check(torch, out, out0.float(), rel=1e-2 if dtype == "bf16" else 2e-3)

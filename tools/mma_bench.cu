@@ -53,6 +53,27 @@ __global__ void mma_loop(int n_mma, uint32_t n, long long* out, int mode) {
               tp::mma_bf16(tmem + j * n, a64 + (((i / 12) & 1) * 18432 + (j * 8 + dy) * 1024) / 16 + 2 * k,
                            b64 + (dy * 4096) / 16 + 2 * k, idesc, 1);
       }
+    } else if (mode >= 30) {  // no-swizzle K-major, 9 taps as 16-B-shifted start addresses (30) / fixed (31)
+      // A: [k-block of 8 ch][180 px][16 B], rows = pixels; M=128 = 16 rows x 8 px; SBO 160 B
+      const uint32_t plane = 180 * 16;
+      uint64_t an = tp::umma_desc(a, plane, 160, 0), bn = tp::umma_desc(b + 40960, 128 * 16 * 2, 128, 0);
+      if (mode == 32) {  // canonical interleaved: K-adjacent cores contiguous (LBO 128), 8-row groups 256 B apart
+        an = tp::umma_desc(a, 128, 256, 0);
+        bn = tp::umma_desc(b + 40960, 128, 256, 0);
+      } else if (mode == 33) {  // swapped roles
+        an = tp::umma_desc(a, 256, 128, 0);
+        bn = tp::umma_desc(b + 40960, 256, 128, 0);
+      } else if (mode == 34) {  // swapped plane layout
+        an = tp::umma_desc(a, 160, plane, 0);
+        bn = tp::umma_desc(b + 40960, 128, 128 * 16 * 2, 0);
+      }
+      for (int i = 0; i < n_mma; i += 9) {
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          const uint32_t off = mode == 30 ? ((t / 3) * 160 + (t % 3) * 16) >> 4 : 0;
+          tp::mma_bf16(tmem, an + off, bn, idesc, 1);
+        }
+      }
     } else if (mode >= 20) {  // warp-convergent; one elect per 12-MMA group (20), + commit (21), + wait (22); 23: one elect for all
       if (mode == 23) {
         if (tp::elect_one()) {
@@ -123,9 +144,9 @@ int main() {
   cudaFuncSetAttribute(mma_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
   const int n_mma = 4096;
   cudaFuncSetAttribute(mma_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
-  for (int mode : {2, 4, 5, 20, 21, 22, 23})
+  for (int mode : {31, 32, 33, 34})
   for (uint32_t n : {32u, 64u, 128u, 256u}) {
-    if (n != 64 && n != 128) continue;
+    
     for (int grid : {148}) {
       mma_loop<<<grid, 128, 120 * 1024>>>(n_mma, n, d, mode);
       cudaDeviceSynchronize();
