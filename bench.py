@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--resample", default="nearest", choices=["nearest", "bilinear"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="torch.profiler kernel table of the timed steps to stderr (not a bench run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--frame", default="4k", choices=sorted(FRAMES))
     ap.add_argument("--preset", default=PRESET)
@@ -65,6 +67,27 @@ def parse():
     global W, H
     W, H = FRAMES[args.frame]
     return args
+
+
+def kernel_table(prof, ms: float, steps: int) -> None:
+    """Per-kernel device time over the timed steps (warm, real overlap), to stderr."""
+    agg: dict[str, list] = {}
+    for ev in prof.events():
+        if ev.device_type != torch_device_type_cuda():
+            continue
+        name = ev.name.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0]
+        a = agg.setdefault(name, [0.0, 0])
+        a[0] += ev.time_range.elapsed_us() / 1e3
+        a[1] += 1
+    busy = sum(v[0] for v in agg.values())
+    print(f"# kernel table: {steps} steps, {ms:.3f} ms wall (device), {busy:.3f} ms kernel busy", file=sys.stderr)
+    for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        print(f"{100 * t / ms:6.2f}% {t / steps:9.3f} ms/step {n // steps:5d}/step  {k}", file=sys.stderr)
+
+
+def torch_device_type_cuda():
+    import torch
+    return torch.autograd.DeviceType.CUDA
 
 
 def clip_objects(rank: int = 0, n_frames: int = 300):
@@ -256,6 +279,10 @@ def main():
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = None
+    if args.profile:  # CUPTI kernel table to stderr; the JSON value of such a run is not a bench number
+        prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
+        prof.__enter__()
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         t0.record(stream)
@@ -264,6 +291,9 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
+    if prof is not None:
+        prof.__exit__(None, None, None)
+        kernel_table(prof, ms, args.steps)
     if world > 1:
         mt = torch.tensor([ms], device="cuda")
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)

@@ -72,6 +72,7 @@ struct ConvParams {
   uint32_t bres_bytes, bchunk_bytes;
   int n_bchunks;
   uint32_t stage_bytes;  // epilogue store staging (TMA-store variants): 8 warps x 2 KB
+  int nbuf;  // box kernel: TMEM accumulator buffers (2 or 4)
   int dbg;  // profiling only (TP_CONV_DEBUG): 1 = skip epilogue math/stores, 2 = skip MMAs
 };
 
@@ -98,6 +99,14 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_
       "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
           reinterpret_cast<uint64_t>(tmap)),
       "r"(tp::smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const void* tmap, const void* smem_src, int32_t c0,
+                                             int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(tp::smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 __device__ __forceinline__ void bulk_commit() {
@@ -1053,29 +1062,34 @@ constexpr int PLANE_W = BOX_TW + 1, PLANE_H = BOX_TH + 1;  // 9 x 17 parity-plan
 template <int BK, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_box_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const ConvParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
   constexpr uint32_t RB = BK * 2;  // bytes per pixel row in smem (one swizzle row)
   constexpr uint32_t LAY = BK == 64 ? 2 : 4;
   constexpr bool PM = EPI == BOX_POOLM;
   constexpr int NACC = PM ? 4 : 1;  // accumulators per tile
+  // plain outputs leave through per-warp SW64 staging slabs + TMA bulk stores (coalesced);
+  // scattered 16-byte stores at a 256-byte pixel pitch were LSU-bound
+  constexpr bool TSTORE = EPI == BOX_PLAIN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int S = p.stages;
   uint8_t* smA = smem;
   uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;  // resident weights, 9 tap chunks
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + p.bres_bytes);
+  uint8_t* smC = smB + p.bres_bytes;  // 1024-aligned: 8 warps x 2 KB staging (TSTORE)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smC + p.stage_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = bars + 2 * S + 2;
-  uint64_t* bres_bar = bars + 2 * S + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
-  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
+  uint64_t* tfull = bars + 2 * S;   // one per accumulator buffer (<= 4)
+  uint64_t* tempty = bars + 2 * S + 4;
+  uint64_t* bres_bar = bars + 2 * S + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 10);
 
   const uint32_t warp = tp::warp_id();
   const uint32_t lane = tp::lane_id();
   const int N = p.bn;
+  const int NB = p.nbuf;  // accumulator buffers: MMA runs up to NB-1 tiles ahead of epilogues
   if (warp == kProdWarp && lane == 0) {
     tp::tma_prefetch(&tmA);
     tp::tma_prefetch(&tmB);
@@ -1083,7 +1097,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::mbar_init(&full[s], 1);
       tp::mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 4; ++a) {
       tp::mbar_init(&tfull[a], 1);
       tp::mbar_init(&tempty[a], 4);
     }
@@ -1117,8 +1131,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       int img = t_begin / per_img, r = t_begin - img * per_img;
       int by = r / p.tiles_x, bx = r - by * p.tiles_x;
+      long long pr_wait = 0;
+      PROF_T0(pr_start);
       for (int i = 0; i < n_tiles; ++i) {
+        PROF_T0(tw);
         tp::mbar_wait(&empty[s], ph ^ 1);
+        PROF_ADD(pr_wait, tw);
         uint8_t* dst = smA + (size_t)s * p.a_stage_bytes;
         // exact box bytes (stages / planes are padded to 1 KB in smem)
         constexpr uint32_t tx = PM ? 4 * PLANE_W * PLANE_H * RB : (BOX_TW + 2) * (BOX_TH + 2) * RB;
@@ -1146,6 +1164,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.dbg & 32) {
+        atomicAdd(&g_conv_prof[0], (unsigned long long)(clock64() - pr_start));
+        atomicAdd(&g_conv_prof[1], (unsigned long long)pr_wait);
+        if (blockIdx.x == 0) atomicAdd(&g_conv_prof[7], 1ull);
+      }
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer (warp-convergent, one elected lane) =================
@@ -1158,12 +1181,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idesc = p.idesc;
     int s = 0;
     uint32_t ph = 0;
-    uint32_t aph[2] = {0, 0};
+    uint32_t aph = 0;  // phase bit per accumulator buffer
+    long long w_te = 0, w_fu = 0;
+    PROF_T0(m_start);
     for (int i = 0; i < n_tiles; ++i) {
-      const int acc = i & 1;
-      tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
-      aph[acc] ^= 1;
+      const int acc = i & (NB - 1);
+      PROF_T0(t1);
+      tp::mbar_wait(&tempty[acc], ((aph >> acc) & 1) ^ 1);
+      PROF_ADD(w_te, t1);
+      aph ^= 1u << acc;
+      PROF_T0(t2);
       tp::mbar_wait(&full[s], ph);
+      PROF_ADD(w_fu, t2);
       tp::tc_fence_after();
       const uint64_t ad = a_desc0 + (uint64_t)(s * a_step);
       const uint32_t d0 = tmem_base + (uint32_t)(acc * NACC * N);
@@ -1199,6 +1228,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ph ^= 1;
       }
     }
+    if ((p.dbg & 32) && lane == 0) {
+      atomicAdd(&g_conv_prof[2], (unsigned long long)(clock64() - m_start));
+      atomicAdd(&g_conv_prof[3], (unsigned long long)w_te);
+      atomicAdd(&g_conv_prof[4], (unsigned long long)w_fu);
+    }
   } else {
     // ================= epilogue: two warpgroups alternate accumulators =================
     const int g = (int)warp >> 2;
@@ -1209,9 +1243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ores = PM || EPI == BOX_POOL ? p.res >> 1 : p.res;
     const int owp = ores + 2, oimg = owp * owp;
     const int nchunks = N >> 4;
-    uint32_t ph = 0;
+    uint32_t ph = 0;  // phase bit per accumulator buffer
     int img = t_begin / per_img, r = t_begin - img * per_img;
     int by = r / p.tiles_x, bx = r - by * p.tiles_x;
+    long long e_wait = 0;
+    PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
       const int timg = img, tby = by, tbx = bx;
       if (++bx == p.tiles_x) {
@@ -1222,21 +1258,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if ((i & 1) != g) continue;
-      tp::mbar_wait(&tfull[g], ph);
-      ph ^= 1;
+      const int acc = i & (NB - 1);
+      PROF_T0(t3);
+      tp::mbar_wait(&tfull[acc], (ph >> acc) & 1);
+      PROF_ADD(e_wait, t3);
+      ph ^= 1u << acc;
       tp::tc_fence_after();
       if (p.dbg & 1) {
         tp::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tp::mbar_arrive(&tempty[g]);
+        if (lane == 0) tp::mbar_arrive(&tempty[acc]);
         continue;
       }
       // this thread's pixel (conv output, or pooled output for POOLM)
       const int x = tbx * BOX_TW + (row & 7), y = tby * BOX_TH + (row >> 3);
       bool store;
       int opx;
-      if (EPI == BOX_POOL) {
-        store = y < p.res && ((x | y) & 1) == 0;
+      if (EPI == BOX_POOL) {  // both lanes of an x pair store (8 channels each)
+        store = y < p.res && (y & 1) == 0;
         opx = timg * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
       } else {
         store = y < ores;
@@ -1244,27 +1283,83 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __nv_bfloat16* o =
           reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)opx * p.out_cstride + p.out_coff;
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * NACC * N);
+      // TSTORE: this warp's 32 pixels are 4 full rows of 8 (res % 4 == 0), all valid or not
+      const bool warp_rows_valid = tby * BOX_TH + (int)q * 4 < p.res;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * NACC * N);
+      // TMEM loads are software-pipelined: chunk c+1 is in flight while chunk c is
+      // converted and stored (its registers are copied out before the next load).
+      uint32_t v0[16], v1[16], v2[16], v3[16];
+      tp::tmem_ld16(t_row, v0);
+      if (PM) {
+        tp::tmem_ld16(t_row + N, v1);
+        tp::tmem_ld16(t_row + 2 * N, v2);
+        tp::tmem_ld16(t_row + 3 * N, v3);
+      }
       for (int c = 0; c < nchunks; ++c) {
         float f[16];
+        tp::tmem_ld_wait();
         if (PM) {
-          uint32_t v0[16], v1[16], v2[16], v3[16];
-          tp::tmem_ld16(t_row + c * 16, v0);
-          tp::tmem_ld16(t_row + N + c * 16, v1);
-          tp::tmem_ld16(t_row + 2 * N + c * 16, v2);
-          tp::tmem_ld16(t_row + 3 * N + c * 16, v3);
-          tp::tmem_ld_wait();
           // bias + leaky are monotonic, so pooling first gives the same value
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             f[j] = fmaxf(fmaxf(__uint_as_float(v0[j]), __uint_as_float(v1[j])),
                          fmaxf(__uint_as_float(v2[j]), __uint_as_float(v3[j])));
         } else {
-          uint32_t v[16];
-          tp::tmem_ld16(t_row + c * 16, v);
-          tp::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v0[j]);
+        }
+        if (c + 1 < nchunks) {
+          const uint32_t tc = t_row + (uint32_t)((c + 1) * 16);
+          tp::tmem_ld16(tc, v0);
+          if (PM) {
+            tp::tmem_ld16(tc + N, v1);
+            tp::tmem_ld16(tc + 2 * N, v2);
+            tp::tmem_ld16(tc + 3 * N, v3);
+          }
+        }
+        if (EPI == BOX_POOL) {
+          // 2x2 pool BEFORE bias + leaky (both monotonic: same value). After the x-pair
+          // exchange (lane^1) the even lane keeps channels 0-7 and the odd lane 8-15, so
+          // the y exchange (lane^8), bias, leaky, pack and store handle 8 values per lane.
+          const bool odd = (lane & 1) != 0;
+          float h8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float send = odd ? f[j] : f[j + 8];
+            const float mine = odd ? f[j + 8] : f[j];
+            h8[j] = fmaxf(mine, __shfl_xor_sync(0xffffffffu, send, 1));
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) h8[j] = fmaxf(h8[j], __shfl_xor_sync(0xffffffffu, h8[j], 8));
+          const int ch = c * 16 + (odd ? 8 : 0);
+          const float4 b0 = *reinterpret_cast<const float4*>(bias_s + ch);
+          const float4 b1 = *reinterpret_cast<const float4*>(bias_s + ch + 4);
+          h8[0] += b0.x;
+          h8[1] += b0.y;
+          h8[2] += b0.z;
+          h8[3] += b0.w;
+          h8[4] += b1.x;
+          h8[5] += b1.y;
+          h8[6] += b1.z;
+          h8[7] += b1.w;
+          if (leaky) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h8[j] = fmaxf(h8[j], 0.1f * h8[j]);
+          }
+          if (!store || ch >= p.cout || (p.dbg & 4)) continue;
+          uint32_t pk[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (f16) {
+              __half2 h = __floats2half2_rn(h8[2 * j], h8[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(h8[2 * j], h8[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+          *reinterpret_cast<uint4*>(o + ch) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          continue;
         }
         const float4* b4 = reinterpret_cast<const float4*>(bias_s + c * 16);
 #pragma unroll
@@ -1279,11 +1374,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
         }
-        if (EPI == BOX_POOL) {  // x pair = lane^1, y pair = lane^8
+        if (TSTORE) {
+          if (!warp_rows_valid) continue;
+          const int cs = c & 1;
+          const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
+          if (cs == 0) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+          }
+          uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
-#pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 8));
+          for (int j = 0; j < 8; ++j) {
+            if (f16) {
+              __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+          const uint32_t rbase = buf + lane * 64, swz = (lane >> 1) & 3;
+          st_shared_v4(rbase + (((2 * cs) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
+          st_shared_v4(rbase + (((2 * cs + 1) ^ swz) << 4), pk[4], pk[5], pk[6], pk[7]);
+          if (cs == 1) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && (p.dbg & 4) == 0) {
+              tma_store_3d(&tmC, smC + warp * 2048, p.out_coff + (c - 1) * 16, tbx * BOX_TW + 1,
+                           timg * owp + tby * BOX_TH + (int)q * 4 + 1);
+              bulk_commit();
+            }
+          }
+          continue;
         }
         if (!store || c * 16 >= p.cout || (p.dbg & 4)) continue;
         uint32_t pk[8];
@@ -1302,7 +1424,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tp::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tp::mbar_arrive(&tempty[g]);
+      if (lane == 0) tp::mbar_arrive(&tempty[acc]);
+    }
+    if (TSTORE && lane == 0) bulk_wait_all();
+    if ((p.dbg & 32) && warp == 0 && lane == 0) {
+      atomicAdd(&g_conv_prof[5], (unsigned long long)(clock64() - e_start));
+      atomicAdd(&g_conv_prof[6], (unsigned long long)e_wait);
     }
   }
   tp::tc_fence_before();
@@ -1624,10 +1751,13 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     const uint32_t rb = (uint32_t)bk * 2;
     const uint32_t stage = pm ? 4 * ((PLANE_W * PLANE_H * rb + 1023) & ~1023u)
                               : ((BOX_TW + 2) * (BOX_TH + 2) * rb + 1023) & ~1023u;
-    const int bfixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
+    const uint32_t staging = (!pool && res % 4 == 0) ? 8 * 2048 : 0;  // TMA-store slabs
+    const int bfixed = 1024 + cout_pad * 4 + (2 * 8 + 10) * 8 + 16 + (int)staging;
     int st = (int)((227 * 1024 - bfixed - (int)bres) / (int)stage);
     if (st > 8) st = 8;
-    const uint32_t need = 2u * (pm ? 4u : 1u) * (uint32_t)cout_pad;
+    const uint32_t per_tile = (pm ? 4u : 1u) * (uint32_t)cout_pad;  // TMEM columns per tile
+    const int nbuf = per_tile <= 128 ? 4 : 2;
+    const uint32_t need = (uint32_t)nbuf * per_tile;
     uint32_t cols = 32;
     while (cols < need) cols <<= 1;
     if (st >= 2 && cols <= 512) {
@@ -1655,18 +1785,25 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       p.bchunk_bytes = cout_pad * rb;
       p.n_bchunks = 9;
       p.bres_bytes = (uint32_t)bres;
-      p.stage_bytes = 0;
+      p.stage_bytes = staging;
       p.sub = 1;
       p.rect = 0;
       p.tiles_x = (pm ? res / 2 : res) / BOX_TW;
       p.tiles_y = ((pm ? res / 2 : res) + BOX_TH - 1) / BOX_TH;
       p.idesc = tp::idesc_f16kind(128, (uint32_t)cout_pad, !f16);
       p.tmem_cols = cols;
+      p.nbuf = nbuf;
       p.stages = st;
       L->box = 1 + epi;
       L->box_bk = bk;
       L->pair = 0;
-      L->smem = 1024 + (size_t)st * stage + bres + (2 * st + 6) * 8 + cout_pad * 4 + 16;
+      if (staging) {  // output store map {cstride, wp, rows}, box {32 ch, 8 px, 4 rows}
+        const uint64_t dims[3] = {(uint64_t)out_cstride, (uint64_t)wp, (uint64_t)max_img * wp};
+        const uint32_t box[3] = {32, BOX_TW, 4};
+        rc = make_tmap(&L->tmC, out, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_64B, f16);
+        if (rc) return rc;
+      }
+      L->smem = 1024 + (size_t)st * stage + bres + staging + (2 * st + 10) * 8 + cout_pad * 4 + 16;
     }
   }
   if (cout_pad > kMaxBias) {
@@ -1690,7 +1827,7 @@ int launch_box(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStr
   const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y;
   if (tiles == 0) return TP_OK;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_box_kernel<BK, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+  conv_box_kernel<BK, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }

@@ -6,11 +6,13 @@
 // north-star downscale: 8-bit fixed-point weights, half-pixel centres, identical
 // integer arithmetic to oracle/resample_ref.py so it is bit-exact as well.
 //
-// One CTA per (tile, output row). Each thread produces whole pixels: 3 bytes of the
-// u8 tile and/or the 32-byte horizontally expanded layer-0 input pixel
-// ([tile][610][610][16] = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000], fp16/bf16),
-// so every activation store is two full, aligned 16-byte vector stores. Source reads are row-local (one or two source rows per CTA), which
-// keeps them L1/L2-resident; the kernel is HBM-bound on the tile writes.
+// One CTA per (tile, 8 output rows); a warp task is 32 consecutive columns of one row
+// (608 = 19 x 32, so a warp never straddles rows). Each lane produces one pixel: 3 bytes
+// of the u8 tile and/or the 32-byte horizontally expanded layer-0 input pixel
+// ([tile][610][610][16] = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000], fp16/bf16), so
+// every activation store is two full, aligned 16-byte vector stores and a warp writes 1 KB
+// contiguous. Index math is 32-bit (divisions by the constant 608 / 1216 become
+// multiply-highs); the value/255 table is built once per CTA. HBM-bound on the writes.
 #include "tp_common.cuh"
 #include "../../include/tilepipe_b200.h"
 
@@ -27,7 +29,8 @@ __device__ __forceinline__ Tap bilinear_tap(int u, int side) {
   // source centre = (u + 0.5) * side / 608 - 0.5 ; fixed point with 8 fraction bits
   int num = (2 * u + 1) * side - S;  // = 1216 * centre
   if (num < 0) num = 0;
-  int s256 = (int)(((long long)num * 256) / (2 * S));
+  // num * 256 < 2^32 for side <= 13000: unsigned 32-bit division by a constant
+  const int s256 = (int)(((uint32_t)num * 256u) / (uint32_t)(2 * S));
   Tap t;
   t.i0 = s256 >> 8;
   t.f = s256 & 255;
@@ -47,6 +50,9 @@ __device__ __forceinline__ void load_px(const uint8_t* __restrict__ frame, int H
   }
 }
 
+constexpr int GATHER_ROWS = 8;  // output rows per CTA
+constexpr int SEGS = S / 32;      // 19 warp tasks per row
+
 __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ frames,
                                                      int64_t frame_stride, int H, int W,
                                                      const tp_tile_job_t* __restrict__ jobs,
@@ -54,46 +60,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      int mode, uint8_t* __restrict__ out_u8,
                                                      __nv_bfloat16* __restrict__ out_act,
                                                      int act_f16) {
-  const int v = blockIdx.x;  // output row
   const int t = blockIdx.y;  // tile
   if (n_jobs_dev != nullptr && t >= *n_jobs_dev) return;
   const tp_tile_job_t job = jobs[t];
   const uint8_t* frame = frames + (int64_t)job.frame * frame_stride;
   const int side = job.side;
 
-  int sy0, sy1 = 0, fy = 0;
-  if (mode == TP_RESAMPLE_NEAREST) {
-    sy0 = job.y + (int)(((long long)v * side) / S);
-  } else {
-    Tap ty = bilinear_tap(v, side);
-    sy0 = job.y + ty.i0;
-    sy1 = job.y + ty.i1;
-    fy = ty.f;
-  }
-
-  // RGB of tile column u on this output row (zero outside [0, 608) and outside the frame)
-  auto sample = [&](int u, int& r, int& g, int& b) {
-    if (u < 0 || u >= S) {
-      r = g = b = 0;
-      return;
-    }
-    if (mode == TP_RESAMPLE_NEAREST) {
-      const int sx = job.x + (int)(((long long)u * side) / S);
-      load_px(frame, H, W, sx, sy0, r, g, b);
-    } else {
-      Tap tx = bilinear_tap(u, side);
-      int r00, g00, b00, r01, g01, b01, r10, g10, b10, r11, g11, b11;
-      load_px(frame, H, W, job.x + tx.i0, sy0, r00, g00, b00);
-      load_px(frame, H, W, job.x + tx.i1, sy0, r01, g01, b01);
-      load_px(frame, H, W, job.x + tx.i0, sy1, r10, g10, b10);
-      load_px(frame, H, W, job.x + tx.i1, sy1, r11, g11, b11);
-      const int w00 = (256 - tx.f) * (256 - fy), w01 = tx.f * (256 - fy);
-      const int w10 = (256 - tx.f) * fy, w11 = tx.f * fy;
-      r = (r00 * w00 + r01 * w01 + r10 * w10 + r11 * w11 + 32768) >> 16;
-      g = (g00 * w00 + g01 * w01 + g10 * w10 + g11 * w11 + 32768) >> 16;
-      b = (b00 * w00 + b01 * w01 + b10 * w10 + b11 * w11 + 32768) >> 16;
-    }
-  };
   // exact value/255 in the activation type, looked up instead of divided (bit-identical)
   __shared__ uint16_t lut[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -108,42 +80,69 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
   __syncthreads();
   auto pk2 = [&](int a, int b) -> uint32_t { return (uint32_t)lut[a] | ((uint32_t)lut[b] << 16); };
 
-  // blockDim = 256 threads, 3 passes cover 608 columns; every warp-lane pair (u, u+-1)
-  // lives in the same warp except at warp edges, where the neighbour is re-sampled.
-  for (int base = 0; base < S; base += blockDim.x) {
-    const int u = base + threadIdx.x;
-    int r = 0, g = 0, b = 0;
-    if (u < S) sample(u, r, g, b);
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t me_rg = pk2(r, g), me_b0 = pk2(b, 0);
-    uint32_t l_rg = __shfl_up_sync(0xffffffffu, me_rg, 1), l_b0 = __shfl_up_sync(0xffffffffu, me_b0, 1);
-    uint32_t r_rg = __shfl_down_sync(0xffffffffu, me_rg, 1), r_b0 = __shfl_down_sync(0xffffffffu, me_b0, 1);
-    if (u >= S) continue;
+  const uint32_t lane = threadIdx.x & 31;
+  for (int task = threadIdx.x >> 5; task < GATHER_ROWS * SEGS; task += blockDim.x >> 5) {
+    const int row = task / SEGS;
+    const int v = blockIdx.x * GATHER_ROWS + row;  // output row
+    const int u = (task - row * SEGS) * 32 + (int)lane;
+    int sy0, sy1 = 0, fy = 0;
+    if (mode == TP_RESAMPLE_NEAREST) {
+      sy0 = job.y + (v * side) / S;
+    } else {
+      const Tap ty = bilinear_tap(v, side);
+      sy0 = job.y + ty.i0;
+      sy1 = job.y + ty.i1;
+      fy = ty.f;
+    }
+    // RGB of tile column uu on this output row (zero outside [0, 608) and the frame)
+    auto sample = [&](int uu, int& r, int& g, int& b) {
+      if (uu < 0 || uu >= S) {
+        r = g = b = 0;
+        return;
+      }
+      if (mode == TP_RESAMPLE_NEAREST) {
+        load_px(frame, H, W, job.x + (uu * side) / S, sy0, r, g, b);
+      } else {
+        const Tap tx = bilinear_tap(uu, side);
+        int r00, g00, b00, r01, g01, b01, r10, g10, b10, r11, g11, b11;
+        load_px(frame, H, W, job.x + tx.i0, sy0, r00, g00, b00);
+        load_px(frame, H, W, job.x + tx.i1, sy0, r01, g01, b01);
+        load_px(frame, H, W, job.x + tx.i0, sy1, r10, g10, b10);
+        load_px(frame, H, W, job.x + tx.i1, sy1, r11, g11, b11);
+        const int w00 = (256 - tx.f) * (256 - fy), w01 = tx.f * (256 - fy);
+        const int w10 = (256 - tx.f) * fy, w11 = tx.f * fy;
+        r = (r00 * w00 + r01 * w01 + r10 * w10 + r11 * w11 + 32768) >> 16;
+        g = (g00 * w00 + g01 * w01 + g10 * w10 + g11 * w11 + 32768) >> 16;
+        b = (b00 * w00 + b01 * w01 + b10 * w10 + b11 * w11 + 32768) >> 16;
+      }
+    };
+    int r, g, b;
+    sample(u, r, g, b);
     if (out_u8 != nullptr) {
       uint8_t* o = out_u8 + (((size_t)t * S + v) * S + u) * 3;
       o[0] = (uint8_t)r;
       o[1] = (uint8_t)g;
       o[2] = (uint8_t)b;
     }
-    if (out_act != nullptr) {
-      if (lane == 0) {
-        int rl, gl, bl;
-        sample(u - 1, rl, gl, bl);
-        l_rg = pk2(rl, gl);
-        l_b0 = pk2(bl, 0);
-      }
-      if (lane == 31) {
-        int rr, gr, br;
-        sample(u + 1, rr, gr, br);
-        r_rg = pk2(rr, gr);
-        r_b0 = pk2(br, 0);
-      }
-      if (u == S - 1) r_rg = r_b0 = 0u;  // right neighbour outside the tile
-      // expanded layer-0 pixel: [p(u-1) rgb0 | p(u) rgb0 | p(u+1) rgb0 | 0 0 0 0]
-      __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 16;
-      *reinterpret_cast<uint4*>(o) = make_uint4(l_rg, l_b0, me_rg, me_b0);
-      *reinterpret_cast<uint4*>(o + 8) = make_uint4(r_rg, r_b0, 0u, 0u);
+    if (out_act == nullptr) continue;
+    const uint32_t me_rg = pk2(r, g), me_b0 = pk2(b, 0);
+    uint32_t l_rg = __shfl_up_sync(0xffffffffu, me_rg, 1), l_b0 = __shfl_up_sync(0xffffffffu, me_b0, 1);
+    uint32_t r_rg = __shfl_down_sync(0xffffffffu, me_rg, 1), r_b0 = __shfl_down_sync(0xffffffffu, me_b0, 1);
+    if (lane == 0) {  // neighbours across the warp's edges are re-sampled
+      int rl, gl, bl;
+      sample(u - 1, rl, gl, bl);
+      l_rg = pk2(rl, gl);
+      l_b0 = pk2(bl, 0);
+    } else if (lane == 31) {
+      int rr, gr, br;
+      sample(u + 1, rr, gr, br);
+      r_rg = pk2(rr, gr);
+      r_b0 = pk2(br, 0);
     }
+    // expanded layer-0 pixel: [p(u-1) rgb0 | p(u) rgb0 | p(u+1) rgb0 | 0 0 0 0]
+    __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 16;
+    *reinterpret_cast<uint4*>(o) = make_uint4(l_rg, l_b0, me_rg, me_b0);
+    *reinterpret_cast<uint4*>(o + 8) = make_uint4(r_rg, r_b0, 0u, 0u);
   }
 }
 
@@ -163,7 +162,8 @@ extern "C" int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int 
     return TP_ERR_ARG;
   }
   if (n_jobs == 0) return TP_OK;
-  dim3 grid(S, n_jobs);
+  static_assert(S % 32 == 0 && S % GATHER_ROWS == 0, "tile side must split into warps/rows");
+  dim3 grid(S / GATHER_ROWS, n_jobs);
   gather_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(frames, frame_stride, H, W, jobs,
                                                         n_jobs_dev, mode, out_u8,
                                                         (__nv_bfloat16*)out_act,
