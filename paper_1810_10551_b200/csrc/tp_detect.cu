@@ -46,6 +46,13 @@ __device__ Cand decode_one(const float* __restrict__ head, int cstride, int tile
                    a * (5 + TP_CLASSES);
   Cand c;
   const float obj = sigmoid_rn(v[4]);
+  // conf = obj / s with s >= 1 exactly (the arg-max term is exp(0) = 1 and the rest are
+  // >= 0), and correctly rounded division is monotonic, so obj < thresh already decides
+  // rejection: skip the 80-class softmax (a dependent expf chain) for those candidates.
+  if (obj < thresh) {
+    c.keep = false;
+    return c;
+  }
   float m = v[5];
   int best = 0;
   for (int k = 1; k < TP_CLASSES; ++k) {
