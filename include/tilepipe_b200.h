@@ -116,7 +116,7 @@ TP_API int tp_yolo_create(int max_tiles, const void* const* weights, const float
                    void* workspace, size_t workspace_bytes, int dtype, tp_yolo_net** out);
 TP_API void* tp_yolo_input(tp_yolo_net* net);        /* 16-bit [max_tiles][610][610][16] */
 TP_API int tp_yolo_num_steps(void);
-TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][21][21][448] */
+TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][19][19][448] */
 TP_API int tp_yolo_head_cstride(void);
 TP_API int tp_yolo_forward(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev, void* stream);
 /* Debug/parity: run layers [first, last] only and expose any layer's output. */
@@ -125,16 +125,18 @@ TP_API int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n
 TP_API int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res, int* cstride);
 TP_API int tp_yolo_destroy(tp_yolo_net* net);
 
-/* Generic implicit-GEMM conv on padded NHWC 16-bit activations (one layer), for tests.
- * cin_stride == 16 with ksize 3 is the layer-0 expanded-input mode; pool != 0 fuses a
- * 2x2/2 max pool (out is then the half-resolution padded buffer). */
+/* Generic implicit-GEMM conv (one layer), for tests. Activations are compact NHWC 16-bit
+ * [n][res][res][cstride]; the zero padding of 3x3 convs is implicit (TMA out-of-bounds
+ * fill). cin_stride == 16 is the layer-0 mode: input is the padded, horizontally expanded
+ * [n][res+2][res+2][16] image and the conv must pool. pool != 0 fuses a 2x2/2 max pool
+ * (out is then [n][res/2][res/2][out_cstride]). */
 TP_API int tp_conv(const void* in, int n_img, int res, int cin_stride, const void* weight,
                    const float* bias, int cout, int cout_pad, int ksize, int leaky, void* out,
                    int out_cstride, int out_coff, int out_fp32, int reorg, int dtype, int pool,
                    void* stream);
 
-/* K5: region decode + threshold + sort + project. head: fp32 padded
- * [n][21][21][cstride]. out: [n][max_per_tile] sorted by (-conf, cell*5+anchor). */
+/* K5: region decode + threshold + sort + project. head: fp32 compact
+ * [n][19][19][cstride]. out: [n][max_per_tile] sorted by (-conf, cell*5+anchor). */
 TP_API int tp_region_decode(const float* head, int head_cstride, int n_tiles, const int32_t* n_tiles_dev,
                      const tp_tile_job_t* jobs, int frame_w, int frame_h, float thresh,
                      const float* anchors_host, tp_det_t* out, int max_per_tile,
@@ -190,12 +192,12 @@ TP_API int tp_render_frames(const int32_t* rects, const uint8_t* colors, const i
                             int n_frames, int max_obj, int H, int W, uint32_t bg_rgb,
                             uint8_t* out, void* stream);
 
-/* 2x2/2 max pool on padded NHWC bf16 (exposed for tests). */
 /* Profiling only (TP_CONV_DEBUG bit 32 set in the environment when the net/conv runs):
  * per-role cycle totals of conv_tc_kernel summed over CTAs — 0 producer, 1 producer
  * empty-wait, 2 MMA issuer, 3 issuer accumulator-wait, 4 issuer stage-wait, 5 epilogue
  * warp 0, 6 epilogue accumulator-wait, 7 launches. No reference counterpart. */
 TP_API int tp_debug_conv_counters(uint64_t* out, int n, int reset);
+/* 2x2/2 max pool on compact NHWC 16-bit activations (exposed for tests). */
 TP_API int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype, void* out,
                         void* stream);
 

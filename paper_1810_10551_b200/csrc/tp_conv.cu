@@ -38,7 +38,7 @@
 
 namespace {
 
-enum ConvMode { MODE_SW128 = 0, MODE_SW64 = 1, MODE_L0X = 2 };
+enum ConvMode { MODE_SW128 = 0, MODE_SW64 = 1 };
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 // Warp roles: the warp scheduler favours HIGHER warp ids, so the two single-thread roles
@@ -49,7 +49,7 @@ constexpr int RECT_W = 16, RECT_H = 8;
 struct ConvParams {
   int n_img;
   const int32_t* n_img_dev;
-  int res, wp, img_px;
+  int res, img_px;  // activations are compact NHWC: img_px = res * res
   int ksize;
   int cin;         // channels per tap used by K (multiple of BK)
   int cout;        // real output channels
@@ -76,10 +76,6 @@ struct ConvParams {
   int dbg;  // profiling only (TP_CONV_DEBUG): 1 = skip epilogue math/stores, 2 = skip MMAs
 };
 
-__device__ __forceinline__ int tap_shift(int tap, int ksize, int wp) {
-  if (ksize == 1) return 0;
-  return (tap / 3 - 1) * wp + (tap % 3 - 1);
-}
 
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar,
                                             int32_t c0, int32_t c1, int32_t c2) {
@@ -88,6 +84,42 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, ui
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(tp::smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(tp::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// 4-D tiled box {C, W, H, N}; out-of-bounds elements (the conv's zero padding) read as 0
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, uint64_t* bar,
+                                            int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(tp::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(tp::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+// im2col box: consecutive output pixels (W, then H, then N inside the map's bounding box),
+// each contributing the input pixel at window corner + (ow, oh); coordinates are the
+// first pixel's window corner. Out-of-bounds pixels read as 0 (tools/im2col_probe.cu).
+__device__ __forceinline__ void tma_load_im2col(void* smem_dst, const void* tmap, uint64_t* bar,
+                                                int32_t c, int32_t w, int32_t h, int32_t n,
+                                                uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(tp::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(tp::smem_u32(bar)), "r"(c), "r"(w), "r"(h),
+      "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+// first compact pixel of an M tile -> (image, y, x)
+struct PixPos {
+  int n, y, x;
+};
+__device__ __forceinline__ PixPos pix_pos(int pix, int res, int img_px) {
+  PixPos r;
+  r.n = pix / img_px;
+  const int rem = pix - r.n * img_px;
+  r.y = rem / res;
+  r.x = rem - r.y * res;
+  return r;
 }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -169,7 +201,7 @@ template <int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
-  constexpr int BK = MODE == MODE_SW128 ? 64 : (MODE == MODE_SW64 ? 32 : 16);
+  constexpr int BK = MODE == MODE_SW128 ? 64 : 32;
   constexpr bool RECT = EPI == EPI_POOL;
   // FLAT plain / fp32 outputs leave through per-warp swizzled smem slabs + TMA stores
   constexpr bool TSTORE = EPI == EPI_PLAIN || EPI == EPI_F32;
@@ -221,7 +253,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int per_cta = total_tiles / (int)gridDim.x, extra = total_tiles % (int)gridDim.x;
   const int t_begin = (int)blockIdx.x * per_cta + min((int)blockIdx.x, extra);
   const int n_tiles = per_cta + ((int)blockIdx.x < extra ? 1 : 0);
-  const int hp = p.res + 2;
 
   if (warp == kProdWarp) {
     if (lane == 0) {
@@ -238,16 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < p.n_bchunks; ++j)
           tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, j * BK, 0);
       }
+      const int lo = p.ksize == 3 ? -1 : 0;  // im2col window corner (zero padding 1 or 0)
       for (int i = 0; i < n_tiles; ++i, it.next(p)) {
         const int n0 = it.nb * p.bn;
-        const int m0 = it.mt * 128;
-        const int rx = 1 + it.bx * RECT_W, ry = it.img * hp + 1 + it.by * RECT_H * p.sub;
+        // RECT: tile origin inside image it.img; FLAT: first compact pixel of the tile
+        const int rx = it.bx * RECT_W, ry = it.by * RECT_H * p.sub;
+        const PixPos f0 = RECT ? PixPos{0, 0, 0} : pix_pos(it.mt * 128, p.res, p.img_px);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           PROF_T0(tw);
-          if (p.dbg & 64)
-            tp::mbar_wait_backoff(&empty[s], ph ^ 1, 32);
-          else
-            tp::mbar_wait(&empty[s], ph ^ 1);
+          tp::mbar_wait(&empty[s], ph ^ 1);
           PROF_ADD(pr_wait, tw);
           uint8_t* a_dst = smA + (size_t)s * p.a_stage_bytes;
           uint8_t* b_dst = smB + (size_t)s * p.b_stage_bytes;
@@ -260,25 +290,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           tp::mbar_arrive_expect_tx(&full[s], tx_bytes);
-          if (RECT && p.halo) {  // halo box {BK, 16, 10} for kernel column dx, channel block cb
-            const int dx = MODE == MODE_L0X ? 0 : kb / p.kb_per_tap - 1;
-            const int cb = MODE == MODE_L0X ? 0 : kb % p.kb_per_tap;
-            tma_load_3d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry - 1);
-          } else if (MODE == MODE_L0X) {  // one k-block per kernel row dy
-            if (RECT)
-              tma_load_3d(a_dst, &tmA, &full[s], 0, rx, ry + kb - 1);
-            else
-              tp::tma_load_2d(a_dst, &tmA, &full[s], 0, m0 + (kb - 1) * p.wp);
-            tp::tma_load_2d(b_dst, &tmB, &full[s], kb * 16, n0);
+          if (RECT && p.halo) {  // halo box {BK, 16, 8*SUB+2} for kernel column dx, block cb
+            const int dx = kb / p.kb_per_tap - 1;
+            const int cb = kb % p.kb_per_tap;
+            tma_load_4d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry - 1, it.img);
           } else {
             const int tap = kb / p.kb_per_tap;
             const int cb = kb - tap * p.kb_per_tap;
             if (RECT) {
               const int dy = p.ksize == 3 ? tap / 3 - 1 : 0;
               const int dx = p.ksize == 3 ? tap % 3 - 1 : 0;
-              tma_load_3d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry + dy);
-            } else {
-              tp::tma_load_2d(a_dst, &tmA, &full[s], cb * BK, m0 + tap_shift(tap, p.ksize, p.wp));
+              tma_load_4d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry + dy, it.img);
+            } else {  // im2col: 128 consecutive compact pixels, window shifted by the tap
+              const int ox = p.ksize == 3 ? tap % 3 : 0, oy = p.ksize == 3 ? tap / 3 : 0;
+              tma_load_im2col(a_dst, &tmA, &full[s], cb * BK, f0.x + lo, f0.y + lo, f0.n,
+                              (uint16_t)ox, (uint16_t)oy);
             }
             tp::tma_load_2d(b_dst, &tmB, &full[s], tap * p.cin + cb * BK, n0);
           }
@@ -309,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // made the single issuing thread the bottleneck for N <= 128 (~90+ cycles/MMA).
       constexpr uint32_t row_bytes = BK * 2;
       constexpr uint32_t sbo = 8 * row_bytes;
-      constexpr uint32_t lay = MODE == MODE_SW128 ? 2 : (MODE == MODE_SW64 ? 4 : 6);
+      constexpr uint32_t lay = MODE == MODE_SW128 ? 2 : 4;
       const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, sbo, lay);
       const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, sbo, lay);
       const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
@@ -337,14 +363,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else if (RECT && p.halo) {
             // three kernel rows dy = sub-windows of the halo box, 16 pixel rows apart
             constexpr uint32_t row16 = RECT_W * row_bytes / 16;  // one pixel row, >> 4
-            const int dx = MODE == MODE_L0X ? 0 : kb / p.kb_per_tap - 1;
-            const int cb = MODE == MODE_L0X ? 0 : kb % p.kb_per_tap;
+            const int dx = kb / p.kb_per_tap - 1;
+            const int cb = kb % p.kb_per_tap;
             for (int j = 0; j < p.sub; ++j) {
               const uint64_t aj = ad0 + (uint64_t)(j * RECT_H * row16);
               const uint32_t dj = d_tmem + j * p.bn;
 #pragma unroll
               for (int dy = 0; dy < 3; ++dy) {
-                const int chunk = MODE == MODE_L0X ? dy : (dy * 3 + dx + 1) * p.kb_per_tap + cb;
+                const int chunk = (dy * 3 + dx + 1) * p.kb_per_tap + cb;
                 const uint64_t aw = aj + dy * row16;
                 const uint64_t bw = b_desc0 + (uint64_t)(chunk * bch);
 #pragma unroll
@@ -382,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
     const bool leaky = p.leaky != 0;
-    const int ores = p.res >> 1, owp = ores + 2, oimg = owp * owp;
+    const int ores = p.res >> 1, oimg = ores * ores;
     const int total_px = n_img * p.img_px;
     const int nchunks = p.bn >> 4;
     uint32_t ph = 0;
@@ -394,10 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if ((i & 1) != g) continue;
       const int n0 = it.nb * p.bn;
       PROF_T0(t3);
-      if (p.dbg & 64)
-        tp::mbar_wait_backoff(&tfull[g], ph, 128);
-      else
-        tp::mbar_wait(&tfull[g], ph);
+      tp::mbar_wait(&tfull[g], ph);
       PROF_ADD(e_wait, t3);
       ph ^= 1;
       tp::tc_fence_after();
@@ -416,22 +439,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int y = (it.by * p.sub + jt) * RECT_H + (row >> 4);
         valid = it.img < n_img && x < p.res && y < p.res;
         writer = ((x | y) & 1) == 0;
-        out_px = it.img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
+        out_px = it.img * oimg + (y >> 1) * ores + (x >> 1);
       } else {
         const int pix = it.mt * 128 + row;
         valid = pix < total_px;
-        if (valid) {
-          const int img = pix / p.img_px;
-          const int rem = pix - img * p.img_px;
-          const int yp = rem / p.wp, xp = rem - yp * p.wp;
-          valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
-          if (EPI == EPI_REORG) {
-            const int y = yp - 1, x = xp - 1;
-            sub = (y & 1) * 2 + (x & 1);
-            out_px = img * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
-          } else {
-            out_px = pix;
-          }
+        out_px = pix;
+        if (valid && EPI == EPI_REORG) {
+          const PixPos q0 = pix_pos(pix, p.res, p.img_px);
+          sub = (q0.y & 1) * 2 + (q0.x & 1);
+          out_px = q0.n * oimg + (q0.y >> 1) * ores + (q0.x >> 1);
         }
       }
       const uint32_t t_row =
@@ -600,6 +616,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, ui
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_im2col_pair(void* dst, const void* tmap,
+                                                     uint32_t leader_bar, int32_t c, int32_t w,
+                                                     int32_t h, int32_t n, uint16_t ow,
+                                                     uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::"
+      "bytes [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(tp::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(ow), "h"(oh)
+      : "memory");
+}
 __device__ __forceinline__ void mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -684,11 +711,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ============ TMA producer (both CTAs; bytes land on the leader's barrier) ============
       int s = 0;
       uint32_t ph = 0;
+      const int lo = p.ksize == 3 ? -1 : 0;  // im2col window corner
       for (int i = 0; i < n_tiles; ++i) {
         const int t = t_begin + i;
         const int mt = t / p.n_blocks_n;
         const int n0 = (t - mt * p.n_blocks_n) * p.bn;
-        const int m0 = mt * 256 + (int)rank * 128;
+        const PixPos f0 = pix_pos(mt * 256 + (int)rank * 128, p.res, p.img_px);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0)
@@ -696,8 +724,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t lbar = mapa_rank(&full[s], 0);
           const int tap = kb / p.kb_per_tap;
           const int cb = kb - tap * p.kb_per_tap;
-          tma_load_2d_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK,
-                           m0 + tap_shift(tap, p.ksize, p.wp));
+          const int ox = p.ksize == 3 ? tap % 3 : 0, oy = p.ksize == 3 ? tap / 3 : 0;
+          tma_load_im2col_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK, f0.x + lo,
+                               f0.y + lo, f0.n, (uint16_t)ox, (uint16_t)oy);
           tma_load_2d_pair(smB + (size_t)s * p.b_stage_bytes, &tmB, lbar, tap * p.cin + cb * BK,
                            n0 + (int)rank * half_bn);
           if (++s == S) {
@@ -762,14 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ph ^= 1;
       tp::tc_fence_after();
       const int rbase = mt * 256 + (int)rank * 128 + (int)q * 32;
-      const int pix = rbase + (int)lane;
-      bool valid = pix < total_px;
-      if (valid) {
-        const int img = pix / p.img_px;
-        const int rem = pix - img * p.img_px;
-        const int yp = rem / p.wp, xp = rem - yp * p.wp;
-        valid = yp >= 1 && yp <= p.res && xp >= 1 && xp <= p.res;
-      }
+      const bool valid = rbase + (int)lane < total_px;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * p.bn);
       const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
       const uint32_t rowa = buf + lane * 64;
@@ -906,7 +928,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
-  const int ores = p.res >> 1, owp = ores + 2, oimg = owp * owp, hp = p.res + 2;
+  // input: the gather's padded expanded image (610^2); output: compact 304^2
+  const int ores = p.res >> 1, oimg = ores * ores, hp = p.res + 2;
   const int txs = ores / 16, tys = ores / 8, per_img = txs * tys;  // 304 = 19*16 = 38*8
   const int total_tiles = n_img * per_img;
   const int per_cta = total_tiles / (int)gridDim.x, extra = total_tiles % (int)gridDim.x;
@@ -994,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::tc_fence_after();
       const int X = bx * 16 + (row & 15), Y = by * 8 + (row >> 4);
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
-                         (size_t)(img * oimg + (Y + 1) * owp + (X + 1)) * p.out_cstride;
+                         (size_t)(img * oimg + Y * ores + X) * p.out_cstride;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 128);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -1112,7 +1135,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
-  const int hp = p.res + 2;
   const int per_img = p.tiles_x * p.tiles_y;
   const int total_tiles = n_img * per_img;
   const int per_cta = total_tiles / (int)gridDim.x, extra = total_tiles % (int)gridDim.x;
@@ -1142,15 +1164,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t tx = PM ? 4 * PLANE_W * PLANE_H * RB : (BOX_TW + 2) * (BOX_TH + 2) * RB;
         tp::mbar_arrive_expect_tx(&full[s], tx);
         if (PM) {
-          // plane (ey, ex) holds padded input (2*X0 + 1 - ex + 2i, 2*Y0 + 1 - ey + 2j)
+          // plane (ey, ex) holds input (2*X0 - ex + 2i, 2*Y0 - ey + 2j); -1 reads as 0
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int ey = b >> 1, ex = b & 1;
-            tma_load_3d(dst + b * (p.a_stage_bytes >> 2), &tmA, &full[s], 0,
-                        2 * BOX_TW * bx + 1 - ex, img * hp + 2 * BOX_TH * by + 1 - ey);
+            tma_load_4d(dst + b * (p.a_stage_bytes >> 2), &tmA, &full[s], 0,
+                        2 * BOX_TW * bx - ex, 2 * BOX_TH * by - ey, img);
           }
-        } else {
-          tma_load_3d(dst, &tmA, &full[s], 0, BOX_TW * bx, img * hp + BOX_TH * by);
+        } else {  // tile + one-pixel halo; the halo outside the image reads as 0
+          tma_load_4d(dst, &tmA, &full[s], 0, BOX_TW * bx - 1, BOX_TH * by - 1, img);
         }
         if (++s == S) {
           s = 0;
@@ -1241,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f16 = p.f16 != 0;
     const bool leaky = p.leaky != 0;
     const int ores = PM || EPI == BOX_POOL ? p.res >> 1 : p.res;
-    const int owp = ores + 2, oimg = owp * owp;
+    const int oimg = ores * ores;
     const int nchunks = N >> 4;
     uint32_t ph = 0;  // phase bit per accumulator buffer
     int img = t_begin / per_img, r = t_begin - img * per_img;
@@ -1276,10 +1298,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int opx;
       if (EPI == BOX_POOL) {  // both lanes of an x pair store (8 channels each)
         store = y < p.res && (y & 1) == 0;
-        opx = timg * oimg + ((y >> 1) + 1) * owp + ((x >> 1) + 1);
+        opx = timg * oimg + (y >> 1) * ores + (x >> 1);
       } else {
         store = y < ores;
-        opx = timg * oimg + (y + 1) * owp + (x + 1);
+        opx = timg * oimg + y * ores + x;
       }
       __nv_bfloat16* o =
           reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)opx * p.out_cstride + p.out_coff;
@@ -1400,8 +1422,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && (p.dbg & 4) == 0) {
-              tma_store_3d(&tmC, smC + warp * 2048, p.out_coff + (c - 1) * 16, tbx * BOX_TW + 1,
-                           timg * owp + tby * BOX_TH + (int)q * 4 + 1);
+              tma_store_3d(&tmC, smC + warp * 2048, p.out_coff + (c - 1) * 16, tbx * BOX_TW,
+                           timg * p.res + tby * BOX_TH + (int)q * 4);
               bulk_commit();
             }
           }
@@ -1443,7 +1465,7 @@ __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img,
                                 int cstride, __nv_bfloat16* __restrict__ out,
                                 const int32_t* __restrict__ n_img_dev, int f16) {
   if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
-  const int ores = res >> 1, iwp = res + 2, owp = ores + 2;
+  const int ores = res >> 1;
   const int cg = cstride >> 3;
   const long long total = (long long)n_img * ores * ores * cg;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -1455,11 +1477,11 @@ __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img,
     const int y = (int)(r % ores);
     const int img = (int)(r / ores);
     const __nv_bfloat16* src =
-        in + (((long long)img * iwp + (2 * y + 1)) * iwp + (2 * x + 1)) * cstride + g * 8;
+        in + (((long long)img * res + 2 * y) * res + 2 * x) * cstride + g * 8;
     uint4 a = *reinterpret_cast<const uint4*>(src);
     uint4 b = *reinterpret_cast<const uint4*>(src + cstride);
-    uint4 c = *reinterpret_cast<const uint4*>(src + (long long)iwp * cstride);
-    uint4 d = *reinterpret_cast<const uint4*>(src + (long long)iwp * cstride + cstride);
+    uint4 c = *reinterpret_cast<const uint4*>(src + (long long)res * cstride);
+    uint4 d = *reinterpret_cast<const uint4*>(src + (long long)res * cstride + cstride);
     uint4 m;
     if (f16) {
       const __half2* pa = reinterpret_cast<const __half2*>(&a);
@@ -1478,7 +1500,7 @@ __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img,
 #pragma unroll
       for (int j = 0; j < 4; ++j) pm[j] = __hmax2(__hmax2(pa[j], pb[j]), __hmax2(pc[j], pd[j]));
     }
-    __nv_bfloat16* dst = out + (((long long)img * owp + (y + 1)) * owp + (x + 1)) * cstride + g * 8;
+    __nv_bfloat16* dst = out + (((long long)img * ores + y) * ores + x) * cstride + g * 8;
     *reinterpret_cast<uint4*>(dst) = m;
   }
 }
@@ -1502,8 +1524,55 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// rank-2 {cols, rows} or rank-3 {cols, width, rows} 16-bit tensor map, cols contiguous.
-// esize 2 = 16-bit (f16 selects fp16 vs bf16), 4 = fp32
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                   cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn get_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  if (fn == nullptr) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(ptr);
+  }
+  return fn;
+}
+
+// im2col map over a compact NHWC activation {cstride, res, res, n}: `pixels` consecutive
+// output pixels x `bk` channels per load; window corner `lo` (-1 = 3x3 with zero padding,
+// 0 = 1x1). Out-of-bounds taps are zero-filled.
+int make_tmap_im2col(CUtensorMap* tm, const void* base, int cstride, int res, int n, int bk,
+                     int pixels, int lo, CUtensorMapSwizzle swz, bool f16) {
+  EncodeIm2colFn enc = get_im2col_fn();
+  if (enc == nullptr) {
+    tp_set_error("cuTensorMapEncodeIm2col unavailable (no CUDA driver?)");
+    return TP_ERR_CUDA;
+  }
+  const cuuint64_t dims[4] = {(cuuint64_t)cstride, (cuuint64_t)res, (cuuint64_t)res,
+                              (cuuint64_t)n};
+  const cuuint64_t strides[3] = {(cuuint64_t)cstride * 2, (cuuint64_t)cstride * 2 * res,
+                                 (cuuint64_t)cstride * 2 * res * res};
+  const int lower[2] = {lo, lo}, upper[2] = {lo, lo};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                   const_cast<void*>(base), dims, strides, lower, upper, (cuuint32_t)bk,
+                   (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    tp_set_error("cuTensorMapEncodeIm2col failed (%d): cstride %d res %d n %d", (int)r, cstride,
+                 res, n);
+    return TP_ERR_CUDA;
+  }
+  return TP_OK;
+}
+
+// rank-2..4 tiled tensor map, dims[0] contiguous (e.g. {C, W, H, N} for NHWC activations).
+// esize 2 = 16-bit (f16 selects fp16 vs bf16), 4 = fp32. Out-of-bounds reads are zero.
 int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
               const uint32_t* box, CUtensorMapSwizzle swz, bool f16, int esize = 2,
               const uint32_t* elem_strides = nullptr) {
@@ -1512,8 +1581,8 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
     tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
     return TP_ERR_CUDA;
   }
-  cuuint64_t gdims[3], strides[2];
-  cuuint32_t gbox[3], estr[3] = {1, 1, 1};
+  cuuint64_t gdims[4], strides[3];
+  cuuint32_t gbox[4], estr[4] = {1, 1, 1, 1};
   uint64_t stride = dims[0] * esize;
   for (int i = 0; i < rank; ++i) {
     gdims[i] = dims[i];
@@ -1562,29 +1631,16 @@ struct ConvLaunch {
   size_t smem;
 };
 
-// cin_used == 16 && ksize == 3 selects the layer-0 expanded-input mode.
-// pool != 0 selects RECT tiles with the 2x2 max pool fused; `out` is then the
-// half-resolution buffer.
+// Activations are compact NHWC [n][res][res][cin_stride] (the conv's zero padding comes
+// from TMA out-of-bounds fill), except layer 0 (cin_used == 16): its input is the gather's
+// padded, horizontally expanded [n][res+2][res+2][16] image, and it must pool.
+// pool != 0 fuses the 2x2 max pool; `out` is then the half-resolution buffer.
 int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_stride, int cin_used,
                  const void* weight, const float* bias, int cout, int cout_pad, int ksize,
                  int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
                  int dtype, int pool) {
   memset(L, 0, sizeof(*L));
   const bool f16 = dtype == TP_DTYPE_F16;
-  int mode, bk;
-  if (cin_used == 16 && ksize == 3) {
-    mode = MODE_L0X;
-    bk = 16;
-  } else if (cin_used % 64 == 0) {
-    mode = MODE_SW128;
-    bk = 64;
-  } else if (cin_used == 32) {
-    mode = MODE_SW64;
-    bk = 32;
-  } else {
-    tp_set_error("conv: unsupported cin %d", cin_used);
-    return TP_ERR_UNSUPPORTED;
-  }
   if (cout_pad % 32 != 0 || cout > cout_pad) {
     tp_set_error("conv: bad cout/cout_pad %d/%d (cout_pad must be a multiple of 32)", cout,
                  cout_pad);
@@ -1594,46 +1650,110 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     tp_set_error("conv: fused pool needs an even side and a 16-bit plain output");
     return TP_ERR_ARG;
   }
+  if (!out_fp32 && (cout % 16 != 0 || out_cstride % 8 != 0 || out_coff % 8 != 0)) {
+    tp_set_error("conv: 16-bit output needs 16-channel multiples");
+    return TP_ERR_ARG;
+  }
+  if (cout_pad > kMaxBias) {
+    tp_set_error("conv: cout_pad %d exceeds %d", cout_pad, kMaxBias);
+    return TP_ERR_UNSUPPORTED;
+  }
+  const int img_px = res * res;
+  if ((long long)max_img * (res + 2) * (res + 2) >= (1ll << 31)) {
+    tp_set_error("conv: %d images of side %d exceed 32-bit pixel indexing", max_img, res);
+    return TP_ERR_CAPACITY;
+  }
+  ConvParams& p = L->p;
+  p.n_img = max_img;
+  p.res = res;
+  p.img_px = img_px;
+  p.ksize = ksize;
+  p.cin = cin_used;
+  p.cout = cout;
+  p.f16 = f16 ? 1 : 0;
+  p.bias = bias;
+  p.out = out;
+  p.out_cstride = out_cstride;
+  p.out_coff = out_coff;
+  p.out_fp32 = out_fp32;
+  p.leaky = leaky;
+  p.reorg = reorg;
+  p.dbg = getenv("TP_CONV_DEBUG") ? atoi(getenv("TP_CONV_DEBUG")) : 0;
+  // everything else in smem: 1 KB alignment slack, bias, barriers (<= 12 stages), TMEM slot
+  const int fixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
+  int rc;
+
+  if (cin_used == 16) {  // layer 0: pool-in-M kernel with stride-2 TMA boxes
+    if (!(ksize == 3 && pool && cout_pad == 32 && cout == 32 && res % 32 == 0)) {
+      tp_set_error("conv: the 16-channel expanded input needs 3x3, 32 outputs, fused pool, "
+                   "side %% 32 == 0");
+      return TP_ERR_UNSUPPORTED;
+    }
+    const int wp = res + 2;
+    {
+      const uint64_t dims[3] = {16, (uint64_t)wp, (uint64_t)max_img * wp};
+      const uint32_t box[3] = {16, 32, 18};
+      const uint32_t estr[3] = {1, 2, 2};
+      rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 2, estr);
+      if (rc) return rc;
+    }
+    {
+      const uint64_t dims[2] = {48, 32};
+      const uint32_t box[2] = {16, 32};
+      rc = make_tmap(&L->tmB, weight, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16);
+      if (rc) return rc;
+    }
+    L->tmC = L->tmA;  // unused
+    L->l0 = 1;
+    int st = (int)((227 * 1024 - fixed - 3 * 1024) / L0_STAGE);
+    if (st > 8) st = 8;
+    p.stages = st;
+    p.bn = 32;
+    p.n_blocks_n = 1;
+    p.idesc = tp::idesc_f16kind(128, 32, !f16);
+    L->smem = 1024 + (size_t)st * L0_STAGE + 3 * 1024 + (2 * st + 6) * 8 + 32 * 4 + 16;
+    return TP_OK;
+  }
+
+  int mode, bk;
+  if (cin_used % 64 == 0) {
+    mode = MODE_SW128;
+    bk = 64;
+  } else if (cin_used == 32) {
+    mode = MODE_SW64;
+    bk = 32;
+  } else {
+    tp_set_error("conv: unsupported cin %d", cin_used);
+    return TP_ERR_UNSUPPORTED;
+  }
   int bn = cout_pad;
   if (bn > 256) {
     bn = 256;
     while (cout_pad % bn != 0 || bn % 32 != 0) bn -= 32;
   }
-  if (!out_fp32 && (cout % 16 != 0 || out_cstride % 8 != 0 || out_coff % 8 != 0)) {
-    tp_set_error("conv: 16-bit output needs 16-channel multiples");
-    return TP_ERR_ARG;
-  }
-  const int wp = res + 2;
-  const int img_px = wp * wp;
-  if ((long long)max_img * img_px >= (1ll << 31)) {
-    tp_set_error("conv: %d images of side %d exceed 32-bit pixel indexing", max_img, res);
-    return TP_ERR_CAPACITY;
-  }
   const int taps = ksize * ksize;
-  const int ktotal = mode == MODE_L0X ? 48 : taps * cin_used;
-  CUtensorMapSwizzle swz = mode == MODE_SW128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                           : mode == MODE_SW64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                               : CU_TENSOR_MAP_SWIZZLE_32B;
+  const int ktotal = taps * cin_used;
+  CUtensorMapSwizzle swz =
+      mode == MODE_SW128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   // halo variant: weights (whole K x N) fit next to the A ring -> resident in smem
   const size_t bres = (size_t)cout_pad * ktotal * 2;
-  const bool halo = pool && cout_pad <= 256 && bres <= 48 * 1024;
+  const bool halo = pool && ksize == 3 && cout_pad <= 256 && bres <= 48 * 1024;
   // super-tile height: SUB x 8 rows per halo box (fewer, larger tiles for the 32/64-channel
   // layers whose per-tile fixed costs dominate); keep SUB x BN <= 256 TMEM columns
   int subt = 1;
   if (halo) {
-    subt = mode == MODE_L0X ? 4 : 2;
+    subt = 2;
     while (subt > 1 && (subt * cout_pad > 256 || res % (RECT_H * subt) != 0)) subt >>= 1;
   }
-  int rc;
-  if (pool) {
-    const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
-    const uint32_t box[3] = {(uint32_t)bk, RECT_W,
-                             halo ? (uint32_t)(RECT_H * subt + 2) : (uint32_t)RECT_H};
-    rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16);
-  } else {
-    const uint64_t dims[2] = {(uint64_t)cin_stride, (uint64_t)max_img * img_px};
-    const uint32_t box[2] = {(uint32_t)bk, 128};
-    rc = make_tmap(&L->tmA, in, 2, dims, box, swz, f16);
+  if (pool) {  // RECT tiles: 4-D boxes {C, 16, rows, 1}, image borders zero-filled
+    const uint64_t dims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res,
+                              (uint64_t)max_img};
+    const uint32_t box[4] = {(uint32_t)bk, RECT_W,
+                             halo ? (uint32_t)(RECT_H * subt + 2) : (uint32_t)RECT_H, 1};
+    rc = make_tmap(&L->tmA, in, 4, dims, box, swz, f16);
+  } else {  // FLAT tiles: im2col over 128 consecutive compact pixels
+    rc = make_tmap_im2col(&L->tmA, in, cin_stride, res, max_img, bk, 128, ksize == 3 ? -1 : 0,
+                          swz, f16);
   }
   if (rc) return rc;
   {
@@ -1652,23 +1772,15 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     L->tmC = L->tmA;  // unused
   }
 
-  ConvParams& p = L->p;
-  p.n_img = max_img;
-  p.res = res;
-  p.wp = wp;
-  p.img_px = img_px;
-  p.ksize = ksize;
-  p.cin = cin_used;
-  p.cout = cout;
   p.bn = bn;
   p.n_blocks_n = cout_pad / bn;
-  p.kb_per_tap = mode == MODE_L0X ? 1 : cin_used / bk;
-  p.num_kb = mode == MODE_L0X ? 3 : taps * p.kb_per_tap;
+  p.kb_per_tap = cin_used / bk;
+  p.num_kb = taps * p.kb_per_tap;
   p.a_stage_bytes = 128 * bk * 2;
   p.b_stage_bytes = bn * bk * 2;
   p.halo = halo ? 1 : 0;
   if (halo) {
-    p.num_kb = mode == MODE_L0X ? 1 : 3 * p.kb_per_tap;  // one stage per (dx, channel block)
+    p.num_kb = 3 * p.kb_per_tap;  // one stage per (dx, channel block)
     p.a_stage_bytes = (RECT_H * subt + 2) * RECT_W * bk * 2;
     p.b_stage_bytes = 0;
     p.bchunk_bytes = bn * bk * 2;
@@ -1677,8 +1789,6 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   }
   p.stage_bytes = tstore ? 8 * 2048 : 0;
   const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
-  // everything else in smem: 1 KB alignment slack, bias, barriers (<= 12 stages), TMEM slot
-  const int fixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
   int stages = (int)((227 * 1024 - fixed - (int)p.bres_bytes - (int)p.stage_bytes) /
                      (int)stage_bytes);
   if (stages > 12) stages = 12;
@@ -1692,37 +1802,12 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   while (cols < (uint32_t)(2 * subt * bn)) cols <<= 1;
   p.tmem_cols = cols;
   p.idesc = tp::idesc_f16kind(128, (uint32_t)bn, !f16);
-  p.f16 = f16 ? 1 : 0;
   p.rect = pool ? 1 : 0;
   p.tiles_x = (res + RECT_W - 1) / RECT_W;
   p.tiles_y = (res + RECT_H * subt - 1) / (RECT_H * subt);
-  p.bias = bias;
-  p.out = out;
-  p.out_cstride = out_cstride;
-  p.out_coff = out_coff;
-  p.out_fp32 = out_fp32;
-  p.leaky = leaky;
-  p.reorg = reorg;
-  p.dbg = getenv("TP_CONV_DEBUG") ? atoi(getenv("TP_CONV_DEBUG")) : 0;
   L->mode = mode;
   L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + p.stage_bytes +
             (2 * stages + 6) * 8 + cout_pad * 4 + 16;
-  // layer 0: pool-in-M kernel with stride-2 TMA boxes (TP_L0=0 disables it)
-  const char* l0e = getenv("TP_L0");
-  if (mode == MODE_L0X && pool && cout_pad == 32 && res % 32 == 0 && !out_fp32 &&
-      (l0e == nullptr || atoi(l0e) != 0)) {
-    const uint64_t dims[3] = {16, (uint64_t)wp, (uint64_t)max_img * wp};
-    const uint32_t box[3] = {16, 32, 18};
-    const uint32_t estr[3] = {1, 2, 2};
-    rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 2, estr);
-    if (rc) return rc;
-    L->l0 = 1;
-    int st = (int)((227 * 1024 - fixed - 3 * 1024) / L0_STAGE);
-    if (st > 8) st = 8;
-    p.stages = st;
-    p.idesc = tp::idesc_f16kind(128, 32, !f16);
-    L->smem = 1024 + (size_t)st * L0_STAGE + 3 * 1024 + (2 * st + 6) * 8 + 32 * 4 + 16;
-  }
   // CTA-pair variant for FLAT SW128 layers (TP_PAIR=0 disables it)
   const char* pe = getenv("TP_PAIR");
   if (tstore && mode == MODE_SW128 && bn == 256 && (pe == nullptr || atoi(pe) != 0)) {
@@ -1761,15 +1846,15 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     uint32_t cols = 32;
     while (cols < need) cols <<= 1;
     if (st >= 2 && cols <= 512) {
+      const uint64_t dims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res,
+                                (uint64_t)max_img};
       if (pm) {
-        const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
-        const uint32_t box[3] = {(uint32_t)bk, 2 * PLANE_W, 2 * PLANE_H};
-        const uint32_t estr[3] = {1, 2, 2};
-        rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16, 2, estr);
+        const uint32_t box[4] = {(uint32_t)bk, 2 * PLANE_W, 2 * PLANE_H, 1};
+        const uint32_t estr[4] = {1, 2, 2, 1};
+        rc = make_tmap(&L->tmA, in, 4, dims, box, swz, f16, 2, estr);
       } else {
-        const uint64_t dims[3] = {(uint64_t)cin_stride, (uint64_t)wp, (uint64_t)max_img * wp};
-        const uint32_t box[3] = {(uint32_t)bk, BOX_TW + 2, BOX_TH + 2};
-        rc = make_tmap(&L->tmA, in, 3, dims, box, swz, f16);
+        const uint32_t box[4] = {(uint32_t)bk, BOX_TW + 2, BOX_TH + 2, 1};
+        rc = make_tmap(&L->tmA, in, 4, dims, box, swz, f16);
       }
       if (rc) return rc;
       {
@@ -1797,18 +1882,14 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       L->box = 1 + epi;
       L->box_bk = bk;
       L->pair = 0;
-      if (staging) {  // output store map {cstride, wp, rows}, box {32 ch, 8 px, 4 rows}
-        const uint64_t dims[3] = {(uint64_t)out_cstride, (uint64_t)wp, (uint64_t)max_img * wp};
+      if (staging) {  // output store map {cstride, res, rows}, box {32 ch, 8 px, 4 rows}
+        const uint64_t dims[3] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)max_img * res};
         const uint32_t box[3] = {32, BOX_TW, 4};
         rc = make_tmap(&L->tmC, out, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_64B, f16);
         if (rc) return rc;
       }
       L->smem = 1024 + (size_t)st * stage + bres + staging + (2 * st + 10) * 8 + cout_pad * 4 + 16;
     }
-  }
-  if (cout_pad > kMaxBias) {
-    tp_set_error("conv: cout_pad %d exceeds %d", cout_pad, kMaxBias);
-    return TP_ERR_UNSUPPORTED;
   }
   return TP_OK;
 }
@@ -1927,11 +2008,10 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
     case EPI_F32: return launch_mode<M, EPI_F32>(L, n_img, n_img_dev, st);     \
     default: return launch_mode<M, EPI_PLAIN>(L, n_img, n_img_dev, st);        \
   }
-  switch (L.mode) {
-    case MODE_SW128: TP_EPI_SWITCH(MODE_SW128)
-    case MODE_SW64: TP_EPI_SWITCH(MODE_SW64)
-    default: TP_EPI_SWITCH(MODE_L0X)
+  if (L.mode == MODE_SW128) {
+    TP_EPI_SWITCH(MODE_SW128)
   }
+  TP_EPI_SWITCH(MODE_SW64)
 #undef TP_EPI_SWITCH
 }
 
@@ -1996,8 +2076,9 @@ const Step kSteps[] = {
 constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
 
 size_t buf_bytes(int b, int max_tiles) {
-  const size_t wp = kBufs[b].res + 2;
-  return (size_t)max_tiles * wp * wp * kBufs[b].ch * kBufs[b].bytes_per;
+  // compact NHWC, except the layer-0 input (padded, written by the gather)
+  const size_t side = kBufs[b].res + (b == I608 ? 2 : 0);
+  return (size_t)max_tiles * side * side * kBufs[b].ch * kBufs[b].bytes_per;
 }
 
 }  // namespace

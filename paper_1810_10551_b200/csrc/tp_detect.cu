@@ -42,7 +42,7 @@ __device__ Cand decode_one(const float* __restrict__ head, int cstride, int tile
                            const Anchors& an, float thresh) {
   const int cell = i / TP_ANCHORS, a = i - cell * TP_ANCHORS;
   const int row = cell / G, col = cell - row * G;
-  const float* v = head + (((long long)tile * (G + 2) + (row + 1)) * (G + 2) + (col + 1)) * cstride +
+  const float* v = head + (((long long)tile * G + row) * G + col) * cstride +
                    a * (5 + TP_CLASSES);
   Cand c;
   const float obj = sigmoid_rn(v[4]);

@@ -182,12 +182,12 @@ class YoloNet:
         return self.workspace[off: off + nbytes]
 
     def head_tensor(self, n_tiles: int):
-        """fp32 head view [n, 21, 21, 448] (padded, channels 425.. are zero)."""
+        """fp32 head view [n, 19, 19, 448] (compact, channels 425.. are zero)."""
         import torch
 
-        nb = n_tiles * 21 * 21 * self.head_cstride * 4
+        nb = n_tiles * 19 * 19 * self.head_cstride * 4
         return self._view(self.head_ptr, nb).view(torch.float32).view(
-            n_tiles, 21, 21, self.head_cstride)
+            n_tiles, 19, 19, self.head_cstride)
 
     def input_tensor(self, n_tiles: int):
         """16-bit expanded layer-0 input view [n, 610, 610, 16]."""
@@ -195,12 +195,12 @@ class YoloNet:
         return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 16)
 
     def step_tensor(self, step: int, n_tiles: int):
-        """16-bit view of a step's output buffer [n, R+2, R+2, C] (padded)."""
+        """16-bit view of a step's output buffer [n, R, R, C] (compact NHWC)."""
         addr, res, cs = self.layer_output(step)
         if step == len(STEPS) - 1:
             return self.head_tensor(n_tiles)
-        nb = n_tiles * (res + 2) * (res + 2) * cs * 2
-        return self._view(addr, nb).view(self.tdtype).view(n_tiles, res + 2, res + 2, cs)
+        nb = n_tiles * res * res * cs * 2
+        return self._view(addr, nb).view(self.tdtype).view(n_tiles, res, res, cs)
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -85,7 +85,7 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
         if src_step < 0:
             xin = net.input_tensor(n)[:, 1:-1, 1:-1, 4:7]
         else:
-            xin = net.step_tensor(src_step, n)[:, 1:-1, 1:-1, :]
+            xin = net.step_tensor(src_step, n)
         xin = xin.float().permute(0, 3, 1, 2)
         w = yolo_ref.unpack_weight(wpacks[li], li).cuda()
         b = torch.from_numpy(biases[li][:cout]).cuda()
@@ -95,7 +95,7 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
         if li in yolo.POOLED:
             ref = torch.nn.functional.max_pool2d(ref, 2)
         ref = ref.permute(0, 2, 3, 1)
-        out = net.step_tensor(step, n)[:, 1:-1, 1:-1, :].float()
+        out = net.step_tensor(step, n).float()
         if li == 20:  # reorg into channels [0,256) of the concat buffer
             ref = ref.reshape(n, 19, 2, 19, 2, 64).permute(0, 1, 3, 2, 4, 5).reshape(n, 19, 19, 256)
             out = out[..., :256]
@@ -115,7 +115,7 @@ def test_head_matches_cpu_oracle(cuda, net, tiles):
     n = _run(cuda, net, tiles)
     net.forward(n)
     torch.cuda.synchronize()
-    got = net.head_tensor(n)[:, 1:-1, 1:-1, :425].cpu().numpy()
+    got = net.head_tensor(n)[..., :425].cpu().numpy()
     wpacks, biases = yolo.make_weights(0, dtype=net.dtype)
     ref = yolo_ref.forward(tiles, wpacks, biases, mode=net.dtype)
     scale = np.abs(ref).max()
