@@ -46,7 +46,7 @@ METRIC = "frames/sec, synthetic 4K & 8K video, 1/2/4/8 B200; crops/sec; % roofli
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=30)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -103,19 +103,49 @@ def clip_objects(rank: int = 0, n_frames: int = 300):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled during the timed region (NVML in-process every
+    20 ms; nvidia-smi every 200 ms if NVML is unavailable)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                   "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index: int):
         self.index, self.samples, self.stop = index, [], threading.Event()
         self.t = threading.Thread(target=self._run, daemon=True)
+        self.nvml = None
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.nvml = pynvml
+        except Exception:
+            self.nvml = None
+
+    def _sample_nvml(self):
+        nv = self.nvml
+        mhz = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+        bits = int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle))
+        flags = ["Active" if bits & self.REASON_BITS[k] else "Not Active"
+                 for k in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                           "sw_power_cap")]
+        return [str(mhz), str(self.max_mhz)] + flags
 
     def _run(self):
         while not self.stop.is_set():
             try:
+                if self.nvml is not None:
+                    self.samples.append(self._sample_nvml())
+                    self.stop.wait(0.02)
+                    continue
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
@@ -134,7 +164,7 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -142,7 +172,7 @@ class ClockSampler:
                           if len(s) > i + 2 and s[i + 2].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def cpu_baseline_frames_per_sec(objs, n_frames=1):
@@ -319,6 +349,11 @@ def main():
     except Exception:
         pass
     peak = float(peaks.get("bf16_tflops_sustained", 1391.0))
+    traffic = {}
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_conv_traffic.json")))
+    except Exception:
+        pass
     stage1 = eng.A * B * args.steps if per_step == 2 else 0
     tiles_per_frame = (stage1 + float(t2[args.warmup:].sum())) / (args.steps * B)
     launches_per_step = (1 + 24 + 1 + 1) + 2 + (1 + 24 + 1 + 1) + 1
@@ -359,9 +394,15 @@ def main():
                        "l2": "inputs exceed L2 (746 MB per step)",
                        "tiles_per_frame": tiles_per_frame,
                        "crops_per_sec": value * tiles_per_frame},
-            "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (23 tcgen05 launches per YOLO "
-                         "forward, 4 with fused 2x2 maxpool, + 1 maxpool)", "achieved": conv_tflops, "peak": peak,
-                         "unit": "TFLOP/s", "frac": conv_tflops / peak, "traffic": None,
+            "roofline": {"bound": "tensor", "kernel": "YOLO v2 conv stack: 23 tcgen05 launches per "
+                         "forward (conv_l0_kernel, 3x conv_box_kernel, 14x conv_pair_kernel, "
+                         "5x conv_tc_kernel) + 1 maxpool", "achieved": conv_tflops, "peak": peak,
+                         "unit": "TFLOP/s", "frac": conv_tflops / peak,
+                         "traffic": traffic.get("dram_MB_per_tile", 0) * 1e6 if traffic else None,
+                         "traffic_unit": "DRAM bytes per 608^2 tile, ncu --set full capture "
+                                         "(profiles/r01_conv_traffic.json)",
+                         "algorithmic_bytes_per_tile": traffic.get("algorithmic_MB_per_tile", 0) * 1e6
+                         if traffic else None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "algorithmic": f"{yolo.GFLOP_PER_TILE:.3f} GFLOP per 608^2 tile",
                          "conv_share_of_step": fwd_ms / ms},
