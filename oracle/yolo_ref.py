@@ -57,8 +57,8 @@ def unpack_weight(wpack, li):
 
     _, cin, cout, k, _ = LAYERS[li]
     w = torch.as_tensor(np.asarray(wpack, dtype=np.float32))
-    if li == 0:  # K = dy(3) x [dx(3)+pad] x [rgb+pad]
-        w = w[:cout, :48].reshape(cout, 3, 4, 4)[:, :, :3, :cin].reshape(cout, 9, cin)
+    if li == 0:  # K = dy(3) x variant(3) x slot(4) x [rgb+pad]; variant 0 slots 0,1,3 = dx -1,0,1
+        w = w[:cout, :144].reshape(cout, 3, 3, 4, 4)[:, :, 0, [0, 1, 3], :cin].reshape(cout, 9, cin)
     else:
         w = w[:cout, : k * k * cin].reshape(cout, k * k, cin)
     return w.reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous()

@@ -4,30 +4,25 @@
 // pkg/src/tilepipe/detector.py:77-96); the topology is yolov2-608 (Darknet-19 +
 // passthrough head) as cited by PAPER.md:85,120, restated in oracle/yolo_ref.py.
 //
-// Activation layout ("padded NHWC"): every feature map of side R lives in a buffer
-// [tile][R+2][R+2][C] (fp16 or bf16) whose 1-pixel halo is zero and never written.
-// A 3x3/1 same conv is a GEMM over output pixels, K = taps x C, and the A operand of
-// tap (dy,dx) is a TMA box shifted by (dy,dx) — no im2col buffer:
-//   * FLAT tiles (non-pooled layers): M tile = 128 consecutive padded pixels; the
-//     shifted box is a plain 2-D box at row m0 + dy*(R+2) + dx. Rows on halo pixels
-//     compute garbage the epilogue never stores (waste = (R+2)^2/R^2).
-//   * RECT tiles (layers followed by a 2x2 maxpool): M tile = a 16x8 pixel rectangle
-//     loaded as a 3-D box {C, 16, 8}; the epilogue pools in registers (lane^1 and
-//     lane^16 shuffles) and writes the half-resolution map directly, so the
-//     full-resolution activation never touches HBM and no pool kernel runs.
-//   * Layer 0 (3 channels) reads a horizontally expanded input (gather writes, per
-//     pixel, [p(x-1) rgb0, p(x) rgb0, p(x+1) rgb0, 0000] = 32 bytes): one 32-byte-wide
-//     box per kernel row dy, K = 16 per MMA, 3 MMAs per tile.
+// Activation layout: compact NHWC [tile][R][R][C] (fp16 or bf16). A 3x3/1 same conv is a
+// GEMM over output pixels, K = taps x C; the zero padding is TMA out-of-bounds fill, so
+// no halo is stored and no M row is wasted on one:
+//   * FLAT tiles (conv_tc_kernel / conv_pair_kernel, non-pooled layers): M tile = 128
+//     consecutive compact pixels (256 for a CTA pair), A loaded per (tap, 64-channel
+//     block) with TMA im2col (window corner -1, tap = im2col offset).
+//   * RECT tiles (conv_tc_kernel, pooled 3x3 layers without a box variant): a 16x8 pixel
+//     rectangle loaded as a 4-D box {C, 16, 8, 1}; the epilogue pools in registers.
+//   * box tiles (conv_box_kernel: 3x3 with cin 32/64 and resident weights): one box
+//     {C, 10, 18} per 8x16 tile, the nine taps are descriptor row offsets into it.
+//   * layer 0 (conv_l0_kernel): reads the gather's padded 16-byte slots
+//     E(X) = [q(X-1) rgb0 | q(X) rgb0] as 32-byte-aligned windows of two slots; even
+//     columns take one MMA per kernel row, odd columns two (see the kernel comment).
 //
-// Kernel: persistent, warp-specialised, one CTA per SM (320 threads):
-//   warp 0      TMA producer (A box + B box per k-block into an S-stage smem ring)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256,
-//               K=16 per instruction, fp32 accumulate in TMEM, double-buffered)
-//   warps 2..9  epilogue: two warpgroups working on alternate tiles (one per TMEM
-//               accumulator), each warp covering one TMEM lane quadrant:
-//               tcgen05.ld -> +bias (BN folded) -> leaky(0.1) -> [2x2 max] -> 16-bit
-//               -> interior-only store (or channel-offset into the route concat
-//               buffer, space-to-depth "reorg", or fp32 for the head)
+// Kernels are persistent and warp-specialised, one CTA per SM (320 threads): warps 0-7
+// epilogue (two warpgroups on alternate accumulators, one TMEM lane quadrant per warp:
+// tcgen05.ld -> +bias (BN folded) -> leaky(0.1) -> [2x2 max] -> 16-bit -> TMA store or
+// direct store / reorg / fp32 head), warp 8 TMA producer, warp 9 TMEM allocator + MMA
+// issuer (warp-convergent loop, one elected lane issues tcgen05.mma).
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -876,12 +871,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ layer 0, pool-in-M
 // Layer 0 (3x3, 3->32, leaky, 2x2 maxpool) has K = 48 but 608^2 outputs per tile, so it
 // is bound by epilogue instructions, not math. Here each M row is one POOLED output
-// pixel: the four pool positions (py,px) accumulate into four TMEM accumulators, fed by
-// TMA boxes with traversal stride 2 in x and y over the expanded input ({16 ch, 32 x/2,
-// 18 y/2}). Per tile (16x8 pooled = 32x16 conv pixels): 4 boxes (x phase px, y phase f),
-// 12 MMAs (4 pool positions x 3 kernel rows, K=16, N=32); the epilogue reads 4 x 32
-// columns per row and does max + bias + leaky + pack per pooled value — ~4.6x fewer
-// instructions per conv output than pooling by shuffles.
+// pixel: the four pool positions (py,px) accumulate into four TMEM accumulators.
+// Input: 16-byte slots E(X) = [q(X-1) | q(X)], read as 32-byte-aligned windows
+// W(k) = E(2k) E(2k+1) = [q(2k-1) q(2k) q(2k) q(2k+1)] ({16 halves, k, row} view, rows at
+// traversal stride 2). Even conv columns x = 2k use W(k) with weights [w-1 w0 0 w+1];
+// odd columns x = 2k+1 use W(k) with [0 w-1 0 w0] plus W(k+1) with [0 w+1 0 0], so no
+// window ever straddles a 32-byte sector. Per tile (16x8 pooled = 32x16 conv pixels):
+// 4 boxes {16, 16 k, 9 rows} (row phase f x window shift 0/1), 18 MMAs (K=16, N=32);
+// the epilogue reads 4 x 32 columns per row and does max + bias + leaky + pack.
 constexpr int L0_BOX_ROWS = 9;                       // strided rows per box
 constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 32;  // 4608
 constexpr int L0_STAGE = 4 * L0_BOX_BYTES;           // 18432
@@ -894,8 +891,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   const int S = p.stages;
   uint8_t* smA = smem;
-  uint8_t* smB = smem + (size_t)S * L0_STAGE;  // resident weights: 3 chunks x 1 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + 3 * 1024);
+  uint8_t* smB = smem + (size_t)S * L0_STAGE;  // resident weights: 9 chunks x 1 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + 9 * 1024);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
@@ -939,8 +936,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kProdWarp) {
     if (lane == 0) {
       if (n_tiles > 0) {
-        tp::mbar_arrive_expect_tx(bres_bar, 3 * 1024);
-        for (int j = 0; j < 3; ++j) tp::tma_load_2d(smB + j * 1024, &tmB, bres_bar, j * 16, 0);
+        tp::mbar_arrive_expect_tx(bres_bar, 9 * 1024);  // chunk dy*3 + variant
+        for (int j = 0; j < 9; ++j) tp::tma_load_2d(smB + j * 1024, &tmB, bres_bar, j * 16, 0);
       }
       int s = 0;
       uint32_t ph = 0;
@@ -952,9 +949,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::mbar_arrive_expect_tx(&full[s], L0_STAGE);
         uint8_t* dst = smA + (size_t)s * L0_STAGE;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {  // b = px * 2 + y phase
-          const int px = b >> 1, f = b & 1;
-          tma_load_3d(dst + b * L0_BOX_BYTES, &tmA, &full[s], 0, 1 + 32 * bx + px,
+        for (int b = 0; b < 4; ++b) {  // b = window shift * 2 + y phase
+          const int sh = b >> 1, f = b & 1;
+          tma_load_3d(dst + b * L0_BOX_BYTES, &tmA, &full[s], 0, 16 * bx + sh,
                       img * hp + 1 + 16 * by + f - 1);
         }
         if (++s == S) {
@@ -986,9 +983,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int dy = 0; dy < 3; ++dy) {
               const int o = py + dy;  // input row offset + 1, in 0..3
-              const int box = px * 2 + (o & 1), start = o >> 1;
-              const uint32_t off16 = (box * L0_BOX_BYTES + start * 16 * 32) >> 4;
-              tp::mma_bf16(d, ad0 + off16, b_desc0 + dy * 64, p.idesc, dy != 0);
+              const int f = o & 1, start = o >> 1;
+              const uint32_t w0 = (f * L0_BOX_BYTES + start * 16 * 32) >> 4;        // W(k)
+              const uint32_t w1 = ((2 + f) * L0_BOX_BYTES + start * 16 * 32) >> 4;  // W(k+1)
+              const uint64_t bw = b_desc0 + (uint64_t)((dy * 3 + px) * 64);
+              tp::mma_bf16(d, ad0 + w0, bw, p.idesc, dy != 0);
+              if (px) tp::mma_bf16(d, ad0 + w1, bw + 64, p.idesc, 1);
             }
           }
           tp::mma_commit(&empty[s]);
@@ -1575,7 +1575,8 @@ int make_tmap_im2col(CUtensorMap* tm, const void* base, int cstride, int res, in
 // esize 2 = 16-bit (f16 selects fp16 vs bf16), 4 = fp32. Out-of-bounds reads are zero.
 int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
               const uint32_t* box, CUtensorMapSwizzle swz, bool f16, int esize = 2,
-              const uint32_t* elem_strides = nullptr) {
+              const uint32_t* elem_strides = nullptr,
+              const cuuint64_t* byte_strides = nullptr) {  // default: dense
   EncodeTiledFn enc = get_encode_fn();
   if (enc == nullptr) {
     tp_set_error("cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
@@ -1589,7 +1590,7 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
     gbox[i] = box[i];
     if (elem_strides != nullptr) estr[i] = elem_strides[i];
     if (i > 0) {
-      strides[i - 1] = stride;
+      strides[i - 1] = byte_strides != nullptr ? byte_strides[i - 1] : stride;
       stride *= dims[i];
     }
   }
@@ -1691,27 +1692,31 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     }
     const int wp = res + 2;
     {
-      const uint64_t dims[3] = {16, (uint64_t)wp, (uint64_t)max_img * wp};
-      const uint32_t box[3] = {16, 32, 18};
-      const uint32_t estr[3] = {1, 2, 2};
-      rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 2, estr);
+      // 16-byte slots E(X) = [q(X-1) | q(X)]; the kernel reads 32-byte-aligned windows
+      // W(k) = E(2k) E(2k+1): a {16 halves, k (32 B), row} view (conv_l0_kernel comment)
+      const uint64_t dims[3] = {16, (uint64_t)(wp / 2), (uint64_t)max_img * wp};
+      const cuuint64_t strides[2] = {32, (cuuint64_t)wp * 16};
+      const uint32_t box[3] = {16, 16, 18};
+      const uint32_t estr[3] = {1, 1, 2};
+      rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 2, estr,
+                     strides);
       if (rc) return rc;
     }
-    {
-      const uint64_t dims[2] = {48, 32};
+    {  // weights [32][144]: per kernel row dy, variants (even, odd W(k), odd W(k+1)) x K 16
+      const uint64_t dims[2] = {144, 32};
       const uint32_t box[2] = {16, 32};
       rc = make_tmap(&L->tmB, weight, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16);
       if (rc) return rc;
     }
     L->tmC = L->tmA;  // unused
     L->l0 = 1;
-    int st = (int)((227 * 1024 - fixed - 3 * 1024) / L0_STAGE);
+    int st = (int)((227 * 1024 - fixed - 9 * 1024) / L0_STAGE);
     if (st > 8) st = 8;
     p.stages = st;
     p.bn = 32;
     p.n_blocks_n = 1;
     p.idesc = tp::idesc_f16kind(128, 32, !f16);
-    L->smem = 1024 + (size_t)st * L0_STAGE + 3 * 1024 + (2 * st + 6) * 8 + 32 * 4 + 16;
+    L->smem = 1024 + (size_t)st * L0_STAGE + 9 * 1024 + (2 * st + 6) * 8 + 32 * 4 + 16;
     return TP_OK;
   }
 
@@ -2029,8 +2034,8 @@ int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStr
 
 // ------------------------------------------------------------------ YOLO v2-608 plan
 // Layer table (darknet layer index, cin, cout, ksize, res). BN is folded into
-// weights+bias by the host; layer 30 is linear (no BN, no leaky). Layer 0's cin is the
-// 16-channel expanded input (3 taps x 4 channels + 4 zeros per pixel).
+// weights+bias by the host; layer 30 is linear (no BN, no leaky). Layer 0's weights are
+// [32][144]: per kernel row, 3 variants (conv_l0_kernel comment) x 4 slots x rgb0.
 struct LayerDef {
   int idx, cin, cout, k, res;
 };
@@ -2051,7 +2056,7 @@ enum Buf {
 struct BufDef {
   int res, ch, bytes_per;  // bytes per element
 };
-const BufDef kBufs[NBUF] = {{608, 16, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
+const BufDef kBufs[NBUF] = {{608, 8, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
                             {152, 64, 2},  {76, 128, 2},  {76, 256, 2},   {76, 128, 2},
                             {38, 256, 2},  {38, 512, 2},  {38, 256, 2},   {38, 512, 2},
                             {19, 512, 2},  {19, 1024, 2}, {19, 512, 2},   {19, 1024, 2},

@@ -8,9 +8,10 @@
 //
 // One CTA per (tile, 8 output rows); a warp task is 32 consecutive columns of one row
 // (608 = 19 x 32, so a warp never straddles rows). Each lane produces one pixel: 3 bytes
-// of the u8 tile and/or the 32-byte horizontally expanded layer-0 input pixel
-// ([tile][610][610][16] = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000], fp16/bf16), so
-// every activation store is two full, aligned 16-byte vector stores and a warp writes 1 KB
+// of the u8 tile and/or one 16-byte slot of the layer-0 input ([tile][610][610][8],
+// fp16/bf16, zero 1-px halo): slot X of a row holds [q(X-1) rgb0 | q(X) rgb0] for tile
+// pixels q (zero outside [0, 608)), so slots x and x+1 are layer 0's 32-byte A row
+// [q(x-1) q(x) q(x) q(x+1)] — the conv's TMA map reads it through an overlapping view. Every store is one aligned 16-byte vector; a warp writes 512 B
 // contiguous. Index math is 32-bit (divisions by the constant 608 / 1216 become
 // multiply-highs); the value/255 table is built once per CTA. HBM-bound on the writes.
 #include "tp_common.cuh"
@@ -19,7 +20,7 @@
 namespace {
 
 constexpr int S = TP_MODEL_SIDE;
-constexpr int SP = S + 2;  // padded side of the layer-0 activation buffer
+constexpr int SP = S + 2;  // padded side of the layer-0 activation buffer (8 halves / slot)
 
 struct Tap {
   int i0, i1, f;  // source offsets (relative to crop origin) and 8-bit weight of i1
@@ -126,23 +127,18 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
     }
     if (out_act == nullptr) continue;
     const uint32_t me_rg = pk2(r, g), me_b0 = pk2(b, 0);
-    uint32_t l_rg = __shfl_up_sync(0xffffffffu, me_rg, 1), l_b0 = __shfl_up_sync(0xffffffffu, me_b0, 1);
     uint32_t r_rg = __shfl_down_sync(0xffffffffu, me_rg, 1), r_b0 = __shfl_down_sync(0xffffffffu, me_b0, 1);
-    if (lane == 0) {  // neighbours across the warp's edges are re-sampled
-      int rl, gl, bl;
-      sample(u - 1, rl, gl, bl);
-      l_rg = pk2(rl, gl);
-      l_b0 = pk2(bl, 0);
-    } else if (lane == 31) {
+    if (lane == 31) {  // the right neighbour across the warp's edge is re-sampled
       int rr, gr, br;
       sample(u + 1, rr, gr, br);
       r_rg = pk2(rr, gr);
       r_b0 = pk2(br, 0);
     }
-    // expanded layer-0 pixel: [p(u-1) rgb0 | p(u) rgb0 | p(u+1) rgb0 | 0 0 0 0]
-    __nv_bfloat16* o = out_act + (((size_t)t * SP + (v + 1)) * SP + (u + 1)) * 16;
-    *reinterpret_cast<uint4*>(o) = make_uint4(l_rg, l_b0, me_rg, me_b0);
-    *reinterpret_cast<uint4*>(o + 8) = make_uint4(r_rg, r_b0, 0u, 0u);
+    // slot u+1 of padded row v+1: [q(u) rgb0 | q(u+1) rgb0]
+    __nv_bfloat16* row_o = out_act + ((size_t)t * SP + (v + 1)) * SP * 8;
+    *reinterpret_cast<uint4*>(row_o + (u + 1) * 8) = make_uint4(me_rg, me_b0, r_rg, r_b0);
+    if (u == 0)  // slot 0: [q(-1) = 0 | q(0)]
+      *reinterpret_cast<uint4*>(row_o) = make_uint4(0u, 0u, me_rg, me_b0);
   }
 }
 

@@ -76,15 +76,25 @@ def round_to(a: np.ndarray, dtype: str) -> np.ndarray:
     return _bf16_round(a)
 
 
+# Layer 0 reads 32-byte windows W(k) = [q(2k-1) q(2k) q(2k) q(2k+1)] (4 pixel slots of
+# rgb0) of its 16-byte-slot input; per kernel row it has 3 weight variants over those
+# slots (csrc/tp_conv.cu conv_l0_kernel): even column x = 2k from W(k), odd column
+# x = 2k+1 from W(k) and W(k+1). Entry [variant][slot] = kernel column dx (-1/0/+1) or None.
+L0_VARIANTS = [(-1, 0, None, 1), (None, -1, None, 0), (None, 1, None, None)]
+
+
 def pack_weight(li: int, w: np.ndarray, dtype: str = "bf16") -> np.ndarray:
     """[cout][cin][k][k] -> packed K-major [cout_pad][K] (dtype-valued fp32)."""
     _, cin, cout, k, _ = LAYERS[li]
     cpad = HEAD_CPAD if li == HEAD else cout
     wt = np.transpose(w, (0, 2, 3, 1))  # cout, ky, kx, cin
-    if li == 0:  # expanded input: K = dy(3) x [dx(3)+pad] x [rgb+pad] = 3 x 4 x 4
-        full = np.zeros((cpad, 3, 4, 4), dtype=np.float32)
-        full[:cout, :, :3, :cin] = wt
-        return round_to(full.reshape(cpad, 48), dtype)
+    if li == 0:  # K = dy(3) x variant(3) x slot(4) x [rgb+pad](4) = 144
+        full = np.zeros((cpad, 3, 3, 4, 4), dtype=np.float32)
+        for v, slots in enumerate(L0_VARIANTS):
+            for s, dx in enumerate(slots):
+                if dx is not None:
+                    full[:cout, :, v, s, :cin] = wt[:, :, dx + 1, :]
+        return round_to(full.reshape(cpad, 144), dtype)
     full = np.zeros((cpad, k * k * cin), dtype=np.float32)
     full[:cout] = wt.reshape(cout, k * k * cin)
     return round_to(full, dtype)
@@ -190,9 +200,10 @@ class YoloNet:
             n_tiles, 19, 19, self.head_cstride)
 
     def input_tensor(self, n_tiles: int):
-        """16-bit expanded layer-0 input view [n, 610, 610, 16]."""
-        nb = n_tiles * 610 * 610 * 16 * 2
-        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 16)
+        """16-bit layer-0 input view [n, 610, 610, 8]: padded rows of 16-byte slots,
+        slot X = [q(X-1) rgb0 | q(X) rgb0] for tile pixels q (zero outside the tile)."""
+        nb = n_tiles * 610 * 610 * 8 * 2
+        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 8)
 
     def step_tensor(self, step: int, n_tiles: int):
         """16-bit view of a step's output buffer [n, R, R, C] (compact NHWC)."""

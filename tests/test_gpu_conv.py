@@ -10,7 +10,7 @@ relative) plus accumulation-order noise.
 import numpy as np
 import pytest
 
-from paper_1810_10551_b200 import native
+from paper_1810_10551_b200 import native, yolo
 
 pytestmark = pytest.mark.gpu
 
@@ -119,28 +119,27 @@ def test_conv_fused_pool_rect_tiles(cuda, cin, cout, res, dtype):
 
 
 def test_conv_layer0_expanded_input(cuda):
-    """Layer-0 mode: padded input pixel = [p(x-1) rgb0 | p(x) rgb0 | p(x+1) rgb0 | 0000],
-    compact pooled output."""
+    """Layer-0 mode: padded rows of 16-byte slots, slot X = [q(X-1) rgb0 | q(X) rgb0]
+    (TMA pairs slots x and x+2 into the 32-byte A row); compact pooled output."""
     torch = cuda
     n, res = 2, 64
     g = torch.Generator(device="cpu").manual_seed(4)
     img = torch.rand(n, res, res, 3, generator=g).half().float()
-    ex = torch.zeros(n, res + 2, res + 2, 16)
-    ex[:, 1:-1, 1:-1, 4:7] = img
-    ex[:, 1:-1, 2:-1, 0:3] = img[:, :, :-1]
-    ex[:, 1:-1, 1:-2, 8:11] = img[:, :, 1:]
+    qpad = torch.zeros(n, res, res + 2, 3)
+    qpad[:, :, 1:-1] = img
+    ex = torch.zeros(n, res + 2, res + 2, 8)
+    ex[:, 1:-1, 0:res + 1, 0:3] = qpad[:, :, 0:res + 1]
+    ex[:, 1:-1, 0:res + 1, 4:7] = qpad[:, :, 1:res + 2]
     ex = ex.half().cuda()
     w = torch.randn(32, 3, 3, 3, generator=g) * 0.3  # cout, ky, kx, cin
-    wpack = torch.zeros(32, 3, 4, 4)
-    wpack[:, :, :3, :3] = w
-    wpack = wpack.reshape(32, 48).half().cuda()
+    wpack = torch.from_numpy(yolo.pack_weight(0, w.permute(0, 3, 1, 2).numpy(), "fp16")).half().cuda()
     bias = (torch.randn(32, generator=g) * 0.1).cuda()
     out = torch.zeros(n, res // 2, res // 2, 32, dtype=torch.float16, device="cuda")
     native.call("tp_conv", native.ptr(ex), n, res, 16, native.ptr(wpack), native.ptr(bias), 32,
                 32, 3, 1, native.ptr(out), 32, 0, 0, 0, native.DTYPES["fp16"], 1,
                 native.stream_handle())
     torch.cuda.synchronize()
-    wq = wpack.float().reshape(32, 3, 4, 4)[:, :, :3, :3].permute(0, 3, 1, 2)
+    wq = w.permute(0, 3, 1, 2).half().float().cuda()
     ref = torch.nn.functional.conv2d(img.cuda().permute(0, 3, 1, 2), wq, bias, padding=1)
     ref = torch.nn.functional.max_pool2d(torch.where(ref > 0, ref, 0.1 * ref), 2)
     _check(torch, out, ref.permute(0, 2, 3, 1), rel=3e-3)

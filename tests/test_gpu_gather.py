@@ -75,15 +75,16 @@ def test_gather_bf16_activation_layout(cuda):
     rng = np.random.default_rng(9)
     frame = rng.integers(0, 256, (700, 900, 3), np.uint8)
     jobs = kernels.jobs_tensor([(0, 0, 50, 40, 640, 0)])
-    act = torch.zeros((1, 610, 610, 16), dtype=torch.bfloat16, device="cuda")
+    act = torch.zeros((1, 610, 610, 8), dtype=torch.bfloat16, device="cuda")
     u8 = torch.empty((1, 608, 608, 3), dtype=torch.uint8, device="cuda")
     kernels.gather(torch.from_numpy(frame).cuda(), 0, 700, 900, jobs, 1, "bilinear", out_u8=u8,
                    out_act_ptr=act.data_ptr())
     ref = torch.from_numpy(resample_ref.cut_tile_bilinear(frame, 50, 40, 640)).float() / 255.0
     ref = ref.to(torch.bfloat16).float()
-    got = act[0, 1:-1, 1:-1].cpu().float()
-    assert torch.equal(got[..., 4:7], ref)
-    assert torch.equal(got[:, 1:, 0:3], ref[:, :-1]) and torch.equal(got[:, :-1, 8:11], ref[:, 1:])
-    assert got[:, 0, 0:3].abs().max().item() == 0 and got[:, -1, 8:11].abs().max().item() == 0
-    assert got[..., [3, 7, 11, 12, 13, 14, 15]].abs().max().item() == 0
-    assert act[0, 0].abs().max().item() == 0 and act[0, :, 609].abs().max().item() == 0
+    # slot X of padded row v+1 = [q(X-1) rgb0 | q(X) rgb0], q = tile pixel (0 outside)
+    got = act[0, 1:-1].cpu().float()
+    assert torch.equal(got[:, 1:609, 0:3], ref) and torch.equal(got[:, 0:608, 4:7], ref)
+    assert got[:, 0, 0:3].abs().max().item() == 0 and got[:, 608, 4:7].abs().max().item() == 0
+    assert got[..., [3, 7]].abs().max().item() == 0
+    assert act[0, 0].abs().max().item() == 0 and act[0, -1].abs().max().item() == 0
+    assert act[0, :, 609].abs().max().item() == 0

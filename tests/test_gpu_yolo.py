@@ -53,13 +53,12 @@ def _run(cuda, net, tiles):
 def test_input_normalisation_matches_oracle(cuda, net, tiles):
     torch = cuda
     n = _run(cuda, net, tiles)
-    x = net.input_tensor(n)[:, 1:-1, 1:-1, :].float().cpu()
+    x = net.input_tensor(n)[:, 1:-1].float().cpu()  # interior rows, slots 0..609
     ref = yolo_ref.tiles_to_input(tiles, net.dtype).permute(0, 2, 3, 1)
-    assert torch.equal(x[..., 4:7], ref)                    # p(x)
-    assert torch.equal(x[:, :, 1:, 0:3], ref[:, :, :-1])     # p(x-1)
-    assert torch.equal(x[:, :, :-1, 8:11], ref[:, :, 1:])    # p(x+1)
-    assert x[:, :, 0, 0:3].abs().max().item() == 0 and x[:, :, -1, 8:11].abs().max().item() == 0
-    assert x[..., [3, 7, 11, 12, 13, 14, 15]].abs().max().item() == 0
+    assert torch.equal(x[:, :, 1:609, 0:3], ref)            # slot X: q(X-1)
+    assert torch.equal(x[:, :, 0:608, 4:7], ref)            # slot X: q(X)
+    assert x[:, :, 0, 0:3].abs().max().item() == 0 and x[:, :, 608, 4:7].abs().max().item() == 0
+    assert x[..., [3, 7]].abs().max().item() == 0 and x[:, :, 609].abs().max().item() == 0
 
 
 def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
@@ -83,7 +82,7 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
         src_step = conv_inputs[step]
         _, cin, cout, k, res = yolo.LAYERS[li]
         if src_step < 0:
-            xin = net.input_tensor(n)[:, 1:-1, 1:-1, 4:7]
+            xin = net.input_tensor(n)[:, 1:-1, 0:608, 4:7]
         else:
             xin = net.step_tensor(src_step, n)
         xin = xin.float().permute(0, 3, 1, 2)
