@@ -16,7 +16,8 @@ frame's share of the H2D copy, ``attention_wait_ms`` its share of stage 1, ...,
 from __future__ import annotations
 
 import json
-from collections.abc import Iterable, Sequence
+from collections.abc import Sequence
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -34,18 +35,31 @@ class StreamAborted(RuntimeError):
         self.completed = tuple(completed)
 
 
-def run_stream(frames: Iterable, settings: PipelineSettings, det=None,
-               policy: MergePolicy | None = None, *, batch: int = 16, engine=None
-               ) -> list[FrameResult]:
-    """Evaluate a frame stream on the GPU, in input order, with ingest overlapped."""
+def run_stream(frames, settings: PipelineSettings, det=None,
+               policy: MergePolicy | None = None, *, batch: int = 16, engine=None,
+               io_threads: int = 8) -> list[FrameResult]:
+    """Evaluate a frame stream on the GPU, in input order, with ingest overlapped.
+
+    ``frames`` is an iterable of ``Frame`` s or a ``frameio.FrameSource`` (a directory of
+    PPM files): source frames are read from disk straight into the pinned staging buffer
+    on ``io_threads`` host threads while the GPU runs the previous batch."""
     from .engine import AttentionPipelineB200
     from .yolo import YoloB200Detector
 
     torch = native.require_cuda()
-    frames = list(frames)
-    if not frames:
+    if hasattr(frames, "load_into"):  # FrameSource
+        source = frames
+        W, H = source.width, source.height
+        items = [(fid, (lambda out, i=i: source.load_into(i, out)))
+                 for i, fid in enumerate(source.frame_ids)]
+    else:
+        frames = list(frames)
+        if not frames:
+            return []
+        W, H = frames[0].width, frames[0].height
+        items = [(fr.frame_id, _frame_loader(fr, W, H)) for fr in frames]
+    if not items:
         return []
-    W, H = frames[0].width, frames[0].height
     if engine is None:
         det = det or YoloB200Detector()
         engine = AttentionPipelineB200(settings, W, H, max_frames=batch, seed=det.seed,
@@ -60,18 +74,16 @@ def run_stream(frames: Iterable, settings: PipelineSettings, det=None,
     copy_start = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     used = [torch.cuda.Event() for _ in range(2)]
     results: list[FrameResult] = []
-    chunks = [frames[i:i + B] for i in range(0, len(frames), B)]
+    chunks = [items[i:i + B] for i in range(0, len(items), B)]
+    pool = ThreadPoolExecutor(max_workers=max(1, io_threads))
 
     def stage_chunk(k: int) -> None:
         slot = k % 2
         chunk = chunks[k]
-        for j, fr in enumerate(chunk):
-            if fr.width != W or fr.height != H:
-                raise ValueError(f"frame {fr.frame_id} is {fr.width}x{fr.height}, "
-                                 f"stream is {W}x{H}")
-            if fr.pixels is None:
-                raise ValueError(f"frame {fr.frame_id} has no pixels")
-            stage[slot][j].numpy()[...] = fr.pixels
+        copied[slot].synchronize()  # the H2D that last read this staging slot is done
+        futs = [pool.submit(load, stage[slot][j].numpy()) for j, (_, load) in enumerate(chunk)]
+        for f in futs:
+            f.result()  # re-raises the first decode / dimension / missing-file error
         with torch.cuda.stream(copy_stream):
             copy_stream.wait_event(used[slot])
             copy_start[slot].record(copy_stream)
@@ -100,14 +112,28 @@ def run_stream(frames: Iterable, settings: PipelineSettings, det=None,
             timing = TimingProfile(io_ms=io, attention_wait_ms=t[0], client_processing_ms=t[1],
                                    final_eval_ms=t[2], postprocess_ms=t[3],
                                    per_worker=((dev_name, busy),))
-            for res, _ in engine.results([f.frame_id for f in chunk], timing):
+            for res, _ in engine.results([fid for fid, _ in chunk], timing):
                 results.append(res)
             cursor += n
             if staging_error is not None:
                 raise staging_error
     except Exception as exc:
         raise StreamAborted(cursor, results, str(exc)) from exc
+    finally:
+        pool.shutdown(wait=True)
     return results
+
+
+def _frame_loader(fr, W: int, H: int):
+    """Staging callback for an in-memory Frame (validated when it is staged)."""
+    def load(out) -> None:
+        if fr.width != W or fr.height != H:
+            raise ValueError(f"frame {fr.frame_id} is {fr.width}x{fr.height}, "
+                             f"stream is {W}x{H}")
+        if fr.pixels is None:
+            raise ValueError(f"frame {fr.frame_id} has no pixels")
+        out[...] = fr.pixels
+    return load
 
 
 def _detection_json(d) -> str:

@@ -245,3 +245,23 @@ def test_run_stream_equals_run_sequence_and_aborts_with_cursor(cuda, clip):
     with pytest.raises(StreamAborted) as ei:
         run_stream(bad, settings, batch=2)
     assert ei.value.cursor == 2 and len(ei.value.completed) == 2
+
+
+def test_run_stream_from_disk_equals_in_memory(cuda, clip, tmp_path):
+    """§8f-2: a FrameSource (PPM directory) streamed from disk straight into pinned staging
+    gives the same results as the in-memory frames; a corrupt file aborts at its batch."""
+    from paper_1810_10551_b200.frameio import FrameSource, frame_file_name, write_ppm
+    from paper_1810_10551_b200.stream import StreamAborted, run_stream
+
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    for fr in clip:
+        write_ppm(tmp_path / frame_file_name(fr.frame_id), fr.pixels)
+    src = FrameSource.open(tmp_path)
+    mem = run_stream(clip, settings, batch=2)
+    disk = run_stream(src, settings, batch=2)
+    assert [(r.frame_id, r.detections, r.active_count, r.total_count) for r in disk] == \
+        [(r.frame_id, r.detections, r.active_count, r.total_count) for r in mem]
+    (tmp_path / frame_file_name(clip[2].frame_id)).write_bytes(b"P6\n1 1\n255\n")
+    with pytest.raises(StreamAborted) as ei:
+        run_stream(FrameSource.open(tmp_path), settings, batch=2)
+    assert ei.value.cursor == 2 and len(ei.value.completed) == 2
