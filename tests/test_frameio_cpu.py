@@ -122,3 +122,38 @@ def test_results_and_timing_files(tmp_path):
     (tmp_path / "bad.jsonl").write_text('{"frame_id": 1}\n')
     with pytest.raises(ValueError):
         read_results(tmp_path / "bad.jsonl")
+
+
+def test_ground_truth_round_trip_and_run_config(tmp_path):
+    from paper_1810_10551_b200.detector import GroundTruthObject
+    from paper_1810_10551_b200.frameio import read_ground_truth, read_run_config, write_ground_truth
+
+    gt = {2: [GroundTruthObject(Rect(10, 20, 30.5, 40), "car", "c1")],
+          0: [GroundTruthObject(Rect(1, 2, 3, 4), "person", "p1")]}
+    write_ground_truth(gt, tmp_path / "gt.jsonl")
+    first = (tmp_path / "gt.jsonl").read_text().splitlines()[0]
+    assert first == '{"class":"person","frame_id":0,"h":4,"object_id":"p1","w":3,"x":1,"y":2}'
+    back = read_ground_truth(tmp_path / "gt.jsonl")
+    assert sorted(back) == [0, 2] and back[2][0].rect.w == 30.5
+    (tmp_path / "frames").mkdir()
+    write_ppm(tmp_path / "frames" / frame_file_name(0), np.zeros((8, 16, 3), np.uint8))
+    cfg = tmp_path / "run.ini"
+    cfg.write_text("[pipeline]\npreset = 1 att, 3 fin, 20 over\n[detector]\nkind = yolo-b200\n"
+                   "batch = 4\n[paths]\nframes = frames\nresults = out.jsonl\n")
+    rc = read_run_config(cfg)
+    assert rc.detector == "yolo-b200" and rc.batch == 4 and rc.ground_truth_path is None
+    assert rc.frames_dir == (tmp_path / "frames").resolve()
+    cfg.write_text("[pipeline]\npreset = 1 att, 3 fin, 20 over\n[detector]\nkind = oracle\n"
+                   "[paths]\nresults = out.jsonl\n[frame]\nwidth = 64\nheight = 32\n")
+    with pytest.raises(ValueError):  # oracle needs ground truth
+        read_run_config(cfg)
+    cfg.write_text("[pipeline]\npreset = 1 att, 3 fin, 20 over\n[detector]\nkind = remote\n"
+                   "[paths]\nground_truth = gt.jsonl\nresults = out.jsonl\n[frame]\nwidth = 64\n"
+                   "height = 32\n")
+    with pytest.raises(ValueError, match="remote"):
+        read_run_config(cfg)
+    cfg.write_text("[pipeline]\nattention_rows = 1\nfinal_rows = 3\noverlap_px = 20\n"
+                   "[detector]\nkind = oracle\nvisibility_threshold = 0.5\n[paths]\n"
+                   "ground_truth = gt.jsonl\nresults = out.jsonl\n[frame]\nwidth = 64\nheight = 32\n")
+    rc = read_run_config(cfg)
+    assert rc.settings.preset_name() == "1 att, 3 fin, 20 over" and rc.visibility_threshold == 0.5

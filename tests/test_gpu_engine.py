@@ -265,3 +265,38 @@ def test_run_stream_from_disk_equals_in_memory(cuda, clip, tmp_path):
     with pytest.raises(StreamAborted) as ei:
         run_stream(FrameSource.open(tmp_path), settings, batch=2)
     assert ei.value.cursor == 2 and len(ei.value.completed) == 2
+
+
+def test_cli_run_yolo_b200_and_oracle(cuda, clip, tmp_path, capsys):
+    """§8f-3: `cli run` with detector kind yolo-b200 (frames dir -> run_stream) writes the
+    same result lines as run_stream; kind oracle equals run_sequence with the scene oracle."""
+    from paper_1810_10551_b200 import cli
+    from paper_1810_10551_b200.frameio import (frame_file_name, read_results, write_ground_truth,
+                                               write_ppm)
+    from paper_1810_10551_b200.stream import result_line, run_stream
+
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    (tmp_path / "frames").mkdir()
+    for fr in clip:
+        write_ppm(tmp_path / "frames" / frame_file_name(fr.frame_id), fr.pixels)
+    (tmp_path / "y.ini").write_text(
+        "[pipeline]\npreset = 1 att, 3 fin, 20 over\n[detector]\nkind = yolo-b200\nbatch = 2\n"
+        "[paths]\nframes = frames\nresults = y.jsonl\n")
+    assert cli.main(["run", "--config", str(tmp_path / "y.ini")]) == 0
+    assert "mode=pipeline frames=3" in capsys.readouterr().out
+    ref = [result_line(r) for r in run_stream(clip, settings, batch=2)]
+    assert (tmp_path / "y.jsonl").read_text().splitlines() == ref
+    assert (tmp_path / "y_timing.csv").is_file()
+
+    gt = synthetic.generate_scene(synthetic.SceneSpec("dense", 3840, 2160, 3, seed=0))
+    write_ground_truth(gt, tmp_path / "gt.jsonl")
+    (tmp_path / "o.ini").write_text(
+        "[pipeline]\npreset = 1 att, 3 fin, 20 over\n[detector]\nkind = oracle\n"
+        "[paths]\nground_truth = gt.jsonl\nresults = o.jsonl\n[frame]\nwidth = 3840\n"
+        "height = 2160\n")
+    assert cli.main(["run", "--config", str(tmp_path / "o.ini")]) == 0
+    oracle = P.oracle_for_scene(3840, 2160, settings, gt)
+    frames = [P.Frame(i, 3840, 2160) for i in sorted(gt)]
+    want = [result_line(r) for r in P.run_sequence(frames, settings, oracle)]
+    assert (tmp_path / "o.jsonl").read_text().splitlines() == want
+    assert [r.frame_id for r in read_results(tmp_path / "o.jsonl")] == sorted(gt)
