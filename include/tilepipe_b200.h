@@ -193,6 +193,20 @@ TP_API int tp_render_frames(const int32_t* rects, const uint8_t* colors, const i
                             int n_frames, int max_obj, int H, int W, uint32_t bg_rgb,
                             uint8_t* out, void* stream);
 
+/* fp32-parity mode (no reference counterpart; serves the north-star 1e-3 score bar):
+ * activations as exact fp16 pairs hi = fp16(x), lo = fp16(x - hi) in a doubled channel
+ * dimension [hi C | lo C] so the 16-bit tcgen05 convs (weights duplicated over both halves,
+ * fp32 epilogue) carry ~22-bit activations.
+ * tp_split_store: fp32 conv output [n][res][res][src_cstride] (C channels used) -> optional
+ * 2x2 max pool or space-to-depth reorg -> dst fp16 compact [n][res'][res'][dst_cstride],
+ * hi at channel coff + c, lo at coff + c + lo_off.
+ * tp_split_input: u8 tiles [n][608][608][3] -> fp16 [n][608][608][32], channels 0..2 =
+ * hi(v/255), 16..18 = lo(v/255), the rest 0. */
+TP_API int tp_split_store(const float* src, int n, int res, int src_cstride, int C, int pool,
+                          int reorg, void* dst, int dst_cstride, int coff, int lo_off,
+                          void* stream);
+TP_API int tp_split_input(const uint8_t* tiles, int n, void* dst, void* stream);
+
 /* Profiling only (TP_CONV_DEBUG bit 32 set in the environment when the net/conv runs):
  * per-role cycle totals of conv_tc_kernel summed over CTAs — 0 producer, 1 producer
  * empty-wait, 2 MMA issuer, 3 issuer accumulator-wait, 4 issuer stage-wait, 5 epilogue

@@ -89,7 +89,7 @@ def forward(tiles_u8, weights, biases, mode="bf16", threads=None, return_feature
     rnd = ROUND[mode]
     feats = {}
     with torch.no_grad():
-        x = tiles_to_input(tiles_u8, mode if mode != "fp32" else "bf16")
+        x = tiles_to_input(tiles_u8, mode)  # fp32: exact v/255, no rounding anywhere
 
         def conv(li, inp, linear=False):
             _, cin, cout, k, _ = LAYERS[li]

@@ -24,7 +24,7 @@ from .geometry import Rect
 from .pipeline_types import AttentionModel, FrameResult, GridPlan, PipelineSettings, \
     StageFailure, TimingProfile
 from .postprocess import LabelTable, MergePolicy, make_policy_struct, ctypes_ref
-from .yolo import COCO_NAMES, DEFAULT_PRECISION, YoloNet
+from .yolo import COCO_NAMES, DEFAULT_PRECISION, SplitNet, YoloNet
 
 MAX_BOXES = 256        # attention boxes per frame (conf >= min_conf)
 MAX_MERGED = 512       # merged window boxes per frame
@@ -55,8 +55,15 @@ class AttentionPipelineB200:
             raise ValueError("final grid too large for the selection/merge kernels")
         mf = self.max_frames
         self.max_tiles = mf * max(self.A, self.F)
-        self.net = net if net is not None else YoloNet(self.max_tiles, seed=seed, head=head,
-                                                       dtype=precision)
+        if net is None:  # precision "fp32" = hi/lo fp16 activation pairs (yolo.SplitNet)
+            net = (SplitNet(self.max_tiles, seed=seed, head=head) if precision == "fp32"
+                   else YoloNet(self.max_tiles, seed=seed, head=head, dtype=precision))
+        self.net = net
+        self.tiles_u8 = None
+        if hasattr(net, "load_tiles"):  # the split input is built from u8 tiles
+            torch = native.require_cuda()
+            self.tiles_u8 = torch.empty((self.max_tiles, 608, 608, 3), dtype=torch.uint8,
+                                        device="cuda")
         self.dtype = self.net.dtype
         if self.net.max_tiles < self.max_tiles:
             raise ValueError("shared YoloNet too small for this batch size")
@@ -165,12 +172,22 @@ class AttentionPipelineB200:
             self._stage1(fr, n, stream, st)
         self._finish(fr, n, stream, st, timed)
 
+    def _gather(self, fr, jobs, n_tiles, n_jobs_dev, stream):
+        """Crop gather into the net's layer-0 input (fp32-parity nets: u8 tiles + split)."""
+        if self.tiles_u8 is None:
+            kernels.gather(fr, self.frame_stride, self.H, self.W, jobs, n_tiles, self.resample,
+                           out_act_ptr=self.net.input_ptr, n_jobs_dev=n_jobs_dev, stream=stream,
+                           dtype=self.dtype)
+        else:
+            kernels.gather(fr, self.frame_stride, self.H, self.W, jobs, n_tiles, self.resample,
+                           out_u8=self.tiles_u8, n_jobs_dev=n_jobs_dev, stream=stream)
+            self.net.load_tiles(self.tiles_u8, n_tiles, stream)
+
     def _stage1(self, fr, n, stream, st):
         K1 = self.K - 1
         try:
             nt1 = n * self.A
-            kernels.gather(fr, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
-                           self.resample, out_act_ptr=self.net.input_ptr, stream=stream, dtype=self.dtype)
+            self._gather(fr, self.att_jobs, nt1, None, stream)
             self.net.forward(nt1, stream=stream)
             kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
                            self.dets1, self.counts1, stream=stream)
@@ -203,9 +220,7 @@ class AttentionPipelineB200:
             if timed:
                 ev[2].record(stream)
             nt2 = n * self.F  # upper bound; kernels read the real count from n_jobs2
-            kernels.gather(fr, self.frame_stride, self.H, self.W, self.jobs2, nt2, self.resample,
-                           out_act_ptr=self.net.input_ptr, n_jobs_dev=self.n_jobs2, stream=stream,
-                           dtype=self.dtype)
+            self._gather(fr, self.jobs2, nt2, self.n_jobs2, stream)
             self.net.forward(nt2, n_tiles_dev=self.n_jobs2, stream=stream)
             kernels.decode(self.net, nt2, self.jobs2, self.W, self.H, self.threshold, self.dets2,
                            self.counts2, n_tiles_dev=self.n_jobs2, stream=stream)
@@ -261,8 +276,7 @@ class AttentionPipelineB200:
         nt1 = self.A
         K1 = self.K - 1
         try:
-            kernels.gather(self.frames, self.frame_stride, self.H, self.W, self.att_jobs, nt1,
-                           self.resample, out_act_ptr=self.net.input_ptr, dtype=self.dtype)
+            self._gather(self.frames, self.att_jobs, nt1, None, None)
             self.net.forward(nt1)
             kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
                            self.dets1, self.counts1)
@@ -363,8 +377,13 @@ def yolo_tagged(det, frame, crops):
         n = len(chunk)
         jobs = kernels.jobs_tensor((0, c.crop_id, int(c.global_rect.x), int(c.global_rect.y),
                                     int(c.global_rect.w), 0) for c in chunk)
-        kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr,
-                       dtype=net.dtype)
+        if hasattr(net, "load_tiles"):
+            u8 = torch.empty((n, 608, 608, 3), dtype=torch.uint8, device="cuda")
+            kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_u8=u8)
+            net.load_tiles(u8, n)
+        else:
+            kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr,
+                           dtype=net.dtype)
         net.forward(n)
         recs, counts = kernels.alloc_dets(n)
         kernels.decode(net, n, jobs, W, H, det.threshold, recs, counts)

@@ -97,6 +97,8 @@ SIGNATURES = {
     "tp_postprocess": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "tp_maxpool2": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "tp_debug_conv_counters": (_I, [_P, _I, _I]),
+    "tp_split_store": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P]),
+    "tp_split_input": (_I, [_P, _I, _P, _P]),
     "tp_render_frames": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_uint32, _P, _P]),
 }
 
