@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--resample", default="nearest", choices=["nearest", "bilinear"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"],
+                    help="activation precision (fp32 = hi/lo fp16 pairs, the parity mode)")
     ap.add_argument("--profile", action="store_true",
                     help="torch.profiler kernel table of the timed steps to stderr (not a bench run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -246,7 +248,8 @@ def main():
     objs = clip_objects(rank, args.clip_frames)
     n_clip = len(objs)
     settings = P.PipelineSettings.from_preset(args.preset)
-    eng = AttentionPipelineB200(settings, W, H, max_frames=B, resample=args.resample)
+    eng = AttentionPipelineB200(settings, W, H, max_frames=B, resample=args.resample,
+                                precision=args.precision)
     clip = torch.empty((n_clip, H, W, 3), dtype=torch.uint8, device="cuda")
     for i in range(0, n_clip, 10):
         synthetic.render_frames_device(W, H, objs[i:i + 10], out=clip[i:i + 10])
@@ -381,8 +384,11 @@ def main():
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": yolo.DEFAULT_PRECISION, "data": "synthetic",
-            "precision": "fp16 operands/activations, fp32 accumulation (tcgen05 kind::f16)",
+            "dtype": args.precision, "data": "synthetic",
+            "precision": ("fp16 operands/activations, fp32 accumulation (tcgen05 kind::f16)"
+                          if args.precision != "fp32" else
+                          "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
+                          "accumulation and epilogue"),
             "config": {"workload": f"{args.frame.upper()} "
                                    f"{'all-crops baseline' if args.mode == 'allcrops' else 'attention pipeline'}"
                                    f"{'' if args.density is None else f' (injected stage-1, density {args.density})'}"

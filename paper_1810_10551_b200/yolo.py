@@ -295,7 +295,11 @@ class SplitNet:
                     native.stream_handle(stream))
 
     def forward(self, n_tiles: int, n_tiles_dev=None, stream=None) -> None:
-        n = int(n_tiles)  # n_tiles_dev is ignored: the whole capacity n is evaluated
+        n = int(n_tiles)
+        if n_tiles_dev is not None:  # parity mode: one host read of the device tile count
+            torch = native.require_cuda()
+            with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                n = min(n, int(n_tiles_dev.item()))
         st = native.stream_handle(stream)
         fp16 = native.DTYPES["fp16"]
         for li, (src, dst, coff, pool, reorg) in enumerate(_SPLIT_PLAN):
