@@ -6,14 +6,15 @@
 // north-star downscale: 8-bit fixed-point weights, half-pixel centres, identical
 // integer arithmetic to oracle/resample_ref.py so it is bit-exact as well.
 //
-// One CTA per (tile, 8 output rows); a warp task is 32 consecutive columns of one row
+// One CTA per (tile, 16 output rows); a warp task is 32 consecutive columns of one row
 // (608 = 19 x 32, so a warp never straddles rows). Each lane produces one pixel: 3 bytes
 // of the u8 tile and/or one 16-byte slot of the layer-0 input ([tile][610][610][8],
 // fp16/bf16, zero 1-px halo): slot X of a row holds [q(X-1) rgb0 | q(X) rgb0] for tile
 // pixels q (zero outside [0, 608)), so slots x and x+1 are layer 0's 32-byte A row
 // [q(x-1) q(x) q(x) q(x+1)] — the conv's TMA map reads it through an overlapping view. Every store is one aligned 16-byte vector; a warp writes 512 B
-// contiguous. Index math is 32-bit (divisions by the constant 608 / 1216 become
-// multiply-highs); the value/255 table is built once per CTA. HBM-bound on the writes.
+// contiguous. Column source offsets / bilinear taps and the value/255 table are built
+// once per CTA in shared memory; a pixel then costs a table read, its byte loads, LUT
+// lookups, one shuffle pair and a 16-byte store.
 #include "tp_common.cuh"
 #include "../../include/tilepipe_b200.h"
 
@@ -39,20 +40,8 @@ __device__ __forceinline__ Tap bilinear_tap(int u, int side) {
   return t;
 }
 
-__device__ __forceinline__ void load_px(const uint8_t* __restrict__ frame, int H, int W, int gx,
-                                        int gy, int& r, int& g, int& b) {
-  if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-    const uint8_t* p = frame + ((size_t)gy * W + gx) * 3;
-    r = p[0];
-    g = p[1];
-    b = p[2];
-  } else {
-    r = g = b = 0;
-  }
-}
-
-constexpr int GATHER_ROWS = 8;  // output rows per CTA
-constexpr int SEGS = S / 32;      // 19 warp tasks per row
+constexpr int GATHER_ROWS = 16;  // output rows per CTA (amortises the column tables)
+constexpr int SEGS = S / 32;       // 19 warp tasks per row
 
 __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ frames,
                                                      int64_t frame_stride, int H, int W,
@@ -66,9 +55,15 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
   const tp_tile_job_t job = jobs[t];
   const uint8_t* frame = frames + (int64_t)job.frame * frame_stride;
   const int side = job.side;
+  const bool nearest = mode == TP_RESAMPLE_NEAREST;
 
-  // exact value/255 in the activation type, looked up instead of divided (bit-identical)
+  // Per-CTA tables, shared by all GATHER_ROWS rows of this tile:
+  //   lut: exact value/255 in the activation type (bit-identical to dividing)
+  //   cx0/cx1: byte offset 3*x of the column's source tap(s) in a frame row, -1 outside
+  //   the frame (or outside the tile for u = 608); cf: bilinear weight of tap 1
   __shared__ uint16_t lut[256];
+  __shared__ int cx0[S + 1], cx1[S + 1];
+  __shared__ int cf[S + 1];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     if (act_f16) {
       __half h = __float2half_rn((float)i / 255.0f);
@@ -78,44 +73,72 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       lut[i] = *reinterpret_cast<uint16_t*>(&h);
     }
   }
+  for (int u = threadIdx.x; u <= S; u += blockDim.x) {
+    int x0, x1 = -1, f = 0;
+    if (nearest) {
+      x0 = job.x + (u * side) / S;
+    } else {
+      const Tap tx = bilinear_tap(u, side);
+      x0 = job.x + tx.i0;
+      x1 = job.x + tx.i1;
+      f = tx.f;
+    }
+    const bool in_tile = u < S;
+    cx0[u] = in_tile && x0 >= 0 && x0 < W ? 3 * x0 : -1;
+    cx1[u] = in_tile && x1 >= 0 && x1 < W ? 3 * x1 : -1;
+    cf[u] = f;
+  }
   __syncthreads();
   auto pk2 = [&](int a, int b) -> uint32_t { return (uint32_t)lut[a] | ((uint32_t)lut[b] << 16); };
 
   const uint32_t lane = threadIdx.x & 31;
+  const size_t row_bytes = (size_t)W * 3;
+  // 4 tasks in flight per warp: their frame loads overlap (long-scoreboard bound otherwise)
+#pragma unroll 4
   for (int task = threadIdx.x >> 5; task < GATHER_ROWS * SEGS; task += blockDim.x >> 5) {
     const int row = task / SEGS;
     const int v = blockIdx.x * GATHER_ROWS + row;  // output row
     const int u = (task - row * SEGS) * 32 + (int)lane;
-    int sy0, sy1 = 0, fy = 0;
-    if (mode == TP_RESAMPLE_NEAREST) {
-      sy0 = job.y + (v * side) / S;
+    // source row(s) of this output row; nullptr = outside the frame (reads as 0)
+    const uint8_t *r0, *r1 = nullptr;
+    int fy = 0;
+    if (nearest) {
+      const int sy = job.y + (v * side) / S;
+      r0 = sy >= 0 && sy < H ? frame + (size_t)sy * row_bytes : nullptr;
     } else {
       const Tap ty = bilinear_tap(v, side);
-      sy0 = job.y + ty.i0;
-      sy1 = job.y + ty.i1;
+      const int s0 = job.y + ty.i0, s1 = job.y + ty.i1;
+      r0 = s0 >= 0 && s0 < H ? frame + (size_t)s0 * row_bytes : nullptr;
+      r1 = s1 >= 0 && s1 < H ? frame + (size_t)s1 * row_bytes : nullptr;
       fy = ty.f;
     }
-    // RGB of tile column uu on this output row (zero outside [0, 608) and the frame)
+    // RGB of tile column uu on this output row (zero outside the tile and the frame)
     auto sample = [&](int uu, int& r, int& g, int& b) {
-      if (uu < 0 || uu >= S) {
-        r = g = b = 0;
+      const int o0 = cx0[uu];
+      if (nearest) {
+        if (o0 < 0 || r0 == nullptr) {
+          r = g = b = 0;
+        } else {
+          r = __ldg(r0 + o0);
+          g = __ldg(r0 + o0 + 1);
+          b = __ldg(r0 + o0 + 2);
+        }
         return;
       }
-      if (mode == TP_RESAMPLE_NEAREST) {
-        load_px(frame, H, W, job.x + (uu * side) / S, sy0, r, g, b);
-      } else {
-        const Tap tx = bilinear_tap(uu, side);
-        int r00, g00, b00, r01, g01, b01, r10, g10, b10, r11, g11, b11;
-        load_px(frame, H, W, job.x + tx.i0, sy0, r00, g00, b00);
-        load_px(frame, H, W, job.x + tx.i1, sy0, r01, g01, b01);
-        load_px(frame, H, W, job.x + tx.i0, sy1, r10, g10, b10);
-        load_px(frame, H, W, job.x + tx.i1, sy1, r11, g11, b11);
-        const int w00 = (256 - tx.f) * (256 - fy), w01 = tx.f * (256 - fy);
-        const int w10 = (256 - tx.f) * fy, w11 = tx.f * fy;
-        r = (r00 * w00 + r01 * w01 + r10 * w10 + r11 * w11 + 32768) >> 16;
-        g = (g00 * w00 + g01 * w01 + g10 * w10 + g11 * w11 + 32768) >> 16;
-        b = (b00 * w00 + b01 * w01 + b10 * w10 + b11 * w11 + 32768) >> 16;
-      }
+      const int o1 = cx1[uu], fx = cf[uu];
+      auto px = [&](const uint8_t* rp, int o, int k) -> int {
+        return (rp != nullptr && o >= 0) ? (int)__ldg(rp + o + k) : 0;
+      };
+      const int w00 = (256 - fx) * (256 - fy), w01 = fx * (256 - fy);
+      const int w10 = (256 - fx) * fy, w11 = fx * fy;
+      int ch[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        ch[k] = (px(r0, o0, k) * w00 + px(r0, o1, k) * w01 + px(r1, o0, k) * w10 +
+                 px(r1, o1, k) * w11 + 32768) >> 16;
+      r = ch[0];
+      g = ch[1];
+      b = ch[2];
     };
     int r, g, b;
     sample(u, r, g, b);
