@@ -226,24 +226,49 @@ __device__ int run_nms(Work& W, int n, double thr, bool per_crop, int* s_int) {
       __syncthreads();
     }
   }
+  // Greedy NMS in batches of 32 candidates (sort order): every thread tests the batch
+  // against the kept list and against itself (32x32 suppression bits), then warp 0
+  // resolves the batch in order with bit operations. Same decisions as the one-at-a-time
+  // scan (candidate c survives iff no KEPT earlier candidate suppresses it); 2 barriers
+  // per 32 candidates instead of 2 per candidate.
+  unsigned* s_sup = reinterpret_cast<unsigned*>(&s_int[4]);  // [0] by-kept mask, [1..32] rows
+  int kn = 0;
   if (threadIdx.x == 0) s_int[0] = 0;
-  __syncthreads();
-  for (int r = 0; r < n; ++r) {
-    const int i = W.order[r];
-    const int kn = s_int[0];
-    bool sup = false;
-    for (int k = threadIdx.x; k < kn && !sup; k += NT) {
-      const int j = W.kept[k];
-      if (W.cls[j] != W.cls[i]) continue;
-      if (per_crop && W.crop[j] != W.crop[i]) continue;
-      sup = !(iou_ref(W, j, i) < thr);
+  for (int base = 0; base < n; base += 32) {
+    const int m = min(32, n - base);
+    for (int t = threadIdx.x; t < 33; t += NT) s_sup[t] = 0u;
+    __syncthreads();
+    // (a) batch candidate c vs kept k
+    for (int t = threadIdx.x; t < m * kn; t += NT) {
+      const int c = t / kn, k = t - c * kn;
+      const int i = W.order[base + c], j = W.kept[k];
+      if (W.cls[j] != W.cls[i] || (per_crop && W.crop[j] != W.crop[i])) continue;
+      if (!(iou_ref(W, j, i) < thr)) atomicOr(&s_sup[0], 1u << c);
     }
-    const int any = __syncthreads_or(sup);
-    if (!any && threadIdx.x == 0) {
-      W.kept[kn] = i;
-      s_int[0] = kn + 1;
+    // (b) c1 < c2 inside the batch: does c1 (if kept) suppress c2?
+    for (int t = threadIdx.x; t < m * m; t += NT) {
+      const int c1 = t / m, c2 = t - c1 * m;
+      if (c2 <= c1) continue;
+      const int i1 = W.order[base + c1], i2 = W.order[base + c2];
+      if (W.cls[i1] != W.cls[i2] || (per_crop && W.crop[i1] != W.crop[i2])) continue;
+      if (!(iou_ref(W, i1, i2) < thr)) atomicOr(&s_sup[1 + c1], 1u << c2);
     }
     __syncthreads();
+    if (threadIdx.x < 32) {  // resolve in order
+      unsigned alive = ~s_sup[0] & (m == 32 ? 0xffffffffu : ((1u << m) - 1u));
+      unsigned keep = 0u;
+      for (int c = 0; c < m; ++c) {
+        if (alive & (1u << c)) {
+          keep |= 1u << c;
+          alive &= ~s_sup[1 + c];
+        }
+      }
+      const int lane = threadIdx.x;
+      if (keep & (1u << lane)) W.kept[kn + __popc(keep & ((1u << lane) - 1u))] = W.order[base + lane];
+      if (lane == 0) s_int[0] = kn + __popc(keep);
+    }
+    __syncthreads();
+    kn = s_int[0];
   }
   return s_int[0];
 }
@@ -257,14 +282,18 @@ __device__ int run_merge(Work& W, int n, const tp_post_policy_t& P, int* s_int) 
     // pairs (a, lo) with a < lo
     for (int a = threadIdx.x; a < lo; a += NT)
       if (can_merge(W, a, lo, P)) atomicMin(&s_int[1], a * MAXN + lo);
-    // pairs lo <= a < b < n
-    const int span = n - lo;
-    const long long tot = (long long)span * span;
-    for (long long t = threadIdx.x; t < tot; t += NT) {
-      const int a = lo + (int)(t / span), b = lo + (int)(t % span);
-      if (b <= a) continue;
-      if (a * MAXN + b >= s_int[1]) continue;  // cannot improve (reads a racy but monotone bound)
-      if (can_merge(W, a, b, P)) atomicMin(&s_int[1], a * MAXN + b);
+    // pairs lo <= a < b < n: row a per warp, columns b per lane; a row is skipped once a
+    // pair of an earlier row is known (racy but monotone bound)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int a = lo + warp; a < n - 1; a += NT / 32) {
+      if (a * MAXN >= *(volatile int*)&s_int[1]) break;
+      for (int b = a + 1 + lane; b < n; b += 32) {
+        if (a * MAXN + b >= *(volatile int*)&s_int[1]) break;
+        if (can_merge(W, a, b, P)) {
+          atomicMin(&s_int[1], a * MAXN + b);
+          break;
+        }
+      }
     }
     __syncthreads();
     const int best = s_int[1];
@@ -299,7 +328,7 @@ __global__ void __launch_bounds__(NT, 1)
                        int32_t* __restrict__ out_counts, int32_t* __restrict__ keep_idx,
                        int32_t* __restrict__ keep_counts) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ int s_int[4];
+  __shared__ int s_int[40];  // [0..3] scalars, [4..36] NMS batch suppression bits
   Work W = carve(smem);
   const int f = blockIdx.x;
   int n = min(counts[f], max_per_frame);
