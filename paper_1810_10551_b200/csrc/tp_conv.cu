@@ -877,8 +877,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // traversal stride 2). Even conv columns x = 2k use W(k) with weights [w-1 w0 0 w+1];
 // odd columns x = 2k+1 use W(k) with [0 w-1 0 w0] plus W(k+1) with [0 w+1 0 0], so no
 // window ever straddles a 32-byte sector. Per tile (16x8 pooled = 32x16 conv pixels):
-// 4 boxes {16, 16 k, 9 rows} (row phase f x window shift 0/1), 18 MMAs (K=16, N=32);
-// the epilogue reads 4 x 32 columns per row and does max + bias + leaky + pack.
+// 4 boxes {16, 16 k, 9 rows} (row phase f x window shift 0/1), 12 MMAs (K=16: per pool
+// row and kernel row one N=64 MMA for both column phases' W(k) term + one N=32 for the
+// odd phase's W(k+1) term); the epilogue reads 4 x 32 columns per row and does max + bias
+// + leaky + pack.
 constexpr int L0_BOX_ROWS = 9;                       // strided rows per box
 constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 32;  // 4608
 constexpr int L0_STAGE = 4 * L0_BOX_BYTES;           // 18432
@@ -965,6 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::mbar_wait(bres_bar, 0);
       const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 256, 6);
       const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 256, 6);
+      const uint32_t idesc64 = tp::idesc_f16kind(128, 64, p.f16 == 0);
       int s = 0;
       uint32_t ph = 0;
       uint32_t aph[2] = {0, 0};
@@ -976,19 +979,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::tc_fence_after();
         const uint64_t ad0 = a_desc0 + (uint64_t)(s * (L0_STAGE >> 4));
         if (tp::elect_one()) {
+          // pool row py: accumulators (py, px=0) and (py, px=1) are adjacent TMEM column
+          // blocks and both read window W(k) first, with adjacent weight chunks (even,
+          // odd-A) — one N=64 MMA; the odd column's W(k+1) term is one N=32 MMA
 #pragma unroll
-          for (int pp = 0; pp < 4; ++pp) {  // pool position (py, px)
-            const int py = pp >> 1, px = pp & 1;
-            const uint32_t d = tmem_base + (uint32_t)(acc * 128 + pp * 32);
+          for (int py = 0; py < 2; ++py) {
+            const uint32_t d = tmem_base + (uint32_t)(acc * 128 + py * 64);
 #pragma unroll
             for (int dy = 0; dy < 3; ++dy) {
               const int o = py + dy;  // input row offset + 1, in 0..3
               const int f = o & 1, start = o >> 1;
               const uint32_t w0 = (f * L0_BOX_BYTES + start * 16 * 32) >> 4;        // W(k)
               const uint32_t w1 = ((2 + f) * L0_BOX_BYTES + start * 16 * 32) >> 4;  // W(k+1)
-              const uint64_t bw = b_desc0 + (uint64_t)((dy * 3 + px) * 64);
-              tp::mma_bf16(d, ad0 + w0, bw, p.idesc, dy != 0);
-              if (px) tp::mma_bf16(d, ad0 + w1, bw + 64, p.idesc, 1);
+              const uint64_t bw = b_desc0 + (uint64_t)(dy * 3 * 64);
+              tp::mma_bf16(d, ad0 + w0, bw, idesc64, dy != 0);
+              tp::mma_bf16(d + 32, ad0 + w1, bw + 128, p.idesc, 1);
             }
           }
           tp::mma_commit(&empty[s]);
