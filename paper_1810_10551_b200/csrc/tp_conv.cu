@@ -943,11 +943,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       int s = 0;
       uint32_t ph = 0;
+      long long pr_wait = 0;
+      PROF_T0(pr_start);
       for (int i = 0; i < n_tiles; ++i) {
         const int t = t_begin + i;
         const int img = t / per_img, r = t - img * per_img;
         const int by = r / txs, bx = r - by * txs;
+        PROF_T0(tw);
         tp::mbar_wait(&empty[s], ph ^ 1);
+        PROF_ADD(pr_wait, tw);
         tp::mbar_arrive_expect_tx(&full[s], L0_STAGE);
         uint8_t* dst = smA + (size_t)s * L0_STAGE;
 #pragma unroll
@@ -961,6 +965,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1;
         }
       }
+      if (p.dbg & 32) {
+        atomicAdd(&g_conv_prof[0], (unsigned long long)(clock64() - pr_start));
+        atomicAdd(&g_conv_prof[1], (unsigned long long)pr_wait);
+        if (blockIdx.x == 0) atomicAdd(&g_conv_prof[7], 1ull);
+      }
     }
   } else if (warp == kMmaWarp) {
     {
@@ -971,11 +980,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t aph[2] = {0, 0};
+      long long w_te = 0, w_fu = 0;
+      PROF_T0(m_start);
       for (int i = 0; i < n_tiles; ++i) {
         const int acc = i & 1;
+        PROF_T0(t1);
         tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        PROF_ADD(w_te, t1);
         aph[acc] ^= 1;
+        PROF_T0(t2);
         tp::mbar_wait(&full[s], ph);
+        PROF_ADD(w_fu, t2);
         tp::tc_fence_after();
         const uint64_t ad0 = a_desc0 + (uint64_t)(s * (L0_STAGE >> 4));
         if (tp::elect_one()) {
@@ -1005,6 +1020,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1;
         }
       }
+      if ((p.dbg & 32) && lane == 0) {
+        atomicAdd(&g_conv_prof[2], (unsigned long long)(clock64() - m_start));
+        atomicAdd(&g_conv_prof[3], (unsigned long long)w_te);
+        atomicAdd(&g_conv_prof[4], (unsigned long long)w_fu);
+      }
     }
   } else {
     const int g = (int)warp >> 2;
@@ -1012,12 +1032,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
     uint32_t ph = 0;
+    long long e_wait = 0;
+    PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
       if ((i & 1) != g) continue;
       const int t = t_begin + i;
       const int img = t / per_img, r = t - img * per_img;
       const int by = r / txs, bx = r - by * txs;
+      PROF_T0(t3);
       tp::mbar_wait(&tfull[g], ph);
+      PROF_ADD(e_wait, t3);
       ph ^= 1;
       tp::tc_fence_after();
       const int X = bx * 16 + (row & 15), Y = by * 8 + (row >> 4);
@@ -1060,6 +1084,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::tc_fence_before();
       __syncwarp();
       if (lane == 0) tp::mbar_arrive(&tempty[g]);
+    }
+    if ((p.dbg & 32) && warp == 0 && lane == 0) {
+      atomicAdd(&g_conv_prof[5], (unsigned long long)(clock64() - e_start));
+      atomicAdd(&g_conv_prof[6], (unsigned long long)e_wait);
     }
   }
   tp::tc_fence_before();

@@ -1,12 +1,13 @@
-"""Per-role cycle breakdown of conv_tc_kernel (TP_CONV_DEBUG bit 32 counters).
+"""Per-role cycle breakdown of the conv kernels (TP_CONV_DEBUG bit 32 counters).
 
     TP_CONV_DEBUG=32 python tools/conv_roles.py [--tiles 120]
 
 For each conv step of the YOLO forward prints, averaged over CTAs: the MMA issuer's
 total cycles and the share it spent waiting for a free accumulator (tempty) and for a
 loaded stage (full), the producer's share waiting for a free stage (empty), and the
-epilogue warp 0's share waiting for a finished accumulator (tfull). Pair / layer-0
-kernels do not carry the counters (their rows read 0).
+epilogue warp 0's share waiting for a finished accumulator (tfull). conv_tc_kernel,
+conv_box_kernel and conv_l0_kernel carry the counters; the CTA-pair kernel does not (its
+rows read 0).
 """
 
 import argparse
