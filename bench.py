@@ -246,6 +246,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch
     objs = clip_objects(rank, args.clip_frames)
+    # every step takes B consecutive clip frames: pad the clip cyclically to a multiple of B
+    objs = [objs[k % len(objs)] for k in range(-(-len(objs) // B) * B)]
     n_clip = len(objs)
     settings = P.PipelineSettings.from_preset(args.preset)
     eng = AttentionPipelineB200(settings, W, H, max_frames=B, resample=args.resample,

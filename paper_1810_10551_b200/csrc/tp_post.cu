@@ -234,6 +234,7 @@ __device__ int run_nms(Work& W, int n, double thr, bool per_crop, int* s_int) {
   unsigned* s_sup = reinterpret_cast<unsigned*>(&s_int[4]);  // [0] by-kept mask, [1..32] rows
   int kn = 0;
   if (threadIdx.x == 0) s_int[0] = 0;
+  __syncthreads();  // n == 0 runs no batch: the count must still be visible to everyone
   for (int base = 0; base < n; base += 32) {
     const int m = min(32, n - base);
     for (int t = threadIdx.x; t < 33; t += NT) s_sup[t] = 0u;

@@ -330,3 +330,21 @@ def test_fp32_parity_engine(cuda, clip):
     det = yolo.YoloB200Detector(precision="fp32")
     seq = list(P.run_sequence(clip[:2], settings, det))
     assert [r.detections for r in seq] == [r.detections for r, _ in out]
+
+
+def test_batch_with_empty_frames(cuda, clip):
+    """Frames with zero raw detections mixed into a batch (the density-0.1 sweep case):
+    every stage must handle per-frame counts of 0; results stay exact for the others."""
+    W, H = 3840, 2160
+    blank = P.Frame(100, W, H, synthetic.render_frame(W, H, []))
+    frames = [blank, clip[0], P.Frame(101, W, H, blank.pixels), clip[1],
+              P.Frame(102, W, H, blank.pixels), P.Frame(103, W, H, blank.pixels)]
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    eng = AttentionPipelineB200(settings, W, H, max_frames=6)
+    for _ in range(3):  # repeated launches reuse shared memory left by other kernels
+        out = eng.evaluate_frames(frames, history=())
+        for k in (0, 2, 4, 5):  # blank frames may inherit active crops (temporal window)
+            assert out[k][0].detections == ()
+        assert out[0][0].active_count == 0 and out[5][0].active_count == 0
+        assert out[1][0].detections and out[3][0].detections
+    _check_selection_and_nms(eng, out, W, H, 6)
