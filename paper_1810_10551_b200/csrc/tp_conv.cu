@@ -973,7 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     {
-      tp::mbar_wait(bres_bar, 0);
+      if (n_tiles > 0) tp::mbar_wait(bres_bar, 0);  // weights load only if this CTA has tiles
       const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 256, 6);
       const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 256, 6);
       const uint32_t idesc64 = tp::idesc_f16kind(128, 64, p.f16 == 0);
@@ -1227,7 +1227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer (warp-convergent, one elected lane) =================
-    tp::mbar_wait(bres_bar, 0);
+    if (n_tiles > 0) tp::mbar_wait(bres_bar, 0);  // weights load only if this CTA has tiles
     constexpr uint32_t pitch = (PM ? PLANE_W : BOX_TW + 2) * RB;  // 8-row group pitch
     const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, pitch, LAY);
     const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 8 * RB, LAY);

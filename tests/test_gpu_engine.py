@@ -348,3 +348,17 @@ def test_batch_with_empty_frames(cuda, clip):
         assert out[0][0].active_count == 0 and out[5][0].active_count == 0
         assert out[1][0].detections and out[3][0].detections
     _check_selection_and_nms(eng, out, W, H, 6)
+
+
+@pytest.mark.timeout(120)
+def test_all_blank_batch_has_no_stage2_tiles(cuda):
+    """A batch with no attention boxes at all: stage 2 has zero tiles (device count 0), so
+    every conv CTA owns no tile — kernels must exit instead of waiting for weights."""
+    W, H = 3840, 2160
+    blank = synthetic.render_frame(W, H, [])
+    frames = [P.Frame(200 + i, W, H, blank) for i in range(3)]
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    eng = AttentionPipelineB200(settings, W, H, max_frames=3)
+    out = eng.evaluate_frames(frames, history=())
+    assert [(r.active_count, r.detections) for r, _ in out] == [(0, ())] * 3
+    assert int(eng.n_jobs2.item()) == 0
