@@ -362,3 +362,13 @@ def test_all_blank_batch_has_no_stage2_tiles(cuda):
     out = eng.evaluate_frames(frames, history=())
     assert [(r.active_count, r.detections) for r, _ in out] == [(0, ())] * 3
     assert int(eng.n_jobs2.item()) == 0
+
+
+def test_bilinear_resample_engine_parity(cuda, clip):
+    """resample="bilinear" (the north-star ingest downscale, integer fixed point) through
+    the whole engine: same selection / NMS exactness contract as nearest."""
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    eng = AttentionPipelineB200(settings, 3840, 2160, max_frames=2, resample="bilinear")
+    out = eng.evaluate_frames(clip[:2], history=())
+    assert all(r.total_count == 18 and r.active_count > 0 and r.detections for r, _ in out)
+    _check_selection_and_nms(eng, out, 3840, 2160, 2)
