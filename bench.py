@@ -202,10 +202,22 @@ def cpu_baseline_frames_per_sec(objs, n_frames=1):
     return n_frames / dt, threads, dt
 
 
+def arm_config(args, n_clip: int, world: int) -> dict:
+    """Workload description shared by the B200 arm and the reference arm."""
+    return {"workload": f"{args.frame.upper()} "
+                        f"{'all-crops baseline' if args.mode == 'allcrops' else 'attention pipeline'}"
+                        f"{'' if args.density is None else f' (injected stage-1, density {args.density})'}"
+                        f" on a {n_clip}-frame synthetic clip "
+                        f"(sparse/dense/mixed, seed=rank), preset '{args.preset}', "
+                        "random-init YOLO v2-608 (seed 0, calibrated head)",
+            "frame": [W, H], "frames_per_step": args.batch, "per_gpu_frames": n_clip,
+            "resample": args.resample, "parallelism": f"frame-dp{world}"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    objs = clip_objects(0)
+    objs = clip_objects(0, args.clip_frames)
     vals = []
     for i in range(args.warmup + args.steps):
         fps, threads, dt = cpu_baseline_frames_per_sec(objs[i % len(objs):], 1)
@@ -217,9 +229,8 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32+bf16-storage", "data": "synthetic",
-            "config": {"workload": "4K attention pipeline, 300-frame synthetic clip "
-                       "(sparse/dense/mixed), preset '1 att, 3 fin, 20 over', YOLO v2-608 seed 0",
-                       "step": "1 frame (bounded CPU sample)"},
+            "config": {**arm_config(args, len(objs), world),
+                       "step": "1 frame of the clip per step (bounded CPU sample of the workload)"},
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
                              "sample": "1 frame per step: oracle run_sequence + torch-CPU YOLO"},
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
@@ -391,14 +402,7 @@ def main():
                           if args.precision != "fp32" else
                           "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
                           "accumulation and epilogue"),
-            "config": {"workload": f"{args.frame.upper()} "
-                                   f"{'all-crops baseline' if args.mode == 'allcrops' else 'attention pipeline'}"
-                                   f"{'' if args.density is None else f' (injected stage-1, density {args.density})'}"
-                                   f" on a {n_clip}-frame synthetic clip "
-                                   f"(sparse/dense/mixed, seed=rank), preset '{args.preset}', "
-                                   "random-init YOLO v2-608 (seed 0, calibrated head)",
-                       "frame": [W, H], "frames_per_step": B, "per_gpu_frames": n_clip,
-                       "resample": args.resample, "parallelism": f"frame-dp{world}",
+            "config": {**arm_config(args, n_clip, world),
                        "l2": "inputs exceed L2 (746 MB per step)",
                        "tiles_per_frame": tiles_per_frame,
                        "crops_per_sec": value * tiles_per_frame},
