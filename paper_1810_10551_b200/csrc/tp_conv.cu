@@ -707,13 +707,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const int lo = p.ksize == 3 ? -1 : 0;  // im2col window corner
+      long long pr_wait = 0;
+      PROF_T0(pr_start);
       for (int i = 0; i < n_tiles; ++i) {
         const int t = t_begin + i;
         const int mt = t / p.n_blocks_n;
         const int n0 = (t - mt * p.n_blocks_n) * p.bn;
         const PixPos f0 = pix_pos(mt * 256 + (int)rank * 128, p.res, p.img_px);
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          PROF_T0(tw);
           tp::mbar_wait(&empty[s], ph ^ 1);
+          PROF_ADD(pr_wait, tw);
           if (rank == 0)
             tp::mbar_arrive_expect_tx(&full[s], 2 * (p.a_stage_bytes + p.b_stage_bytes));
           const uint32_t lbar = mapa_rank(&full[s], 0);
@@ -730,6 +734,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if ((p.dbg & 32) && rank == 0) {
+        atomicAdd(&g_conv_prof[0], (unsigned long long)(clock64() - pr_start));
+        atomicAdd(&g_conv_prof[1], (unsigned long long)pr_wait);
+        if (blockIdx.x == 0) atomicAdd(&g_conv_prof[7], 1ull);
+      }
     }
   } else if (warp == kMmaWarp) {
     if (rank == 0) {
@@ -740,14 +749,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       uint32_t aph[2] = {0, 0};
+      long long w_te = 0, w_fu = 0;
+      PROF_T0(m_start);
       for (int i = 0; i < n_tiles; ++i) {
         const int acc = i & 1;
+        PROF_T0(t1);
         tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        PROF_ADD(w_te, t1);
         aph[acc] ^= 1;
         tp::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          PROF_T0(t2);
           tp::mbar_wait(&full[s], ph);
+          PROF_ADD(w_fu, t2);
           tp::tc_fence_after();
           const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
           const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
@@ -767,6 +782,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tp::elect_one()) commit_pair_mc(&tfull[acc]);  // both CTAs' epilogues may read
         __syncwarp();
       }
+      if ((p.dbg & 32) && lane == 0) {
+        atomicAdd(&g_conv_prof[2], (unsigned long long)(clock64() - m_start));
+        atomicAdd(&g_conv_prof[3], (unsigned long long)w_te);
+        atomicAdd(&g_conv_prof[4], (unsigned long long)w_fu);
+      }
     }
   } else {
     // ============ epilogue: both CTAs, own 128 rows; groups alternate accumulators ============
@@ -777,12 +797,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nchunks = p.bn >> 4;
     const uint32_t leader_tempty[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
     uint32_t ph = 0;
+    long long e_wait = 0;
+    PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
       if ((i & 1) != g) continue;
       const int t = t_begin + i;
       const int mt = t / p.n_blocks_n;
       const int n0 = (t - mt * p.n_blocks_n) * p.bn;
+      PROF_T0(t3);
       tp::mbar_wait(&tfull[g], ph);
+      PROF_ADD(e_wait, t3);
       ph ^= 1;
       tp::tc_fence_after();
       const int rbase = mt * 256 + (int)rank * 128 + (int)q * 32;
@@ -857,6 +881,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive_cluster(leader_tempty[g]);
     }
     if (lane == 0) bulk_wait_all();
+    if ((p.dbg & 32) && warp == 0 && lane == 0 && rank == 0) {
+      atomicAdd(&g_conv_prof[5], (unsigned long long)(clock64() - e_start));
+      atomicAdd(&g_conv_prof[6], (unsigned long long)e_wait);
+    }
   }
 
   tp::tc_fence_before();

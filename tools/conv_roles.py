@@ -5,9 +5,10 @@
 For each conv step of the YOLO forward prints, averaged over CTAs: the MMA issuer's
 total cycles and the share it spent waiting for a free accumulator (tempty) and for a
 loaded stage (full), the producer's share waiting for a free stage (empty), and the
-epilogue warp 0's share waiting for a finished accumulator (tfull). conv_tc_kernel,
-conv_box_kernel and conv_l0_kernel carry the counters; the CTA-pair kernel does not (its
-rows read 0).
+epilogue warp 0's share waiting for a finished accumulator (tfull). All conv kernels carry
+the counters; for the CTA-pair kernel only the leader CTAs count, so its kcyc columns read
+half the per-SM value (the percentages are unaffected). An issuer waiting on `full` is not
+an idle tensor pipe: MMAs are queued asynchronously (check ncu tensor-pipe activity).
 """
 
 import argparse
