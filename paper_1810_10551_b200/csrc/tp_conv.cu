@@ -139,6 +139,9 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, const void* smem_
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {  // <= 1 bulk group still reading smem
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -409,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0;
     TileIter it;
     it.init(t_begin, p);
+    uint32_t slab = 0;  // TSTORE staging slabs used by this warp
     long long e_wait = 0;
     PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i, it.next(p)) {
@@ -485,11 +489,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (TSTORE) {
           // 64-byte-per-row slabs (2 fp16 chunks or 1 fp32 chunk) staged with the SW64
           // pattern, then one TMA store of {slab, 32 rows}; halo rows are written as zeros
+          // two slabs per warp alternate: staging the next one only waits for the store
+          // issued two slabs ago (bulk_wait_read1), not for the one just issued
           constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
           const int cs = c % CPS;
-          const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
+          const uint32_t slab_off = warp * 4096 + (slab & 1) * 2048;
+          const uint32_t buf = tp::smem_u32(smC) + slab_off;
           if (cs == 0) {
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) bulk_wait_read1();
             __syncwarp();
           }
           const uint32_t rbase = buf + lane * 64;
@@ -521,10 +528,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && (p.dbg & 4) == 0) {
-              tma_store_2d(&tmC, smC + warp * 2048, p.out_coff + ch0 - 16 * cs,
+              tma_store_2d(&tmC, smC + slab_off, p.out_coff + ch0 - 16 * cs,
                            it.mt * 128 + (int)q * 32);
               bulk_commit();
             }
+            ++slab;
           }
           continue;
         }
@@ -797,6 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nchunks = p.bn >> 4;
     const uint32_t leader_tempty[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
     uint32_t ph = 0;
+    uint32_t slab = 0;  // TSTORE staging slabs used by this warp
     long long e_wait = 0;
     PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
@@ -812,8 +821,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rbase = mt * 256 + (int)rank * 128 + (int)q * 32;
       const bool valid = rbase + (int)lane < total_px;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * p.bn);
-      const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
-      const uint32_t rowa = buf + lane * 64;
       const uint32_t swz = (lane >> 1) & 3;
       uint32_t v[16];
       tp::tmem_ld16(t_row, v);
@@ -839,8 +846,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
         const int cs = c % CPS;
+        const uint32_t slab_off = warp * 4096 + (slab & 1) * 2048;  // two alternating slabs
+        const uint32_t rowa = tp::smem_u32(smC) + slab_off + lane * 64;
         if (cs == 0) {
-          if (lane == 0) bulk_wait_read0();
+          if (lane == 0) bulk_wait_read1();
           __syncwarp();
         }
         if (EPI == EPI_F32) {
@@ -870,9 +879,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, smC + warp * 2048, p.out_coff + ch0 - 16 * cs, rbase);
+            tma_store_2d(&tmC, smC + slab_off, p.out_coff + ch0 - 16 * cs, rbase);
             bulk_commit();
           }
+          ++slab;
         }
       }
       tp::tmem_ld_wait();
@@ -1327,6 +1337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int oimg = ores * ores;
     const int nchunks = N >> 4;
     uint32_t ph = 0;  // phase bit per accumulator buffer
+    uint32_t slab = 0;  // TSTORE staging slabs used by this warp
     int img = t_begin / per_img, r = t_begin - img * per_img;
     int by = r / p.tiles_x, bx = r - by * p.tiles_x;
     long long e_wait = 0;
@@ -1460,9 +1471,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (TSTORE) {
           if (!warp_rows_valid) continue;
           const int cs = c & 1;
-          const uint32_t buf = tp::smem_u32(smC) + warp * 2048;
+          const uint32_t slab_off = warp * 4096 + (slab & 1) * 2048;  // two alternating slabs
+          const uint32_t buf = tp::smem_u32(smC) + slab_off;
           if (cs == 0) {
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) bulk_wait_read1();
             __syncwarp();
           }
           uint32_t pk[8];
@@ -1483,10 +1495,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && (p.dbg & 4) == 0) {
-              tma_store_3d(&tmC, smC + warp * 2048, p.out_coff + (c - 1) * 16, tbx * BOX_TW,
+              tma_store_3d(&tmC, smC + slab_off, p.out_coff + (c - 1) * 16, tbx * BOX_TW,
                            timg * p.res + tby * BOX_TH + (int)q * 4);
               bulk_commit();
             }
+            ++slab;
           }
           continue;
         }
@@ -1853,7 +1866,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     p.n_bchunks = ktotal / bk;
     p.bres_bytes = (uint32_t)bres;
   }
-  p.stage_bytes = tstore ? 8 * 2048 : 0;
+  p.stage_bytes = tstore ? 8 * 4096 : 0;  // 8 epilogue warps x 2 alternating 2 KB slabs
   const uint32_t stage_bytes = p.a_stage_bytes + p.b_stage_bytes;
   int stages = (int)((227 * 1024 - fixed - (int)p.bres_bytes - (int)p.stage_bytes) /
                      (int)stage_bytes);
@@ -1902,7 +1915,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     const uint32_t rb = (uint32_t)bk * 2;
     const uint32_t stage = pm ? 4 * ((PLANE_W * PLANE_H * rb + 1023) & ~1023u)
                               : ((BOX_TW + 2) * (BOX_TH + 2) * rb + 1023) & ~1023u;
-    const uint32_t staging = (!pool && res % 4 == 0) ? 8 * 2048 : 0;  // TMA-store slabs
+    const uint32_t staging = (!pool && res % 4 == 0) ? 8 * 4096 : 0;  // 2 slabs per warp
     const int bfixed = 1024 + cout_pad * 4 + (2 * 8 + 10) * 8 + 16 + (int)staging;
     int st = (int)((227 * 1024 - bfixed - (int)bres) / (int)stage);
     if (st > 8) st = 8;
