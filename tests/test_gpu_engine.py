@@ -372,3 +372,13 @@ def test_bilinear_resample_engine_parity(cuda, clip):
     out = eng.evaluate_frames(clip[:2], history=())
     assert all(r.total_count == 18 and r.active_count > 0 and r.detections for r, _ in out)
     _check_selection_and_nms(eng, out, 3840, 2160, 2)
+
+
+def test_capacity_overflow_fails_loudly(cuda, clip):
+    """Maximum sizes: with detector threshold 0 every candidate (1805 per tile) survives
+    decode, so a frame's raw stage-2 detections exceed the 2048-record postprocess capacity;
+    the engine must raise StageFailure instead of silently truncating."""
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    eng = AttentionPipelineB200(settings, 3840, 2160, max_frames=1, threshold=0.0)
+    with pytest.raises(P.StageFailure):
+        eng.evaluate_frames(clip[:1], history=())
