@@ -910,18 +910,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Layer 0 (3x3, 3->32, leaky, 2x2 maxpool) has K = 48 but 608^2 outputs per tile, so it
 // is bound by epilogue instructions, not math. Here each M row is one POOLED output
 // pixel: the four pool positions (py,px) accumulate into four TMEM accumulators.
-// Input: 16-byte slots E(X) = [q(X-1) | q(X)], read as 32-byte-aligned windows
-// W(k) = E(2k) E(2k+1) = [q(2k-1) q(2k) q(2k) q(2k+1)] ({16 halves, k, row} view, rows at
-// traversal stride 2). Even conv columns x = 2k use W(k) with weights [w-1 w0 0 w+1];
-// odd columns x = 2k+1 use W(k) with [0 w-1 0 w0] plus W(k+1) with [0 w+1 0 0], so no
-// window ever straddles a 32-byte sector. Per tile (16x8 pooled = 32x16 conv pixels):
-// 4 boxes {16, 16 k, 9 rows} (row phase f x window shift 0/1), 12 MMAs (K=16: per pool
-// row and kernel row one N=64 MMA for both column phases' W(k) term + one N=32 for the
-// odd phase's W(k+1) term); the epilogue reads 4 x 32 columns per row and does max + bias
-// + leaky + pack.
+// Input: 16-byte slots E(X) = [q(X-1) | q(X)]; windows W(k) = E(2k) E(2k+1) =
+// [q(2k-1) q(2k) q(2k) q(2k+1)] are 32-byte aligned. Even conv columns x = 2k use W(k)
+// with weights [w-1 w0 0 w+1]; odd columns x = 2k+1 use W(k) with [0 w-1 0 w0] plus
+// W(k+1) with [0 w+1 0 0], so no window straddles a 32-byte sector. Both column phases of
+// window index k share one 64-byte A row [W(k) | W(k+1)] (SW64, K = 32): TMA loads one box
+// {32 halves, 16 k, 9 rows (stride 2)} per input row phase — 288 box rows per tile, the
+// TMA row rate was this kernel's limit at 32-byte rows. Per tile (16x8 pooled = 32x16
+// conv pixels): 12 MMAs (K=16: per pool row and kernel row one N=64 MMA for both column
+// phases' W(k) term + one N=32 for the odd phase's W(k+1) term at +32 B); the epilogue
+// reads 4 x 32 columns per row and does max + bias + leaky + pack.
 constexpr int L0_BOX_ROWS = 9;                       // strided rows per box
-constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 32;  // 4608
-constexpr int L0_STAGE = 4 * L0_BOX_BYTES;           // 18432
+constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 64;  // 9216: 9 rows x 16 windows x 64 B
+constexpr int L0_STAGE = 2 * L0_BOX_BYTES;           // 18432: one box per input row phase
 
 __global__ void __launch_bounds__(kThreads, 1)
     conv_l0_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -993,11 +994,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::mbar_arrive_expect_tx(&full[s], L0_STAGE);
         uint8_t* dst = smA + (size_t)s * L0_STAGE;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {  // b = window shift * 2 + y phase
-          const int sh = b >> 1, f = b & 1;
-          tma_load_3d(dst + b * L0_BOX_BYTES, &tmA, &full[s], 0, 16 * bx + sh,
+        for (int f = 0; f < 2; ++f)  // input row phase; both column phases share the rows
+          tma_load_3d(dst + f * L0_BOX_BYTES, &tmA, &full[s], 0, 16 * bx,
                       img * hp + 1 + 16 * by + f - 1);
-        }
         if (++s == S) {
           s = 0;
           ph ^= 1;
@@ -1012,7 +1011,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     {
       if (n_tiles > 0) tp::mbar_wait(bres_bar, 0);  // weights load only if this CTA has tiles
-      const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 256, 6);
+      // A: SW64 rows of 64 B = [W(k) | W(k+1)]; B: SW32 rows of 32 B (K = 16)
+      const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 512, 4);
       const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 256, 6);
       const uint32_t idesc64 = tp::idesc_f16kind(128, 64, p.f16 == 0);
       int s = 0;
@@ -1042,11 +1042,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int dy = 0; dy < 3; ++dy) {
               const int o = py + dy;  // input row offset + 1, in 0..3
               const int f = o & 1, start = o >> 1;
-              const uint32_t w0 = (f * L0_BOX_BYTES + start * 16 * 32) >> 4;        // W(k)
-              const uint32_t w1 = ((2 + f) * L0_BOX_BYTES + start * 16 * 32) >> 4;  // W(k+1)
+              const uint32_t w0 = (f * L0_BOX_BYTES + start * 16 * 64) >> 4;  // W(k): K 0..15
               const uint64_t bw = b_desc0 + (uint64_t)(dy * 3 * 64);
               tp::mma_bf16(d, ad0 + w0, bw, idesc64, dy != 0);
-              tp::mma_bf16(d + 32, ad0 + w1, bw + 128, p.idesc, 1);
+              tp::mma_bf16(d + 32, ad0 + w0 + 2, bw + 128, p.idesc, 1);  // W(k+1): +32 B
             }
           }
           tp::mma_commit(&empty[s]);
@@ -1766,13 +1765,14 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     }
     const int wp = res + 2;
     {
-      // 16-byte slots E(X) = [q(X-1) | q(X)]; the kernel reads 32-byte-aligned windows
-      // W(k) = E(2k) E(2k+1): a {16 halves, k (32 B), row} view (conv_l0_kernel comment)
-      const uint64_t dims[3] = {16, (uint64_t)(wp / 2), (uint64_t)max_img * wp};
+      // 16-byte slots E(X) = [q(X-1) | q(X)]; the kernel reads 64-byte rows [W(k) | W(k+1)]
+      // (W(k) = E(2k) E(2k+1)) through a {32 halves, k (32 B apart: rows overlap), row} view
+      // with the SW64 swizzle (tools/tma_overlap_probe.cu)
+      const uint64_t dims[3] = {32, (uint64_t)(wp / 2 - 1), (uint64_t)max_img * wp};
       const cuuint64_t strides[2] = {32, (cuuint64_t)wp * 16};
-      const uint32_t box[3] = {16, 16, 18};
+      const uint32_t box[3] = {32, 16, 18};
       const uint32_t estr[3] = {1, 1, 2};
-      rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 2, estr,
+      rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_64B, f16, 2, estr,
                      strides);
       if (rc) return rc;
     }

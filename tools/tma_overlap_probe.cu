@@ -12,9 +12,9 @@ void tp_set_error(const char*, ...) {}
 constexpr int W = 40, H = 6;
 
 __global__ void probe(const __grid_constant__ CUtensorMap tm, int x0, int y0, float* out) {
-  __shared__ __align__(1024) __half buf[8 * 2 * 8 * 3];
+  __shared__ __align__(1024) __half buf[32 * 8 * 3];
   __shared__ uint64_t bar;
-  for (int i = threadIdx.x; i < 8 * 2 * 8 * 3; i += blockDim.x) buf[i] = __float2half(-1.0f);
+  for (int i = threadIdx.x; i < 32 * 8 * 3; i += blockDim.x) buf[i] = __float2half(-1.0f);
   if (threadIdx.x == 0) {
     tp::mbar_init(&bar, 1);
     tp::fence_mbar_init();
@@ -22,7 +22,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, int x0, int y0, fl
   __syncthreads();
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
-    tp::mbar_arrive_expect_tx(&bar, 8 * 2 * 8 * 3 * 2);
+    tp::mbar_arrive_expect_tx(&bar, 32 * 8 * 3 * 2);
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(tp::smem_u32(buf)),
@@ -30,7 +30,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap tm, int x0, int y0, fl
         : "memory");
   }
   tp::mbar_wait(&bar, 0);
-  for (int i = threadIdx.x; i < 8 * 2 * 8 * 3; i += blockDim.x) out[i] = __half2float(buf[i]);
+  for (int i = threadIdx.x; i < 32 * 8 * 3; i += blockDim.x) out[i] = __half2float(buf[i]);
 }
 
 int main() {
@@ -44,7 +44,7 @@ int main() {
   cudaMalloc(&d, sizeof(h));
   cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice);
   float* dout;
-  cudaMalloc(&dout, 8 * 2 * 8 * 3 * sizeof(float));
+  cudaMalloc(&dout, 32 * 8 * 3 * sizeof(float));
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -54,17 +54,17 @@ int main() {
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
   for (int sw = 0; sw < 2; ++sw)
     for (int es : {1, 2}) {
-      // 3-D view {16 halves = slots x and x+1, slot x (16 B apart: overlapping), row}
+      // 3-D view {32 halves = slots 2k..2k+3, k (32 B apart: overlapping), row}
       CUtensorMap tm;
-      cuuint64_t dims[3] = {16, W - 1, H};
-      cuuint64_t strides[2] = {16, W * 16};
-      cuuint32_t box[3] = {16, (cuuint32_t)(8 * es), (cuuint32_t)(3 * es)};
+      cuuint64_t dims[3] = {32, W / 2 - 1, H};
+      cuuint64_t strides[2] = {32, W * 16};
+      cuuint32_t box[3] = {32, (cuuint32_t)(8 * es), (cuuint32_t)(3 * es)};
       cuuint32_t estr[3] = {1, (cuuint32_t)es, (cuuint32_t)es};
       CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, d, dims, strides, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE,
-                       sw ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                       sw ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      printf("swizzle %s estride %d: encode %d\n", sw ? "32B" : "none", es, (int)r);
+      printf("swizzle %s estride %d: encode %d\n", sw ? "64B" : "none", es, (int)r);
       if (r != CUDA_SUCCESS) continue;
       probe<<<1, 128>>>(tm, 3, 1, dout);
       cudaError_t e = cudaDeviceSynchronize();
@@ -72,12 +72,13 @@ int main() {
         printf("  launch error %s\n", cudaGetErrorString(e));
         return 1;
       }
-      float o[8 * 2 * 8 * 3];
+      float o[32 * 8 * 3];
       cudaMemcpy(o, dout, sizeof(o), cudaMemcpyDeviceToHost);
-      // row r of 32 B (16 halves) per (y, x): print halves 0, 4, 8, 12 (raw smem order)
+      // row r of 64 B (32 halves) per (y, k): halves 0, 4, ..., 28 (raw smem order)
       for (int row = 0; row < 24; ++row)
-        printf("  smem row %2d: %6.1f %6.1f %6.1f %6.1f\n", row, o[row * 16], o[row * 16 + 4],
-               o[row * 16 + 8], o[row * 16 + 12]);
+        printf("  smem row %2d: %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f %6.1f\n", row,
+               o[row * 32], o[row * 32 + 4], o[row * 32 + 8], o[row * 32 + 12], o[row * 32 + 16],
+               o[row * 32 + 20], o[row * 32 + 24], o[row * 32 + 28]);
     }
   return 0;
 }
