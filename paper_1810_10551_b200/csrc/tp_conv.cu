@@ -68,7 +68,9 @@ struct ConvParams {
   int n_bchunks;
   uint32_t stage_bytes;  // epilogue store staging (TMA-store variants): 8 warps x 2 KB
   int nbuf;  // box kernel: TMEM accumulator buffers (2 or 4)
-  int dbg;  // profiling only (TP_CONV_DEBUG): 1 = skip epilogue math/stores, 2 = skip MMAs
+  // profiling only (TP_CONV_DEBUG bits): 1 skip epilogue, 2 skip MMAs, 4 skip stores,
+  // 8 skip TMEM loads, 16 no TMA (stale operands), 32 role cycle counters (g_conv_prof)
+  int dbg;
 };
 
 
