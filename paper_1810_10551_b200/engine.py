@@ -299,17 +299,51 @@ class AttentionPipelineB200:
 
     def results(self, frame_ids, timing: TimingProfile | None = None):
         """Download and convert the last batch to (FrameResult, AttentionModel) pairs."""
+        return self.results_from(self.snapshot(), frame_ids, timing)
+
+    def snapshot(self, slot: int = 0):
+        """Queue stream-ordered D2H copies of the last batch's results into pinned host
+        buffers (slot 0/1 double-buffers them), so the next batch may be launched before
+        the host reads these: returns a handle for results_from()."""
         torch = self.torch
         n = self._n
-        torch.cuda.current_stream().synchronize()
-        oc = self.ocounts[:n].cpu().numpy()
-        pc = self.pcounts[:n].cpu().numpy()
+        K1 = self.K - 1
+        bufs = self.__dict__.setdefault("_snap_bufs", {})
+        if slot not in bufs:
+            mf, rec = self.max_frames, native.PDET_DTYPE.itemsize
+            pin = dict(pin_memory=True)
+            bufs[slot] = {"oc": torch.empty(mf, dtype=torch.int32, **pin),
+                          "pc": torch.empty(mf, dtype=torch.int32, **pin),
+                          "ac": torch.empty(mf, dtype=torch.int32, **pin),
+                          "bc": torch.empty(mf, dtype=torch.int32, **pin),
+                          "boxes": torch.empty((mf, MAX_BOXES, 4), dtype=torch.float64, **pin),
+                          "rec": torch.empty(mf * MAX_PER_FRAME * rec, dtype=torch.uint8, **pin),
+                          "event": torch.cuda.Event()}
+        s = bufs[slot]
+        rb = n * MAX_PER_FRAME * native.PDET_DTYPE.itemsize
+        s["oc"][:n].copy_(self.ocounts[:n], non_blocking=True)
+        s["pc"][:n].copy_(self.pcounts[:n], non_blocking=True)
+        s["ac"][:n].copy_(self.active_counts[:n], non_blocking=True)
+        # after run_device the batch's own box slots are K1..K1+n-1
+        s["bc"][:n].copy_(self.box_counts[K1:K1 + n], non_blocking=True)
+        s["boxes"][:n].copy_(self.boxes[K1:K1 + n], non_blocking=True)
+        s["rec"][:rb].copy_(self.outp.view(-1)[:rb], non_blocking=True)
+        s["event"].record()
+        return (n, s)
+
+    def results_from(self, snap, frame_ids, timing: TimingProfile | None = None):
+        """(FrameResult, AttentionModel) pairs from a snapshot (waits for its copies)."""
+        n, s = snap
+        s["event"].synchronize()
+        oc, pc, ac = s["oc"][:n].numpy(), s["pc"][:n].numpy(), s["ac"][:n].numpy()
         if (pc > MAX_PER_FRAME).any():
             raise StageFailure("final", int(frame_ids[int(np.argmax(pc))]))
-        ac = self.active_counts[:n].cpu().numpy()
-        rec = self.outp.view(-1)[: n * MAX_PER_FRAME * native.PDET_DTYPE.itemsize].cpu().numpy()
+        cnt = s["bc"][:n].numpy()
+        if (cnt > MAX_BOXES).any():
+            raise StageFailure("attention", -1)
+        bx = s["boxes"][:n].numpy()
+        rec = s["rec"][: n * MAX_PER_FRAME * native.PDET_DTYPE.itemsize].numpy()
         rec = rec.view(native.PDET_DTYPE).reshape(n, MAX_PER_FRAME)
-        bc = self.box_counts_snapshot(n)
         out = []
         timing = timing or TimingProfile()
         for f in range(n):
@@ -318,7 +352,8 @@ class AttentionPipelineB200:
                           self.labels.names[int(r["cls"])], float(r["conf"]))
                 for r in rec[f, : oc[f]])
             res = FrameResult(int(frame_ids[f]), dets, int(ac[f]), self.F, timing)
-            boxes = tuple(Rect(int(b[0]), int(b[1]), int(b[2]), int(b[3])) for b in bc[f])
+            boxes = tuple(Rect(int(b[0]), int(b[1]), int(b[2]), int(b[3]))
+                          for b in bx[f, : cnt[f]])
             out.append((res, AttentionModel(int(frame_ids[f]), boxes, (int(frame_ids[f]),))))
         return out
 

@@ -91,32 +91,50 @@ def run_stream(frames, settings: PipelineSettings, det=None,
             copied[slot].record(copy_stream)
 
     engine.reset_history(())
+    ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(2)]
     cursor = 0
+
+    def emit(k: int, snap) -> None:
+        """Results of batch k (its snapshot and events; the GPU may run batch k+1)."""
+        nonlocal cursor
+        slot = k % 2
+        chunk = chunks[k]
+        n = len(chunk)
+        res = engine.results_from(snap, [fid for fid, _ in chunk])
+        e = ev_sets[slot]
+        t = [e[i].elapsed_time(e[i + 1]) / n for i in range(4)]
+        io = copy_start[slot].elapsed_time(copied[slot]) / n
+        timing = TimingProfile(io_ms=io, attention_wait_ms=t[0], client_processing_ms=t[1],
+                               final_eval_ms=t[2], postprocess_ms=t[3],
+                               per_worker=((dev_name, sum(t)),))
+        for r, _ in res:
+            results.append(FrameResult(r.frame_id, r.detections, r.active_count, r.total_count,
+                                       timing))
+        cursor += n
+
     try:
         stage_chunk(0)
-        for k, chunk in enumerate(chunks):
+        pending = None  # (batch index, snapshot) launched but not yet emitted
+        for k in range(len(chunks)):
             slot = k % 2
-            n = len(chunk)
+            n = len(chunks[k])
             torch.cuda.current_stream().wait_event(copied[slot])
+            engine.events = ev_sets[slot]
             engine.run_device(n, frames=dev[slot], timed=True)
             used[slot].record()
-            staging_error = None
+            snap = engine.snapshot(slot)
+            if pending is not None:  # batch k-1 finishes while batch k is queued
+                emit(*pending)
+            pending = (k, snap)
             if k + 1 < len(chunks):
-                try:  # host packing + H2D of the next batch overlap this one
+                try:  # host packing + H2D of the next batch overlap batch k on the GPU
                     stage_chunk(k + 1)
-                except Exception as exc:  # reported after this batch's results are kept
-                    staging_error = exc
-            t = [v / n for v in engine.stage_times_ms()]
-            io = copy_start[slot].elapsed_time(copied[slot]) / n
-            busy = sum(t)
-            timing = TimingProfile(io_ms=io, attention_wait_ms=t[0], client_processing_ms=t[1],
-                                   final_eval_ms=t[2], postprocess_ms=t[3],
-                                   per_worker=((dev_name, busy),))
-            for res, _ in engine.results([fid for fid, _ in chunk], timing):
-                results.append(res)
-            cursor += n
-            if staging_error is not None:
-                raise staging_error
+                except Exception:
+                    emit(*pending)  # keep the finished batch's results, then abort
+                    pending = None
+                    raise
+        if pending is not None:
+            emit(*pending)
     except Exception as exc:
         raise StreamAborted(cursor, results, str(exc)) from exc
     finally:
