@@ -437,9 +437,13 @@ def run_e2e(eng, clip, B, args, world, dist, launch):
     from paper_1810_10551_b200 import native
     from paper_1810_10551_b200.engine import MAX_PER_FRAME
 
-    n_clip = clip.shape[0]
-    host = torch.empty(clip.shape, dtype=torch.uint8, pin_memory=True)
-    host.copy_(clip.cpu())
+    # pinned host source = the clip (same frames as the device-resident run), capped at
+    # 16 GB per rank (binds only at 8K, where e2e is bound by the H2D copy itself)
+    frame_bytes = int(np.prod(clip.shape[1:]))
+    cap = max(B, (16 << 30) // frame_bytes // B * B)
+    n_clip = min(clip.shape[0], cap)
+    host = torch.empty((n_clip,) + tuple(clip.shape[1:]), dtype=torch.uint8, pin_memory=True)
+    host.copy_(clip[:n_clip].cpu())
     dev = [torch.empty((B, H, W, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
     copy_stream = torch.cuda.Stream()
     done_copy = [torch.cuda.Event() for _ in range(2)]
