@@ -382,3 +382,16 @@ def test_capacity_overflow_fails_loudly(cuda, clip):
     eng = AttentionPipelineB200(settings, 3840, 2160, max_frames=1, threshold=0.0)
     with pytest.raises(P.StageFailure):
         eng.evaluate_frames(clip[:1], history=())
+
+
+@pytest.mark.parametrize("W,H,precision", [(1280, 720, "fp16"), (1920, 1080, "bf16")])
+def test_engine_other_sizes_and_bf16(cuda, W, H, precision):
+    """720p / 1080p frames (other crop sides, partial edge crops) and bf16 activations:
+    same selection / NMS exactness contract."""
+    gt = synthetic.generate_scene(synthetic.SceneSpec("dense", W, H, 2, seed=1))
+    frames = [P.Frame(i, W, H, synthetic.render_frame(W, H, gt[i])) for i in range(2)]
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    eng = AttentionPipelineB200(settings, W, H, max_frames=2, precision=precision)
+    out = eng.evaluate_frames(frames, history=())
+    assert all(r.total_count == eng.F for r, _ in out)
+    _check_selection_and_nms(eng, out, W, H, 2)
