@@ -395,3 +395,25 @@ def test_engine_other_sizes_and_bf16(cuda, W, H, precision):
     out = eng.evaluate_frames(frames, history=())
     assert all(r.total_count == eng.F for r, _ in out)
     _check_selection_and_nms(eng, out, W, H, 2)
+
+
+def test_cuda_graph_step_matches_eager(cuda, clip):
+    """engine.capture(): a CUDA-graph replay of the device step gives the eager results."""
+    torch = cuda
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    frames = torch.from_numpy(np.stack([f.pixels for f in clip[:1]])).cuda()
+    eager = AttentionPipelineB200(settings, 3840, 2160, max_frames=1)
+    eager.reset_history(())
+    want = []
+    for _ in range(3):
+        eager.run_device(1, frames=frames)
+        want.append([(r.detections, r.active_count) for r, _ in eager.results([0])])
+    eng = AttentionPipelineB200(settings, 3840, 2160, max_frames=1)
+    eng.reset_history(())
+    step = eng.capture(1, frames)  # capture performs one warm-up step (history advances)
+    eng.reset_history(())
+    got = []
+    for _ in range(3):
+        step()
+        got.append([(r.detections, r.active_count) for r, _ in eng.results([0])])
+    assert got == want and want[0][0][0]
