@@ -193,6 +193,18 @@ TP_API int tp_render_frames(const int32_t* rects, const uint8_t* colors, const i
                             int n_frames, int max_obj, int H, int W, uint32_t bg_rgb,
                             uint8_t* out, void* stream);
 
+/* Crop-parallel stage 2 (replaces the reference's remote dispatch of one
+ * frame's tiles, pkg/src/tilepipe/distribution/client.py:82-96). tp_slice_jobs copies rank's
+ * contiguous slice of the device job list (sizes differ by <= 1, larger first) and writes
+ * its count; tp_unslice_dets maps all-gathered per-rank padded slices ([world][max_slice]
+ * tiles of max_per_tile records + counts) back to global job order. */
+TP_API int tp_slice_jobs(const tp_tile_job_t* jobs, const int32_t* n_jobs_dev, int rank,
+                         int world, tp_tile_job_t* out, int32_t* n_out_dev, int max_out,
+                         void* stream);
+TP_API int tp_unslice_dets(const tp_det_t* gathered, const int32_t* gathered_counts,
+                           int max_slice, const int32_t* n_jobs_dev, int world, int max_jobs,
+                           int max_per_tile, tp_det_t* dets, int32_t* counts, void* stream);
+
 /* fp32-parity mode (no reference counterpart; serves the north-star 1e-3 score bar):
  * activations as exact fp16 pairs hi = fp16(x), lo = fp16(x - hi) in a doubled channel
  * dimension [hi C | lo C] so the 16-bit tcgen05 convs (weights duplicated over both halves,

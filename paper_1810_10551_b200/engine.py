@@ -16,6 +16,8 @@ Results equal the reference's run_sequence (pipeline.py:442-457) frame by frame.
 
 from __future__ import annotations
 
+from contextlib import nullcontext
+
 import numpy as np
 
 from . import kernels, native
@@ -31,12 +33,28 @@ MAX_MERGED = 512       # merged window boxes per frame
 MAX_PER_FRAME = 2048   # raw stage-2 detections per frame (postprocess capacity)
 
 
+def _dist_exchange(local_dets, local_counts, all_dets, all_counts):
+    """Default crop_shard exchange: all-gather every rank's padded stage-2 slice in rank
+    order over the default process group (NCCL on GPUs: one collective per tensor)."""
+    import torch.distributed as dist
+    for loc, out in ((local_dets, all_dets), (local_counts, all_counts)):
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(out, loc)
+        else:
+            dist.all_gather(list(out.view(dist.get_world_size(), -1).unbind(0)), loc)
+
+
 class AttentionPipelineB200:
     def __init__(self, settings: PipelineSettings, frame_w: int, frame_h: int, *,
                  max_frames: int = 8, seed: int = 0, threshold: float = 0.25,
                  policy: MergePolicy | None = None, resample: str = "nearest",
                  head: str = "calibrated", net: YoloNet | None = None,
-                 precision: str = DEFAULT_PRECISION):
+                 precision: str = DEFAULT_PRECISION,
+                 crop_shard: tuple[int, int] | None = None, exchange=None):
+        """crop_shard=(rank, world): crop-parallel stage 2 — every rank runs
+        stage 1 + selection for the same frames and evaluates its contiguous slice of the
+        active crops; `exchange(local_dets, local_counts, all_dets, all_counts)` all-gathers
+        the padded slices in rank order (default: torch.distributed, NCCL on GPUs)."""
         torch = native.require_cuda()
         if resample not in native.RESAMPLE:
             raise ValueError(f"resample must be one of {tuple(native.RESAMPLE)}")
@@ -95,6 +113,21 @@ class AttentionPipelineB200:
         self.frame_job_start = torch.zeros(mf + 1, dtype=torch.int32, device=dev)
         self.n_jobs2 = torch.zeros(1, dtype=torch.int32, device=dev)
         self.dets2, self.counts2 = kernels.alloc_dets(mf * self.F)
+        self.crop_shard = None
+        if crop_shard is not None:
+            rank, world = (int(v) for v in crop_shard)
+            if not (world >= 1 and 0 <= rank < world):
+                raise ValueError(f"bad crop_shard {crop_shard}")
+            self.crop_shard = (rank, world)
+            self.max_slice = -(-mf * self.F // world)
+            det_b = kernels.MAX_PER_TILE * native.DET_DTYPE.itemsize
+            self.jobs_local = torch.zeros(self.max_slice * native.JOB_DTYPE.itemsize,
+                                          dtype=torch.uint8, device=dev)
+            self.n_local = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.all_dets = torch.zeros(world * self.max_slice * det_b, dtype=torch.uint8,
+                                        device=dev)
+            self.all_counts = torch.zeros(world * self.max_slice, dtype=torch.int32, device=dev)
+            self.exchange = exchange or _dist_exchange
         rec = native.PDET_DTYPE.itemsize
         self.pdets = torch.zeros(mf * MAX_PER_FRAME * rec, dtype=torch.uint8, device=dev)
         self.pcounts = torch.zeros(mf, dtype=torch.int32, device=dev)
@@ -243,10 +276,73 @@ class AttentionPipelineB200:
             if timed:
                 ev[2].record(stream)
             nt2 = n * self.F  # upper bound; kernels read the real count from n_jobs2
-            self._gather(fr, self.jobs2, nt2, self.n_jobs2, stream)
-            self.net.forward(nt2, n_tiles_dev=self.n_jobs2, stream=stream)
-            kernels.decode(self.net, nt2, self.jobs2, self.W, self.H, self.threshold, self.dets2,
-                           self.counts2, n_tiles_dev=self.n_jobs2, stream=stream)
+            if self.crop_shard is None:
+                self._gather(fr, self.jobs2, nt2, self.n_jobs2, stream)
+                self.net.forward(nt2, n_tiles_dev=self.n_jobs2, stream=stream)
+                kernels.decode(self.net, nt2, self.jobs2, self.W, self.H, self.threshold,
+                               self.dets2, self.counts2, n_tiles_dev=self.n_jobs2, stream=stream)
+            else:
+                self._stage2_slice(fr, nt2, stream, st)
+                if self._split_phase:  # run_local(): the caller exchanges and finishes
+                    self._pending = (n, stream, st, timed)
+                    return
+                with self.torch.cuda.stream(stream) if stream is not None else nullcontext():
+                    self.exchange(*self.local_results(), self.all_dets, self.all_counts)
+                self._unslice(nt2, st)
+        except native.NativeError as exc:
+            raise StageFailure("final", -1) from exc
+        self._post(n, stream, st, timed)
+
+    # ---- crop-parallel stage 2 (crop_shard) ----
+    _split_phase = False
+
+    def _stage2_slice(self, fr, nt2, stream, st):
+        rank, world = self.crop_shard
+        native.call("tp_slice_jobs", native.ptr(self.jobs2), native.ptr(self.n_jobs2), rank,
+                    world, native.ptr(self.jobs_local), native.ptr(self.n_local), self.max_slice,
+                    st)
+        ntl = min(-(-nt2 // world), self.max_slice)  # host upper bound of the slice
+        self._gather(fr, self.jobs_local, ntl, self.n_local, stream)
+        self.net.forward(ntl, n_tiles_dev=self.n_local, stream=stream)
+        kernels.decode(self.net, ntl, self.jobs_local, self.W, self.H, self.threshold,
+                       self.dets2, self.counts2, n_tiles_dev=self.n_local, stream=stream)
+
+    def _unslice(self, nt2, st):
+        rank, world = self.crop_shard
+        native.call("tp_unslice_dets", native.ptr(self.all_dets), native.ptr(self.all_counts),
+                    self.max_slice, native.ptr(self.n_jobs2), world, nt2, kernels.MAX_PER_TILE,
+                    native.ptr(self.dets2), native.ptr(self.counts2), st)
+
+    def local_results(self):
+        """This rank's padded stage-2 slice: (dets bytes, counts) device tensors."""
+        det_b = kernels.MAX_PER_TILE * native.DET_DTYPE.itemsize
+        return self.dets2[: self.max_slice * det_b], self.counts2[: self.max_slice]
+
+    def run_local(self, n: int, frames=None, stream=None, timed: bool = False):
+        """crop_shard phase 1: stages 1 + selection + this rank's stage-2 slice; then
+        fill all_dets / all_counts (rank-order concatenation of every rank's
+        local_results()) and call finish_local()."""
+        if self.crop_shard is None:
+            raise ValueError("run_local needs crop_shard")
+        self._split_phase = True
+        try:
+            self.run_device(n, frames=frames, stream=stream, timed=timed)
+        finally:
+            self._split_phase = False
+
+    def finish_local(self):
+        """crop_shard phase 2: unslice the gathered slices, collect, postprocess."""
+        n, stream, st, timed = self._pending
+        try:
+            self._unslice(n * self.F, st)
+        except native.NativeError as exc:
+            raise StageFailure("final", -1) from exc
+        self._post(n, stream, st, timed)
+
+    def _post(self, n, stream, st, timed):
+        ev = self.events
+        K1 = self.K - 1
+        try:
             native.call("tp_collect_final", native.ptr(self.dets2), native.ptr(self.counts2),
                         kernels.MAX_PER_TILE, native.ptr(self.jobs2),
                         native.ptr(self.frame_job_start), n, native.ptr(self.pdets),

@@ -99,6 +99,8 @@ SIGNATURES = {
     "tp_debug_conv_counters": (_I, [_P, _I, _I]),
     "tp_split_store": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P]),
     "tp_split_input": (_I, [_P, _I, _P, _P]),
+    "tp_slice_jobs": (_I, [_P, _P, _I, _I, _P, _P, _I, _P]),
+    "tp_unslice_dets": (_I, [_P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "tp_render_frames": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_uint32, _P, _P]),
 }
 

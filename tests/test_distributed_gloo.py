@@ -78,3 +78,66 @@ def test_gather_restores_global_frame_order(n_frames):
         assert c == len(exp)
         rec = np.frombuffer(raw, dtype=native.PDET_DTYPE)[:c]
         assert (rec == exp).all()
+
+
+# ---- crop-parallel stage 2 (engine crop_shard): rank-order exchange of padded slices ----
+
+def _crop_worker(rank, world, port, n_jobs, max_slice, per_tile, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_10551_b200.engine import _dist_exchange
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b = D.shard_ranges(n_jobs, world)[rank]  # == tp_shard.cu slice_of()
+    dets = torch.full((max_slice, per_tile), -1, dtype=torch.int32)
+    counts = torch.zeros(max_slice, dtype=torch.int32)
+    for i, j in enumerate(range(a, b)):  # job j's "records": j*100 + k
+        counts[i] = j % (per_tile + 1)
+        dets[i, : counts[i]] = j * 100 + torch.arange(int(counts[i]), dtype=torch.int32)
+    all_dets = torch.empty(world * max_slice * per_tile, dtype=torch.int32)
+    all_counts = torch.empty(world * max_slice, dtype=torch.int32)
+    _dist_exchange(dets.view(-1), counts, all_dets, all_counts)
+    if rank == 0:
+        q.put((all_dets.tolist(), all_counts.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _unslice(all_dets, all_counts, n_jobs, world, max_slice, per_tile):
+    """Restatement of tp_shard.cu unslice_kernel's job -> (rank, index) map."""
+    base, extra = divmod(n_jobs, world)
+    out = []
+    for j in range(n_jobs):
+        if j < extra * (base + 1):
+            r, i = divmod(j, base + 1)
+        else:
+            jj = j - extra * (base + 1)
+            r = extra + jj // base
+            i = jj - (r - extra) * base
+        s = r * max_slice + i
+        c = all_counts[s]
+        out.append(all_dets[s * per_tile: s * per_tile + c])
+    return out
+
+
+@pytest.mark.parametrize("n_jobs", [11, 1])
+def test_crop_exchange_rank_order_and_unslice(n_jobs):
+    world, per_tile = 2, 3
+    max_slice = -(-16 // world)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + n_jobs + os.getpid() % 500
+    procs = [ctx.Process(target=_crop_worker,
+                         args=(r, world, port, n_jobs, max_slice, per_tile, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    all_dets, all_counts = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = _unslice(all_dets, all_counts, n_jobs, world, max_slice, per_tile)
+    assert got == [[j * 100 + k for k in range(j % (per_tile + 1))] for j in range(n_jobs)]
