@@ -44,8 +44,15 @@ extern "C" {
 #define TP_HEAD_CH 425 /* 5 * (4 + 1 + 80) */
 
 enum { TP_RESAMPLE_NEAREST = 0, TP_RESAMPLE_BILINEAR = 1 };
-/* 16-bit operand/activation format of the conv stack (fp32 accumulation either way). */
-enum { TP_DTYPE_BF16 = 0, TP_DTYPE_F16 = 1 };
+/* 16-bit operand/activation format of the conv stack (fp32 accumulation either way).
+ * TP_DTYPE_F16X2 is the fp32-parity plan (no reference counterpart; serves the north-star
+ * 1e-3 score bar against the fp32 CPU reference): every activation is stored as exact fp16
+ * pairs hi = fp16(x), lo = fp16(x - hi), interleaved per 16 channels ([hi 16 | lo 16]: real
+ * channel c at stored channel 32*(c/16) + c%16, its lo part 16 further), so a C-channel
+ * tensor has 2C stored channels and K spans both parts (weights duplicated per 16-channel
+ * group); products are exact and accumulate in fp32, so activations carry ~22 bits. The
+ * gather writes integer pixel values (exact in fp16) and layer 0 scales by 1/255 in fp32. */
+enum { TP_DTYPE_BF16 = 0, TP_DTYPE_F16 = 1, TP_DTYPE_F16X2 = 2 };
 
 /* One 608x608 tile to produce: crop square (x, y, side) of batch frame `frame`. */
 typedef struct tp_tile_job {
@@ -112,7 +119,7 @@ TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, i
  * BN folded in (layer 0: [32][144], 3 kernel rows x 3 window variants x 16 — see
  * paper_1810_10551_b200/yolo.py L0_VARIANTS); biases fp32 [cout_pad]. */
 typedef struct tp_yolo_net tp_yolo_net;
-TP_API size_t tp_yolo_workspace_bytes(int max_tiles);
+TP_API size_t tp_yolo_workspace_bytes(int max_tiles, int dtype);
 TP_API int tp_yolo_create(int max_tiles, const void* const* weights, const float* const* biases,
                    void* workspace, size_t workspace_bytes, int dtype, tp_yolo_net** out);
 TP_API void* tp_yolo_input(tp_yolo_net* net);        /* 16-bit [max_tiles][610][610][8] slots */
@@ -205,19 +212,6 @@ TP_API int tp_unslice_dets(const tp_det_t* gathered, const int32_t* gathered_cou
                            int max_slice, const int32_t* n_jobs_dev, int world, int max_jobs,
                            int max_per_tile, tp_det_t* dets, int32_t* counts, void* stream);
 
-/* fp32-parity mode (no reference counterpart; serves the north-star 1e-3 score bar):
- * activations as exact fp16 pairs hi = fp16(x), lo = fp16(x - hi) in a doubled channel
- * dimension [hi C | lo C] so the 16-bit tcgen05 convs (weights duplicated over both halves,
- * fp32 epilogue) carry ~22-bit activations.
- * tp_split_store: fp32 conv output [n][res][res][src_cstride] (C channels used) -> optional
- * 2x2 max pool or space-to-depth reorg -> dst fp16 compact [n][res'][res'][dst_cstride],
- * hi at channel coff + c, lo at coff + c + lo_off.
- * tp_split_input: u8 tiles [n][608][608][3] -> fp16 [n][608][608][32], channels 0..2 =
- * hi(v/255), 16..18 = lo(v/255), the rest 0. */
-TP_API int tp_split_store(const float* src, int n, int res, int src_cstride, int C, int pool,
-                          int reorg, void* dst, int dst_cstride, int coff, int lo_off,
-                          void* stream);
-TP_API int tp_split_input(const uint8_t* tiles, int n, void* dst, void* stream);
 
 /* Profiling only (TP_CONV_DEBUG bit 32 set in the environment when the net/conv runs):
  * per-role cycle totals of conv_tc_kernel summed over CTAs — 0 producer, 1 producer

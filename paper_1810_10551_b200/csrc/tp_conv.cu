@@ -68,6 +68,11 @@ struct ConvParams {
   int n_bchunks;
   uint32_t stage_bytes;  // epilogue store staging (TMA-store variants): 8 warps x 2 KB
   int nbuf;  // box kernel: TMEM accumulator buffers (2 or 4)
+  // fp32-parity plan (TP_DTYPE_F16X2): outputs leave as exact fp16 pairs hi = fp16(v),
+  // lo = fp16(v - hi), interleaved per 16 channels ([hi 16 | lo 16], stored channel of real
+  // channel c = 32 (c / 16) + c % 16, its lo part +16); out_coff is in stored channels.
+  int split;
+  float alpha;  // layer 0: accumulator scale (1/255 when the input holds integer pixels)
   // profiling only (TP_CONV_DEBUG bits): 1 skip epilogue, 2 skip MMAs, 4 skip stores,
   // 8 skip TMEM loads, 16 no TMA (stale operands), 32 role cycle counters (g_conv_prof)
   int dbg;
@@ -165,8 +170,30 @@ __device__ unsigned long long g_conv_prof[8];
 #define PROF_ADD(acc, t0) \
   if (p.dbg & 32) acc += clock64() - (t0)
 
-// Epilogue variants, chosen at compile time.
-enum Epi { EPI_PLAIN = 0, EPI_POOL = 1, EPI_REORG = 2, EPI_F32 = 3 };
+// Epilogue variants, chosen at compile time (EPI_SPLIT: TMA-stored hi/lo fp16 pairs).
+enum Epi { EPI_PLAIN = 0, EPI_POOL = 1, EPI_REORG = 2, EPI_F32 = 3, EPI_SPLIT = 4 };
+
+// 2*NP fp32 values -> NP packed fp16 pairs hi = fp16(v) and NP packed lo = fp16(v - hi)
+template <int NP>
+__device__ __forceinline__ void split_pairs(const float* f, uint32_t* hi, uint32_t* lo) {
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+    const float2 hf = __half22float2(h);
+    __half2 l = __floats2half2_rn(f[2 * j] - hf.x, f[2 * j + 1] - hf.y);
+    hi[j] = *reinterpret_cast<uint32_t*>(&h);
+    lo[j] = *reinterpret_cast<uint32_t*>(&l);
+  }
+}
+// 16 split values to a stored [hi 16 | lo 16] group at o (16-bit elements)
+__device__ __forceinline__ void store_split16(__nv_bfloat16* o, const float* f) {
+  uint32_t hi[8], lo[8];
+  split_pairs<8>(f, hi, lo);
+  *reinterpret_cast<uint4*>(o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(o + 8) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+  *reinterpret_cast<uint4*>(o + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  *reinterpret_cast<uint4*>(o + 24) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+}
 constexpr int kMaxBias = 1024;
 
 // Walks a CTA's contiguous tile range: t = mt * n_blocks_n + nb, and for RECT tiles
@@ -203,8 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
   constexpr int BK = MODE == MODE_SW128 ? 64 : 32;
   constexpr bool RECT = EPI == EPI_POOL;
-  // FLAT plain / fp32 outputs leave through per-warp swizzled smem slabs + TMA stores
-  constexpr bool TSTORE = EPI == EPI_PLAIN || EPI == EPI_F32;
+  // FLAT plain / fp32 / split outputs leave through per-warp swizzled smem slabs + TMA stores
+  constexpr bool TSTORE = EPI == EPI_PLAIN || EPI == EPI_F32 || EPI == EPI_SPLIT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -493,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // pattern, then one TMA store of {slab, 32 rows}; halo rows are written as zeros
           // two slabs per warp alternate: staging the next one only waits for the store
           // issued two slabs ago (bulk_wait_read1), not for the one just issued
-          constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
+          constexpr int CPS = EPI == EPI_F32 || EPI == EPI_SPLIT ? 1 : 2;
           const int cs = c % CPS;
           const uint32_t slab_off = warp * 4096 + (slab & 1) * 2048;
           const uint32_t buf = tp::smem_u32(smC) + slab_off;
@@ -503,7 +530,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const uint32_t rbase = buf + lane * 64;
           const uint32_t swz = (lane >> 1) & 3;
-          if (EPI == EPI_F32) {
+          if (EPI == EPI_SPLIT) {  // one 64-byte row = [hi 16 | lo 16]
+            uint32_t hi[8], lo[8];
+            split_pairs<8>(f, hi, lo);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              hi[j] = valid ? hi[j] : 0u;
+              lo[j] = valid ? lo[j] : 0u;
+            }
+            st_shared_v4(rbase + ((0 ^ swz) << 4), hi[0], hi[1], hi[2], hi[3]);
+            st_shared_v4(rbase + ((1 ^ swz) << 4), hi[4], hi[5], hi[6], hi[7]);
+            st_shared_v4(rbase + ((2 ^ swz) << 4), lo[0], lo[1], lo[2], lo[3]);
+            st_shared_v4(rbase + ((3 ^ swz) << 4), lo[4], lo[5], lo[6], lo[7]);
+          } else if (EPI == EPI_F32) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float a0 = valid ? f[4 * k] : 0.f, a1 = valid ? f[4 * k + 1] : 0.f;
@@ -530,7 +569,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0 && (p.dbg & 4) == 0) {
-              tma_store_2d(&tmC, smC + slab_off, p.out_coff + ch0 - 16 * cs,
+              tma_store_2d(&tmC, smC + slab_off,
+                           EPI == EPI_SPLIT ? p.out_coff + 2 * ch0 : p.out_coff + ch0 - 16 * cs,
                            it.mt * 128 + (int)q * 32);
               bulk_commit();
             }
@@ -539,7 +579,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (!valid || !writer || ch0 >= p.cout || (p.dbg & 4)) continue;
-        if (EPI == EPI_F32) {
+        if (p.split) {
+          const int creal = (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
+          store_split16(reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride +
+                            p.out_coff + 2 * creal,
+                        f);
+        } else if (EPI == EPI_F32) {
           float* o = reinterpret_cast<float*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
           if (ch0 + 16 <= p.cout) {
 #pragma unroll
@@ -846,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
         }
-        constexpr int CPS = EPI == EPI_F32 ? 1 : 2;
+        constexpr int CPS = EPI == EPI_F32 || EPI == EPI_SPLIT ? 1 : 2;
         const int cs = c % CPS;
         const uint32_t slab_off = warp * 4096 + (slab & 1) * 2048;  // two alternating slabs
         const uint32_t rowa = tp::smem_u32(smC) + slab_off + lane * 64;
@@ -854,7 +899,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) bulk_wait_read1();
           __syncwarp();
         }
-        if (EPI == EPI_F32) {
+        if (EPI == EPI_SPLIT) {  // one 64-byte row = [hi 16 | lo 16]
+          uint32_t hi[8], lo[8];
+          split_pairs<8>(f, hi, lo);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            hi[j] = valid ? hi[j] : 0u;
+            lo[j] = valid ? lo[j] : 0u;
+          }
+          st_shared_v4(rowa + ((0 ^ swz) << 4), hi[0], hi[1], hi[2], hi[3]);
+          st_shared_v4(rowa + ((1 ^ swz) << 4), hi[4], hi[5], hi[6], hi[7]);
+          st_shared_v4(rowa + ((2 ^ swz) << 4), lo[0], lo[1], lo[2], lo[3]);
+          st_shared_v4(rowa + ((3 ^ swz) << 4), lo[4], lo[5], lo[6], lo[7]);
+        } else if (EPI == EPI_F32) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const float a0 = valid ? f[4 * k] : 0.f, a1 = valid ? f[4 * k + 1] : 0.f;
@@ -881,7 +938,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmC, smC + slab_off, p.out_coff + ch0 - 16 * cs, rbase);
+            tma_store_2d(&tmC, smC + slab_off,
+                         EPI == EPI_SPLIT ? p.out_coff + 2 * ch0 : p.out_coff + ch0 - 16 * cs,
+                         rbase);
             bulk_commit();
           }
           ++slab;
@@ -1095,18 +1154,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::tmem_ld16(t_row + 64 + c * 16, v2);
         tp::tmem_ld16(t_row + 96 + c * 16, v3);
         tp::tmem_ld_wait();
+        float fv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float m = fmaxf(fmaxf(__uint_as_float(v0[j]), __uint_as_float(v1[j])),
+                                fmaxf(__uint_as_float(v2[j]), __uint_as_float(v3[j])));
+          // scale (alpha > 0), bias and leaky are monotonic: pooling first is the same value
+          const float a = fmaf(m, p.alpha, bias_s[c * 16 + j]);
+          fv[j] = fmaxf(a, 0.1f * a);
+        }
+        if (p.split) {
+          if (img < n_img) store_split16(o + c * 32, fv);
+          continue;
+        }
         uint32_t pk[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float a = fmaxf(fmaxf(__uint_as_float(v0[2 * j]), __uint_as_float(v1[2 * j])),
-                          fmaxf(__uint_as_float(v2[2 * j]), __uint_as_float(v3[2 * j])));
-          float b = fmaxf(fmaxf(__uint_as_float(v0[2 * j + 1]), __uint_as_float(v1[2 * j + 1])),
-                          fmaxf(__uint_as_float(v2[2 * j + 1]), __uint_as_float(v3[2 * j + 1])));
-          // bias + leaky are monotonic, so pooling first gives the same value
-          a += bias_s[c * 16 + 2 * j];
-          b += bias_s[c * 16 + 2 * j + 1];
-          a = fmaxf(a, 0.1f * a);
-          b = fmaxf(b, 0.1f * b);
+          const float a = fv[2 * j], b = fv[2 * j + 1];
           if (f16) {
             __half2 h = __floats2half2_rn(a, b);
             pk[j] = *reinterpret_cast<uint32_t*>(&h);
@@ -1442,6 +1506,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 8; ++j) h8[j] = fmaxf(h8[j], 0.1f * h8[j]);
           }
           if (!store || ch >= p.cout || (p.dbg & 4)) continue;
+          if (p.split) {
+            uint32_t hi[4], lo[4];
+            split_pairs<4>(h8, hi, lo);
+            __nv_bfloat16* os = o + 2 * c * 16 + (odd ? 8 : 0);
+            *reinterpret_cast<uint4*>(os) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(os + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            continue;
+          }
           uint32_t pk[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -1471,12 +1543,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (TSTORE) {
           if (!warp_rows_valid) continue;
-          const int cs = c & 1;
+          const bool spl = p.split != 0;  // split: one slab ([hi 16 | lo 16]) per chunk
+          const int cs = spl ? 0 : (c & 1);
           const uint32_t slab_off = warp * 4096 + (slab & 1) * 2048;  // two alternating slabs
           const uint32_t buf = tp::smem_u32(smC) + slab_off;
           if (cs == 0) {
             if (lane == 0) bulk_wait_read1();
             __syncwarp();
+          }
+          if (spl) {
+            uint32_t hi[8], lo[8];
+            split_pairs<8>(f, hi, lo);
+            const uint32_t rbase = buf + lane * 64, swz = (lane >> 1) & 3;
+            st_shared_v4(rbase + ((0 ^ swz) << 4), hi[0], hi[1], hi[2], hi[3]);
+            st_shared_v4(rbase + ((1 ^ swz) << 4), hi[4], hi[5], hi[6], hi[7]);
+            st_shared_v4(rbase + ((2 ^ swz) << 4), lo[0], lo[1], lo[2], lo[3]);
+            st_shared_v4(rbase + ((3 ^ swz) << 4), lo[4], lo[5], lo[6], lo[7]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0 && (p.dbg & 4) == 0) {
+              tma_store_3d(&tmC, smC + slab_off, p.out_coff + 2 * c * 16, tbx * BOX_TW,
+                           timg * p.res + tby * BOX_TH + (int)q * 4);
+              bulk_commit();
+            }
+            ++slab;
+            continue;
           }
           uint32_t pk[8];
 #pragma unroll
@@ -1505,6 +1596,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (!store || c * 16 >= p.cout || (p.dbg & 4)) continue;
+        if (p.split) {
+          store_split16(o + 2 * c * 16, f);
+          continue;
+        }
         uint32_t pk[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -1577,6 +1672,50 @@ __global__ void maxpool2_kernel(const __nv_bfloat16* __restrict__ in, int n_img,
     }
     __nv_bfloat16* dst = out + (((long long)img * ores + y) * ores + x) * cstride + g * 8;
     *reinterpret_cast<uint4*>(dst) = m;
+  }
+}
+
+// 2x2/2 max pool of a split (hi/lo interleaved) tensor: each thread pools 8 channels,
+// comparing the exact fp32 values hi + lo (exact: |lo| <= ulp(hi) / 2), and re-splits.
+__global__ void maxpool2_split_kernel(const __half* __restrict__ in, int n_img, int res,
+                                      int cstride, __half* __restrict__ out,
+                                      const int32_t* __restrict__ n_img_dev) {
+  if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
+  const int ores = res >> 1;
+  const int cg = cstride >> 4;  // 8-channel hi blocks: two per 32-channel group
+  const long long total = (long long)n_img * ores * ores * cg;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % cg);
+    long long r = i / cg;
+    const int x = (int)(r % ores);
+    r /= ores;
+    const int y = (int)(r % ores);
+    const int img = (int)(r / ores);
+    const int coff = (g >> 1) * 32 + (g & 1) * 8;
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half* src = in + (((long long)img * res + 2 * y + (k >> 1)) * res + 2 * x + (k & 1)) *
+                                   cstride + coff;
+      const uint4 h = *reinterpret_cast<const uint4*>(src);
+      const uint4 l = *reinterpret_cast<const uint4*>(src + 16);
+      const __half2* ph = reinterpret_cast<const __half2*>(&h);
+      const __half2* pl = reinterpret_cast<const __half2*>(&l);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 a = __half22float2(ph[j]), b = __half22float2(pl[j]);
+        m[2 * j] = fmaxf(m[2 * j], a.x + b.x);
+        m[2 * j + 1] = fmaxf(m[2 * j + 1], a.y + b.y);
+      }
+    }
+    uint32_t hi[4], lo[4];
+    split_pairs<4>(m, hi, lo);
+    __half* dst = out + (((long long)img * ores + y) * ores + x) * cstride + coff;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(dst + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
 }
 
@@ -1714,9 +1853,11 @@ struct ConvLaunch {
 int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_stride, int cin_used,
                  const void* weight, const float* bias, int cout, int cout_pad, int ksize,
                  int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
-                 int dtype, int pool) {
+                 int dtype, int pool, float alpha = 1.0f) {
   memset(L, 0, sizeof(*L));
-  const bool f16 = dtype == TP_DTYPE_F16;
+  const bool f16 = dtype != TP_DTYPE_BF16;
+  // TP_DTYPE_F16X2: split (hi/lo) 16-bit outputs; the fp32 head output stays fp32
+  const int split = dtype == TP_DTYPE_F16X2 && !out_fp32 ? 1 : 0;
   if (cout_pad % 32 != 0 || cout > cout_pad) {
     tp_set_error("conv: bad cout/cout_pad %d/%d (cout_pad must be a multiple of 32)", cout,
                  cout_pad);
@@ -1754,6 +1895,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.out_fp32 = out_fp32;
   p.leaky = leaky;
   p.reorg = reorg;
+  p.split = split;
+  p.alpha = alpha;
   p.dbg = getenv("TP_CONV_DEBUG") ? atoi(getenv("TP_CONV_DEBUG")) : 0;
   // everything else in smem: 1 KB alignment slack, bias, barriers (<= 12 stages), TMEM slot
   const int fixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
@@ -1910,9 +2053,11 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   const bool box_ok = ksize == 3 && (cin_used == 32 || cin_used == 64) && cout_pad <= 256 &&
                       cout == cout_pad && !reorg && !out_fp32 && res % 8 == 0 &&
                       bres <= 160 * 1024 && (be == nullptr || atoi(be) != 0);
-  if (box_ok) {
-    // pool-in-M: 4 pool accumulators x 2 buffers must fit TMEM; pooled side in 8-px tiles
-    const bool pm = pool && cout_pad <= 64 && (res / 2) % 8 == 0;
+  // pool-in-M first (4 pool accumulators x 2 buffers must fit TMEM; pooled side in 8-px
+  // tiles), then the shuffle-pool / plain box if its four parity planes do not fit smem
+  for (int try_pm = 1; box_ok && try_pm >= 0 && !L->box; --try_pm) {
+    const bool pm = try_pm && pool && cout_pad <= 64 && (res / 2) % 8 == 0;
+    if (try_pm && !pm) continue;
     const int epi = pm ? BOX_POOLM : pool ? BOX_POOL : BOX_PLAIN;
     const uint32_t rb = (uint32_t)bk * 2;
     const uint32_t stage = pm ? 4 * ((PLANE_W * PLANE_H * rb + 1023) & ~1023u)
@@ -2063,6 +2208,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
   }
   if (L.pair)
     return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
+           : L.p.split  ? launch_pair<EPI_SPLIT>(L, n_img, n_img_dev, st)
                         : launch_pair<EPI_PLAIN>(L, n_img, n_img_dev, st);
   if (L.l0) {
     static bool configured = false;
@@ -2081,12 +2227,14 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
     TP_LAUNCH_CHECK();
     return TP_OK;
   }
-  const int epi = L.p.rect ? EPI_POOL : L.p.reorg ? EPI_REORG : L.p.out_fp32 ? EPI_F32 : EPI_PLAIN;
+  const int epi = L.p.rect ? EPI_POOL : L.p.reorg ? EPI_REORG : L.p.out_fp32 ? EPI_F32
+                : L.p.split ? EPI_SPLIT : EPI_PLAIN;
 #define TP_EPI_SWITCH(M)                                                  \
   switch (epi) {                                                          \
     case EPI_POOL: return launch_mode<M, EPI_POOL>(L, n_img, n_img_dev, st);   \
     case EPI_REORG: return launch_mode<M, EPI_REORG>(L, n_img, n_img_dev, st); \
     case EPI_F32: return launch_mode<M, EPI_F32>(L, n_img, n_img_dev, st);     \
+    case EPI_SPLIT: return launch_mode<M, EPI_SPLIT>(L, n_img, n_img_dev, st); \
     default: return launch_mode<M, EPI_PLAIN>(L, n_img, n_img_dev, st);        \
   }
   if (L.mode == MODE_SW128) {
@@ -2097,11 +2245,17 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
 }
 
 int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st,
-             const int32_t* n_img_dev, int f16) {
-  const long long total = (long long)n_img * (res / 2) * (res / 2) * (cstride / 8);
+             const int32_t* n_img_dev, int f16, int split = 0) {
+  const long long total = (long long)n_img * (res / 2) * (res / 2) * (cstride / (split ? 16 : 8));
   if (total == 0) return TP_OK;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  if (split) {
+    maxpool2_split_kernel<<<(int)blocks, 256, 0, st>>>((const __half*)in, n_img, res, cstride,
+                                                      (__half*)out, n_img_dev);
+    TP_LAUNCH_CHECK();
+    return TP_OK;
+  }
   maxpool2_kernel<<<(int)blocks, 256, 0, st>>>((const __nv_bfloat16*)in, n_img, res, cstride,
                                                (__nv_bfloat16*)out, n_img_dev, f16);
   TP_LAUNCH_CHECK();
@@ -2156,10 +2310,16 @@ const Step kSteps[] = {
     {0, 20, E38, CAT19, 0, 1, 0}, {0, 21, CAT19, A19, 0, 0, 0}, {0, 22, A19, HEAD, 0, 0, 0}};
 constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
 
-size_t buf_bytes(int b, int max_tiles) {
+// channels stored per pixel: the split plan doubles every activation except the layer-0
+// slots (integer pixel values, exact in fp16) and the fp32 head
+int buf_ch(int b, int dtype) {
+  return kBufs[b].ch * (dtype == TP_DTYPE_F16X2 && b != I608 && b != HEAD ? 2 : 1);
+}
+
+size_t buf_bytes(int b, int max_tiles, int dtype) {
   // compact NHWC, except the layer-0 input (padded, written by the gather)
   const size_t side = kBufs[b].res + (b == I608 ? 2 : 0);
-  return (size_t)max_tiles * side * side * kBufs[b].ch * kBufs[b].bytes_per;
+  return (size_t)max_tiles * side * side * buf_ch(b, dtype) * kBufs[b].bytes_per;
 }
 
 }  // namespace
@@ -2171,9 +2331,9 @@ struct tp_yolo_net {
   ConvLaunch convs[23];
 };
 
-extern "C" size_t tp_yolo_workspace_bytes(int max_tiles) {
+extern "C" size_t tp_yolo_workspace_bytes(int max_tiles, int dtype) {
   size_t total = 0;
-  for (int b = 0; b < NBUF; ++b) total += (buf_bytes(b, max_tiles) + 1023) & ~size_t(1023);
+  for (int b = 0; b < NBUF; ++b) total += (buf_bytes(b, max_tiles, dtype) + 1023) & ~size_t(1023);
   return total;
 }
 
@@ -2185,7 +2345,11 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
     tp_set_error("tp_yolo_create: bad argument");
     return TP_ERR_ARG;
   }
-  if (workspace_bytes < tp_yolo_workspace_bytes(max_tiles)) {
+  if (dtype != TP_DTYPE_BF16 && dtype != TP_DTYPE_F16 && dtype != TP_DTYPE_F16X2) {
+    tp_set_error("tp_yolo_create: bad dtype %d", dtype);
+    return TP_ERR_ARG;
+  }
+  if (workspace_bytes < tp_yolo_workspace_bytes(max_tiles, dtype)) {
     tp_set_error("tp_yolo_create: workspace too small");
     return TP_ERR_CAPACITY;
   }
@@ -2195,10 +2359,10 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
   uint8_t* w = reinterpret_cast<uint8_t*>(workspace);
   for (int b = 0; b < NBUF; ++b) {
     net->bufs[b] = w;
-    w += (buf_bytes(b, max_tiles) + 1023) & ~size_t(1023);
+    w += (buf_bytes(b, max_tiles, dtype) + 1023) & ~size_t(1023);
   }
   // halos (and every never-written byte) must be zero
-  cudaError_t e = cudaMemset(workspace, 0, tp_yolo_workspace_bytes(max_tiles));
+  cudaError_t e = cudaMemset(workspace, 0, tp_yolo_workspace_bytes(max_tiles, dtype));
   if (e != cudaSuccess) {
     delete net;
     tp_set_error("tp_yolo_create: memset: %s", cudaGetErrorString(e));
@@ -2210,10 +2374,16 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
     const LayerDef& L = kConvs[st.conv];
     const int cout_pad = L.cout == 425 ? kHeadCstride : L.cout;
     const bool head = (st.out == HEAD);
+    // split plan: K covers the interleaved hi/lo input (duplicated weights); layer 0 reads
+    // integer pixels and scales its accumulators by 1/255
+    const bool split = dtype == TP_DTYPE_F16X2;
+    const int cin = split && st.conv != 0 ? 2 * L.cin : L.cin;
+    const int coff = split ? 2 * st.coff : st.coff;
     int rc = prepare_conv(&net->convs[st.conv], net->bufs[st.in], max_tiles, L.res,
-                          kBufs[st.in].ch, L.cin, weights[st.conv], biases[st.conv], L.cout,
-                          cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], kBufs[st.out].ch,
-                          st.coff, head ? 1 : 0, st.reorg, dtype, st.fpool);
+                          buf_ch(st.in, dtype), cin, weights[st.conv], biases[st.conv], L.cout,
+                          cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], buf_ch(st.out, dtype),
+                          coff, head ? 1 : 0, st.reorg, dtype, st.fpool,
+                          split && st.conv == 0 ? 1.0f / 255.0f : 1.0f);
     if (rc) {
       delete net;
       return rc;
@@ -2241,8 +2411,9 @@ extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_
     const Step& sp = kSteps[s];
     int rc;
     if (sp.is_pool) {
-      rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, kBufs[sp.in].ch, net->bufs[sp.out],
-                    st, n_tiles_dev, net->dtype == TP_DTYPE_F16);
+      rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, buf_ch(sp.in, net->dtype),
+                    net->bufs[sp.out], st, n_tiles_dev, net->dtype != TP_DTYPE_BF16,
+                    net->dtype == TP_DTYPE_F16X2);
     } else {
       rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
     }
@@ -2266,7 +2437,7 @@ extern "C" int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int
   const int b = kSteps[layer].out;
   *ptr = net->bufs[b];
   *res = kBufs[b].res;
-  *cstride = kBufs[b].ch;
+  *cstride = buf_ch(b, net->dtype);
   return TP_OK;
 }
 
@@ -2285,8 +2456,10 @@ extern "C" int tp_conv(const void* in, int n_img, int res, int cin_stride, const
     return TP_ERR_ARG;
   }
   ConvLaunch L;
+  const float alpha = dtype == TP_DTYPE_F16X2 && cin_stride == 16 ? 1.0f / 255.0f : 1.0f;
   int rc = prepare_conv(&L, in, n_img, res, cin_stride, cin_stride, weight, bias, cout, cout_pad,
-                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg, dtype, pool);
+                        ksize, leaky, out, out_cstride, out_coff, out_fp32, reorg, dtype, pool,
+                        alpha);
   if (rc) return rc;
   return run_conv(L, n_img, nullptr, (cudaStream_t)stream);
 }
@@ -2313,10 +2486,11 @@ extern "C" int tp_debug_conv_counters(uint64_t* out, int n, int reset) {
 
 extern "C" int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype,
                            void* out, void* stream) {
-  if (in == nullptr || out == nullptr || (res & 1) || (cstride & 7)) {
+  const int split = dtype == TP_DTYPE_F16X2;
+  if (in == nullptr || out == nullptr || (res & 1) || (cstride & (split ? 31 : 7))) {
     tp_set_error("tp_maxpool2: bad argument");
     return TP_ERR_ARG;
   }
   return run_pool(in, n_img, res, cstride, out, (cudaStream_t)stream, nullptr,
-                  dtype == TP_DTYPE_F16);
+                  dtype != TP_DTYPE_BF16, split);
 }

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      const int32_t* __restrict__ n_jobs_dev,
                                                      int mode, uint8_t* __restrict__ out_u8,
                                                      __nv_bfloat16* __restrict__ out_act,
-                                                     int act_f16) {
+                                                     int act_dtype) {
   const int t = blockIdx.y;  // tile
   if (n_jobs_dev != nullptr && t >= *n_jobs_dev) return;
   const tp_tile_job_t job = jobs[t];
@@ -58,14 +58,18 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
   const bool nearest = mode == TP_RESAMPLE_NEAREST;
 
   // Per-CTA tables, shared by all GATHER_ROWS rows of this tile:
-  //   lut: exact value/255 in the activation type (bit-identical to dividing)
+  //   lut: exact value/255 in the activation type (bit-identical to dividing); the
+  //   integer value itself for TP_DTYPE_F16X2 (layer 0 then scales by 1/255 in fp32)
   //   cx0/cx1: byte offset 3*x of the column's source tap(s) in a frame row, -1 outside
   //   the frame (or outside the tile for u = 608); cf: bilinear weight of tap 1
   __shared__ uint16_t lut[256];
   __shared__ int cx0[S + 1], cx1[S + 1];
   __shared__ int cf[S + 1];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    if (act_f16) {
+    if (act_dtype == TP_DTYPE_F16X2) {  // fp32-parity plan: the integer value (exact)
+      __half h = __float2half_rn((float)i);
+      lut[i] = *reinterpret_cast<uint16_t*>(&h);
+    } else if (act_dtype == TP_DTYPE_F16) {
       __half h = __float2half_rn((float)i / 255.0f);
       lut[i] = *reinterpret_cast<uint16_t*>(&h);
     } else {
@@ -186,7 +190,7 @@ extern "C" int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int 
   gather_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(frames, frame_stride, H, W, jobs,
                                                         n_jobs_dev, mode, out_u8,
                                                         (__nv_bfloat16*)out_act,
-                                                        act_dtype == TP_DTYPE_F16);
+                                                        act_dtype);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }

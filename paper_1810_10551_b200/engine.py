@@ -26,7 +26,7 @@ from .geometry import Rect
 from .pipeline_types import AttentionModel, FrameResult, GridPlan, PipelineSettings, \
     StageFailure, TimingProfile
 from .postprocess import LabelTable, MergePolicy, make_policy_struct, ctypes_ref
-from .yolo import COCO_NAMES, DEFAULT_PRECISION, SplitNet, YoloNet
+from .yolo import COCO_NAMES, DEFAULT_PRECISION, YoloNet
 
 MAX_BOXES = 256        # attention boxes per frame (conf >= min_conf)
 MAX_MERGED = 512       # merged window boxes per frame
@@ -73,15 +73,9 @@ class AttentionPipelineB200:
             raise ValueError("final grid too large for the selection/merge kernels")
         mf = self.max_frames
         self.max_tiles = mf * max(self.A, self.F)
-        if net is None:  # precision "fp32" = hi/lo fp16 activation pairs (yolo.SplitNet)
-            net = (SplitNet(self.max_tiles, seed=seed, head=head) if precision == "fp32"
-                   else YoloNet(self.max_tiles, seed=seed, head=head, dtype=precision))
+        if net is None:  # precision "fp32" = the hi/lo fp16 activation-pair plan
+            net = YoloNet(self.max_tiles, seed=seed, head=head, dtype=precision)
         self.net = net
-        self.tiles_u8 = None
-        if hasattr(net, "load_tiles"):  # the split input is built from u8 tiles
-            torch = native.require_cuda()
-            self.tiles_u8 = torch.empty((self.max_tiles, 608, 608, 3), dtype=torch.uint8,
-                                        device="cuda")
         self.dtype = self.net.dtype
         if self.net.max_tiles < self.max_tiles:
             raise ValueError("shared YoloNet too small for this batch size")
@@ -229,15 +223,10 @@ class AttentionPipelineB200:
         return replay
 
     def _gather(self, fr, jobs, n_tiles, n_jobs_dev, stream):
-        """Crop gather into the net's layer-0 input (fp32-parity nets: u8 tiles + split)."""
-        if self.tiles_u8 is None:
-            kernels.gather(fr, self.frame_stride, self.H, self.W, jobs, n_tiles, self.resample,
-                           out_act_ptr=self.net.input_ptr, n_jobs_dev=n_jobs_dev, stream=stream,
-                           dtype=self.dtype)
-        else:
-            kernels.gather(fr, self.frame_stride, self.H, self.W, jobs, n_tiles, self.resample,
-                           out_u8=self.tiles_u8, n_jobs_dev=n_jobs_dev, stream=stream)
-            self.net.load_tiles(self.tiles_u8, n_tiles, stream)
+        """Crop gather into the net's layer-0 input slots."""
+        kernels.gather(fr, self.frame_stride, self.H, self.W, jobs, n_tiles, self.resample,
+                       out_act_ptr=self.net.input_ptr, n_jobs_dev=n_jobs_dev, stream=stream,
+                       dtype=self.dtype)
 
     def _stage1(self, fr, n, stream, st):
         K1 = self.K - 1
@@ -531,13 +520,8 @@ def yolo_tagged(det, frame, crops):
         n = len(chunk)
         jobs = kernels.jobs_tensor((0, c.crop_id, int(c.global_rect.x), int(c.global_rect.y),
                                     int(c.global_rect.w), 0) for c in chunk)
-        if hasattr(net, "load_tiles"):
-            u8 = torch.empty((n, 608, 608, 3), dtype=torch.uint8, device="cuda")
-            kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_u8=u8)
-            net.load_tiles(u8, n)
-        else:
-            kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr,
-                           dtype=net.dtype)
+        kernels.gather(dev, 0, H, W, jobs, n, "nearest", out_act_ptr=net.input_ptr,
+                       dtype=net.dtype)
         net.forward(n)
         recs, counts = kernels.alloc_dets(n)
         kernels.decode(net, n, jobs, W, H, det.threshold, recs, counts)

@@ -65,11 +65,8 @@ def detect_tiles_device(net, tiles_dev, thresh: float):
     so the layer-0 input normalisation is the same kernel as the pipeline's."""
     n = int(tiles_dev.shape[0])
     jobs = jobs_tensor((i, 0, 0, 0, MODEL_SIDE, 0) for i in range(n))
-    if hasattr(net, "load_tiles"):  # fp32-parity net: hi/lo split input
-        net.load_tiles(tiles_dev.contiguous(), n)
-    else:
-        gather(tiles_dev, MODEL_SIDE * MODEL_SIDE * 3, MODEL_SIDE, MODEL_SIDE, jobs, n,
-               "nearest", out_act_ptr=net.input_ptr, dtype=net.dtype)
+    gather(tiles_dev, MODEL_SIDE * MODEL_SIDE * 3, MODEL_SIDE, MODEL_SIDE, jobs, n,
+           "nearest", out_act_ptr=net.input_ptr, dtype=net.dtype)
     net.forward(n)
     out, counts = alloc_dets(n)
     decode(net, n, jobs, MODEL_SIDE, MODEL_SIDE, thresh, out, counts)

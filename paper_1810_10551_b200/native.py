@@ -34,7 +34,7 @@ PDET_DTYPE = np.dtype(
 assert JOB_DTYPE.itemsize == 32 and DET_DTYPE.itemsize == 48 and PDET_DTYPE.itemsize == 56
 
 RESAMPLE = {"nearest": 0, "bilinear": 1}
-DTYPES = {"bf16": 0, "fp16": 1}
+DTYPES = {"bf16": 0, "fp16": 1, "fp32": 2}  # "fp32" = TP_DTYPE_F16X2 (hi/lo pair plan)
 TP_MAX_CLASSES = 128
 RULES = {"vertical": 1, "horizontal": 2, "both": 3}
 
@@ -76,7 +76,7 @@ SIGNATURES = {
     "tp_version": (_I, []),
     "tp_device_sm_count": (_I, [_P]),
     "tp_gather_tiles": (_I, [_P, _I64, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P]),
-    "tp_yolo_workspace_bytes": (_SZ, [_I]),
+    "tp_yolo_workspace_bytes": (_SZ, [_I, _I]),
     "tp_yolo_create": (_I, [_I, _P, _P, _P, _SZ, _I, _P]),
     "tp_yolo_input": (_P, [_P]),
     "tp_yolo_head": (_P, [_P]),
@@ -97,8 +97,6 @@ SIGNATURES = {
     "tp_postprocess": (_I, [_P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
     "tp_maxpool2": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "tp_debug_conv_counters": (_I, [_P, _I, _I]),
-    "tp_split_store": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P]),
-    "tp_split_input": (_I, [_P, _I, _P, _P]),
     "tp_slice_jobs": (_I, [_P, _P, _I, _I, _P, _P, _I, _P]),
     "tp_unslice_dets": (_I, [_P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "tp_render_frames": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_uint32, _P, _P]),

@@ -150,17 +150,24 @@ class YoloNet:
 
     def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated",
                  dtype: str = DEFAULT_PRECISION):
+        """dtype "fp16" / "bf16": 16-bit activations; "fp32": the fp32-parity plan
+        (TP_DTYPE_F16X2 — exact hi/lo fp16 activation pairs, same kernels, 2x K)."""
         torch = native.require_cuda()
         lib = native.load()
         if dtype not in native.DTYPES:
             raise ValueError(f"dtype must be one of {tuple(native.DTYPES)}")
         self.dtype = dtype
-        self.tdtype = torch.float16 if dtype == "fp16" else torch.bfloat16
-        wpacks, biases = weights if weights is not None else make_weights(seed, head, dtype)
+        self.split = dtype == "fp32"
+        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float16
+        wdtype = "fp16" if self.split else dtype
+        self.weight_dtype = wdtype  # value grid of the weights (make_weights dtype)
+        wpacks, biases = weights if weights is not None else make_weights(seed, head, wdtype)
+        if self.split:
+            wpacks = [split_weight(li, w) for li, w in enumerate(wpacks)]
         self.max_tiles = int(max_tiles)
         self.w_dev = [torch.from_numpy(w).to(self.tdtype).cuda() for w in wpacks]
         self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
-        nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles))
+        nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles, native.DTYPES[dtype]))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
         wptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.w_dev])
         bptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.b_dev])
@@ -201,17 +208,29 @@ class YoloNet:
 
     def input_tensor(self, n_tiles: int):
         """16-bit layer-0 input view [n, 610, 610, 8]: padded rows of 16-byte slots,
-        slot X = [q(X-1) rgb0 | q(X) rgb0] for tile pixels q (zero outside the tile)."""
+        slot X = [q(X-1) rgb0 | q(X) rgb0] for tile pixels q (zero outside the tile);
+        q = value/255, or the integer value itself in the fp32-parity plan."""
         nb = n_tiles * 610 * 610 * 8 * 2
         return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 8)
 
     def step_tensor(self, step: int, n_tiles: int):
-        """16-bit view of a step's output buffer [n, R, R, C] (compact NHWC)."""
+        """16-bit view of a step's output buffer [n, R, R, C] (compact NHWC; in the
+        fp32-parity plan C is the stored channel count, hi/lo interleaved — see
+        step_values)."""
         addr, res, cs = self.layer_output(step)
         if step == len(STEPS) - 1:
             return self.head_tensor(n_tiles)
         nb = n_tiles * res * res * cs * 2
         return self._view(addr, nb).view(self.tdtype).view(n_tiles, res, res, cs)
+
+    def step_values(self, step: int, n_tiles: int):
+        """A step's output as fp32 [n, R, R, C] real channels (hi + lo in the parity plan)."""
+        t = self.step_tensor(step, n_tiles)
+        if not self.split or step == len(STEPS) - 1:
+            return t.float()
+        n, r, _, cs = t.shape
+        g = t.view(n, r, r, cs // 32, 2, 16).float()
+        return (g[:, :, :, :, 0] + g[:, :, :, :, 1]).reshape(n, r, r, cs // 2)
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -220,37 +239,17 @@ class YoloNet:
             self.handle = None
 
 
-# fp32-parity plan (csrc/tp_split.cu): logical buffers (side, channels) and per conv slot
-# (input buffer, output buffer, output channel offset, pool, reorg) — the same dataflow as
-# csrc/tp_conv.cu kSteps, with the max pool after layer 16 folded into its store.
-_SPLIT_BUFS = {"I": (608, 16), "P304": (304, 32), "P152": (152, 64), "A152": (152, 128),
-               "B152": (152, 64), "P76": (76, 128), "A76": (76, 256), "B76": (76, 128),
-               "P38": (38, 256), "A38": (38, 512), "B38": (38, 256), "E38": (38, 512),
-               "P19": (19, 512), "A19": (19, 1024), "B19": (19, 512), "C19": (19, 1024),
-               "CAT19": (19, 1280)}
-_SPLIT_PLAN = [("I", "P304", 0, 1, 0), ("P304", "P152", 0, 1, 0), ("P152", "A152", 0, 0, 0),
-               ("A152", "B152", 0, 0, 0), ("B152", "P76", 0, 1, 0), ("P76", "A76", 0, 0, 0),
-               ("A76", "B76", 0, 0, 0), ("B76", "P38", 0, 1, 0), ("P38", "A38", 0, 0, 0),
-               ("A38", "B38", 0, 0, 0), ("B38", "A38", 0, 0, 0), ("A38", "B38", 0, 0, 0),
-               ("B38", "E38", 0, 0, 0), ("P19", "A19", 0, 0, 0), ("A19", "B19", 0, 0, 0),
-               ("B19", "C19", 0, 0, 0), ("C19", "B19", 0, 0, 0), ("B19", "A19", 0, 0, 0),
-               ("A19", "C19", 0, 0, 0), ("C19", "CAT19", 256, 0, 0), ("E38", "CAT19", 0, 0, 1),
-               ("CAT19", "A19", 0, 0, 0), ("A19", None, 0, 0, 0)]
-
-
 def split_weight(li: int, wpack: np.ndarray) -> np.ndarray:
-    """Packed 16-bit weights of layer li -> [cout_pad][taps x 2 cin'] for hi/lo activations
-    (the [cout][cin][k][k] kernel duplicated over both channel halves; layer 0's logical
-    input has cin' = 16: rgb + 13 zero channels)."""
+    """Packed fp16 weights of layer li -> the fp32-parity plan's [cout_pad][taps x 2 cin]:
+    each 16-input-channel group duplicated, matching the interleaved [hi 16 | lo 16]
+    activations (TP_DTYPE_F16X2). Layer 0 reads the unsplit integer slots: unchanged."""
+    if li == 0:
+        return wpack
     _, cin, cout, k, _ = LAYERS[li]
-    cpad = HEAD_CPAD if li == HEAD else cout
-    w = _unpack(wpack, li)  # [cout][cin][k][k]
-    cl = 16 if li == 0 else cin
-    wt = np.zeros((cpad, k, k, 2 * cl), dtype=np.float32)
-    wk = np.transpose(w, (0, 2, 3, 1))
-    wt[:cout, :, :, :cin] = wk
-    wt[:cout, :, :, cl:cl + cin] = wk
-    return wt.reshape(cpad, k * k * 2 * cl)
+    cpad = wpack.shape[0]
+    g = np.asarray(wpack, dtype=np.float32)[:, : k * k * cin].reshape(cpad, k * k, cin // 16, 1, 16)
+    return np.ascontiguousarray(np.broadcast_to(g, (cpad, k * k, cin // 16, 2, 16))).reshape(
+        cpad, k * k * 2 * cin)
 
 
 def _unpack(wpack: np.ndarray, li: int) -> np.ndarray:
@@ -262,68 +261,6 @@ def _unpack(wpack: np.ndarray, li: int) -> np.ndarray:
         return np.ascontiguousarray(np.transpose(w, (0, 3, 1, 2)))  # cout, cin, ky, kx
     w = w[:cout, : k * k * cin].reshape(cout, k, k, cin)
     return np.ascontiguousarray(np.transpose(w, (0, 3, 1, 2)))
-
-
-class SplitNet:
-    """fp32-parity YOLO v2-608 (precision="fp32"): every activation stored as exact fp16
-    (hi, lo) pairs, convs on the same tcgen05 kernels (FLAT / CTA-pair im2col tiles, fp32
-    epilogue), pooling / reorg / splitting by tp_split_store. Slower than the fp16 plan
-    (2x K, fp32 round trips); it exists to meet the north-star 1e-3 score bar against the
-    fp32 CPU reference. Same interface as YoloNet (load_tiles replaces the gather input)."""
-
-    def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated"):
-        torch = native.require_cuda()
-        self.dtype = "fp16"
-        self.tdtype = torch.float16
-        self.max_tiles = int(max_tiles)
-        wpacks, biases = weights if weights is not None else make_weights(seed, head, "fp16")
-        self.w_dev = [torch.from_numpy(split_weight(li, w)).to(torch.float16).cuda()
-                      for li, w in enumerate(wpacks)]
-        self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
-        n = self.max_tiles
-        self.bufs = {k: torch.zeros((n, s, s, 2 * c), dtype=torch.float16, device="cuda")
-                     for k, (s, c) in _SPLIT_BUFS.items()}
-        self.scratch = torch.zeros(n * 608 * 608 * 32, dtype=torch.float32, device="cuda")
-        self.head = torch.zeros((n, 19, 19, HEAD_CPAD), dtype=torch.float32, device="cuda")
-        self.head_ptr = self.head.data_ptr()
-        self.head_cstride = HEAD_CPAD
-        self.input_ptr = None  # the gather's 16-byte-slot input is not used in this mode
-
-    def load_tiles(self, tiles_u8, n: int, stream=None) -> None:
-        """u8 tiles [>= n][608][608][3] (device) -> the split layer-0 input."""
-        native.call("tp_split_input", native.ptr(tiles_u8), int(n), native.ptr(self.bufs["I"]),
-                    native.stream_handle(stream))
-
-    def forward(self, n_tiles: int, n_tiles_dev=None, stream=None) -> None:
-        n = int(n_tiles)
-        if n_tiles_dev is not None:  # parity mode: one host read of the device tile count
-            torch = native.require_cuda()
-            with torch.cuda.stream(stream or torch.cuda.current_stream()):
-                n = min(n, int(n_tiles_dev.item()))
-        st = native.stream_handle(stream)
-        fp16 = native.DTYPES["fp16"]
-        for li, (src, dst, coff, pool, reorg) in enumerate(_SPLIT_PLAN):
-            _, cin, cout, k, res = LAYERS[li]
-            s_side, s_c = _SPLIT_BUFS[src]
-            leaky = 0 if li == HEAD else 1
-            if dst is None:  # head: fp32 straight into the head buffer
-                native.call("tp_conv", native.ptr(self.bufs[src]), n, res, 2 * s_c,
-                            native.ptr(self.w_dev[li]), native.ptr(self.b_dev[li]), cout,
-                            HEAD_CPAD, k, leaky, self.head_ptr, HEAD_CPAD, 0, 1, 0, fp16, 0, st)
-                continue
-            native.call("tp_conv", native.ptr(self.bufs[src]), n, res, 2 * s_c,
-                        native.ptr(self.w_dev[li]), native.ptr(self.b_dev[li]), cout, cout, k,
-                        leaky, native.ptr(self.scratch), cout, 0, 1, 0, fp16, 0, st)
-            d_side, d_c = _SPLIT_BUFS[dst]
-            native.call("tp_split_store", native.ptr(self.scratch), n, res, cout, cout, pool,
-                        reorg, native.ptr(self.bufs[dst]), 2 * d_c, coff, d_c, st)
-            if li == 12:  # layer 16 -> E38, and its 2x2 pool -> P19 (layer 18's input)
-                p_side, p_c = _SPLIT_BUFS["P19"]
-                native.call("tp_split_store", native.ptr(self.scratch), n, res, cout, cout, 1,
-                            0, native.ptr(self.bufs["P19"]), 2 * p_c, 0, p_c, st)
-
-    def head_tensor(self, n_tiles: int):
-        return self.head[:n_tiles]
 
 
 # step list of csrc/tp_conv.cu kSteps: ("conv", layer slot) or ("pool", None); layers 0, 2,
@@ -359,11 +296,8 @@ class YoloB200Detector(Detector):
     @property
     def net(self):
         if self._net is None:
-            if self.precision == "fp32":
-                self._net = SplitNet(self.max_tiles, seed=self.seed, head=self.head)
-            else:
-                self._net = YoloNet(self.max_tiles, seed=self.seed, head=self.head,
-                                    dtype=self.precision)
+            self._net = YoloNet(self.max_tiles, seed=self.seed, head=self.head,
+                                dtype=self.precision)
         return self._net
 
     def detect_tiles(self, tiles_u8) -> list[list[Detection]]:

@@ -95,7 +95,9 @@ def test_library_loads_and_exports_every_header_symbol():
     for name in declared:
         assert getattr(lib, name) is not None
     assert lib.tp_version() == 1
-    assert lib.tp_yolo_workspace_bytes(1) > 20_000_000
+    assert lib.tp_yolo_workspace_bytes(1, 1) > 20_000_000
+    # the fp32-parity plan doubles every activation buffer but the input slots and head
+    assert lib.tp_yolo_workspace_bytes(1, 2) > 1.8 * lib.tp_yolo_workspace_bytes(1, 1)
 
 
 def test_product_never_imports_oracle():
