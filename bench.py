@@ -13,10 +13,14 @@ on 2 attention tiles/frame, selection, stage-2 YOLO on the active crops, NMS+mer
 * e2e: the same through the public engine API from pinned HOST frames: per step the
   H2D copy of the batch and the D2H of the results are inside the timed region
   (copy of batch i+1 overlaps compute of batch i on a second stream).
+* precision (default "fp32"): the fp32-parity plan — activations as exact fp16 hi/lo
+  pairs, fp32 accumulation — the mode inside the north-star 1e-3 score tolerance;
+  --precision fp16 runs the ~2x faster 16-bit-activation mode.
 * roofline: the dominant kernel is the tcgen05 implicit-GEMM conv (23 launches per
-  YOLO forward, +5 maxpools): achieved = 62.938 GFLOP x tiles / measured forward time.
+  YOLO forward + 1 maxpool): achieved = 62.938 GFLOP x tiles / measured forward time
+  (algorithmic FLOPs; `executed_tflops` counts the parity plan's doubled K).
 * cpu_baseline: the CPU oracle port (oracle/: reference pipeline restatement + torch
-  CPU YOLO) on one frame of the same clip, all host threads.
+  CPU fp32 YOLO) on one frame of the same clip, all host threads.
 Multi-GPU (torchrun): frames shard across ranks (each rank streams its own 300-frame
 clip: weak scaling); the only collective is the NCCL gather of per-frame results.
 """
@@ -52,8 +56,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--resample", default="nearest", choices=["nearest", "bilinear"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"],
-                    help="activation precision (fp32 = hi/lo fp16 pairs, the parity mode)")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp16", "bf16"],
+                    help="activation precision: fp32 = hi/lo fp16 pairs, the parity plan "
+                         "(default); fp16/bf16 = 16-bit activations, ~2x faster")
     ap.add_argument("--profile", action="store_true",
                     help="torch.profiler kernel table of the timed steps to stderr (not a bench run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -186,13 +191,13 @@ def cpu_baseline_frames_per_sec(objs, n_frames=1):
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
-    wpacks, biases = yolo.make_weights(0, dtype=yolo.DEFAULT_PRECISION)
+    wpacks, biases = yolo.make_weights(0, dtype="fp16")
     plan = R.Plan(W, H, 1, 3, 20)
     frames = [synthetic.render_frame(W, H, objs[i]) for i in range(n_frames)]
 
     def detect(fid, crop):
         tile = R.cut_tile_nearest(frames[fid], crop)
-        head = yolo_ref.forward(tile[None], wpacks, biases, mode=yolo.DEFAULT_PRECISION)
+        head = yolo_ref.forward(tile[None], wpacks, biases, mode="fp32")  # the reference: fp32
         return [(r, yolo.COCO_NAMES[c], conf) for r, c, conf, _ in
                 yolo_ref.region_decode(head, 0.25)[0]]
 
@@ -228,11 +233,11 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32+bf16-storage", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {**arm_config(args, len(objs), world),
                        "step": "1 frame of the clip per step (bounded CPU sample of the workload)"},
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
-                             "sample": "1 frame per step: oracle run_sequence + torch-CPU YOLO"},
+                             "sample": "1 frame per step: oracle run_sequence + torch-CPU fp32 YOLO"},
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -366,10 +371,13 @@ def main():
         pass
     peak = float(peaks.get("bf16_tflops_sustained", 1391.0))
     traffic = {}
+    tfile = "r01_conv_traffic.json" if args.precision != "fp32" else "r01_conv_traffic_fp32.json"
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_conv_traffic.json")))
+        traffic = json.load(open(os.path.join(ROOT, "profiles", tfile)))
     except Exception:
         pass
+    exec_scale = (yolo.EXEC_GFLOP_PER_TILE_FP32 / yolo.GFLOP_PER_TILE
+                  if args.precision == "fp32" else 1.0)
     stage1 = eng.A * B * args.steps if per_step == 2 else 0
     tiles_per_frame = (stage1 + float(t2[args.warmup:].sum())) / (args.steps * B)
     launches_per_step = (1 + 24 + 1 + 1) + 2 + (1 + 24 + 1 + 1) + 1
@@ -391,14 +399,14 @@ def main():
         fps, threads, dt = cpu_baseline_frames_per_sec(objs, 1)
         cpu = {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
                "sample": f"1 frame (frame 0 of the clip, {dt:.1f}s): oracle run_sequence + "
-                         "torch-CPU YOLO v2 (bf16-rounded activations), all host threads"}
+                         "torch-CPU fp32 YOLO v2, all host threads"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic",
-            "precision": ("fp16 operands/activations, fp32 accumulation (tcgen05 kind::f16)"
+            "precision": (f"{args.precision} operands/activations, fp32 accumulation (tcgen05 kind::f16)"
                           if args.precision != "fp32" else
                           "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
                           "accumulation and epilogue"),
@@ -407,16 +415,22 @@ def main():
                        "tiles_per_frame": tiles_per_frame,
                        "crops_per_sec": value * tiles_per_frame},
             "roofline": {"bound": "tensor", "kernel": "YOLO v2 conv stack: 23 tcgen05 launches per "
-                         "forward (conv_l0_kernel, 3x conv_box_kernel, 14x conv_pair_kernel, "
-                         "5x conv_tc_kernel) + 1 maxpool", "achieved": conv_tflops, "peak": peak,
+                         f"forward ({eng.net.kernel_summary()}) + 1 maxpool",
+                         "achieved": conv_tflops, "peak": peak,
                          "unit": "TFLOP/s", "frac": conv_tflops / peak,
                          "traffic": traffic.get("dram_MB_per_tile", 0) * 1e6 if traffic else None,
                          "traffic_unit": "DRAM bytes per 608^2 tile, ncu --set full capture "
-                                         "(profiles/r01_conv_traffic.json)",
+                                         f"(profiles/{tfile})",
                          "algorithmic_bytes_per_tile": traffic.get("algorithmic_MB_per_tile", 0) * 1e6
                          if traffic else None,
                          "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                          "algorithmic": f"{yolo.GFLOP_PER_TILE:.3f} GFLOP per 608^2 tile",
+                         "executed_tflops": conv_tflops * exec_scale,
+                         "executed_frac": conv_tflops * exec_scale / peak,
+                         "executed": ("tensor-core FLOPs issued: hi/lo activations double K on "
+                                      f"every layer but layer 0 ({yolo.EXEC_GFLOP_PER_TILE_FP32:.1f} "
+                                      "GFLOP per tile)") if args.precision == "fp32"
+                         else "same as algorithmic",
                          "conv_share_of_step": fwd_ms / ms},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -751,10 +751,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int total_px = n_img * p.img_px;
   const int m_blocks = (total_px + 255) / 256;
   const int total_tiles = m_blocks * p.n_blocks_n;
+  // Tiles are dealt round-robin (cluster cid takes t = cid, cid + n_clusters, ...) in a
+  // grouped raster: groups of GM M-blocks, N-block-major inside a group, so one wave of
+  // clusters covers GM M-blocks x (n_clusters / GM) N-blocks. The live L2 set is then GM
+  // activation blocks + a few weight slices instead of every weight slice at once (the
+  // 2x-K parity plan's 38-47 MB weights otherwise thrash L2: 20x the DRAM reads).
   const int n_clusters = (int)gridDim.x >> 1, cid = (int)blockIdx.x >> 1;
-  const int per = total_tiles / n_clusters, extra = total_tiles % n_clusters;
-  const int t_begin = cid * per + min(cid, extra);
-  const int n_tiles = per + (cid < extra ? 1 : 0);
+  const int n_tiles = cid < total_tiles ? (total_tiles - cid + n_clusters - 1) / n_clusters : 0;
+  const int GM = max(1, n_clusters / min(p.n_blocks_n, 2));
+  auto tile_at = [&](int i, int& mt, int& nb) {
+    const int t = cid + i * n_clusters;
+    const int grp = t / (GM * p.n_blocks_n);
+    const int gm = min(GM, m_blocks - grp * GM);
+    const int tl = t - grp * GM * p.n_blocks_n;
+    nb = tl / gm;
+    mt = grp * GM + (tl - nb * gm);
+  };
 
   if (warp == kProdWarp) {
     if (lane == 0) {
@@ -765,9 +777,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       long long pr_wait = 0;
       PROF_T0(pr_start);
       for (int i = 0; i < n_tiles; ++i) {
-        const int t = t_begin + i;
-        const int mt = t / p.n_blocks_n;
-        const int n0 = (t - mt * p.n_blocks_n) * p.bn;
+        int mt, nb;
+        tile_at(i, mt, nb);
+        const int n0 = nb * p.bn;
         const PixPos f0 = pix_pos(mt * 256 + (int)rank * 128, p.res, p.img_px);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           PROF_T0(tw);
@@ -857,9 +869,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
       if ((i & 1) != g) continue;
-      const int t = t_begin + i;
-      const int mt = t / p.n_blocks_n;
-      const int n0 = (t - mt * p.n_blocks_n) * p.bn;
+      int mt, nb;
+      tile_at(i, mt, nb);
+      const int n0 = nb * p.bn;
       PROF_T0(t3);
       tp::mbar_wait(&tfull[g], ph);
       PROF_ADD(e_wait, t3);
@@ -2032,9 +2044,12 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   L->mode = mode;
   L->smem = 1024 + (size_t)stages * stage_bytes + p.bres_bytes + p.stage_bytes +
             (2 * stages + 6) * 8 + cout_pad * 4 + 16;
-  // CTA-pair variant for FLAT SW128 layers (TP_PAIR=0 disables it)
+  // CTA-pair variant for FLAT SW128 layers (TP_PAIR=0 disables it): N = 256 tiles, and
+  // N >= 128 for 3x3 layers / the fp32 head (measured: 1x1 layers with N < 256 are HBM-bound
+  // and lose ~10-40% to the pair's coarser tiles)
   const char* pe = getenv("TP_PAIR");
-  if (tstore && mode == MODE_SW128 && bn == 256 && (pe == nullptr || atoi(pe) != 0)) {
+  const bool pair_shape = bn == 256 || (bn >= 128 && (ksize == 3 || out_fp32));
+  if (tstore && mode == MODE_SW128 && pair_shape && (pe == nullptr || atoi(pe) != 0)) {
     const uint64_t dims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
     const uint32_t box[2] = {(uint32_t)bk, (uint32_t)(bn / 2)};
     rc = make_tmap(&L->tmB, weight, 2, dims, box, swz, f16);
@@ -2439,6 +2454,17 @@ extern "C" int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int
   *res = kBufs[b].res;
   *cstride = buf_ch(b, net->dtype);
   return TP_OK;
+}
+
+// Kernel chosen for conv slot `conv` of the plan: 0 conv_tc_kernel, 1 conv_pair_kernel,
+// 2 conv_l0_kernel, 3 conv_box_kernel.
+extern "C" int tp_yolo_layer_kernel(tp_yolo_net* net, int conv) {
+  if (net == nullptr || conv < 0 || conv >= 23) {
+    tp_set_error("tp_yolo_layer_kernel: bad conv slot %d", conv);
+    return -1;
+  }
+  const ConvLaunch& L = net->convs[conv];
+  return L.box ? 3 : L.l0 ? 2 : L.pair ? 1 : 0;
 }
 
 extern "C" int tp_yolo_destroy(tp_yolo_net* net) {

@@ -77,6 +77,7 @@ SIGNATURES = {
     "tp_device_sm_count": (_I, [_P]),
     "tp_gather_tiles": (_I, [_P, _I64, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P]),
     "tp_yolo_workspace_bytes": (_SZ, [_I, _I]),
+    "tp_yolo_layer_kernel": (_I, [_P, _I]),
     "tp_yolo_create": (_I, [_I, _P, _P, _P, _SZ, _I, _P]),
     "tp_yolo_input": (_P, [_P]),
     "tp_yolo_head": (_P, [_P]),

@@ -37,6 +37,9 @@ HEAD_CPAD = 448
 ANCHORS = np.array([0.57273, 0.677385, 1.87446, 2.06253, 3.33843, 5.47434, 7.88282, 3.52778,
                     9.77052, 9.16828], dtype=np.float32)
 GFLOP_PER_TILE = sum(2.0 * (s * s) * cout * cin * k * k for _, cin, cout, k, s in LAYERS) / 1e9
+# tensor-core work actually issued per tile in the fp32-parity plan: K doubled (hi + lo)
+# on every layer but layer 0 (its K = 3 taps x 48 slot halves vs 27 algorithmic MACs)
+EXEC_GFLOP_PER_TILE_FP32 = (2 * GFLOP_PER_TILE - 2.0 * 608 * 608 * 32 * 3 * 9 / 1e9)
 
 COCO_NAMES = (
     "person", "bicycle", "car", "motorbike", "aeroplane", "bus", "train", "truck", "boat",
@@ -59,7 +62,10 @@ def head_path(seed: int) -> str:
     return os.path.join(DATA_DIR, f"yolo_head_seed{seed}.npz")
 
 
-DEFAULT_PRECISION = "fp16"
+# "fp32": the fp32-parity plan (hi/lo fp16 activation pairs, TP_DTYPE_F16X2) — the mode
+# that meets the north-star 1e-3 score tolerance against the fp32 reference; "fp16" is
+# the 2x faster 16-bit-activation mode (scores within ~5e-3)
+DEFAULT_PRECISION = "fp32"
 
 
 def _bf16_round(a: np.ndarray) -> np.ndarray:
@@ -103,13 +109,16 @@ def pack_weight(li: int, w: np.ndarray, dtype: str = "bf16") -> np.ndarray:
 _CACHE: dict = {}
 
 
-def make_weights(seed: int = 0, head: str = "calibrated", dtype: str = DEFAULT_PRECISION):
+def make_weights(seed: int = 0, head: str = "calibrated", dtype: str = "fp16"):
     """Deterministic YOLO v2 weights: (packed weights [23], biases [23]) as numpy fp32
-    holding values exactly representable in `dtype` ("bf16" or "fp16").
+    holding values exactly representable in `dtype` ("bf16" or "fp16"; "fp32" — the
+    parity plan — uses the fp16 grid).
 
     head="calibrated" uses the committed probe head for this seed when present,
     head="random" always uses a random head.
     """
+    if dtype == "fp32":
+        dtype = "fp16"
     key = (seed, head, dtype)
     if key in _CACHE:
         return _CACHE[key]
@@ -193,6 +202,18 @@ class YoloNet:
         native.call("tp_yolo_layer_output", self.handle, step, ctypes.byref(p), ctypes.byref(r),
                     ctypes.byref(c))
         return int(p.value), r.value, c.value
+
+    KERNEL_NAMES = ("conv_tc_kernel", "conv_pair_kernel", "conv_l0_kernel", "conv_box_kernel")
+
+    def layer_kernels(self) -> list[str]:
+        """Kernel the plan chose for each of the 23 conv slots."""
+        lib = native.load()
+        return [self.KERNEL_NAMES[int(lib.tp_yolo_layer_kernel(self.handle, i))]
+                for i in range(len(LAYERS))]
+
+    def kernel_summary(self) -> str:
+        ks = self.layer_kernels()
+        return ", ".join(f"{ks.count(k)}x {k}" for k in self.KERNEL_NAMES if k in ks)
 
     def _view(self, addr: int, nbytes: int):
         off = addr - self.workspace.data_ptr()

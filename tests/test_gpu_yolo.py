@@ -133,3 +133,14 @@ def test_head_matches_cpu_oracle(cuda, net, tiles):
     print("head max rel err vs oracle", rel, "mean abs", np.abs(got - ref).mean())
 
 
+
+
+def test_plan_kernel_choice(net):
+    """The plan's kernel per conv slot (tp_yolo_layer_kernel): layer 0 has its own kernel,
+    the deep 3x3 layers run on CTA pairs in every precision."""
+    ks = net.layer_kernels()
+    print(net.dtype, net.kernel_summary())
+    assert ks[0] == "conv_l0_kernel"
+    assert all(ks[i] == "conv_pair_kernel" for i in (5, 8, 10, 12, 13, 15, 17, 18, 19, 21))
+    if net.dtype != "fp32":
+        assert ks[1] == ks[2] == ks[4] == "conv_box_kernel"
