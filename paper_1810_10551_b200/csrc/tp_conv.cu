@@ -996,17 +996,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int L0_BOX_ROWS = 9;                       // strided rows per box
 constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 64;  // 9216: 9 rows x 16 windows x 64 B
 constexpr int L0_STAGE = 2 * L0_BOX_BYTES;           // 18432: one box per input row phase
+constexpr int L0_STAGING = 8 * 2 * 4096;             // epilogue store slabs
 
 __global__ void __launch_bounds__(kThreads, 1)
     conv_l0_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const ConvParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int S = p.stages;
   uint8_t* smA = smem;
   uint8_t* smB = smem + (size_t)S * L0_STAGE;  // resident weights: 9 chunks x 1 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + 9 * 1024);
+  uint8_t* smC = smB + 9 * 1024;  // output staging: 8 warps x 2 slabs x 4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smC + L0_STAGING);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
@@ -1139,9 +1141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int g = (int)warp >> 2;
     const uint32_t q = warp & 3;
-    const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
-    uint32_t ph = 0;
+    uint32_t ph = 0, nslab = 0;
     long long e_wait = 0;
     PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
@@ -1154,10 +1155,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_ADD(e_wait, t3);
       ph ^= 1;
       tp::tc_fence_after();
-      const int X = bx * 16 + (row & 15), Y = by * 8 + (row >> 4);
+      // split outputs: this warp's 32 pooled pixels (2 output rows x 16) are staged as 32
+      // SW128 smem rows [hi 16 | lo 16] x 2 and written by one TMA store — per-thread
+      // 16-byte stores at a 128-byte pixel pitch were LSU-bound (0.86 -> 0.44 ms per 120
+      // tiles). Plain 64-byte pixels are stored directly (staging measured 13% slower).
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 128);
+      const bool spl = p.split != 0;
+      const uint32_t slab = tp::smem_u32(smC) + warp * 8192 + (nslab & 1) * 4096;
+      const int X = bx * 16 + (int)(lane & 15), Y = by * 8 + 2 * (int)q + (int)(lane >> 4);
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
                          (size_t)(img * oimg + Y * ores + X) * p.out_cstride;
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 128);
+      if (spl) {
+        if (lane == 0) bulk_wait_read1();
+        __syncwarp();
+      }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t v0[16], v1[16], v2[16], v3[16];
@@ -1175,8 +1186,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float a = fmaf(m, p.alpha, bias_s[c * 16 + j]);
           fv[j] = fmaxf(a, 0.1f * a);
         }
-        if (p.split) {
-          if (img < n_img) store_split16(o + c * 32, fv);
+        if (spl) {  // SW128 rows: 16-byte unit u at u ^ (row & 7)
+          uint32_t hi[8], lo[8];
+          split_pairs<8>(fv, hi, lo);
+          const uint32_t rb = slab + lane * 128, sw = lane & 7;
+          st_shared_v4(rb + (((4 * c + 0) ^ sw) << 4), hi[0], hi[1], hi[2], hi[3]);
+          st_shared_v4(rb + (((4 * c + 1) ^ sw) << 4), hi[4], hi[5], hi[6], hi[7]);
+          st_shared_v4(rb + (((4 * c + 2) ^ sw) << 4), lo[0], lo[1], lo[2], lo[3]);
+          st_shared_v4(rb + (((4 * c + 3) ^ sw) << 4), lo[4], lo[5], lo[6], lo[7]);
           continue;
         }
         uint32_t pk[8];
@@ -1191,15 +1208,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             pk[j] = *reinterpret_cast<uint32_t*>(&h);
           }
         }
-        if (img < n_img) {
-          *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        *reinterpret_cast<uint4*>(o + c * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(o + c * 16 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      if (spl) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && (p.dbg & 4) == 0) {
+          tma_store_3d(&tmC, smC + (slab - tp::smem_u32(smC)), 0, bx * 16,
+                       img * ores + by * 8 + 2 * (int)q);
+          bulk_commit();
         }
+        ++nslab;
       }
       tp::tc_fence_before();
       __syncwarp();
       if (lane == 0) tp::mbar_arrive(&tempty[g]);
     }
+    if (lane == 0) bulk_wait_all();
     if ((p.dbg & 32) && warp == 0 && lane == 0) {
       atomicAdd(&g_conv_prof[5], (unsigned long long)(clock64() - e_start));
       atomicAdd(&g_conv_prof[6], (unsigned long long)e_wait);
@@ -1939,15 +1965,26 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       rc = make_tmap(&L->tmB, weight, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16);
       if (rc) return rc;
     }
-    L->tmC = L->tmA;  // unused
+    {  // output store map {stored channels, X, image rows}: box = one warp's 2 rows x 16 px
+      const int ores = res / 2;
+      const uint64_t dims[3] = {(uint64_t)out_cstride, (uint64_t)ores, (uint64_t)max_img * ores};
+      const uint32_t box[3] = {(uint32_t)out_cstride, 16, 2};
+      if (out_cstride != (split ? 64 : 32) || out_coff != 0) {
+        tp_set_error("conv: layer 0 writes a dense [n][res/2][res/2][%d] output", split ? 64 : 32);
+        return TP_ERR_UNSUPPORTED;
+      }
+      rc = make_tmap(&L->tmC, out, 3, dims, box,
+                     split ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, f16);
+      if (rc) return rc;
+    }
     L->l0 = 1;
-    int st = (int)((227 * 1024 - fixed - 9 * 1024) / L0_STAGE);
+    int st = (int)((227 * 1024 - fixed - 9 * 1024 - L0_STAGING) / L0_STAGE);
     if (st > 8) st = 8;
     p.stages = st;
     p.bn = 32;
     p.n_blocks_n = 1;
     p.idesc = tp::idesc_f16kind(128, 32, !f16);
-    L->smem = 1024 + (size_t)st * L0_STAGE + 9 * 1024 + (2 * st + 6) * 8 + 32 * 4 + 16;
+    L->smem = 1024 + (size_t)st * L0_STAGE + 9 * 1024 + L0_STAGING + (2 * st + 6) * 8 + 32 * 4 + 16;
     return TP_OK;
   }
 
@@ -2238,7 +2275,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
     const long long tiles = (long long)n_img * (p.res / 32) * (p.res / 16);
     if (tiles == 0) return TP_OK;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    conv_l0_kernel<<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+    conv_l0_kernel<<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
     TP_LAUNCH_CHECK();
     return TP_OK;
   }
