@@ -6,7 +6,7 @@
 set -u
 TAG=${1:-r01}
 CMD="python bench.py --steps 1 --warmup 1 --batch 30 --no-e2e --no-cpu-baseline"
-KERN='regex:conv_tc_kernel|conv_pair_kernel|conv_l0_kernel|conv_box_kernel|gather_kernel|decode_kernel|select_kernel|postprocess_kernel|maxpool2_kernel|collect_final_kernel|attention_boxes_kernel|build_jobs_kernel'
+KERN='regex:conv_tc_kernel|conv_pair_kernel|conv_l0_kernel|conv_box_kernel|gather_kernel|decode_kernel|select_kernel|postprocess_kernel|maxpool2_kernel|maxpool2_split_kernel|collect_final_kernel|slice_jobs_kernel|unslice_kernel|attention_boxes_kernel|build_jobs_kernel'
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/plain_$TAG.log; exit 1; }
 tail -1 gpurun_out/plain_$TAG.log | cut -c1-400
