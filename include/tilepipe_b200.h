@@ -132,7 +132,7 @@ TP_API int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n
                           int first, int last, void* stream);
 TP_API int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res, int* cstride);
 /* Kernel the plan chose for conv slot 0..22: 0 conv_tc, 1 conv_pair (cta_group::2),
- * 2 conv_l0, 3 conv_box; -1 on a bad argument. */
+ * 2 conv_l0, 3 conv_box, 4 conv_pair_rect (cta_group::2, pooled); -1 on a bad argument. */
 TP_API int tp_yolo_layer_kernel(tp_yolo_net* net, int conv);
 TP_API int tp_yolo_destroy(tp_yolo_net* net);
 

@@ -584,18 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           store_split16(reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride +
                             p.out_coff + 2 * creal,
                         f);
-        } else if (EPI == EPI_F32) {
-          float* o = reinterpret_cast<float*>(p.out) + (size_t)out_px * p.out_cstride + p.out_coff + ch0;
-          if (ch0 + 16 <= p.cout) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              *reinterpret_cast<float4*>(o + j) = make_float4(f[j], f[j + 1], f[j + 2], f[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (ch0 + j < p.cout) o[j] = f[j];
-          }
-        } else {
+        } else {  // (fp32 outputs always take the TMA-store path above)
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -967,6 +956,256 @@ __global__ void __launch_bounds__(kThreads, 1)
     if ((p.dbg & 32) && warp == 0 && lane == 0 && rank == 0) {
       atomicAdd(&g_conv_prof[5], (unsigned long long)(clock64() - e_start));
       atomicAdd(&g_conv_prof[6], (unsigned long long)e_wait);
+    }
+  }
+
+  tp::tc_fence_before();
+  cluster_sync_all();
+  tp::tc_fence_after();
+  if (warp == kMmaWarp)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(p.tmem_cols)
+                 : "memory");
+}
+
+// ------------------------------------------------------------------ CTA-pair pooled 3x3
+// Pooled 3x3 layers whose weights do not fit in shared memory (16-bit plan: layer 10;
+// parity plan: layers 6 and 10, K = 1152 / 2304): a 2-CTA cluster computes a 16 x 16
+// output block (each CTA one 16 x 8 half, M = 256) x N with tcgen05.mma.cta_group::2.
+// One stage per (kernel column dx, 64-channel block): a halo box {64, 16, 10} whose three
+// kernel rows are descriptor offsets of 16 box rows, plus the three taps' half-N weight
+// slices — A is fetched 3x per tile instead of 9x (RECT tiles) and each CTA stages only
+// half of B. The epilogue pools 2x2 in registers (x pair lane^1, y pair lane^16) and
+// stores the pooled pixels directly (16-bit, or hi/lo pairs in the parity plan).
+__device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* tmap, uint32_t leader_bar,
+                                                 int32_t c0, int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(tp::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(leader_bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+constexpr int PR_W = 16, PR_H = 8;  // per-CTA output half-tile; the pair covers 16 x 16
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_pair_rect_kernel(const __grid_constant__ CUtensorMap tmA,
+                          const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
+  constexpr int BK = 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = p.stages;
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + (size_t)S * p.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smB + (size_t)S * p.b_stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
+
+  const uint32_t warp = tp::warp_id();
+  const uint32_t lane = tp::lane_id();
+  const uint32_t rank = cluster_rank();
+  const int cout_pad = p.bn * p.n_blocks_n;
+  const int half_bn = p.bn >> 1;
+
+  if (warp == kProdWarp && lane == 0) {
+    tp::tma_prefetch(&tmA);
+    tp::tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      tp::mbar_init(&full[s], 1);
+      tp::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tp::mbar_init(&tfull[a], 1);
+      tp::mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    tp::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tp::smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
+  tp::tc_fence_before();
+  cluster_sync_all();
+  tp::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
+  const int per_img = p.tiles_x * p.tiles_y;
+  const int m_blocks = n_img * per_img;
+  const int total_tiles = m_blocks * p.n_blocks_n;
+  const int n_clusters = (int)gridDim.x >> 1, cid = (int)blockIdx.x >> 1;
+  const int n_tiles = cid < total_tiles ? (total_tiles - cid + n_clusters - 1) / n_clusters : 0;
+  const int GM = max(1, n_clusters / min(p.n_blocks_n, 2));
+  auto tile_at = [&](int i, int& img, int& y0, int& x0, int& nb) {
+    const int t = cid + i * n_clusters;
+    const int grp = t / (GM * p.n_blocks_n);
+    const int gm = min(GM, m_blocks - grp * GM);
+    const int tl = t - grp * GM * p.n_blocks_n;
+    nb = tl / gm;
+    const int mt = grp * GM + (tl - nb * gm);
+    img = mt / per_img;
+    const int r = mt - img * per_img;
+    const int by = r / p.tiles_x;
+    x0 = (r - by * p.tiles_x) * PR_W;
+    y0 = by * 2 * PR_H + (int)rank * PR_H;  // this CTA's 8-row half
+  };
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs; bytes land on the leader's barrier) =====
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t b_slice = (uint32_t)half_bn * BK * 2;
+      for (int i = 0; i < n_tiles; ++i) {
+        int img, y0, x0, nb;
+        tile_at(i, img, y0, x0, nb);
+        const int n0 = nb * p.bn;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0)
+            tp::mbar_arrive_expect_tx(&full[s], 2 * (p.a_stage_bytes + p.b_stage_bytes));
+          const uint32_t lbar = mapa_rank(&full[s], 0);
+          const int dx = kb / p.kb_per_tap - 1;
+          const int cb = kb - (dx + 1) * p.kb_per_tap;
+          tma_load_4d_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK, x0 + dx,
+                           y0 - 1, img);
+          uint8_t* bdst = smB + (size_t)s * p.b_stage_bytes;
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+            tma_load_2d_pair(bdst + dy * b_slice, &tmB, lbar,
+                             (dy * 3 + dx + 1) * p.cin + cb * BK, n0 + (int)rank * half_bn);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (rank == 0) {
+      // ===== MMA issuer: leader CTA, warp-convergent loop, one elected lane =====
+      const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 1024, 2);
+      const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 1024, 2);
+      const uint32_t a_step = p.a_stage_bytes >> 4, b_step = p.b_stage_bytes >> 4;
+      constexpr uint32_t a_row16 = PR_W * BK * 2 / 16;  // one box row of 16 pixels, >> 4
+      const uint32_t b_slice16 = (uint32_t)half_bn * BK * 2 / 16;
+      int s = 0;
+      uint32_t ph = 0;
+      uint32_t aph[2] = {0, 0};
+      for (int i = 0; i < n_tiles; ++i) {
+        const int acc = i & 1;
+        tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        aph[acc] ^= 1;
+        tp::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&full[s], ph);
+          tp::tc_fence_after();
+          const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
+          const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
+          if (tp::elect_one()) {
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_pair(d_tmem, ad0 + dy * a_row16 + 2 * k, bd0 + dy * b_slice16 + 2 * k, p.idesc,
+                         (kb | dy | k) != 0);
+            commit_pair_mc(&empty[s]);
+          }
+          __syncwarp();
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        if (tp::elect_one()) commit_pair_mc(&tfull[acc]);
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===== epilogue: both CTAs, own 16 x 8 half; groups alternate accumulators =====
+    const int g = (int)warp >> 2;
+    const uint32_t q = warp & 3;
+    const int row = (int)(q * 32 + lane);
+    const bool f16 = p.f16 != 0, leaky = p.leaky != 0, spl = p.split != 0;
+    const int ores = p.res >> 1, oimg = ores * ores;
+    const int nchunks = p.bn >> 4;
+    const uint32_t leader_tempty[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
+    uint32_t ph = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      if ((i & 1) != g) continue;
+      int img, y0, x0, nb;
+      tile_at(i, img, y0, x0, nb);
+      const int n0 = nb * p.bn;
+      tp::mbar_wait(&tfull[g], ph);
+      ph ^= 1;
+      tp::tc_fence_after();
+      const int x = x0 + (row & (PR_W - 1)), y = y0 + (row >> 4);
+      const bool store = x < p.res && y < p.res && ((x | y) & 1) == 0;
+      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                         (size_t)(img * oimg + (y >> 1) * ores + (x >> 1)) * p.out_cstride +
+                         p.out_coff;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * p.bn);
+      uint32_t v[16];
+      tp::tmem_ld16(t_row, v);
+      for (int c = 0; c < nchunks; ++c) {
+        tp::tmem_ld_wait();
+        float f[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+        if (c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);
+        // 2x2 max first (bias and leaky are monotonic: the same value), x pair lane^1,
+        // y pair lane^16
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], PR_W));
+        const int ch0 = n0 + c * 16;
+        const float4* b4 = reinterpret_cast<const float4*>(bias_s + ch0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 bb = b4[j];
+          f[4 * j + 0] += bb.x;
+          f[4 * j + 1] += bb.y;
+          f[4 * j + 2] += bb.z;
+          f[4 * j + 3] += bb.w;
+        }
+        if (leaky) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
+        }
+        if (!store || ch0 >= p.cout || (p.dbg & 4)) continue;
+        if (spl) {
+          store_split16(o + 2 * ch0, f);
+          continue;
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (f16) {
+            __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          } else {
+            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+          }
+        }
+        *reinterpret_cast<uint4*>(o + ch0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(o + ch0 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      tp::tmem_ld_wait();
+      tp::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty[g]);
     }
   }
 
@@ -1878,6 +2117,7 @@ struct ConvLaunch {
   int pair;  // CTA-pair (cta_group::2) kernel
   int l0;    // layer-0 pool-in-M kernel
   int box;   // full-halo box kernel: 0 off, else 1 + BoxEpi
+  int prect; // CTA-pair pooled 3x3 kernel (conv_pair_rect_kernel)
   int box_bk;
   CUtensorMap tmA, tmB, tmC;
   ConvParams p;
@@ -2100,6 +2340,49 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     p.stages = st;
     L->smem = 1024 + (size_t)st * sb + p.stage_bytes + (2 * st + 6) * 8 + cout_pad * 4 + 16;
   }
+  // CTA-pair pooled kernel for pooled 3x3 SW128 layers whose weights are not resident
+  // (TP_PRECT=0 disables it); the box kernel below still wins where it applies
+  const char* pr = getenv("TP_PRECT");
+  if (pool && ksize == 3 && mode == MODE_SW128 && !halo && bn >= 128 &&
+      (pr == nullptr || atoi(pr) != 0)) {
+    const uint64_t adims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
+    const uint32_t abox[4] = {(uint32_t)bk, PR_W, PR_H + 2, 1};
+    ConvLaunch P = *L;
+    rc = make_tmap(&P.tmA, in, 4, adims, abox, swz, f16);
+    if (rc) return rc;
+    const uint64_t bdims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+    const uint32_t bbox[2] = {(uint32_t)bk, (uint32_t)(bn / 2)};
+    rc = make_tmap(&P.tmB, weight, 2, bdims, bbox, swz, f16);
+    if (rc) return rc;
+    ConvParams& q = P.p;
+    q.bn = bn;
+    q.n_blocks_n = cout_pad / bn;
+    q.kb_per_tap = cin_used / bk;
+    q.num_kb = 3 * q.kb_per_tap;
+    q.a_stage_bytes = PR_W * (PR_H + 2) * bk * 2;
+    q.b_stage_bytes = 3 * (bn / 2) * bk * 2;
+    q.bres_bytes = 0;
+    q.stage_bytes = 0;
+    q.halo = 0;
+    q.sub = 1;
+    q.rect = 1;
+    q.tiles_x = (res + PR_W - 1) / PR_W;
+    q.tiles_y = (res + 2 * PR_H - 1) / (2 * PR_H);
+    uint32_t pcols = 32;
+    while (pcols < (uint32_t)(2 * bn)) pcols <<= 1;
+    q.tmem_cols = pcols;
+    q.idesc = tp::idesc_f16kind(256, (uint32_t)bn, !f16);
+    const uint32_t sb = q.a_stage_bytes + q.b_stage_bytes;
+    int st = (int)((227 * 1024 - fixed) / (int)sb);
+    if (st > 8) st = 8;
+    if (st >= 2 && pcols <= 512) {
+      q.stages = st;
+      P.smem = 1024 + (size_t)st * sb + (2 * st + 6) * 8 + cout_pad * 4 + 16;
+      P.prect = 1;
+      P.pair = 0;
+      *L = P;
+    }
+  }
   // full-halo box kernel (TP_BOX=0 disables it): 3x3, one K block, resident weights
   const char* be = getenv("TP_BOX");
   const bool box_ok = ksize == 3 && (cin_used == 32 || cin_used == 64) && cout_pad <= 256 &&
@@ -2160,6 +2443,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       L->box = 1 + epi;
       L->box_bk = bk;
       L->pair = 0;
+      L->prect = 0;
       if (staging) {  // output store map {cstride, res, rows}, box {32 ch, 8 px, 4 rows}
         const uint64_t dims[3] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)max_img * res};
         const uint32_t box[3] = {32, BOX_TW, 4};
@@ -2243,6 +2527,36 @@ int launch_pair(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   return TP_OK;
 }
 
+int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_pair_rect_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  ConvParams p = L.p;
+  p.n_img = n_img;
+  p.n_img_dev = n_img_dev;
+  const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y * p.n_blocks_n;
+  if (tiles == 0) return TP_OK;
+  const int max_clusters = num_sms() / 2;
+  const int clusters = (int)(tiles < max_clusters ? tiles : max_clusters);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_rect_kernel, L.tmA, L.tmB, p));
+  return TP_OK;
+}
+
 int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
   if (n_img > L.p.n_img) {
     tp_set_error("conv: n_img %d exceeds planned %d", n_img, L.p.n_img);
@@ -2258,6 +2572,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
            : epi == BOX_POOL ? launch_box<32, BOX_POOL>(L, n_img, n_img_dev, st)
                              : launch_box<32, BOX_PLAIN>(L, n_img, n_img_dev, st);
   }
+  if (L.prect) return launch_pair_rect(L, n_img, n_img_dev, st);
   if (L.pair)
     return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
            : L.p.split  ? launch_pair<EPI_SPLIT>(L, n_img, n_img_dev, st)
@@ -2494,14 +2809,14 @@ extern "C" int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int
 }
 
 // Kernel chosen for conv slot `conv` of the plan: 0 conv_tc_kernel, 1 conv_pair_kernel,
-// 2 conv_l0_kernel, 3 conv_box_kernel.
+// 2 conv_l0_kernel, 3 conv_box_kernel, 4 conv_pair_rect_kernel.
 extern "C" int tp_yolo_layer_kernel(tp_yolo_net* net, int conv) {
   if (net == nullptr || conv < 0 || conv >= 23) {
     tp_set_error("tp_yolo_layer_kernel: bad conv slot %d", conv);
     return -1;
   }
   const ConvLaunch& L = net->convs[conv];
-  return L.box ? 3 : L.l0 ? 2 : L.pair ? 1 : 0;
+  return L.box ? 3 : L.l0 ? 2 : L.pair ? 1 : L.prect ? 4 : 0;
 }
 
 extern "C" int tp_yolo_destroy(tp_yolo_net* net) {
