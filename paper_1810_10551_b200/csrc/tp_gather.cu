@@ -70,8 +70,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
   //   cx0/cx1: byte offset 3*x of the column's source tap(s) in a frame row, -1 outside
   //   the frame (or outside the tile for u = 608); cf: bilinear weight of tap 1
   __shared__ uint16_t lut[256];
-  __shared__ int cx0[S + 1], cx1[S + 1];
-  __shared__ int cf[S + 1];
+  // nearest: int cx0[S + 1]; bilinear: int4 {cx0, cx1, cf, 0}[S + 1] (one 16-byte read)
+  __shared__ __align__(16) uint8_t tabmem[(S + 1) * (nearest ? 4 : 16)];
+  int* cx0 = reinterpret_cast<int*>(tabmem);
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     if (act_dtype == TP_DTYPE_F16X2) {  // fp32-parity plan: the integer value (exact)
       __half h = __float2half_rn((float)i);
@@ -95,9 +96,11 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       f = tx.f;
     }
     const bool in_tile = u < S;
-    cx0[u] = in_tile && x0 >= 0 && x0 < W ? 3 * x0 : -1;
-    cx1[u] = in_tile && x1 >= 0 && x1 < W ? 3 * x1 : -1;
-    cf[u] = f;
+    const int o0 = in_tile && x0 >= 0 && x0 < W ? 3 * x0 : -1;
+    if (nearest)
+      cx0[u] = o0;
+    else
+      reinterpret_cast<int4*>(tabmem)[u] = make_int4(o0, in_tile && x1 >= 0 && x1 < W ? 3 * x1 : -1, f, 0);
   }
   __syncthreads();
   auto pk2 = [&](int a, int b) -> uint32_t { return (uint32_t)lut[a] | ((uint32_t)lut[b] << 16); };
@@ -111,22 +114,48 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
   };
 
   if constexpr (!nearest) {
-  if (3 * (BCHUNK * side / S + 3) + 32 <= BSTAGE && row_bytes % 16 == 0 &&
+  if (3 * (BCHUNK * side / S + 3) + 32 <= BSTAGE - 16 && row_bytes % 16 == 0 &&
       (reinterpret_cast<uintptr_t>(frame) & 15) == 0) {
+    // The last 16 bytes of each staging row stay zero: out-of-frame taps point there, so
+    // the tap loads need no predicates.
     __shared__ __align__(16) uint8_t stg[8][2][BSTAGE];
+    constexpr int ZOFF = BSTAGE - 16;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* st0 = stg[warp][0];
     uint8_t* st1 = stg[warp][1];
+    if (lane < 2) reinterpret_cast<uint4*>(stg[warp][lane] + ZOFF)[0] = make_uint4(0u, 0u, 0u, 0u);
+    const bool exact_int = act_dtype == TP_DTYPE_F16X2;
+    // q(u) packed as two 32-bit words (rg, b0) in the activation type. The parity plan
+    // stores the integer value itself: fp16(1024 + n) has bits 0x6400 + n, so one packed
+    // half2 subtraction of 1024 turns two bytes into two exact fp16 integers.
+    auto pack = [&](int r, int g, int b, uint32_t& rg, uint32_t& b0) {
+      if (exact_int) {
+        const __half2 k1024 = __halves2half2(__ushort_as_half(0x6400), __ushort_as_half(0x6400));
+        __half2 hrg = __hsub2(__halves2half2(__ushort_as_half((unsigned short)(0x6400 | r)),
+                                             __ushort_as_half((unsigned short)(0x6400 | g))), k1024);
+        __half2 hb = __hsub2(__halves2half2(__ushort_as_half((unsigned short)(0x6400 | b)),
+                                            __ushort_as_half(0x6400)), k1024);
+        rg = *reinterpret_cast<uint32_t*>(&hrg);
+        b0 = *reinterpret_cast<uint32_t*>(&hb);
+      } else {
+        rg = pk2(r, g);
+        b0 = pk2(b, 0);
+      }
+    };
     for (int rr = (int)warp; rr < GATHER_ROWS; rr += 8) {
       const int v = blockIdx.x * GATHER_ROWS + rr;
       const Tap ty = bilinear_tap(v, side);
-      const int s0 = job.y + ty.i0, s1 = job.y + ty.i1, fy = ty.f;
+      const int s0 = job.y + ty.i0, s1 = job.y + ty.i1, fy = ty.f, fy0 = 256 - fy;
       const uint8_t* r0 = s0 >= 0 && s0 < H ? frame + (size_t)s0 * row_bytes : nullptr;
       const uint8_t* r1 = s1 >= 0 && s1 < H ? frame + (size_t)s1 * row_bytes : nullptr;
+      __nv_bfloat16* row_o = out_act != nullptr ? out_act + ((size_t)t * SP + (v + 1)) * SP * 8 : nullptr;
+      // slot u of the padded row = [q(u-1) | q(u)] is written by the lane owning q(u);
+      // q(u-1) comes from the lane to the left, or from the previous 32 columns (carried)
+      uint32_t prev_rg = 0u, prev_b0 = 0u;
       for (int c0 = 0; c0 < S; c0 += BCHUNK) {
-        // source columns of outputs c0 .. c0 + BCHUNK (the last one is lane 31's neighbour)
+        // source columns of outputs c0 .. c0 + BCHUNK - 1
         const int xa = max(job.x + bilinear_tap(c0, side).i0, 0);
-        const int xb = min(job.x + bilinear_tap(min(c0 + BCHUNK, S - 1), side).i1, W - 1);
+        const int xb = min(job.x + bilinear_tap(min(c0 + BCHUNK - 1, S - 1), side).i1, W - 1);
         const int base = (3 * xa) & ~15;
         const int nvec = xb >= xa ? (3 * xb + 3 - base + 15) >> 4 : 0;
         __syncwarp();  // the previous chunk's smem reads are done
@@ -138,44 +167,39 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
               r1 ? __ldg(reinterpret_cast<const uint4*>(r1 + base) + k) : z;
         }
         __syncwarp();
-        auto sample_s = [&](int uu, int& r, int& g, int& b) {
-          const int o0 = cx0[uu], o1 = cx1[uu], fx = cf[uu];
-          const int w00 = (256 - fx) * (256 - fy), w01 = fx * (256 - fy);
-          const int w10 = (256 - fx) * fy, w11 = fx * fy;
-          int ch[3];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-            const int a0 = o0 >= 0 ? st0[o0 - base + k] : 0, a1 = o1 >= 0 ? st0[o1 - base + k] : 0;
-            const int b0 = o0 >= 0 ? st1[o0 - base + k] : 0, b1 = o1 >= 0 ? st1[o1 - base + k] : 0;
-            ch[k] = (a0 * w00 + a1 * w01 + b0 * w10 + b1 * w11 + 32768) >> 16;
-          }
-          r = ch[0];
-          g = ch[1];
-          b = ch[2];
-        };
 #pragma unroll
         for (int j = 0; j < BCHUNK / 32; ++j) {
           const int u = c0 + j * 32 + (int)lane;  // S % 32 == 0: uniform per warp
           if (c0 + j * 32 >= S) break;
-          int r, g, b;
-          sample_s(u, r, g, b);
+          const int4 tb = reinterpret_cast<const int4*>(tabmem)[u];  // o0, o1, fx
+          const int i0 = tb.x >= 0 ? tb.x - base : ZOFF, i1 = tb.y >= 0 ? tb.y - base : ZOFF;
+          const int fx = tb.z, fx0 = 256 - fx;
+          int ch[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {  // separable form of the 2x2 weights: exact
+            const int h0 = st0[i0 + k] * fx0 + st0[i1 + k] * fx;
+            const int h1 = st1[i0 + k] * fx0 + st1[i1 + k] * fx;
+            ch[k] = (h0 * fy0 + h1 * fy + 32768) >> 16;
+          }
           if (out_u8 != nullptr) {
             uint8_t* o = out_u8 + (((size_t)t * S + v) * S + u) * 3;
-            o[0] = (uint8_t)r;
-            o[1] = (uint8_t)g;
-            o[2] = (uint8_t)b;
+            o[0] = (uint8_t)ch[0];
+            o[1] = (uint8_t)ch[1];
+            o[2] = (uint8_t)ch[2];
           }
-          if (out_act == nullptr) continue;
-          const uint32_t me_rg = pk2(r, g), me_b0 = pk2(b, 0);
-          uint32_t r_rg = __shfl_down_sync(0xffffffffu, me_rg, 1);
-          uint32_t r_b0 = __shfl_down_sync(0xffffffffu, me_b0, 1);
-          if (lane == 31) {  // right neighbour across the warp's edge, from the same span
-            int rr2, gr, br;
-            sample_s(u + 1, rr2, gr, br);
-            r_rg = pk2(rr2, gr);
-            r_b0 = pk2(br, 0);
+          if (row_o == nullptr) continue;
+          uint32_t me_rg, me_b0;
+          pack(ch[0], ch[1], ch[2], me_rg, me_b0);
+          uint32_t l_rg = __shfl_up_sync(0xffffffffu, me_rg, 1);
+          uint32_t l_b0 = __shfl_up_sync(0xffffffffu, me_b0, 1);
+          if (lane == 0) {
+            l_rg = prev_rg;
+            l_b0 = prev_b0;
           }
-          emit(v, u, me_rg, me_b0, r_rg, r_b0);
+          prev_rg = __shfl_sync(0xffffffffu, me_rg, 31);
+          prev_b0 = __shfl_sync(0xffffffffu, me_b0, 31);
+          *reinterpret_cast<uint4*>(row_o + u * 8) = make_uint4(l_rg, l_b0, me_rg, me_b0);
+          if (u == S - 1) *reinterpret_cast<uint4*>(row_o + S * 8) = make_uint4(me_rg, me_b0, 0u, 0u);
         }
       }
     }
@@ -205,7 +229,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
     }
     // RGB of tile column uu on this output row (zero outside the tile and the frame)
     auto sample = [&](int uu, int& r, int& g, int& b) {
-      const int o0 = cx0[uu];
+      const int o0 = nearest ? cx0[uu] : reinterpret_cast<const int4*>(tabmem)[uu].x;
       if (nearest) {
         if (o0 < 0 || r0 == nullptr) {
           r = g = b = 0;
@@ -216,7 +240,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         }
         return;
       }
-      const int o1 = cx1[uu], fx = cf[uu];
+      const int4 tb = reinterpret_cast<const int4*>(tabmem)[uu];
+      const int o1 = tb.y, fx = tb.z;
       auto px = [&](const uint8_t* rp, int o, int k) -> int {
         return (rp != nullptr && o >= 0) ? (int)__ldg(rp + o + k) : 0;
       };

@@ -88,3 +88,33 @@ def test_gather_bf16_activation_layout(cuda):
     assert got[..., [3, 7]].abs().max().item() == 0
     assert act[0, 0].abs().max().item() == 0 and act[0, -1].abs().max().item() == 0
     assert act[0, :, 609].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("mode", ["nearest", "bilinear"])
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_gather_slot_layout_per_plan(cuda, mode, dtype):
+    """Layer-0 slots in the parity plan (exact integer values) and the fp16 plan
+    (value/255), crops partly outside the frame and down/up-scaled, both resample modes."""
+    torch = cuda
+    rng = np.random.default_rng(11)
+    H, W = 2160, 3840
+    frame = rng.integers(0, 256, (H, W, 3), np.uint8)
+    for (x, y, s) in [(3104, 1424, 736), (-30, 2000, 554), (0, 0, 2160), (3500, 2100, 1098),
+                      (100, 100, 300)]:
+        jobs = kernels.jobs_tensor([(0, 0, x, y, s, 0)])
+        act = torch.zeros((1, 610, 610, 8), dtype=torch.float16, device="cuda")
+        kernels.gather(torch.from_numpy(frame).cuda(), 0, H, W, jobs, 1, mode,
+                       out_act_ptr=act.data_ptr(), dtype=dtype)
+        if mode == "nearest":
+            tile = pipeline_ref.cut_tile_nearest(frame, (0, 0, 0, x, y, s, s / 608))
+        else:
+            tile = resample_ref.cut_tile_bilinear(frame, x, y, s)
+        ref = torch.from_numpy(tile).float()
+        if dtype == "fp16":
+            ref = (ref / 255.0).to(torch.float16).float()
+        got = act[0, 1:-1].cpu().float()
+        assert torch.equal(got[:, 1:609, 0:3], ref) and torch.equal(got[:, 0:608, 4:7], ref), (x, y, s)
+        assert got[:, 0, 0:3].abs().max().item() == 0 and got[:, 608, 4:7].abs().max().item() == 0
+        assert got[..., [3, 7]].abs().max().item() == 0
+        assert act[0, 0].abs().max().item() == 0 and act[0, -1].abs().max().item() == 0
+        assert act[0, :, 609].abs().max().item() == 0
