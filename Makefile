@@ -17,7 +17,7 @@ build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/tp_common.cuh include/tilepipe_b200.h
 
 $(LIB): $(OBJS)
 	@mkdir -p $(LIB_DIR)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fvisibility=hidden
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fvisibility=hidden -ldl
 
 clean:
 	rm -rf build $(LIB)

@@ -17,6 +17,8 @@
  *   tp_attention_boxes       pipeline.py:313-316 (attention_pass confidence filter + box list)
  *   tp_select_active         pipeline.py:319-354 (merge_temporal + select_active)
  *   tp_build_jobs            pipeline.py:366     (final_pass: sorted(active_ids) tile order)
+ *   tp_nccl_gather_dets      distribution/client.py:176-203, 242-377 (result collection from
+ *                            workers, frame order)
  *   tp_collect_final         pipeline.py:357-375 (final_pass tagged list, crop-id order)
  *   tp_postprocess           postprocess.py:54-187 + pipeline.py:378-385
  *                            (nms_keep_indices, merge_split, postprocess, finish_detections)
@@ -214,6 +216,18 @@ TP_API int tp_slice_jobs(const tp_tile_job_t* jobs, const int32_t* n_jobs_dev, i
 TP_API int tp_unslice_dets(const tp_det_t* gathered, const int32_t* gathered_counts,
                            int max_slice, const int32_t* n_jobs_dev, int world, int max_jobs,
                            int max_per_tile, tp_det_t* dets, int32_t* counts, void* stream);
+
+/* Result gather (replaces the reference's collection of worker results,
+ * pkg/src/tilepipe/distribution/client.py:176-203 evaluate_remote and :242-377): all-gather
+ * every rank's padded record slice (rec_bytes_per_rank bytes) and counts (counts_per_rank
+ * int32) in rank order, both inside one ncclGroupStart/End on `stream`. `nccl_comm` is an
+ * ncclComm_t borrowed from the caller (torch.distributed's ProcessGroupNCCL._comm_ptr());
+ * NCCL is resolved from the libnccl.so.2 already loaded in the process. Either size may be
+ * 0 (that gather is skipped). tp_nccl_available() = 1 when NCCL resolves. */
+TP_API int tp_nccl_available(void);
+TP_API int tp_nccl_gather_dets(void* nccl_comm, const void* local_recs, int64_t rec_bytes_per_rank,
+                               const int32_t* local_counts, int64_t counts_per_rank,
+                               void* all_recs, int32_t* all_counts, void* stream);
 
 
 /* Profiling only (TP_CONV_DEBUG bit 32 set in the environment when the net/conv runs):

@@ -7,7 +7,8 @@ split into contiguous chunks whose sizes differ by at most one (the reference's
 re-running stage 1 on the K-1 frames just before its chunk (2 tiles per frame at
 preset P1) instead of exchanging attention boxes, so the data path has no collective;
 the only collective is the result gather to rank 0 (``gather_records``), a fixed-size
-padded all-gather (NCCL on GPUs, gloo on CPU).
+padded all-gather: on GPUs one fused NCCL launch through the C-ABI
+(``tp_nccl_gather_dets`` on torch.distributed's own communicator), gloo on CPU.
 """
 
 from __future__ import annotations
@@ -44,6 +45,36 @@ def pack_records(rows: list[np.ndarray], max_rows: int, dtype: np.dtype) -> tupl
     return counts, buf
 
 
+def nccl_comm(group=None) -> int:
+    """The ncclComm_t torch.distributed holds for this rank's device (borrowed, never
+    freed here). torch creates communicators lazily; one tiny all-reduce forces it."""
+    import torch
+    import torch.distributed as dist
+
+    backend = (group or dist.group.WORLD)._get_backend(torch.device("cuda"))
+    try:
+        ptr = int(backend._comm_ptr())
+    except RuntimeError:
+        ptr = 0
+    if not ptr:
+        dist.all_reduce(torch.zeros(1, device="cuda"), group=group)
+        ptr = int(backend._comm_ptr())
+    if not ptr:
+        raise RuntimeError("torch.distributed exposes no NCCL communicator for this device")
+    return ptr
+
+
+def nccl_all_gather(local_recs, all_recs, local_counts, all_counts, group=None, stream=None):
+    """Rank-order all-gather of a padded record slice and its counts in one fused NCCL
+    launch on `stream` (tp_nccl_gather_dets). Shapes: all_* = world x local_*."""
+    from . import native
+
+    native.call("tp_nccl_gather_dets", nccl_comm(group), native.ptr(local_recs),
+                int(local_recs.numel() * local_recs.element_size()) if local_recs is not None else 0,
+                native.ptr(local_counts), int(local_counts.numel()) if local_counts is not None else 0,
+                native.ptr(all_recs), native.ptr(all_counts), native.stream_handle(stream))
+
+
 def gather_records(counts, records, frames_per_rank: list[int], group=None, to_host=True):
     """All-gather per-frame (count, padded records) from every rank; returns the
     concatenation in rank (= frame) order as a list of per-frame record arrays.
@@ -63,8 +94,11 @@ def gather_records(counts, records, frames_per_rank: list[int], group=None, to_h
     r[: records.shape[0]] = records
     call = torch.empty(world * n_max, dtype=torch.int32, device=dev)
     rall = torch.empty((world * n_max, records.shape[1]), dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(call, c, group=group)
-    dist.all_gather_into_tensor(rall, r, group=group)
+    if dist.get_backend(group) == "nccl":
+        nccl_all_gather(r, rall, c, call, group)
+    else:
+        dist.all_gather_into_tensor(call, c, group=group)
+        dist.all_gather_into_tensor(rall, r, group=group)
     if not to_host:  # stay on device (no host sync): [world*n_max] counts, records
         return call, rall
     call = call.cpu().numpy().reshape(world, n_max)

@@ -35,13 +35,15 @@ MAX_PER_FRAME = 2048   # raw stage-2 detections per frame (postprocess capacity)
 
 def _dist_exchange(local_dets, local_counts, all_dets, all_counts):
     """Default crop_shard exchange: all-gather every rank's padded stage-2 slice in rank
-    order over the default process group (NCCL on GPUs: one collective per tensor)."""
+    order over the default process group (NCCL on GPUs: records and counts in one fused
+    launch through tp_nccl_gather_dets; gloo on CPU)."""
     import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        from .distributed import nccl_all_gather
+        nccl_all_gather(local_dets, all_dets, local_counts, all_counts)
+        return
     for loc, out in ((local_dets, all_dets), (local_counts, all_counts)):
-        if dist.get_backend() == "nccl":
-            dist.all_gather_into_tensor(out, loc)
-        else:
-            dist.all_gather(list(out.view(dist.get_world_size(), -1).unbind(0)), loc)
+        dist.all_gather(list(out.view(dist.get_world_size(), -1).unbind(0)), loc)
 
 
 class AttentionPipelineB200:

@@ -101,6 +101,8 @@ SIGNATURES = {
     "tp_slice_jobs": (_I, [_P, _P, _I, _I, _P, _P, _I, _P]),
     "tp_unslice_dets": (_I, [_P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
     "tp_render_frames": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_uint32, _P, _P]),
+    "tp_nccl_available": (_I, []),
+    "tp_nccl_gather_dets": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P]),
 }
 
 _lib = None

@@ -98,6 +98,9 @@ def test_library_loads_and_exports_every_header_symbol():
     assert lib.tp_yolo_workspace_bytes(1, 1) > 20_000_000
     # the fp32-parity plan doubles every activation buffer but the input slots and head
     assert lib.tp_yolo_workspace_bytes(1, 2) > 1.8 * lib.tp_yolo_workspace_bytes(1, 1)
+    # the result gather rejects a missing communicator before touching NCCL or CUDA
+    assert lib.tp_nccl_gather_dets(None, None, 0, None, 0, None, None, None) == 1
+    assert b"bad argument" in lib.tp_last_error()
 
 
 def test_product_never_imports_oracle():
