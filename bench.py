@@ -257,9 +257,17 @@ def main():
     from paper_1810_10551_b200 import distributed as D, native, pipeline as P, synthetic, yolo
     from paper_1810_10551_b200.engine import AttentionPipelineB200
 
-    torch.cuda.set_device(local)
+    # TP_BENCH_SHARED_GPU=1: logic check of the multi-rank path on a one-GPU box (every
+    # rank on cuda:0, gloo collectives, ranks never wait on each other's kernels); such a
+    # run is flagged in its config and is not a scaling measurement
+    shared_gpu = os.environ.get("TP_BENCH_SHARED_GPU") == "1"
+    dev_idx = 0 if shared_gpu else local
+    torch.cuda.set_device(dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     B = args.batch
     objs = clip_objects(rank, args.clip_frames)
     # every step takes B consecutive clip frames: pad the clip cyclically to a multiple of B
@@ -334,7 +342,7 @@ def main():
     if args.profile:  # CUPTI kernel table to stderr; the JSON value of such a run is not a bench number
         prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
         prof.__enter__()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_idx) as clocks:
         torch.cuda.synchronize()
         t0.record(stream)
         for i in range(args.warmup, n_steps):
@@ -411,6 +419,8 @@ def main():
                           "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
                           "accumulation and epilogue"),
             "config": {**arm_config(args, n_clip, world),
+                       **({"shared_gpu_logic_check": "all ranks on cuda:0 over gloo: not a "
+                                                     "scaling measurement"} if shared_gpu else {}),
                        "l2": "inputs exceed L2 (746 MB per step)",
                        "tiles_per_frame": tiles_per_frame,
                        "crops_per_sec": value * tiles_per_frame},

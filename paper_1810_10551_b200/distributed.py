@@ -96,9 +96,12 @@ def gather_records(counts, records, frames_per_rank: list[int], group=None, to_h
     rall = torch.empty((world * n_max, records.shape[1]), dtype=torch.uint8, device=dev)
     if dist.get_backend(group) == "nccl":
         nccl_all_gather(r, rall, c, call, group)
-    else:
-        dist.all_gather_into_tensor(call, c, group=group)
-        dist.all_gather_into_tensor(rall, r, group=group)
+    else:  # gloo gathers host tensors
+        ch, rh = call.cpu(), rall.cpu()
+        dist.all_gather_into_tensor(ch, c.cpu(), group=group)
+        dist.all_gather_into_tensor(rh, r.cpu(), group=group)
+        call.copy_(ch)
+        rall.copy_(rh)
     if not to_host:  # stay on device (no host sync): [world*n_max] counts, records
         return call, rall
     call = call.cpu().numpy().reshape(world, n_max)
