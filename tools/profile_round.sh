@@ -6,14 +6,28 @@
 set -u
 TAG=${1:-r01}
 CMD="python bench.py --steps 1 --warmup 1 --batch 30 --no-e2e --no-cpu-baseline"
-KERN='regex:conv_tc_kernel|conv_pair_kernel|conv_l0_kernel|conv_box_kernel|gather_kernel|decode_kernel|select_kernel|postprocess_kernel|maxpool2_kernel|maxpool2_split_kernel|collect_final_kernel|slice_jobs_kernel|unslice_kernel|attention_boxes_kernel|build_jobs_kernel'
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/plain_$TAG.log; exit 1; }
 tail -1 gpurun_out/plain_$TAG.log | cut -c1-400
-ncu --metrics gpu__time_duration.sum --clock-control none -k "$KERN" --csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
     --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launches_$TAG.log 2>&1
 echo "launch list rc=$?"
 # conv launches: warm-up step = 2 forwards (46 launches); timed step stage-1 = 23 more
 ncu --set full --clock-control none --import-source on -k regex:conv_ -s 69 -c 23 \
     -o gpurun_out/conv_full_$TAG $CMD > gpurun_out/ncu_full_$TAG.log 2>&1
 echo "full rc=$?"
+# HBM-bound side kernels (gather, decode, select, postprocess) of the same command
+ncu --set full --clock-control none --import-source on \
+    -k 'regex:gather_kernel|decode_kernel|select_kernel|postprocess_kernel|build_jobs_kernel|collect_final_kernel|maxpool2' \
+    -c 16 -o gpurun_out/aux_full_$TAG $CMD > gpurun_out/ncu_aux_$TAG.log 2>&1
+echo "aux rc=$?"
+python tools/layer_times.py --tiles 120 > gpurun_out/layer_times_$TAG.txt 2>&1
+echo "layer_times rc=$?"
+# summaries on the box (the .ncu-rep files exceed what gpurun brings back)
+python tools/launch_summary.py gpurun_out/launches_$TAG.csv "$TAG" "$CMD" > gpurun_out/launch_summary_$TAG.txt
+python tools/ncu_conv_table.py gpurun_out/conv_full_$TAG.ncu-rep > gpurun_out/conv_layers_$TAG.csv
+ncu -i gpurun_out/conv_full_$TAG.ncu-rep --page raw --csv > gpurun_out/conv_raw_$TAG.csv
+ncu -i gpurun_out/aux_full_$TAG.ncu-rep --page raw --csv > gpurun_out/aux_raw_$TAG.csv
+gzip -f gpurun_out/conv_raw_$TAG.csv gpurun_out/aux_raw_$TAG.csv
+ls -la gpurun_out/*.ncu-rep
+rm -f gpurun_out/*.ncu-rep
