@@ -16,6 +16,8 @@ from __future__ import annotations
 import ctypes
 import os
 
+import threading
+
 import numpy as np
 
 from . import native
@@ -298,9 +300,10 @@ class YoloB200Detector(Detector):
     """YOLO v2-608 on the B200 behind the reference Detector interface.
 
     ``detect`` takes one 608x608x3 uint8 tile and returns crop-local detections sorted
-    by descending confidence (ties: cell-major, anchor order). Calls are serialised on
-    the current CUDA stream; the batched pipeline (engine.AttentionPipelineB200) bypasses
-    per-tile calls entirely. The class labels are COCO-80 names.
+    by descending confidence (ties: cell-major, anchor order). Safe for concurrent
+    calls (detector.py:80-82): one lock serialises the device work, which shares one
+    workspace; the batched pipeline (engine.AttentionPipelineB200) bypasses per-tile
+    calls entirely. The class labels are COCO-80 names.
     """
 
     def __init__(self, seed: int = 0, threshold: float = 0.25, max_tiles: int = 32,
@@ -314,6 +317,7 @@ class YoloB200Detector(Detector):
         self.max_tiles = max_tiles
         self.precision = precision
         self._net = None
+        self._lock = threading.Lock()
 
     @property
     def net(self):
@@ -329,6 +333,12 @@ class YoloB200Detector(Detector):
         torch = native.require_cuda()
         t = tiles_u8 if not isinstance(tiles_u8, np.ndarray) else torch.from_numpy(
             np.ascontiguousarray(tiles_u8)).cuda()
+        with self._lock:
+            return self._detect_locked(t)
+
+    def _detect_locked(self, t) -> list[list[Detection]]:
+        from . import kernels
+
         n = int(t.shape[0])
         out = []
         for s in range(0, n, self.net.max_tiles):
@@ -342,13 +352,18 @@ class YoloB200Detector(Detector):
 
     def detect(self, frame_id: int, crop_id: int, tile: np.ndarray | None = None
                ) -> list[Detection]:
+        self.check_tile(tile)
+        return self.detect_tiles(tile[None])[0]
+
+    def check_tile(self, tile) -> None:
+        """The ValueError ``detect`` raises for this tile, if any (bad input is rejected
+        before any device work, detector.py:176-182)."""
         side = self.profile.input_side
         if tile is None:
             raise ValueError("YoloB200Detector needs tile pixels (got None)")
         if not isinstance(tile, np.ndarray) or tile.shape != (side, side, 3):
             got = tile.shape if isinstance(tile, np.ndarray) else type(tile)
             raise ValueError(f"tile must be {side}x{side}x3, got {got}")
-        return self.detect_tiles(tile[None])[0]
 
 
 def _local_rect(r):
