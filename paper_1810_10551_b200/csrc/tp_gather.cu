@@ -47,7 +47,7 @@ constexpr int SEGS = S / 32;       // 19 warp tasks per row
 // loads, then samples the 2x2 taps from there (12 byte loads per pixel from global were
 // LSU/latency bound: 35% of the HBM peak).
 constexpr int BCHUNK = 64;
-constexpr int BSTAGE = 2048;  // bytes per staged row span: side <= ~6300 px
+constexpr int BSTAGE = 1536;  // bytes per staged row span: side <= ~4600 px (8K attention crops); 6 CTAs per SM
 
 template <int MODE>
 __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ frames,
