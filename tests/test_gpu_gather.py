@@ -55,7 +55,8 @@ def test_batched_gather_matches_oracle(cuda, mode):
     H, W = 2160, 3840
     frames = rng.integers(0, 256, (2, H, W, 3), np.uint8)
     crops = [(0, 0, 2160), (1680, 0, 2160), (0, 0, 736), (3104, 1424, 736), (-30, 2000, 554),
-             (3500, 2100, 1098), (0, 0, 3840), (100, 100, 300)]
+             (3500, 2100, 1098), (0, 0, 3840), (100, 100, 300), (-500, -300, 4320),
+             (3300, 700, 4320), (3833, 5, 608), (1000, 1000, 7000)]
     rows = [(f, 0, x, y, s, 0) for f in range(2) for (x, y, s) in crops]
     jobs = kernels.jobs_tensor(rows)
     dev = torch.from_numpy(frames).cuda()
