@@ -986,12 +986,19 @@ __device__ __forceinline__ void tma_load_4d_pair(void* dst, const void* tmap, ui
       : "memory");
 }
 
-constexpr int PR_W = 16, PR_H = 8;  // per-CTA output half-tile; the pair covers 16 x 16
+constexpr int PR_W = 16, PR_H = 8;  // one M = 128 block: 16 x 8 output pixels
 
+// MH = M blocks per CTA (1: 16 x 8 per CTA, the pair covers 16 x 16; 2: 16 x 16 per CTA,
+// one {64, 16, 18} halo box serves both blocks, so the A + B bytes each stage brings per
+// MMA drop from 44 KB / 12 to 60 KB / 24 — for N = 128 the fill rate from L2, not the
+// tensor pipe, bounds the MH = 1 tile). POOL: fused 2x2 max pool, else every pixel is
+// stored (16-bit or hi/lo pairs).
+template <int MH, bool POOL>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_pair_rect_kernel(const __grid_constant__ CUtensorMap tmA,
                           const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
   constexpr int BK = 64;
+  constexpr int CH = PR_H * MH;  // output rows per CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1056,7 +1063,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = mt - img * per_img;
     const int by = r / p.tiles_x;
     x0 = (r - by * p.tiles_x) * PR_W;
-    y0 = by * 2 * PR_H + (int)rank * PR_H;  // this CTA's 8-row half
+    y0 = by * 2 * CH + (int)rank * CH;  // this CTA's half of the pair's rows
   };
 
   if (warp == kProdWarp) {
@@ -1106,7 +1113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
         aph[acc] ^= 1;
         tp::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * MH * p.bn);
         for (int kb = 0; kb < p.num_kb; ++kb) {
           tp::mbar_wait(&full[s], ph);
           tp::tc_fence_after();
@@ -1116,9 +1123,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_pair(d_tmem, ad0 + dy * a_row16 + 2 * k, bd0 + dy * b_slice16 + 2 * k, p.idesc,
-                         (kb | dy | k) != 0);
+              for (int h = 0; h < MH; ++h)  // M block h: output rows 8h .. 8h+7 of the CTA
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  mma_pair(d_tmem + (uint32_t)(h * p.bn), ad0 + (dy + PR_H * h) * a_row16 + 2 * k,
+                           bd0 + dy * b_slice16 + 2 * k, p.idesc, (kb | dy | k) != 0);
             commit_pair_mc(&empty[s]);
           }
           __syncwarp();
@@ -1132,12 +1141,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===== epilogue: both CTAs, own 16 x 8 half; groups alternate accumulators =====
+    // ===== epilogue: both CTAs, own rows; groups alternate accumulators =====
     const int g = (int)warp >> 2;
     const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0, leaky = p.leaky != 0, spl = p.split != 0;
-    const int ores = p.res >> 1, oimg = ores * ores;
+    const int ores = POOL ? p.res >> 1 : p.res, oimg = ores * ores;
     const int nchunks = p.bn >> 4;
     const uint32_t leader_tempty[2] = {mapa_rank(&tempty[0], 0), mapa_rank(&tempty[1], 0)};
     uint32_t ph = 0;
@@ -1149,60 +1158,65 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::mbar_wait(&tfull[g], ph);
       ph ^= 1;
       tp::tc_fence_after();
-      const int x = x0 + (row & (PR_W - 1)), y = y0 + (row >> 4);
-      const bool store = x < p.res && y < p.res && ((x | y) & 1) == 0;
-      __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
-                         (size_t)(img * oimg + (y >> 1) * ores + (x >> 1)) * p.out_cstride +
-                         p.out_coff;
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * p.bn);
-      uint32_t v[16];
-      tp::tmem_ld16(t_row, v);
-      for (int c = 0; c < nchunks; ++c) {
-        tp::tmem_ld_wait();
-        float f[16];
+#pragma unroll 1
+      for (int h = 0; h < MH; ++h) {
+        const int x = x0 + (row & (PR_W - 1)), y = y0 + PR_H * h + (row >> 4);
+        const bool store = x < p.res && y < p.res && (!POOL || ((x | y) & 1) == 0);
+        const int ox = POOL ? x >> 1 : x, oy = POOL ? y >> 1 : y;
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
+                           (size_t)(img * oimg + oy * ores + ox) * p.out_cstride + p.out_coff;
+        const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)((g * MH + h) * p.bn);
+        uint32_t v[16];
+        tp::tmem_ld16(t_row, v);
+        for (int c = 0; c < nchunks; ++c) {
+          tp::tmem_ld_wait();
+          float f[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
-        if (c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);
-        // 2x2 max first (bias and leaky are monotonic: the same value), x pair lane^1,
-        // y pair lane^16
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+          if (c + 1 < nchunks) tp::tmem_ld16(t_row + (uint32_t)((c + 1) * 16), v);
+          if (POOL) {
+            // 2x2 max first (bias and leaky are monotonic: the same value), x pair lane^1,
+            // y pair lane^16
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
+            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], 1));
 #pragma unroll
-        for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], PR_W));
-        const int ch0 = n0 + c * 16;
-        const float4* b4 = reinterpret_cast<const float4*>(bias_s + ch0);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 bb = b4[j];
-          f[4 * j + 0] += bb.x;
-          f[4 * j + 1] += bb.y;
-          f[4 * j + 2] += bb.z;
-          f[4 * j + 3] += bb.w;
-        }
-        if (leaky) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
-        }
-        if (!store || ch0 >= p.cout || (p.dbg & 4)) continue;
-        if (spl) {
-          store_split16(o + 2 * ch0, f);
-          continue;
-        }
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (f16) {
-            __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
-            pk[j] = *reinterpret_cast<uint32_t*>(&h);
-          } else {
-            __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
-            pk[j] = *reinterpret_cast<uint32_t*>(&h);
+            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], __shfl_xor_sync(0xffffffffu, f[j], PR_W));
           }
+          const int ch0 = n0 + c * 16;
+          const float4* b4 = reinterpret_cast<const float4*>(bias_s + ch0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 bb = b4[j];
+            f[4 * j + 0] += bb.x;
+            f[4 * j + 1] += bb.y;
+            f[4 * j + 2] += bb.z;
+            f[4 * j + 3] += bb.w;
+          }
+          if (leaky) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
+          }
+          if (!store || ch0 >= p.cout || (p.dbg & 4)) continue;
+          if (spl) {
+            store_split16(o + 2 * ch0, f);
+            continue;
+          }
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (f16) {
+              __half2 hh = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&hh);
+            } else {
+              __nv_bfloat162 hh = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+              pk[j] = *reinterpret_cast<uint32_t*>(&hh);
+            }
+          }
+          *reinterpret_cast<uint4*>(o + ch0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(o + ch0 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
-        *reinterpret_cast<uint4*>(o + ch0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(o + ch0 + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        tp::tmem_ld_wait();
       }
-      tp::tmem_ld_wait();
       tp::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty[g]);
@@ -2340,13 +2354,20 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     p.stages = st;
     L->smem = 1024 + (size_t)st * sb + p.stage_bytes + (2 * st + 6) * 8 + cout_pad * 4 + 16;
   }
-  // CTA-pair pooled kernel for pooled 3x3 SW128 layers whose weights are not resident
-  // (TP_PRECT=0 disables it); the box kernel below still wins where it applies
+  // CTA-pair halo-box kernel for pooled 3x3 SW128 layers whose weights are not resident
+  // (TP_PRECT=0 disables it, TP_PRECT_MH=1 keeps one M block per CTA; the box kernel below
+  // still wins where it applies). TP_PRECT_PLAIN=1 also routes unpooled N = 128 layers
+  // here: measured slower than the im2col pair kernel (parity layer 4: 0.96 vs 0.84 ms per
+  // 120 tiles; its direct 16-byte stores of 4x the pooled bytes cap the epilogue)
   const char* pr = getenv("TP_PRECT");
-  if (pool && ksize == 3 && mode == MODE_SW128 && !halo && bn >= 128 &&
-      (pr == nullptr || atoi(pr) != 0)) {
+  const char* prm = getenv("TP_PRECT_MH");
+  const char* prp = getenv("TP_PRECT_PLAIN");
+  const bool plain_ok = bn == 128 && prp != nullptr && atoi(prp) == 1;
+  if ((pool || plain_ok) && ksize == 3 && mode == MODE_SW128 && !halo && bn >= 128 &&
+      !out_fp32 && !reorg && (pr == nullptr || atoi(pr) != 0)) {
+    const int mh = bn <= 128 && (prm == nullptr || atoi(prm) != 1) ? 2 : 1;
     const uint64_t adims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
-    const uint32_t abox[4] = {(uint32_t)bk, PR_W, PR_H + 2, 1};
+    const uint32_t abox[4] = {(uint32_t)bk, PR_W, (uint32_t)(PR_H * mh + 2), 1};
     ConvLaunch P = *L;
     rc = make_tmap(&P.tmA, in, 4, adims, abox, swz, f16);
     if (rc) return rc;
@@ -2359,17 +2380,17 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     q.n_blocks_n = cout_pad / bn;
     q.kb_per_tap = cin_used / bk;
     q.num_kb = 3 * q.kb_per_tap;
-    q.a_stage_bytes = PR_W * (PR_H + 2) * bk * 2;
+    q.a_stage_bytes = PR_W * (PR_H * mh + 2) * bk * 2;
     q.b_stage_bytes = 3 * (bn / 2) * bk * 2;
     q.bres_bytes = 0;
     q.stage_bytes = 0;
     q.halo = 0;
-    q.sub = 1;
-    q.rect = 1;
+    q.sub = mh;
+    q.rect = pool ? 1 : 0;
     q.tiles_x = (res + PR_W - 1) / PR_W;
-    q.tiles_y = (res + 2 * PR_H - 1) / (2 * PR_H);
+    q.tiles_y = (res + 2 * PR_H * mh - 1) / (2 * PR_H * mh);
     uint32_t pcols = 32;
-    while (pcols < (uint32_t)(2 * bn)) pcols <<= 1;
+    while (pcols < (uint32_t)(2 * mh * bn)) pcols <<= 1;
     q.tmem_cols = pcols;
     q.idesc = tp::idesc_f16kind(256, (uint32_t)bn, !f16);
     const uint32_t sb = q.a_stage_bytes + q.b_stage_bytes;
@@ -2527,10 +2548,11 @@ int launch_pair(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   return TP_OK;
 }
 
+template <int MH, bool POOL>
 int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_pair_rect_kernel,
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_pair_rect_kernel<MH, POOL>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
@@ -2553,7 +2575,7 @@ int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_rect_kernel, L.tmA, L.tmB, p));
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_rect_kernel<MH, POOL>, L.tmA, L.tmB, p));
   return TP_OK;
 }
 
@@ -2572,7 +2594,14 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
            : epi == BOX_POOL ? launch_box<32, BOX_POOL>(L, n_img, n_img_dev, st)
                              : launch_box<32, BOX_PLAIN>(L, n_img, n_img_dev, st);
   }
-  if (L.prect) return launch_pair_rect(L, n_img, n_img_dev, st);
+  if (L.prect) {
+    const bool pool = L.p.rect != 0;
+    if (L.p.sub == 2)
+      return pool ? launch_pair_rect<2, true>(L, n_img, n_img_dev, st)
+                  : launch_pair_rect<2, false>(L, n_img, n_img_dev, st);
+    return pool ? launch_pair_rect<1, true>(L, n_img, n_img_dev, st)
+                : launch_pair_rect<1, false>(L, n_img, n_img_dev, st);
+  }
   if (L.pair)
     return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
            : L.p.split  ? launch_pair<EPI_SPLIT>(L, n_img, n_img_dev, st)
