@@ -1232,6 +1232,226 @@ __global__ void __launch_bounds__(kThreads, 1)
                  : "memory");
 }
 
+// ------------------------------------------------------------------ swapped operands, N = 128
+// 3x3 layers with 128 output channels (parity plan: layers 4 and 6). With pixels as the M
+// operand, every K = 16 step of a 128 x 128 MMA reads 4 KB of A + 4 KB of B from shared
+// memory in its 64 cycles of math — the operand reads, not the tensor pipe, bound those
+// layers (~55-78% pipe activity). Swapped, the weights are A (M = 128 output channels)
+// and the pixels are B (N = 256 = a 16 x 16 output block): 4 KB + 8 KB per 128 cycles.
+// One stage per (kernel column dx, 32-channel block): a halo box {32, 16, 18} of the input
+// (SW64) whose three kernel rows dy are descriptor offsets of 16 box rows, plus the three
+// taps' weight slices {32, 128}. The accumulator is channel-major (TMEM lane = output
+// channel, column = pixel), so the epilogue stores each pixel's channels as one
+// warp-contiguous 64-byte run per 16-bit plane (hi and lo planes in the parity plan) and
+// pools 2 x 2 inside a thread (columns x, x+1 of rows y, y+1).
+constexpr int SW_BK = 32, SW_W = 16, SW_H = 16;
+
+template <bool POOL>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const ConvParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int S = p.stages;
+  uint8_t* smX = smem;                                   // pixel boxes (B operand)
+  uint8_t* smW = smem + (size_t)S * p.a_stage_bytes;     // weight slices (A operand)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smW + (size_t)S * p.b_stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* tfull = bars + 2 * S;
+  uint64_t* tempty = bars + 2 * S + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 5);
+
+  const uint32_t warp = tp::warp_id();
+  const uint32_t lane = tp::lane_id();
+  const int cout_pad = 128 * p.n_blocks_n;
+  if (warp == kProdWarp && lane == 0) {
+    tp::tma_prefetch(&tmA);
+    tp::tma_prefetch(&tmB);
+    for (int i = 0; i < S; ++i) {
+      tp::mbar_init(&full[i], 1);
+      tp::mbar_init(&empty[i], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tp::mbar_init(&tfull[a], 1);
+      tp::mbar_init(&tempty[a], 4);
+    }
+    tp::fence_mbar_init();
+  }
+  if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, 512);
+  for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
+  const int per_img = p.tiles_x * p.tiles_y;
+  const int total_tiles = n_img * per_img * p.n_blocks_n;
+  const int n_tiles = (int)blockIdx.x < total_tiles
+                          ? (total_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
+                          : 0;
+  auto tile_at = [&](int i, int& img, int& y0, int& x0, int& nb) {
+    const int t = (int)blockIdx.x + i * (int)gridDim.x;
+    const int mt = t / p.n_blocks_n;
+    nb = t - mt * p.n_blocks_n;
+    img = mt / per_img;
+    const int r = mt - img * per_img;
+    const int by = r / p.tiles_x;
+    x0 = (r - by * p.tiles_x) * SW_W;
+    y0 = by * SW_H;
+  };
+
+  if (warp == kProdWarp) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t w_slice = 128 * SW_BK * 2;
+      for (int i = 0; i < n_tiles; ++i) {
+        int img, y0, x0, nb;
+        tile_at(i, img, y0, x0, nb);
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          tp::mbar_wait(&empty[s], ph ^ 1);
+          tp::mbar_arrive_expect_tx(&full[s], p.a_stage_bytes + p.b_stage_bytes);
+          const int dx = kb / p.kb_per_tap - 1;
+          const int cb = kb - (dx + 1) * p.kb_per_tap;
+          tma_load_4d(smX + (size_t)s * p.a_stage_bytes, &tmA, &full[s], cb * SW_BK, x0 + dx,
+                      y0 - 1, img);
+          uint8_t* wdst = smW + (size_t)s * p.b_stage_bytes;
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+            tp::tma_load_2d(wdst + dy * w_slice, &tmB, &full[s],
+                            (dy * 3 + dx + 1) * p.cin + cb * SW_BK, nb * 128);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    constexpr uint32_t row_bytes = SW_BK * 2, sbo = 8 * row_bytes;
+    const uint64_t x_desc0 = tp::umma_desc(tp::smem_u32(smX), 16, sbo, 4);  // SW64
+    const uint64_t w_desc0 = tp::umma_desc(tp::smem_u32(smW), 16, sbo, 4);
+    const uint32_t x_step = p.a_stage_bytes >> 4, w_step = p.b_stage_bytes >> 4;
+    constexpr uint32_t x_row16 = SW_W * row_bytes / 16;   // one box row of 16 pixels, >> 4
+    constexpr uint32_t w_slice16 = 128 * row_bytes / 16;  // one tap's weight slice, >> 4
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t aph[2] = {0, 0};
+    for (int i = 0; i < n_tiles; ++i) {
+      const int acc = i & 1;
+      tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+      aph[acc] ^= 1;
+      tp::tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        tp::mbar_wait(&full[s], ph);
+        tp::tc_fence_after();
+        const uint64_t xd = x_desc0 + (uint64_t)(s * x_step);
+        const uint64_t wd = w_desc0 + (uint64_t)(s * w_step);
+        if (tp::elect_one()) {
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int k = 0; k < SW_BK / 16; ++k)
+              tp::mma_bf16(d_tmem, wd + dy * w_slice16 + 2 * k, xd + dy * x_row16 + 2 * k, p.idesc,
+                           (kb | dy | k) != 0);
+          tp::mma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == S) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+      if (tp::elect_one()) tp::mma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else {
+    // epilogue: group g takes tiles i % 2 == g; warp q owns output channels q*32 .. q*32+31
+    const int g = (int)warp >> 2;
+    const uint32_t q = warp & 3;
+    const bool f16 = p.f16 != 0, leaky = p.leaky != 0, spl = p.split != 0;
+    const int ores = POOL ? p.res >> 1 : p.res;
+    uint32_t ph = 0;
+    for (int i = 0; i < n_tiles; ++i) {
+      if ((i & 1) != g) continue;
+      int img, y0, x0, nb;
+      tile_at(i, img, y0, x0, nb);
+      const int co = nb * 128 + (int)(q * 32 + lane);
+      const bool live = !(p.dbg & 4);  // the plan requires cout == 128
+      // stored channel of co: hi/lo planes interleaved per 16 channels in the parity plan
+      const int sc = p.out_coff + (spl ? 32 * (co >> 4) + (co & 15) : co);
+      const float bco = bias_s[co];
+      tp::mbar_wait(&tfull[g], ph);
+      ph ^= 1;
+      tp::tc_fence_after();
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 256);
+      // a warp writes one pixel's 32 channels per instruction (64 B, or 2 x 32 B hi/lo runs)
+      auto put = [&](int y, int x, float v) {
+        v += bco;
+        if (leaky) v = fmaxf(v, 0.1f * v);
+        __half* o = reinterpret_cast<__half*>(p.out) +
+                    ((size_t)(img * ores + y) * ores + x) * p.out_cstride + sc;
+        if (spl) {
+          const __half h = __float2half_rn(v);
+          o[0] = h;
+          o[16] = __float2half_rn(v - __half2float(h));
+        } else if (f16) {
+          o[0] = __float2half_rn(v);
+        } else {
+          *reinterpret_cast<__nv_bfloat16*>(o) = __float2bfloat16_rn(v);
+        }
+      };
+      if (POOL) {
+        for (int r = 0; r < SW_H / 2; ++r) {
+          uint32_t a[16], b[16];
+          tp::tmem_ld16(t_row + (uint32_t)(2 * r * 16), a);
+          tp::tmem_ld16(t_row + (uint32_t)((2 * r + 1) * 16), b);
+          tp::tmem_ld_wait();
+          const int oy = (y0 >> 1) + r;
+          if (!live || oy >= ores) continue;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int ox = (x0 >> 1) + j;
+            // 2x2 max before bias + leaky (both monotonic)
+            const float m = fmaxf(fmaxf(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1])),
+                                  fmaxf(__uint_as_float(b[2 * j]), __uint_as_float(b[2 * j + 1])));
+            if (ox < ores) put(oy, ox, m);
+          }
+        }
+      } else {
+        uint32_t v[16];
+        tp::tmem_ld16(t_row, v);
+        for (int r = 0; r < SW_H; ++r) {
+          tp::tmem_ld_wait();
+          float f[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
+          if (r + 1 < SW_H) tp::tmem_ld16(t_row + (uint32_t)((r + 1) * 16), v);
+          const int y = y0 + r;
+          if (!live || y >= ores) continue;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (x0 + j < ores) put(y, x0 + j, f[j]);
+        }
+        tp::tmem_ld_wait();
+      }
+      tp::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tp::mbar_arrive(&tempty[g]);
+    }
+  }
+
+  tp::tc_fence_before();
+  __syncthreads();
+  tp::tc_fence_after();
+  if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, 512);
+}
+
 // ------------------------------------------------------------------ layer 0, pool-in-M
 // Layer 0 (3x3, 3->32, leaky, 2x2 maxpool) has K = 48 but 608^2 outputs per tile, so it
 // is bound by epilogue instructions, not math. Here each M row is one POOLED output
@@ -2132,6 +2352,7 @@ struct ConvLaunch {
   int l0;    // layer-0 pool-in-M kernel
   int box;   // full-halo box kernel: 0 off, else 1 + BoxEpi
   int prect; // CTA-pair pooled 3x3 kernel (conv_pair_rect_kernel)
+  int swap;  // swapped-operand 3x3 kernel for 128 output channels (conv_swap_kernel)
   int box_bk;
   CUtensorMap tmA, tmB, tmC;
   ConvParams p;
@@ -2404,6 +2625,52 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       *L = P;
     }
   }
+  // swapped-operand kernel for pooled 3x3 layers with 128 output channels whose weights are
+  // not resident (TP_SWAP=0 disables it; the box kernel below still wins where it applies).
+  // TP_SWAP=2 also takes unpooled ones: measured slower than the im2col pair kernel on
+  // parity layer 4 (1.09 vs 0.84 ms per 120 tiles: the 4x larger channel-major output
+  // makes the epilogue, not the tensor pipe, the bound)
+  const char* sw = getenv("TP_SWAP");
+  const int swap_mode = sw == nullptr ? 1 : atoi(sw);
+  if (ksize == 3 && cout_pad == 128 && cout == 128 && cin_used % SW_BK == 0 && !halo &&
+      !out_fp32 && !reorg && (swap_mode == 2 || (swap_mode == 1 && pool))) {
+    ConvLaunch P = *L;
+    const uint64_t xdims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
+    const uint32_t xbox[4] = {SW_BK, SW_W, SW_H + 2, 1};
+    rc = make_tmap(&P.tmA, in, 4, xdims, xbox, CU_TENSOR_MAP_SWIZZLE_64B, f16);
+    if (rc) return rc;
+    const uint64_t wdims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+    const uint32_t wbox[2] = {SW_BK, 128};
+    rc = make_tmap(&P.tmB, weight, 2, wdims, wbox, CU_TENSOR_MAP_SWIZZLE_64B, f16);
+    if (rc) return rc;
+    ConvParams& q = P.p;
+    q.bn = 128;
+    q.n_blocks_n = 1;
+    q.kb_per_tap = cin_used / SW_BK;
+    q.num_kb = 3 * q.kb_per_tap;
+    q.a_stage_bytes = SW_W * (SW_H + 2) * SW_BK * 2;  // pixel box (MMA B operand)
+    q.b_stage_bytes = 3 * 128 * SW_BK * 2;              // three weight slices (MMA A operand)
+    q.bres_bytes = 0;
+    q.stage_bytes = 0;
+    q.halo = 0;
+    q.sub = 1;
+    q.rect = pool ? 1 : 0;
+    q.tiles_x = (res + SW_W - 1) / SW_W;
+    q.tiles_y = (res + SW_H - 1) / SW_H;
+    q.tmem_cols = 512;
+    q.idesc = tp::idesc_f16kind(128, 256, !f16);
+    const uint32_t sb = q.a_stage_bytes + q.b_stage_bytes;
+    int st = (int)((227 * 1024 - fixed) / (int)sb);
+    if (st > 8) st = 8;
+    if (st >= 2) {
+      q.stages = st;
+      P.smem = 1024 + (size_t)st * sb + (2 * st + 6) * 8 + cout_pad * 4 + 16;
+      P.swap = 1;
+      P.prect = 0;
+      P.pair = 0;
+      *L = P;
+    }
+  }
   // full-halo box kernel (TP_BOX=0 disables it): 3x3, one K block, resident weights
   const char* be = getenv("TP_BOX");
   const bool box_ok = ksize == 3 && (cin_used == 32 || cin_used == 64) && cout_pad <= 256 &&
@@ -2465,6 +2732,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       L->box_bk = bk;
       L->pair = 0;
       L->prect = 0;
+      L->swap = 0;
       if (staging) {  // output store map {cstride, res, rows}, box {32 ch, 8 px, 4 rows}
         const uint64_t dims[3] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)max_img * res};
         const uint32_t box[3] = {32, BOX_TW, 4};
@@ -2579,6 +2847,25 @@ int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, c
   return TP_OK;
 }
 
+template <bool POOL>
+int launch_swap(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_swap_kernel<POOL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  ConvParams p = L.p;
+  p.n_img = n_img;
+  p.n_img_dev = n_img_dev;
+  const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y * p.n_blocks_n;
+  if (tiles == 0) return TP_OK;
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  conv_swap_kernel<POOL><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+  TP_LAUNCH_CHECK();
+  return TP_OK;
+}
+
 int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
   if (n_img > L.p.n_img) {
     tp_set_error("conv: n_img %d exceeds planned %d", n_img, L.p.n_img);
@@ -2594,6 +2881,9 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
            : epi == BOX_POOL ? launch_box<32, BOX_POOL>(L, n_img, n_img_dev, st)
                              : launch_box<32, BOX_PLAIN>(L, n_img, n_img_dev, st);
   }
+  if (L.swap)
+    return L.p.rect ? launch_swap<true>(L, n_img, n_img_dev, st)
+                    : launch_swap<false>(L, n_img, n_img_dev, st);
   if (L.prect) {
     const bool pool = L.p.rect != 0;
     if (L.p.sub == 2)
@@ -2838,14 +3128,14 @@ extern "C" int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int
 }
 
 // Kernel chosen for conv slot `conv` of the plan: 0 conv_tc_kernel, 1 conv_pair_kernel,
-// 2 conv_l0_kernel, 3 conv_box_kernel, 4 conv_pair_rect_kernel.
+// 2 conv_l0_kernel, 3 conv_box_kernel, 4 conv_pair_rect_kernel, 5 conv_swap_kernel.
 extern "C" int tp_yolo_layer_kernel(tp_yolo_net* net, int conv) {
   if (net == nullptr || conv < 0 || conv >= 23) {
     tp_set_error("tp_yolo_layer_kernel: bad conv slot %d", conv);
     return -1;
   }
   const ConvLaunch& L = net->convs[conv];
-  return L.box ? 3 : L.l0 ? 2 : L.pair ? 1 : L.prect ? 4 : 0;
+  return L.box ? 3 : L.l0 ? 2 : L.pair ? 1 : L.prect ? 4 : L.swap ? 5 : 0;
 }
 
 extern "C" int tp_yolo_destroy(tp_yolo_net* net) {

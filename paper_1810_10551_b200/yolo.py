@@ -206,7 +206,7 @@ class YoloNet:
         return int(p.value), r.value, c.value
 
     KERNEL_NAMES = ("conv_tc_kernel", "conv_pair_kernel", "conv_l0_kernel", "conv_box_kernel",
-                    "conv_pair_rect_kernel")
+                    "conv_pair_rect_kernel", "conv_swap_kernel")
 
     def layer_kernels(self) -> list[str]:
         """Kernel the plan chose for each of the 23 conv slots."""
