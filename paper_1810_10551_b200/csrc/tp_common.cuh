@@ -138,6 +138,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// tcgen05.wait::ld that also pins the loaded registers: the compiler cannot schedule a
+// use of v[] above the wait (the registers are written asynchronously by tcgen05.ld)
+template <int N>
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&v)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(v[i]));
+}
 
 // UMMA shared-memory matrix descriptor (sm_100 "version 1" format).
 //   layout: 0 none, 2 SW128, 4 SW64, 6 SW32. lbo/sbo in bytes.

@@ -1245,18 +1245,45 @@ __global__ void __launch_bounds__(kThreads, 1)
 // warp-contiguous 64-byte run per 16-bit plane (hi and lo planes in the parity plan) and
 // pools 2 x 2 inside a thread (columns x, x+1 of rows y, y+1).
 constexpr int SW_BK = 32, SW_W = 16, SW_H = 16;
+constexpr int SW_STAGING = 8 * 2 * 2048;  // unpooled epilogue: 2 slabs of 16 px x 128 B per warp
+
+// 16 TMEM lanes x 16 columns in the mma-fragment layout: thread t holds lane t/4 (v0, v1;
+// v4, v5) and lane t/4 + 8 (v2, v3; v6, v7), columns 2(t%4), 2(t%4)+1 (+8 for v4..v7)
+__device__ __forceinline__ void tmem_ld_16x256b_x2(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+// four 8x8 b16 fragments stored transposed: smem row j (address from thread 8m + j for
+// matrix m) receives column j of fragment m
+__device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t r0, uint32_t r1,
+                                                  uint32_t r2, uint32_t r3) {
+  asm volatile("stmatrix.sync.aligned.x4.trans.m8n8.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
+               "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const void* tmap, const void* smem_src, int32_t c0,
+                                             int32_t c1, int32_t c2, int32_t c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(tp::smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 
 template <bool POOL>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const ConvParams p) {
+                     const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int S = p.stages;
   uint8_t* smX = smem;                                   // pixel boxes (B operand)
   uint8_t* smW = smem + (size_t)S * p.a_stage_bytes;     // weight slices (A operand)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smW + (size_t)S * p.b_stage_bytes);
+  uint8_t* smC = smW + (size_t)S * p.b_stage_bytes;    // unpooled: output staging slabs
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smC + p.stage_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* tfull = bars + 2 * S;
@@ -1424,21 +1451,63 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
-        uint32_t v[16];
-        tp::tmem_ld16(t_row, v);
-        for (int r = 0; r < SW_H; ++r) {
-          tp::tmem_ld_wait();
-          float f[16];
+        // unpooled (parity plan): per output row, the warp's 32 channels x 16 pixels leave
+        // through a 16 x 128 B smem slab (SW128) written transposed by stmatrix, then one TMA
+        // store (out-of-image pixels are clipped by the tensor map). Fragment rows =
+        // channels, columns = pixels (tcgen05.ld 16x256b), so stmatrix .trans lands each
+        // pixel's [hi 16 | lo 16] channel groups contiguously.
+        const uint32_t slab0 = tp::smem_u32(smC) + warp * 4096;
+        const int m = (int)lane >> 3, j = (int)lane & 7;  // stmatrix: matrix m, row j
+        const int cq = (int)lane >> 2;                     // fragment row (channel) of this thread
+        float bq[2][2];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) f[j] = __uint_as_float(v[j]);
-          if (r + 1 < SW_H) tp::tmem_ld16(t_row + (uint32_t)((r + 1) * 16), v);
-          const int y = y0 + r;
-          if (!live || y >= ores) continue;
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (x0 + j < ores) put(y, x0 + j, f[j]);
+        for (int h = 0; h < 2; ++h) {
+          bq[h][0] = bias_s[nb * 128 + (int)q * 32 + 16 * h + cq];
+          bq[h][1] = bias_s[nb * 128 + (int)q * 32 + 16 * h + cq + 8];
         }
-        tp::tmem_ld_wait();
+#pragma unroll 1
+        for (int r = 0; r < SW_H; ++r) {
+          const uint32_t slab = slab0 + (uint32_t)(r & 1) * 2048;
+          if (lane == 0) bulk_wait_read0();  // the slab ring is not trusted with read1 (see DESIGN)
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // channels 16h .. 16h+15 of the warp
+            uint32_t v[8];
+            tmem_ld_16x256b_x2(t_row + ((uint32_t)(16 * h) << 16) + (uint32_t)(r * 16), v);
+            tp::tmem_ld_wait_regs(v);
+#pragma unroll
+            for (int cg = 0; cg < 2; ++cg) {  // pixels 8cg .. 8cg+7
+              uint32_t hi[2], lo[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {  // e: channel cq (+8)
+                float a = __uint_as_float(v[4 * cg + 2 * e]) + bq[h][e];
+                float b = __uint_as_float(v[4 * cg + 2 * e + 1]) + bq[h][e];
+                if (leaky) {
+                  a = fmaxf(a, 0.1f * a);
+                  b = fmaxf(b, 0.1f * b);
+                }
+                const __half2 hh = __floats2half2_rn(a, b);
+                hi[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+                lo[e] = *reinterpret_cast<const uint32_t*>(&ll);
+              }
+              // matrices: 0 hi ch 0-7, 1 hi ch 8-15, 2 lo ch 0-7, 3 lo ch 8-15 of this half
+              // -> 16-byte chunk 4h + m of the pixel's 128-byte row
+              const int pix = 8 * cg + j;
+              const uint32_t addr = slab + (uint32_t)(pix * 128) +
+                                    (uint32_t)((((4 * h + m) ^ (pix & 7)) & 7) * 16);
+              stmatrix_x4_trans(addr, hi[0], hi[1], lo[0], lo[1]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && live && y0 + r < ores) {
+            tma_store_4d(&tmC, smC + (slab - tp::smem_u32(smC)),
+                         p.out_coff + 64 * (nb * 4 + (int)q), x0, y0 + r, img);
+            bulk_commit();
+          }
+        }
       }
       tp::tc_fence_before();
       __syncwarp();
@@ -1446,6 +1515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (!POOL && warp < kEpiWarps && lane == 0) bulk_wait_all();
   tp::tc_fence_before();
   __syncthreads();
   tp::tc_fence_after();
@@ -2625,15 +2695,13 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       *L = P;
     }
   }
-  // swapped-operand kernel for pooled 3x3 layers with 128 output channels whose weights are
-  // not resident (TP_SWAP=0 disables it; the box kernel below still wins where it applies).
-  // TP_SWAP=2 also takes unpooled ones: measured slower than the im2col pair kernel on
-  // parity layer 4 (1.09 vs 0.84 ms per 120 tiles: the 4x larger channel-major output
-  // makes the epilogue, not the tensor pipe, the bound)
+  // swapped-operand kernel for 3x3 layers with 128 output channels whose weights are not
+  // resident — pooled ones, and unpooled ones of the parity plan (their hi/lo output
+  // leaves through stmatrix + TMA stores). TP_SWAP=0 disables it; the box kernel below
+  // still wins where it applies.
   const char* sw = getenv("TP_SWAP");
-  const int swap_mode = sw == nullptr ? 1 : atoi(sw);
   if (ksize == 3 && cout_pad == 128 && cout == 128 && cin_used % SW_BK == 0 && !halo &&
-      !out_fp32 && !reorg && (swap_mode == 2 || (swap_mode == 1 && pool))) {
+      !out_fp32 && !reorg && (pool || split) && (sw == nullptr || atoi(sw) != 0)) {
     ConvLaunch P = *L;
     const uint64_t xdims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
     const uint32_t xbox[4] = {SW_BK, SW_W, SW_H + 2, 1};
@@ -2651,20 +2719,27 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     q.a_stage_bytes = SW_W * (SW_H + 2) * SW_BK * 2;  // pixel box (MMA B operand)
     q.b_stage_bytes = 3 * 128 * SW_BK * 2;              // three weight slices (MMA A operand)
     q.bres_bytes = 0;
-    q.stage_bytes = 0;
+    q.stage_bytes = pool ? 0 : SW_STAGING;
     q.halo = 0;
     q.sub = 1;
     q.rect = pool ? 1 : 0;
+    if (!pool) {  // store map {stored channels, x, y, image}, box = 16 px x 128 B of one row
+      const uint64_t cdims[4] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)res,
+                                 (uint64_t)max_img};
+      const uint32_t cbox[4] = {64, SW_W, 1, 1};
+      rc = make_tmap(&P.tmC, out, 4, cdims, cbox, CU_TENSOR_MAP_SWIZZLE_128B, f16);
+      if (rc) return rc;
+    }
     q.tiles_x = (res + SW_W - 1) / SW_W;
     q.tiles_y = (res + SW_H - 1) / SW_H;
     q.tmem_cols = 512;
     q.idesc = tp::idesc_f16kind(128, 256, !f16);
     const uint32_t sb = q.a_stage_bytes + q.b_stage_bytes;
-    int st = (int)((227 * 1024 - fixed) / (int)sb);
+    int st = (int)((227 * 1024 - fixed - (int)q.stage_bytes) / (int)sb);
     if (st > 8) st = 8;
     if (st >= 2) {
       q.stages = st;
-      P.smem = 1024 + (size_t)st * sb + (2 * st + 6) * 8 + cout_pad * 4 + 16;
+      P.smem = 1024 + (size_t)st * sb + q.stage_bytes + (2 * st + 6) * 8 + cout_pad * 4 + 16;
       P.swap = 1;
       P.prect = 0;
       P.pair = 0;
@@ -2861,7 +2936,7 @@ int launch_swap(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y * p.n_blocks_n;
   if (tiles == 0) return TP_OK;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_swap_kernel<POOL><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, p);
+  conv_swap_kernel<POOL><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
