@@ -74,7 +74,8 @@ struct ConvParams {
   int split;
   float alpha;  // layer 0: accumulator scale (1/255 when the input holds integer pixels)
   // profiling only (TP_CONV_DEBUG bits): 1 skip epilogue, 2 skip MMAs, 4 skip stores,
-  // 8 skip TMEM loads, 16 no TMA (stale operands), 32 role cycle counters (g_conv_prof)
+  // 8 skip TMEM loads, 16 no TMA (stale operands), 32 role cycle counters (g_conv_prof),
+  // 64 unmerged pool-in-M MMAs (box kernel A/B)
   int dbg;
 };
 
@@ -1936,24 +1937,61 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t ad = a_desc0 + (uint64_t)(s * a_step);
       const uint32_t d0 = tmem_base + (uint32_t)(acc * NACC * N);
       if (tp::elect_one() && (p.dbg & 2) == 0) {
+        if (PM && (p.dbg & 64)) {  // profiling: unmerged pool-in-M (6 N-wide MMAs per row)
 #pragma unroll
-        for (int pp = 0; pp < NACC; ++pp) {
-          const uint32_t d = d0 + (uint32_t)(pp * N);
+          for (int pp = 0; pp < NACC; ++pp) {
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+              const int dy = tap / 3, dx = tap % 3;
+              const int sy = (pp >> 1) + dy, sx = (pp & 1) + dx;
+              const int plane = ((sy + 1) & 1) * 2 + ((sx + 1) & 1);
+              const uint32_t off = plane * plane16 + (((sy >> 1) * PLANE_W + (sx >> 1)) * RB >> 4);
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                tp::mma_bf16(d0 + (uint32_t)(pp * N), ad + off + 2 * k, b_desc0 + tap * bch + 2 * k,
+                             idesc, (tap | k) != 0);
+            }
+          }
+        } else if (PM) {
+          // The two x pool positions of a pooled row share input columns: sample column
+          // sx = px + dx in {0..3}; sx = 1 and 2 serve (px 0, dx sx) and (px 1, dx sx-1)
+          // with ONE A operand, so one N = 2N MMA against the adjacent weight chunks
+          // [W(dy, sx-1); W(dy, sx)] fills both accumulators of the pair: columns [0, N) =
+          // px 1, [N, 2N) = px 0 (the pooling epilogue takes a max over all four, so the
+          // accumulator order is free). sx = 0 / 3 are single N MMAs. Per pooled row: 2
+          // MMAs at N = 2N + 2 at N instead of 6 at N (N = 64: 224 vs 288 cycles).
+          const uint32_t idesc2 = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(2 * N) >> 3 << 17);
+#pragma unroll
+          for (int py = 0; py < 2; ++py) {
+            const uint32_t dpair = d0 + (uint32_t)(2 * py * N);  // [px 1 | px 0]
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy) {
+              const int sy = py + dy;
+#pragma unroll
+              for (int o = 0; o < 4; ++o) {
+                const int sx = o == 0 ? 1 : o == 1 ? 2 : o == 2 ? 0 : 3;  // merged ones first
+                const int plane = ((sy + 1) & 1) * 2 + ((sx + 1) & 1);
+                const uint32_t off = plane * plane16 + (((sy >> 1) * PLANE_W + (sx >> 1)) * RB >> 4);
+                // weights: merged -> chunks (dy, sx-1), (dy, sx); sx = 0 -> (dy, 0) into
+                // px 0; sx = 3 -> (dy, 2) into px 1
+                const int chunk = 3 * dy + (o < 2 ? sx - 1 : o == 2 ? 0 : 2);
+                const uint32_t d = o == 2 ? dpair + (uint32_t)N : dpair;
+                const uint32_t id = o < 2 ? idesc2 : idesc;
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  tp::mma_bf16(d, ad + off + 2 * k, b_desc0 + chunk * bch + 2 * k, id,
+                               (dy | o | k) != 0);
+              }
+            }
+          }
+        } else {
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const int dy = tap / 3, dx = tap % 3;
-            uint32_t off;
-            if (PM) {
-              const int sy = (pp >> 1) + dy, sx = (pp & 1) + dx;
-              const int plane = ((sy + 1) & 1) * 2 + ((sx + 1) & 1);
-              off = plane * plane16 + (((sy >> 1) * PLANE_W + (sx >> 1)) * RB >> 4);
-            } else {
-              off = (dy * (BOX_TW + 2) + dx) * RB >> 4;
-            }
+            const uint32_t off = (dy * (BOX_TW + 2) + dx) * RB >> 4;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              tp::mma_bf16(d, ad + off + 2 * k, b_desc0 + tap * bch + 2 * k, idesc,
-                           (tap | k) != 0);
+              tp::mma_bf16(d0, ad + off + 2 * k, b_desc0 + tap * bch + 2 * k, idesc, (tap | k) != 0);
           }
         }
       }
