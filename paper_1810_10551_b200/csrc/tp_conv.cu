@@ -1469,18 +1469,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
         for (int r = 0; r < SW_H; ++r) {
           const uint32_t slab = slab0 + (uint32_t)(r & 1) * 2048;
-          if (lane == 0) bulk_wait_read0();  // the slab ring is not trusted with read1 (see DESIGN)
-          __syncwarp();
+          // TMEM -> registers -> hi/lo pairs first: this overlaps the previous row's TMA
+          // store, which must finish reading its slab before the stmatrix writes below
+          uint32_t hs[2][2][2], ls[2][2][2];  // [half h][pixel group cg][channel cq (+8)]
 #pragma unroll
           for (int h = 0; h < 2; ++h) {  // channels 16h .. 16h+15 of the warp
             uint32_t v[8];
             tmem_ld_16x256b_x2(t_row + ((uint32_t)(16 * h) << 16) + (uint32_t)(r * 16), v);
             tp::tmem_ld_wait_regs(v);
 #pragma unroll
-            for (int cg = 0; cg < 2; ++cg) {  // pixels 8cg .. 8cg+7
-              uint32_t hi[2], lo[2];
+            for (int cg = 0; cg < 2; ++cg)  // pixels 8cg .. 8cg+7
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {  // e: channel cq (+8)
+              for (int e = 0; e < 2; ++e) {
                 float a = __uint_as_float(v[4 * cg + 2 * e]) + bq[h][e];
                 float b = __uint_as_float(v[4 * cg + 2 * e + 1]) + bq[h][e];
                 if (leaky) {
@@ -1488,19 +1488,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                   b = fmaxf(b, 0.1f * b);
                 }
                 const __half2 hh = __floats2half2_rn(a, b);
-                hi[e] = *reinterpret_cast<const uint32_t*>(&hh);
+                hs[h][cg][e] = *reinterpret_cast<const uint32_t*>(&hh);
                 const float2 hf = __half22float2(hh);
                 const __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
-                lo[e] = *reinterpret_cast<const uint32_t*>(&ll);
+                ls[h][cg][e] = *reinterpret_cast<const uint32_t*>(&ll);
               }
+          }
+          if (lane == 0) bulk_wait_read0();  // the slab ring is not trusted with read1 (see DESIGN)
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int cg = 0; cg < 2; ++cg) {
               // matrices: 0 hi ch 0-7, 1 hi ch 8-15, 2 lo ch 0-7, 3 lo ch 8-15 of this half
               // -> 16-byte chunk 4h + m of the pixel's 128-byte row
               const int pix = 8 * cg + j;
               const uint32_t addr = slab + (uint32_t)(pix * 128) +
                                     (uint32_t)((((4 * h + m) ^ (pix & 7)) & 7) * 16);
-              stmatrix_x4_trans(addr, hi[0], hi[1], lo[0], lo[1]);
+              stmatrix_x4_trans(addr, hs[h][cg][0], hs[h][cg][1], ls[h][cg][0], ls[h][cg][1]);
             }
-          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && live && y0 + r < ores) {
