@@ -63,7 +63,7 @@ def test_input_normalisation_matches_oracle(cuda, net, tiles):
     assert x[..., [3, 7]].abs().max().item() == 0 and x[:, :, 609].abs().max().item() == 0
 
 
-def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
+def _check_layers(cuda, net, tiles):
     torch = cuda
     torch.backends.cudnn.allow_tf32 = False
     n = _run(cuda, net, tiles)
@@ -113,7 +113,22 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
         # left is fp32 accumulation order over K up to 23040 (measured <= 2.3e-5)
         tol = 5e-5 if net.dtype == "fp32" else 1e-2
         assert err < tol, f"layer {yolo.LAYERS[li][0]}: rel err {err}"
-    print("worst per-layer rel err", worst)
+    return worst
+
+
+def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
+    print("worst per-layer rel err", _check_layers(cuda, net, tiles))
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+def test_each_conv_layer_many_tiles(cuda, dtype):
+    """40 tiles: every persistent CTA / CTA pair runs several tiles on each TMEM
+    accumulator buffer and reuses its epilogue staging slabs (the 3-tile test gives the
+    19^2-38^2 layers at most one tile per cluster)."""
+    rng = np.random.default_rng(21)
+    tiles = rng.integers(0, 256, (40, 608, 608, 3), np.uint8)
+    net = yolo.YoloNet(40, seed=0, dtype=dtype)
+    print("worst per-layer rel err (40 tiles)", _check_layers(cuda, net, tiles))
 
 
 def test_head_matches_cpu_oracle(cuda, net, tiles):
