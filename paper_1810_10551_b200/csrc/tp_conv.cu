@@ -1468,6 +1468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll 1
         for (int r = 0; r < SW_H; ++r) {
+          // rows below the image are neither staged nor stored: a staged row without a
+          // committed store would let wait_group.read 1 pass while the store two slabs back
+          // is still reading
+          if (!live || y0 + r >= ores) break;
           const uint32_t slab = slab0 + (uint32_t)(r & 1) * 2048;
           // TMEM -> registers -> hi/lo pairs first: this overlaps the previous row's TMA
           // store, which must finish reading its slab before the stmatrix writes below
@@ -1494,7 +1498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ls[h][cg][e] = *reinterpret_cast<const uint32_t*>(&ll);
               }
           }
-          if (lane == 0) bulk_wait_read0();  // the slab ring is not trusted with read1 (see DESIGN)
+          if (lane == 0) bulk_wait_read1();  // the store two rows back has read this slab
           __syncwarp();
 #pragma unroll
           for (int h = 0; h < 2; ++h)
@@ -1509,7 +1513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0 && live && y0 + r < ores) {
+          if (lane == 0) {
             tma_store_4d(&tmC, smC + (slab - tp::smem_u32(smC)),
                          p.out_coff + 64 * (nb * 4 + (int)q), x0, y0 + r, img);
             bulk_commit();
