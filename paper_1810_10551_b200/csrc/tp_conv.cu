@@ -1245,7 +1245,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 // channel, column = pixel), so the epilogue stores each pixel's channels as one
 // warp-contiguous 64-byte run per 16-bit plane (hi and lo planes in the parity plan) and
 // pools 2 x 2 inside a thread (columns x, x+1 of rows y, y+1).
-constexpr int SW_BK = 32, SW_W = 16, SW_H = 16;
+// The SW_CL CTAs of a cluster take consecutive pixel blocks and share the weights: each
+// loads 1/SW_CL of every weight slice and multicasts it to all, so a stage brings 18 KB of
+// pixels + 24/SW_CL KB of weights per CTA instead of 18 + 24 (the L2 -> SM fill rate,
+// ~55 B/clk per SM unshared, held the MMA issuer on `full` 16-38% of the time).
+constexpr int SW_BK = 32, SW_W = 16, SW_H = 16, SW_CL = 2;  // 4-CTA clusters: not all co-resident (1.7x slower)
 constexpr int SW_STAGING = 8 * 2 * 2048;  // unpooled epilogue: 2 slabs of 16 px x 128 B per warp
 
 // 16 TMEM lanes x 16 columns in the mma-fragment layout: thread t holds lane t/4 (v0, v1;
@@ -1263,6 +1267,23 @@ __device__ __forceinline__ void stmatrix_x4_trans(uint32_t addr, uint32_t r0, ui
   asm volatile("stmatrix.sync.aligned.x4.trans.m8n8.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(addr),
                "r"(r0), "r"(r1), "r"(r2), "r"(r3)
                : "memory");
+}
+// 2-D box multicast to every CTA in cta_mask (same smem offset and barrier offset in each)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* tmap, uint64_t* bar,
+                                               int32_t c0, int32_t c1, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(tp::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(tp::smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
+      : "memory");
+}
+// single-CTA MMA completion arriving on the same barrier in every CTA of cta_mask
+__device__ __forceinline__ void commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(tp::smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
 }
 __device__ __forceinline__ void tma_store_4d(const void* tmap, const void* smem_src, int32_t c0,
                                              int32_t c1, int32_t c2, int32_t c3) {
@@ -1300,7 +1321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tp::tma_prefetch(&tmB);
     for (int i = 0; i < S; ++i) {
       tp::mbar_init(&full[i], 1);
-      tp::mbar_init(&empty[i], 1);
+      tp::mbar_init(&empty[i], SW_CL);  // every CTA's MMAs must have drained the stage
     }
     for (int a = 0; a < 2; ++a) {
       tp::mbar_init(&tfull[a], 1);
@@ -1311,18 +1332,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, 512);
   for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
   tp::tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // the peer's barriers are initialised before any multicast lands
   tp::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const uint32_t rank = cluster_rank();
 
   const int n_img = p.n_img_dev != nullptr ? min(*p.n_img_dev, p.n_img) : p.n_img;
   const int per_img = p.tiles_x * p.tiles_y;
   const int total_tiles = n_img * per_img * p.n_blocks_n;
-  const int n_tiles = (int)blockIdx.x < total_tiles
-                          ? (total_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x
-                          : 0;
+  // the CTAs of a cluster run the same number of tiles (they feed each other's weight
+  // stages): tile group j of cluster c = tiles SW_CL (c + j * clusters) + rank; a CTA whose
+  // tile is past the end recomputes the last tile and stores nothing
+  const int n_clusters = (int)gridDim.x / SW_CL, cid = (int)blockIdx.x / SW_CL;
+  const int total_groups = (total_tiles + SW_CL - 1) / SW_CL;
+  const int n_tiles = cid < total_groups ? (total_groups - cid + n_clusters - 1) / n_clusters : 0;
   auto tile_at = [&](int i, int& img, int& y0, int& x0, int& nb) {
-    const int t = (int)blockIdx.x + i * (int)gridDim.x;
+    const int t = min(SW_CL * (cid + i * n_clusters) + (int)rank, total_tiles - 1);
     const int mt = t / p.n_blocks_n;
     nb = t - mt * p.n_blocks_n;
     img = mt / per_img;
@@ -1347,11 +1372,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int cb = kb - (dx + 1) * p.kb_per_tap;
           tma_load_4d(smX + (size_t)s * p.a_stage_bytes, &tmA, &full[s], cb * SW_BK, x0 + dx,
                       y0 - 1, img);
-          uint8_t* wdst = smW + (size_t)s * p.b_stage_bytes;
+          // this CTA's 128 / SW_CL output channels of each tap's slice, to every CTA
+          uint8_t* wdst = smW + (size_t)s * p.b_stage_bytes + rank * (w_slice / SW_CL);
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy)
-            tp::tma_load_2d(wdst + dy * w_slice, &tmB, &full[s],
-                            (dy * 3 + dx + 1) * p.cin + cb * SW_BK, nb * 128);
+            tma_load_2d_mc(wdst + dy * w_slice, &tmB, &full[s],
+                           (dy * 3 + dx + 1) * p.cin + cb * SW_BK,
+                           nb * 128 + (128 / SW_CL) * (int)rank, (uint16_t)((1 << SW_CL) - 1));
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -1369,14 +1396,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     uint32_t aph[2] = {0, 0};
+    long long w_te = 0, w_fu = 0;
+    PROF_T0(m_start);
     for (int i = 0; i < n_tiles; ++i) {
       const int acc = i & 1;
+      PROF_T0(t1);
       tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+      PROF_ADD(w_te, t1);
       aph[acc] ^= 1;
       tp::tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
       for (int kb = 0; kb < p.num_kb; ++kb) {
+        PROF_T0(t2);
         tp::mbar_wait(&full[s], ph);
+        PROF_ADD(w_fu, t2);
         tp::tc_fence_after();
         const uint64_t xd = x_desc0 + (uint64_t)(s * x_step);
         const uint64_t wd = w_desc0 + (uint64_t)(s * w_step);
@@ -1387,7 +1420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < SW_BK / 16; ++k)
               tp::mma_bf16(d_tmem, wd + dy * w_slice16 + 2 * k, xd + dy * x_row16 + 2 * k, p.idesc,
                            (kb | dy | k) != 0);
-          tp::mma_commit(&empty[s]);
+          commit_mc(&empty[s], (uint16_t)((1 << SW_CL) - 1));  // frees it for every producer
         }
         __syncwarp();
         if (++s == S) {
@@ -1397,6 +1430,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (tp::elect_one()) tp::mma_commit(&tfull[acc]);
       __syncwarp();
+    }
+    if ((p.dbg & 32) && lane == 0) {
+      atomicAdd(&g_conv_prof[2], (unsigned long long)(clock64() - m_start));
+      atomicAdd(&g_conv_prof[3], (unsigned long long)w_te);
+      atomicAdd(&g_conv_prof[4], (unsigned long long)w_fu);
+      if (blockIdx.x == 0) atomicAdd(&g_conv_prof[7], 1ull);
     }
   } else {
     // epilogue: group g takes tiles i % 2 == g; warp q owns output channels q*32 .. q*32+31
@@ -1410,7 +1449,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int img, y0, x0, nb;
       tile_at(i, img, y0, x0, nb);
       const int co = nb * 128 + (int)(q * 32 + lane);
-      const bool live = !(p.dbg & 4);  // the plan requires cout == 128
+      // the plan requires cout == 128; a recomputed last tile (odd count) stores nothing
+      const bool live = !(p.dbg & 4) && SW_CL * (cid + i * n_clusters) + (int)rank < total_tiles;
       // stored channel of co: hi/lo planes interleaved per 16 channels in the parity plan
       const int sc = p.out_coff + (spl ? 32 * (co >> 4) + (co & 15) : co);
       const float bco = bias_s[co];
@@ -1528,7 +1568,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (!POOL && warp < kEpiWarps && lane == 0) bulk_wait_all();
   tp::tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while its peer may still signal its barriers
   tp::tc_fence_after();
   if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, 512);
 }
@@ -2756,7 +2796,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     rc = make_tmap(&P.tmA, in, 4, xdims, xbox, CU_TENSOR_MAP_SWIZZLE_64B, f16);
     if (rc) return rc;
     const uint64_t wdims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
-    const uint32_t wbox[2] = {SW_BK, 128};
+    const uint32_t wbox[2] = {SW_BK, 128 / SW_CL};  // each CTA of a cluster loads a share
     rc = make_tmap(&P.tmB, weight, 2, wdims, wbox, CU_TENSOR_MAP_SWIZZLE_64B, f16);
     if (rc) return rc;
     ConvParams& q = P.p;
@@ -2983,9 +3023,22 @@ int launch_swap(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   p.n_img_dev = n_img_dev;
   const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y * p.n_blocks_n;
   if (tiles == 0) return TP_OK;
-  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_swap_kernel<POOL><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
-  TP_LAUNCH_CHECK();
+  const long long groups = (tiles + SW_CL - 1) / SW_CL;
+  const int max_clusters = num_sms() / SW_CL;
+  const int clusters = (int)(groups < max_clusters ? groups : max_clusters);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(SW_CL * clusters, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = L.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = SW_CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_swap_kernel<POOL>, L.tmA, L.tmB, L.tmC, p));
   return TP_OK;
 }
 
