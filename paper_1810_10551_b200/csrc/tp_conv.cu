@@ -1914,8 +1914,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= TMA producer: one box (or 4 parity planes) per tile =================
       if (n_tiles > 0) {
         tp::mbar_arrive_expect_tx(bres_bar, p.bres_bytes);
-        for (int j = 0; j < 9; ++j)
-          tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, j * BK, 0);
+        for (int j = 0; j < p.n_bchunks; ++j) {  // chunk j = (K block j / 9, tap j % 9)
+          const int cb = j / 9, tap = j - cb * 9;
+          tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, tap * p.cin + cb * BK, 0);
+        }
       }
       int s = 0;
       uint32_t ph = 0;
@@ -1923,7 +1925,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int by = r / p.tiles_x, bx = r - by * p.tiles_x;
       long long pr_wait = 0;
       PROF_T0(pr_start);
+      const int nkb = PM ? p.num_kb : 1;
       for (int i = 0; i < n_tiles; ++i) {
+       for (int cb = 0; cb < nkb; ++cb) {  // K blocks of the tile (PM with 64 channels: 2)
         PROF_T0(tw);
         tp::mbar_wait(&empty[s], ph ^ 1);
         PROF_ADD(pr_wait, tw);
@@ -1936,7 +1940,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int ey = b >> 1, ex = b & 1;
-            tma_load_4d(dst + b * (p.a_stage_bytes >> 2), &tmA, &full[s], 0,
+            tma_load_4d(dst + b * (p.a_stage_bytes >> 2), &tmA, &full[s], cb * BK,
                         2 * BOX_TW * bx - ex, 2 * BOX_TH * by - ey, img);
           }
         } else {  // tile + one-pixel halo; the halo outside the image reads as 0
@@ -1946,6 +1950,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           s = 0;
           ph ^= 1;
         }
+       }
         if (++bx == p.tiles_x) {
           bx = 0;
           if (++by == p.tiles_y) {
@@ -1965,7 +1970,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (n_tiles > 0) tp::mbar_wait(bres_bar, 0);  // weights load only if this CTA has tiles
     constexpr uint32_t pitch = (PM ? PLANE_W : BOX_TW + 2) * RB;  // 8-row group pitch
     const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, pitch, LAY);
-    const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 8 * RB, LAY);
+    const uint64_t b_desc_base = tp::umma_desc(tp::smem_u32(smB), 16, 8 * RB, LAY);
     const uint32_t a_step = p.a_stage_bytes >> 4, bch = p.bchunk_bytes >> 4;
     const uint32_t plane16 = (p.a_stage_bytes >> 2) >> 4;
     const uint32_t idesc = p.idesc;
@@ -1980,12 +1985,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::mbar_wait(&tempty[acc], ((aph >> acc) & 1) ^ 1);
       PROF_ADD(w_te, t1);
       aph ^= 1u << acc;
+      const int nkb = PM ? p.num_kb : 1;
+      for (int cb = 0; cb < nkb; ++cb) {
       PROF_T0(t2);
       tp::mbar_wait(&full[s], ph);
       PROF_ADD(w_fu, t2);
       tp::tc_fence_after();
       const uint64_t ad = a_desc0 + (uint64_t)(s * a_step);
       const uint32_t d0 = tmem_base + (uint32_t)(acc * NACC * N);
+      const uint64_t b_desc0 = b_desc_base + (uint64_t)(cb * 9 * bch);  // this K block's taps
       if (tp::elect_one() && (p.dbg & 2) == 0) {
         if (PM && (p.dbg & 64)) {  // profiling: unmerged pool-in-M (6 N-wide MMAs per row)
 #pragma unroll
@@ -1999,7 +2007,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k = 0; k < BK / 16; ++k)
                 tp::mma_bf16(d0 + (uint32_t)(pp * N), ad + off + 2 * k, b_desc0 + tap * bch + 2 * k,
-                             idesc, (tap | k) != 0);
+                             idesc, (cb | tap | k) != 0);
             }
           }
         } else if (PM) {
@@ -2030,7 +2038,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k)
                   tp::mma_bf16(d, ad + off + 2 * k, b_desc0 + chunk * bch + 2 * k, id,
-                               (dy | o | k) != 0);
+                               (cb | dy | o | k) != 0);
               }
             }
           }
@@ -2047,13 +2055,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (tp::elect_one()) {
         tp::mma_commit(&empty[s]);
-        tp::mma_commit(&tfull[acc]);
+        if (cb == nkb - 1) tp::mma_commit(&tfull[acc]);
       }
       __syncwarp();
       if (++s == S) {
         s = 0;
         ph ^= 1;
       }
+      }  // K blocks
     }
     if ((p.dbg & 32) && lane == 0) {
       atomicAdd(&g_conv_prof[2], (unsigned long long)(clock64() - m_start));
@@ -2845,7 +2854,14 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     const bool pm = try_pm && pool && cout_pad <= 64 && (res / 2) % 8 == 0;
     if (try_pm && !pm) continue;
     const int epi = pm ? BOX_POOLM : pool ? BOX_POOL : BOX_PLAIN;
-    const uint32_t rb = (uint32_t)bk * 2;
+    // pool-in-M with 64 input channels (the parity plan's layer 2): four 64-channel planes
+    // plus the resident weights leave room for one stage only, so the planes come in two
+    // 32-channel K blocks (SW64) per tile
+    const int kbk = pm && cin_used == 64 &&
+                    4 * ((PLANE_W * PLANE_H * 128 + 1023) & ~1023) * 2 + (int)bres > 200 * 1024
+                        ? 32 : bk;
+    const CUtensorMapSwizzle kswz = kbk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const uint32_t rb = (uint32_t)kbk * 2;
     const uint32_t stage = pm ? 4 * ((PLANE_W * PLANE_H * rb + 1023) & ~1023u)
                               : ((BOX_TW + 2) * (BOX_TH + 2) * rb + 1023) & ~1023u;
     const uint32_t staging = (!pool && res % 4 == 0) ? 8 * 4096 : 0;  // 2 slabs per warp
@@ -2861,9 +2877,9 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       const uint64_t dims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res,
                                 (uint64_t)max_img};
       if (pm) {
-        const uint32_t box[4] = {(uint32_t)bk, 2 * PLANE_W, 2 * PLANE_H, 1};
+        const uint32_t box[4] = {(uint32_t)kbk, 2 * PLANE_W, 2 * PLANE_H, 1};
         const uint32_t estr[4] = {1, 2, 2, 1};
-        rc = make_tmap(&L->tmA, in, 4, dims, box, swz, f16, 2, estr);
+        rc = make_tmap(&L->tmA, in, 4, dims, box, kswz, f16, 2, estr);
       } else {
         const uint32_t box[4] = {(uint32_t)bk, BOX_TW + 2, BOX_TH + 2, 1};
         rc = make_tmap(&L->tmA, in, 4, dims, box, swz, f16);
@@ -2871,8 +2887,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       if (rc) return rc;
       {
         const uint64_t dims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
-        const uint32_t box[2] = {(uint32_t)bk, (uint32_t)cout_pad};
-        rc = make_tmap(&L->tmB, weight, 2, dims, box, swz, f16);
+        const uint32_t box[2] = {(uint32_t)kbk, (uint32_t)cout_pad};
+        rc = make_tmap(&L->tmB, weight, 2, dims, box, kswz, f16);
         if (rc) return rc;
       }
       p.bn = cout_pad;
@@ -2880,7 +2896,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       p.a_stage_bytes = stage;
       p.b_stage_bytes = 0;
       p.bchunk_bytes = cout_pad * rb;
-      p.n_bchunks = 9;
+      p.num_kb = cin_used / kbk;        // K blocks per tile (stages per tile)
+      p.n_bchunks = 9 * p.num_kb;       // resident weight chunks: [K block][tap]
       p.bres_bytes = (uint32_t)bres;
       p.stage_bytes = staging;
       p.sub = 1;
@@ -2892,7 +2909,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       p.nbuf = nbuf;
       p.stages = st;
       L->box = 1 + epi;
-      L->box_bk = bk;
+      L->box_bk = kbk;
       L->pair = 0;
       L->prect = 0;
       L->swap = 0;
