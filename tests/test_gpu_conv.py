@@ -108,12 +108,16 @@ def test_conv_reorg_and_channel_offset(cuda):
 
 
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
-@pytest.mark.parametrize("cin,cout,res", [(32, 64, 32), (64, 128, 40), (128, 256, 76),
-                                          (64, 128, 152)])
-def test_conv_fused_pool_rect_tiles(cuda, cin, cout, res, dtype):
-    """RECT 16x8 tiles (3-D TMA boxes) + 2x2 max pool in the epilogue, incl. partial tiles."""
+@pytest.mark.parametrize("cin,cout,res,n", [(32, 64, 32, 2), (64, 128, 40, 2), (128, 256, 76, 2),
+                                            (64, 128, 152, 2), (128, 128, 48, 3),
+                                            (128, 128, 152, 5)])
+def test_conv_fused_pool_rect_tiles(cuda, cin, cout, res, n, dtype):
+    """RECT 16x8 tiles (3-D TMA boxes) + 2x2 max pool in the epilogue, incl. partial tiles.
+    cin = cout = 128 runs the swapped-operand kernel in 2-CTA clusters: 3 x 9 blocks of
+    16x16 is an odd count (one CTA recomputes the last block and stores nothing), 5 x 100
+    blocks give every cluster several tiles per accumulator buffer."""
     torch = cuda
-    x = _input(torch, 2, res, cin, seed=res, dtype=dtype)
+    x = _input(torch, n, res, cin, seed=res, dtype=dtype)
     out, ref = _run_conv(torch, x, res, cin, cout, cout, 3, leaky=True, dtype=dtype, pool=True)
     _check(torch, out, ref, rel=2e-2 if dtype == "bf16" else 3e-3)
 
