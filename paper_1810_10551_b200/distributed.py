@@ -45,6 +45,9 @@ def pack_records(rows: list[np.ndarray], max_rows: int, dtype: np.dtype) -> tupl
     return counts, buf
 
 
+_warned = False
+
+
 def nccl_comm(group=None) -> int:
     """The ncclComm_t torch.distributed holds for this rank's device (borrowed, never
     freed here). torch creates communicators lazily; one tiny all-reduce forces it."""
@@ -66,10 +69,29 @@ def nccl_comm(group=None) -> int:
 
 def nccl_all_gather(local_recs, all_recs, local_counts, all_counts, group=None, stream=None):
     """Rank-order all-gather of a padded record slice and its counts in one fused NCCL
-    launch on `stream` (tp_nccl_gather_dets). Shapes: all_* = world x local_*."""
+    launch on `stream` (tp_nccl_gather_dets). Shapes: all_* = world x local_*.
+
+    If this torch build exposes no communicator pointer, the same two all-gathers go
+    through torch.distributed's own NCCL calls (still on the GPU; one warning)."""
+    import torch.distributed as dist
+
     from . import native
 
-    native.call("tp_nccl_gather_dets", nccl_comm(group), native.ptr(local_recs),
+    try:
+        comm = nccl_comm(group)
+    except (RuntimeError, AttributeError) as exc:
+        global _warned
+        if not _warned:
+            import warnings
+
+            warnings.warn(f"tp_nccl_gather_dets unavailable ({exc}); using torch NCCL all-gathers")
+            _warned = True
+        if local_recs is not None:
+            dist.all_gather_into_tensor(all_recs.view(-1), local_recs.reshape(-1), group=group)
+        if local_counts is not None:
+            dist.all_gather_into_tensor(all_counts.view(-1), local_counts.reshape(-1), group=group)
+        return
+    native.call("tp_nccl_gather_dets", comm, native.ptr(local_recs),
                 int(local_recs.numel() * local_recs.element_size()) if local_recs is not None else 0,
                 native.ptr(local_counts), int(local_counts.numel()) if local_counts is not None else 0,
                 native.ptr(all_recs), native.ptr(all_counts), native.stream_handle(stream))
