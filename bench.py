@@ -100,13 +100,7 @@ def torch_device_type_cuda():
 def clip_objects(rank: int = 0, n_frames: int = 300):
     from paper_1810_10551_b200 import synthetic
 
-    objs = []
-    per = max(1, n_frames // len(CLIP))
-    for kind, _ in CLIP:
-        n = per
-        gt = synthetic.generate_scene(synthetic.SceneSpec(kind, W, H, n, seed=rank))
-        objs += [gt[i] for i in range(n)]
-    return objs
+    return synthetic.bench_clip(W, H, n_frames, seed=rank)
 
 
 class ClockSampler:

@@ -117,6 +117,22 @@ def generate_scene(spec: SceneSpec) -> dict[int, list[GroundTruthObject]]:
     return scene
 
 
+CLIP_KINDS = ("sparse", "dense", "mixed")
+
+
+def bench_clip(width: int, height: int, n_frames: int = 300, seed: int = 0
+               ) -> list[list[GroundTruthObject]]:
+    """The measurement clip of BASELINE configs[1]/[3] (SURVEY §8d): n_frames // 3 frames
+    each of a sparse, a dense and a mixed scene (generate_scene, this seed), in that
+    order; clip frame i of the middle third is scene frame i - n_frames // 3, etc."""
+    per = max(1, n_frames // len(CLIP_KINDS))
+    out = []
+    for kind in CLIP_KINDS:
+        gt = generate_scene(SceneSpec(kind, width, height, per, seed=seed))
+        out += [gt[i] for i in range(per)]
+    return out
+
+
 def _boxes(width, height, objects):
     for o in objects:
         x0, y0 = max(0, round(o.rect.x)), max(0, round(o.rect.y))

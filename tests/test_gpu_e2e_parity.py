@@ -1,0 +1,204 @@
+"""End-to-end parity of the B200 pipeline with the CPU reference on the bench workload.
+
+The CPU side is the reference pipeline restated in oracle/pipeline_ref (pinned to
+reference goldens) with the fp32 CPU YOLO v2-608 (oracle/yolo_ref) as its detector;
+the GPU side is the drop-in API (pipeline.run_sequence with YoloB200Detector) and the
+bench's own batched engine run of the whole clip. Contract (BASELINE north star,
+reference pipeline.py:388-457):
+  * attention boxes, active-crop id sets and the final NMS/merge keep-set identical;
+  * boxes and scores within 1e-3 relative (scores) / 1 px rounding (integer boxes);
+  * every threshold-edge / rounding-edge flip is counted and printed; a frame whose
+    inputs hold no edge case must match exactly.
+Workload: BASELINE configs[0] (one dense 4K frame, P1) and a stratified sample of the
+300-frame bench clip (bench.py / synthetic.bench_clip): frames 0, 50 (sparse), 100,
+150 (dense), 200, 250 (mixed), each with its predecessor for the K=2 window.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import e2e as E
+from oracle import pipeline_ref as R
+from paper_1810_10551_b200 import native, pipeline as P, synthetic, yolo
+from paper_1810_10551_b200.engine import MAX_BOXES, MAX_PER_FRAME, AttentionPipelineB200
+
+pytestmark = pytest.mark.gpu
+
+W, H = 3840, 2160
+SAMPLE = (0, 50, 100, 150, 200, 250)
+SETTINGS = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+
+
+@pytest.fixture(scope="module")
+def clip():
+    return synthetic.bench_clip(W, H, 300, seed=0)
+
+
+@pytest.fixture(scope="module")
+def cpu(clip):
+    cache = {}
+
+    def pixels_of(fid):
+        if fid not in cache:
+            cache[fid] = synthetic.render_frame(W, H, clip[fid])
+        return cache[fid]
+    return E.CpuYolo(pixels_of, yolo.COCO_NAMES), pixels_of
+
+
+def _gpu_dets(res):
+    return [((d.rect.x, d.rect.y, d.rect.w, d.rect.h), d.class_label, d.confidence)
+            for d in res.detections]
+
+
+def _check_frame(plan, det, fid, ref, gpu_res, gpu_att, gpu_active, hist_fids, report):
+    """Compare one frame; returns True when it matched (exactly or within flips)."""
+    dets, active, att = ref
+    window = set(hist_fids) | {fid}
+    edges = E.edge_detections(det, window)
+    rounds = E.rounding_edges(plan, det, window)
+    ok_att, n1_att = E.compare_boxes(att, [(b.x, b.y, b.w, b.h) for b in gpu_att.boxes])
+    cmp = E.compare_dets(dets, _gpu_dets(gpu_res))
+    same_active = sorted(active) == sorted(gpu_active)
+    flips = n1_att + cmp["n_1px"]
+    line = (f"frame {fid:3d}: active {len(active):2d} {'==' if same_active else '!='} "
+            f"{len(gpu_active):2d}, dets {cmp['n']:2d}/{len(gpu_res.detections):2d}, "
+            f"score rel {cmp['score_rel']:.2e}, 1px flips {flips}, order flips "
+            f"{cmp['order_flips']}, threshold-edge raw "
+            f"{len(edges)}, rounding-edge raw {len(rounds)}")
+    report.append(line)
+    exact = ok_att and cmp["ok"] and same_active and gpu_res.active_count == len(active)
+    if exact:
+        if flips:
+            assert rounds, f"1-px differences without a rounding edge: {line}"
+        return True
+    # a mismatch must be explained by an edge case in this frame's window
+    assert edges or rounds, f"unexplained mismatch: {line}"
+    report.append(f"  (frame {fid} differs: att {ok_att}, dets {cmp.get('first_diff')}; "
+                  f"edge cases {edges[:3]} {rounds[:3]})")
+    return False
+
+
+def test_config0_dense_frame_matches_cpu_reference(cuda, cpu):
+    """BASELINE configs[0]: one 4K dense frame (seed 0), preset P1, full pipeline."""
+    gt = synthetic.generate_scene(synthetic.SceneSpec("dense", W, H, 1, seed=0))[0]
+    px = synthetic.render_frame(W, H, gt)
+    plan = R.Plan(W, H, 1, 3, 20)
+    det = E.CpuYolo(lambda fid: px, yolo.COCO_NAMES)
+    ref = E.reference_frame(plan, 0, det, [])
+    gdet = yolo.YoloB200Detector()
+    frame = P.Frame(0, W, H, px)
+    res, att = P.evaluate_frame(frame, SETTINGS, gdet)
+    eng = P._engine_for(gdet, SETTINGS, W, H, None)
+    n_act = int(eng.active_counts[0])
+    gpu_active = eng.active_ids[0, :n_act].cpu().tolist()
+    report = []
+    matched = _check_frame(plan, det, 0, ref, res, att, gpu_active, [], report)
+    print("\n".join(report))
+    print(f"config 0: {'exact' if matched else 'differs by counted edge cases'}; "
+          f"{len(det.raw)} CPU YOLO tiles")
+    assert len(ref[0]) > 0 and len(ref[1]) > 8  # a dense frame: many crops, detections
+
+
+def test_bench_clip_sample_matches_cpu_reference(cuda, cpu):
+    """Stratified sample of the bench clip through the drop-in API (run_sequence on
+    [f-1, f]: the K=2 window) vs the CPU reference with the same history."""
+    det, pixels_of = cpu
+    plan = R.Plan(W, H, 1, 3, 20)
+    gdet = yolo.YoloB200Detector()
+    report, exact = [], 0
+    for fid in SAMPLE:
+        hist_fids = [fid - 1] if fid > 0 else []
+        hist = []
+        for h in hist_fids:  # attention of the previous frame (its stage 1 only)
+            det.prefetch(h, plan.att[3])
+            hist.append(R.attention_pass(plan, h, det, 0.3))
+        ref = E.reference_frame(plan, fid, det, hist)
+        frames = [P.Frame(i, W, H, pixels_of(i)) for i in hist_fids + [fid]]
+        eng = P._engine_for(gdet, SETTINGS, W, H, None)
+        out = eng.evaluate_frames(frames, history=())
+        res, att = out[-1]
+        n_act = int(eng.active_counts[len(frames) - 1])
+        gpu_active = eng.active_ids[len(frames) - 1, :n_act].cpu().tolist()
+        # the public generator API gives the same FrameResult as the engine call
+        api = list(P.run_sequence(frames, SETTINGS, gdet))[-1]
+        assert api.detections == res.detections and api.active_count == res.active_count
+        exact += _check_frame(plan, det, fid, ref, res, att, gpu_active, hist_fids, report)
+    print("\n".join(report))
+    n_tiles = len(det.raw)
+    print(f"{exact}/{len(SAMPLE)} frames exact; {n_tiles} CPU YOLO tiles evaluated")
+    assert exact == len(SAMPLE)
+    # raw per-tile detections (608-space local rects, before projection) of every tile
+    # the CPU reference evaluated, through the plugin's batched detect
+    keys = sorted(det.tiles)
+    gpu = gdet.detect_tiles(np.stack([det.tiles[k] for k in keys]))
+    n, box_err, conf_err, flips = 0, 0.0, 0.0, 0
+    for k, g_list in zip(keys, gpu):
+        r_list = list(det.raw[k])
+        for g in g_list:
+            gr = (g.rect.x, g.rect.y, g.rect.w, g.rect.h)
+            cand = [(max(abs(a - b) for a, b in zip(rr, gr)), j)
+                    for j, (rr, lab, c) in enumerate(r_list) if lab == g.class_label]
+            d, j = min(cand) if cand else (1e9, -1)
+            if d / 608 > 1e-3:
+                assert abs(g.confidence - 0.25) < E.EDGE, (k, g)
+                flips += 1
+                continue
+            c = r_list.pop(j)[2]
+            n += 1
+            box_err = max(box_err, d / 608)
+            conf_err = max(conf_err, abs(c - g.confidence) / c)
+        for rr, lab, c in r_list:  # CPU-only detections: threshold edge only
+            assert abs(c - 0.25) < E.EDGE, (k, rr, lab, c)
+            flips += 1
+    print(f"raw detections on {len(keys)} tiles: {n} matched, max box err/608 {box_err:.2e}, "
+          f"max score rel err {conf_err:.2e}, threshold flips {flips}")
+    assert box_err <= 1e-3 and conf_err <= 1e-3
+
+
+def test_bench_engine_run_equals_api_on_sample(cuda, cpu, clip):
+    """The bench's own device path (whole clip in 30-frame batches, frames rendered on
+    the GPU, history carried on device) gives the API's FrameResults at the sampled
+    frames, and over all 300 frames selection / NMS keep-sets are bit-exact given the
+    GPU's own stage-1 boxes and raw stage-2 detections."""
+    det, pixels_of = cpu
+    B = 30
+    eng = AttentionPipelineB200(SETTINGS, W, H, max_frames=B)
+    torch = native.require_cuda()
+    frames = torch.empty((B, H, W, 3), dtype=torch.uint8, device="cuda")
+    plan = R.Plan(W, H, 1, 3, 20)
+    cell_of = R.cell_map(plan)
+    eng.reset_history(())
+    by_fid = {}
+    hist = []
+    n_frames_checked = n_raw = 0
+    for s in range(0, len(clip), B):
+        synthetic.render_frames_device(W, H, clip[s:s + B], out=frames)
+        eng.run_device(B, frames=frames)
+        out = eng.results(list(range(s, s + B)))
+        ids = eng.active_ids[:B].cpu().numpy()
+        cnt = eng.active_counts[:B].cpu().numpy()
+        pc = eng.pcounts[:B].cpu().numpy()
+        raw = eng.pdets.view(-1)[: B * MAX_PER_FRAME * 56].cpu().numpy().view(
+            native.PDET_DTYPE).reshape(B, MAX_PER_FRAME)
+        for j, (res, att) in enumerate(out):
+            boxes = [(b.x, b.y, b.w, b.h) for b in att.boxes]
+            assert len(boxes) <= MAX_BOXES
+            merged = R.merge_temporal(hist + [boxes], 2)
+            act = R.select_active(plan.fin, merged, 20, W, H)
+            assert sorted(ids[j, : cnt[j]].tolist()) == act, f"frame {s + j}"
+            tagged = [(int(r["crop_id"]), ((float(r["x"]), float(r["y"]), float(r["w"]),
+                                            float(r["h"])), yolo.COCO_NAMES[int(r["cls"])],
+                                           float(r["conf"]))) for r in raw[j, : pc[j]]]
+            assert R.finish(tagged, cell_of, 0.3) == _gpu_dets(res), f"frame {s + j}"
+            n_raw += len(tagged)
+            hist = [boxes]
+            by_fid[s + j] = res
+            n_frames_checked += 1
+    print(f"{n_frames_checked} frames: selection and NMS/merge keep-sets bit-exact given the "
+          f"GPU's stage-1 boxes and {n_raw} raw stage-2 detections")
+    gdet = yolo.YoloB200Detector()
+    for fid in SAMPLE:
+        fr = [P.Frame(i, W, H, pixels_of(i)) for i in ([fid - 1] if fid else []) + [fid]]
+        api = list(P.run_sequence(fr, SETTINGS, gdet))[-1]
+        assert api.detections == by_fid[fid].detections, f"frame {fid}"
+        assert api.active_count == by_fid[fid].active_count

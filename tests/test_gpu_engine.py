@@ -150,13 +150,19 @@ def _check_selection_and_nms(engine, out, W, H, n):
     GPU's raw stage-2 detections (last batch of n frames)."""
     plan = R.Plan(W, H, engine.settings.attention.rows, engine.settings.final.rows,
                   engine.settings.final.overlap_px)
-    hist = []
+    hist, acts = [], []
     for res, att in out:
         boxes = [(b.x, b.y, b.w, b.h) for b in att.boxes]
         merged = R.merge_temporal(hist + [boxes], engine.K)
         act = R.select_active(plan.fin, merged, engine.settings.attention_margin_px, W, H)
         assert len(act) == res.active_count
+        acts.append(act)
         hist = (hist + [boxes])[-(engine.K - 1):] if engine.K > 1 else []
+    # the id sets (not just counts) of the last batch, read from the device
+    ids = engine.active_ids[:n].cpu().numpy()
+    cnt = engine.active_counts[:n].cpu().numpy()
+    for f in range(n):
+        assert sorted(ids[f, : cnt[f]].tolist()) == acts[len(acts) - n + f]
     pc = engine.pcounts[:n].cpu().numpy()
     raw = engine.pdets.view(-1)[: n * MAX_PER_FRAME * 56].cpu().numpy().view(
         native.PDET_DTYPE).reshape(n, MAX_PER_FRAME)
