@@ -8,8 +8,21 @@ LIB_DIR := paper_1810_10551_b200/_lib
 SRCS := $(wildcard $(SRC_DIR)/*.cu)
 OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
 LIB := $(LIB_DIR)/libtilepipe_b200.so
+# debug variant: every mbarrier wait is bounded (~2 s at 2 GHz) and traps on timeout
+DBG_OBJS := $(patsubst $(SRC_DIR)/%.cu,build/debug/%.o,$(SRCS))
+DBG_LIB := $(LIB_DIR)/libtilepipe_b200_debug.so
 
 all: $(LIB)
+
+debug: $(DBG_LIB)
+
+build/debug/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/tp_common.cuh include/tilepipe_b200.h
+	@mkdir -p build/debug
+	$(NVCC) $(NVFLAGS) -DTP_MBAR_TIMEOUT_CYCLES=4000000000LL -c $< -o $@ 2> build/debug/$*.ptxas.log || (cat build/debug/$*.ptxas.log; exit 1)
+
+$(DBG_LIB): $(DBG_OBJS)
+	@mkdir -p $(LIB_DIR)
+	$(NVCC) $(ARCH) -shared -o $@ $(DBG_OBJS) -Xcompiler -fvisibility=hidden -ldl
 
 build/%.o: $(SRC_DIR)/%.cu $(SRC_DIR)/tp_common.cuh include/tilepipe_b200.h
 	@mkdir -p build
@@ -20,6 +33,6 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xcompiler -fvisibility=hidden -ldl
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(DBG_LIB)
 
-.PHONY: all clean
+.PHONY: all clean debug

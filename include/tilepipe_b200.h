@@ -171,7 +171,9 @@ TP_API int tp_attention_boxes(const tp_det_t* dets, const int32_t* counts, int m
  * slot-indexed: slot s holds frame (s - (window-1)) of the batch, so slots
  * 0..window-2 carry history. crops: fp64 [n_crops][4]. Outputs per frame:
  * active bitmask words [n_frames][mask_words], sorted active crop ids,
- * counts, and the first-seen-deduplicated merged box list. */
+ * counts, and the first-seen-deduplicated merged box list. max_merged <= 512 (the
+ * kernel's window capacity); a window holding more than 512 boxes reports its true box
+ * count in merged_counts (> max_merged) and must be treated as a failure. */
 TP_API int tp_select_active(const double* boxes, const int32_t* box_counts, int max_boxes,
                      int n_frames, int window, const double* crops, int n_crops,
                      int crop_id_base, double margin, double frame_w, double frame_h,
@@ -208,14 +210,17 @@ TP_API int tp_render_frames(const int32_t* rects, const uint8_t* colors, const i
 /* Crop-parallel stage 2 (replaces the reference's remote dispatch of one
  * frame's tiles, pkg/src/tilepipe/distribution/client.py:82-96). tp_slice_jobs copies rank's
  * contiguous slice of the device job list (sizes differ by <= 1, larger first) and writes
- * its count; tp_unslice_dets maps all-gathered per-rank padded slices ([world][max_slice]
- * tiles of max_per_tile records + counts) back to global job order. */
+ * its count; tp_unslice_dets maps all-gathered per-rank compact slices ([world][max_slice]
+ * tiles of src_per_tile records + the tiles' true counts) back to global job order
+ * (dst_per_tile records per tile). A tile with more than src_per_tile records is clamped
+ * and sets *overflow (may be NULL) — the caller must fail, not use the result. */
 TP_API int tp_slice_jobs(const tp_tile_job_t* jobs, const int32_t* n_jobs_dev, int rank,
                          int world, tp_tile_job_t* out, int32_t* n_out_dev, int max_out,
                          void* stream);
 TP_API int tp_unslice_dets(const tp_det_t* gathered, const int32_t* gathered_counts,
                            int max_slice, const int32_t* n_jobs_dev, int world, int max_jobs,
-                           int max_per_tile, tp_det_t* dets, int32_t* counts, void* stream);
+                           int src_per_tile, int dst_per_tile, tp_det_t* dets, int32_t* counts,
+                           int32_t* overflow, void* stream);
 
 /* Result gather (replaces the reference's collection of worker results,
  * pkg/src/tilepipe/distribution/client.py:176-203 evaluate_remote and :242-377): all-gather

@@ -9,6 +9,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/tilepipe_b200.h"
 
@@ -66,8 +67,32 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Blocking wait on an mbarrier phase. The debug build of the library (make debug ->
+// libtilepipe_b200_debug.so, selected by TP_LIB_VARIANT=debug) defines
+// TP_MBAR_TIMEOUT_CYCLES: a wait that does not complete within that many SM cycles
+// (a pipeline protocol bug: a lost arrive, a wrong expect_tx byte count or parity)
+// prints the barrier and traps, so the launch fails instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
+#ifdef TP_MBAR_TIMEOUT_CYCLES
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (long long)(TP_MBAR_TIMEOUT_CYCLES)) {
+      printf("tp: mbarrier wait timed out (block %d thread %d, smem 0x%x, parity %u)\n",
+             (int)blockIdx.x, (int)threadIdx.x, addr, parity);
+      __trap();
+    }
+  }
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
@@ -75,6 +100,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity)
       : "memory");
+#endif
 }
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {

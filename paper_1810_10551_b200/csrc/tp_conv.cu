@@ -28,6 +28,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "tp_common.cuh"
 #include "../../include/tilepipe_b200.h"
 
@@ -2501,15 +2504,39 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
   return TP_OK;
 }
 
-int g_num_sms = 0;
+// SM count of the current device (cached per device: a process may drive several GPUs)
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
   }
-  return g_num_sms;
+  return cache[dev];
+}
+
+// The 227 KB dynamic-smem opt-in is a per-device function attribute: set it once per
+// (kernel, device), thread-safely (kernels of one signature share a template
+// instantiation here, so the record is keyed by the kernel's address).
+template <typename Kernel>
+int ensure_smem_optin(Kernel kernel) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  const void* key = reinterpret_cast<const void*>(kernel);
+  std::lock_guard<std::mutex> lock(mu);
+  uint64_t& mask = done[key];
+  if (!(mask & bit)) {
+    TP_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+    mask |= bit;
+  }
+  return TP_OK;
 }
 
 // A fully prepared layer launch (tensor maps encoded once).
@@ -2927,12 +2954,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
 
 template <int BK, int EPI>
 int launch_box(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_box_kernel<BK, EPI>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  if (int rc = ensure_smem_optin(conv_box_kernel<BK, EPI>)) return rc;
   ConvParams p = L.p;
   p.n_img = n_img;
   p.n_img_dev = n_img_dev;
@@ -2946,12 +2968,7 @@ int launch_box(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStr
 
 template <int MODE, int EPI>
 int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_tc_kernel<MODE, EPI>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  if (int rc = ensure_smem_optin(conv_tc_kernel<MODE, EPI>)) return rc;
   ConvParams p = L.p;
   p.n_img = n_img;
   p.n_img_dev = n_img_dev;
@@ -2967,12 +2984,7 @@ int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
 
 template <int EPI>
 int launch_pair(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_pair_kernel<EPI>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  if (int rc = ensure_smem_optin(conv_pair_kernel<EPI>)) return rc;
   ConvParams p = L.p;
   p.n_img = n_img;
   p.n_img_dev = n_img_dev;
@@ -2998,12 +3010,7 @@ int launch_pair(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
 
 template <int MH, bool POOL>
 int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_pair_rect_kernel<MH, POOL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  if (int rc = ensure_smem_optin(conv_pair_rect_kernel<MH, POOL>)) return rc;
   ConvParams p = L.p;
   p.n_img = n_img;
   p.n_img_dev = n_img_dev;
@@ -3029,12 +3036,7 @@ int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, c
 
 template <bool POOL>
 int launch_swap(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(conv_swap_kernel<POOL>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    configured = true;
-  }
+  if (int rc = ensure_smem_optin(conv_swap_kernel<POOL>)) return rc;
   ConvParams p = L.p;
   p.n_img = n_img;
   p.n_img_dev = n_img_dev;
@@ -3090,12 +3092,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
            : L.p.split  ? launch_pair<EPI_SPLIT>(L, n_img, n_img_dev, st)
                         : launch_pair<EPI_PLAIN>(L, n_img, n_img_dev, st);
   if (L.l0) {
-    static bool configured = false;
-    if (!configured) {
-      TP_CUDA_CHECK(cudaFuncSetAttribute(conv_l0_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-      configured = true;
-    }
+    if (int rc = ensure_smem_optin(conv_l0_kernel)) return rc;
     ConvParams p = L.p;
     p.n_img = n_img;
     p.n_img_dev = n_img_dev;

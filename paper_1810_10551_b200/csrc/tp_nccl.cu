@@ -21,20 +21,37 @@
 
 namespace {
 
-// nccl.h (2.x) values: ncclUint8 = 1, ncclInt32 = 2, ncclSuccess = 0.
+// nccl.h (2.x) values: ncclUint8 = 1, ncclInt32 = 2, ncclSuccess = 0, ncclInProgress = 7
+// (returned by non-blocking communicators, e.g. TORCH_NCCL_USE_COMM_NONBLOCKING=1).
 constexpr int kNcclUint8 = 1;
 constexpr int kNcclInt32 = 2;
+constexpr int kNcclInProgress = 7;
 
 using AllGatherFn = int (*)(const void*, void*, size_t, int, void*, cudaStream_t);
 using GroupFn = int (*)();
 using ErrorStringFn = const char* (*)(int);
+using AsyncErrorFn = int (*)(void*, int*);
 
 struct NcclApi {
   AllGatherFn all_gather = nullptr;
   GroupFn group_start = nullptr, group_end = nullptr;
   ErrorStringFn error_string = nullptr;
+  AsyncErrorFn async_error = nullptr;
   bool ok = false;
 };
+
+// A non-blocking communicator answers ncclInProgress until the enqueue completes: poll
+// ncclCommGetAsyncError until it settles (success or a real error).
+int settle(const NcclApi& api, void* comm, int rc) {
+  if (rc != kNcclInProgress) return rc;
+  if (api.async_error == nullptr) return rc;
+  int state = kNcclInProgress;
+  while (true) {
+    const int q = api.async_error(comm, &state);
+    if (q != 0) return q;
+    if (state != kNcclInProgress) return state;
+  }
+}
 
 const NcclApi& nccl_api() {
   static NcclApi api;
@@ -48,6 +65,7 @@ const NcclApi& nccl_api() {
     api.group_start = reinterpret_cast<GroupFn>(dlsym(h, "ncclGroupStart"));
     api.group_end = reinterpret_cast<GroupFn>(dlsym(h, "ncclGroupEnd"));
     api.error_string = reinterpret_cast<ErrorStringFn>(dlsym(h, "ncclGetErrorString"));
+    api.async_error = reinterpret_cast<AsyncErrorFn>(dlsym(h, "ncclCommGetAsyncError"));
     api.ok = api.all_gather && api.group_start && api.group_end;
   });
   return api;
@@ -74,12 +92,12 @@ extern "C" int tp_nccl_gather_dets(void* nccl_comm, const void* local_recs,
   }
   cudaStream_t s = (cudaStream_t)stream;
   int rc = api.group_start();
-  if (rc == 0 && rec_bytes_per_rank > 0)
+  if ((rc == 0 || rc == kNcclInProgress) && rec_bytes_per_rank > 0)
     rc = api.all_gather(local_recs, all_recs, (size_t)rec_bytes_per_rank, kNcclUint8, nccl_comm, s);
-  if (rc == 0 && counts_per_rank > 0)
+  if ((rc == 0 || rc == kNcclInProgress) && counts_per_rank > 0)
     rc = api.all_gather(local_counts, all_counts, (size_t)counts_per_rank, kNcclInt32, nccl_comm, s);
-  const int rc_end = api.group_end();
-  if (rc == 0) rc = rc_end;
+  const int rc_end = settle(api, nccl_comm, api.group_end());
+  if (rc == 0 || rc == kNcclInProgress) rc = rc_end;
   if (rc != 0) {
     tp_set_error(api.error_string ? api.error_string(rc) : "tp_nccl_gather_dets: NCCL error");
     return TP_ERR_CUDA;

@@ -16,6 +16,8 @@
 //    pairs whose first index is >= i can have changed, so the rescan starts there —
 //    this returns the same first pair the full restart would.
 // One CTA (512 threads) per frame; all working state in shared memory (<= 2048 entries).
+#include <mutex>
+
 #include "tp_common.cuh"
 #include "../../include/tilepipe_b200.h"
 
@@ -413,12 +415,19 @@ extern "C" int tp_postprocess(const tp_pdet_t* dets, const int32_t* counts, int 
     return TP_ERR_CAPACITY;
   }
   if (n_frames <= 0) return TP_OK;
-  static bool configured = false;
-  if (!configured) {
-    TP_CUDA_CHECK(cudaFuncSetAttribute(postprocess_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSmemBytes));
-    configured = true;
+  {  // dynamic-smem opt-in: a per-device function attribute, set once per device
+    static std::mutex mu;
+    static uint64_t done = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!(done & bit)) {
+      TP_CUDA_CHECK(cudaFuncSetAttribute(postprocess_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSmemBytes));
+      done |= bit;
+    }
   }
   postprocess_kernel<<<n_frames, NT, kSmemBytes, (cudaStream_t)stream>>>(
       dets, counts, max_per_frame, *policy, out, out_counts, keep_idx, keep_counts);

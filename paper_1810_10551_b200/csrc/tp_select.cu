@@ -30,13 +30,14 @@ __global__ void __launch_bounds__(256) select_kernel(
   __shared__ unsigned char keep[MAX_IN];
   __shared__ double dx1[MAX_IN], dy1[MAX_IN], dw[MAX_IN], dh[MAX_IN];
   __shared__ int warp_tot[8];
-  __shared__ int n_in_s, n_kept_s;
+  __shared__ int n_in_s, n_kept_s, n_total_s;
   const int f = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
 
   if (tid == 0) {
     int n = 0;
     for (int s = 0; s < window; ++s) n += min(box_counts[f + s], max_boxes);
+    n_total_s = n;
     n_in_s = min(n, MAX_IN);
   }
   __syncthreads();
@@ -139,7 +140,9 @@ __global__ void __launch_bounds__(256) select_kernel(
     }
     if (lane == 0) {
       active_counts[f] = n;
-      merged_counts[f] = n_kept;
+      // a window holding more than MAX_IN boxes was truncated: report its true size
+      // (> MAX_IN >= max_merged) so the host raises instead of using the partial result
+      merged_counts[f] = n_total_s > MAX_IN ? n_total_s : n_kept;
     }
   }
 }
@@ -192,8 +195,8 @@ extern "C" int tp_select_active(const double* boxes, const int32_t* box_counts, 
   if (boxes == nullptr || box_counts == nullptr || crops == nullptr || active_mask == nullptr ||
       active_ids == nullptr || active_counts == nullptr || merged == nullptr ||
       merged_counts == nullptr || window < 1 || n_crops < 1 || n_crops > MAX_CROPS ||
-      mask_words < (n_crops + 31) / 32 || margin < 0) {
-    tp_set_error("tp_select_active: bad argument");
+      mask_words < (n_crops + 31) / 32 || margin < 0 || max_merged < 1 || max_merged > MAX_IN) {
+    tp_set_error("tp_select_active: bad argument (max_merged must be 1..%d)", MAX_IN);
     return TP_ERR_ARG;
   }
   if (n_frames <= 0) return TP_OK;

@@ -29,11 +29,14 @@ __global__ void slice_jobs_kernel(const tp_tile_job_t* __restrict__ jobs,
   if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = cnt;
 }
 
-// gathered: [world][max_slice] tiles of max_per_tile records (+ counts); dst: global order
+// gathered: [world][max_slice] tiles of src_per_tile records (+ the tiles' TRUE counts);
+// dst: global job order, dst_per_tile records per tile. A tile whose count exceeds
+// src_per_tile lost records in the compact exchange: it is clamped and *overflow set
+// (the host raises StageFailure; never a silent truncation).
 __global__ void unslice_kernel(const tp_det_t* __restrict__ src, const int32_t* __restrict__ src_counts,
                                int max_slice, const int32_t* __restrict__ n_dev, int world,
-                               int max_per_tile, tp_det_t* __restrict__ dst,
-                               int32_t* __restrict__ dst_counts) {
+                               int src_per_tile, int dst_per_tile, tp_det_t* __restrict__ dst,
+                               int32_t* __restrict__ dst_counts, int32_t* __restrict__ overflow) {
   const int j = blockIdx.x;  // global job index
   const int n = *n_dev;
   if (j >= n) return;
@@ -49,10 +52,15 @@ __global__ void unslice_kernel(const tp_det_t* __restrict__ src, const int32_t* 
     i = jj - (r - extra) * base;
   }
   const long long s = (long long)r * max_slice + i;
-  const int cnt = src_counts[s];
+  int cnt = src_counts[s];
+  if (cnt > src_per_tile) {
+    if (threadIdx.x == 0 && overflow != nullptr) atomicOr(overflow, 1);
+    cnt = src_per_tile;
+  }
+  if (cnt > dst_per_tile) cnt = dst_per_tile;
   if (threadIdx.x == 0) dst_counts[j] = cnt;
   for (int k = threadIdx.x; k < cnt; k += blockDim.x)
-    dst[(long long)j * max_per_tile + k] = src[s * max_per_tile + k];
+    dst[(long long)j * dst_per_tile + k] = src[s * src_per_tile + k];
 }
 
 }  // namespace
@@ -74,15 +82,17 @@ extern "C" int tp_slice_jobs(const tp_tile_job_t* jobs, const int32_t* n_jobs_de
 
 extern "C" int tp_unslice_dets(const tp_det_t* gathered, const int32_t* gathered_counts,
                                int max_slice, const int32_t* n_jobs_dev, int world, int max_jobs,
-                               int max_per_tile, tp_det_t* dets, int32_t* counts, void* stream) {
+                               int src_per_tile, int dst_per_tile, tp_det_t* dets, int32_t* counts,
+                               int32_t* overflow, void* stream) {
   if (gathered == nullptr || gathered_counts == nullptr || n_jobs_dev == nullptr ||
       dets == nullptr || counts == nullptr || world < 1 || max_slice < 1 || max_jobs < 1 ||
-      max_per_tile < 1) {
+      src_per_tile < 1 || dst_per_tile < 1) {
     tp_set_error("tp_unslice_dets: bad argument");
     return TP_ERR_ARG;
   }
   unslice_kernel<<<max_jobs, 256, 0, (cudaStream_t)stream>>>(
-      gathered, gathered_counts, max_slice, n_jobs_dev, world, max_per_tile, dets, counts);
+      gathered, gathered_counts, max_slice, n_jobs_dev, world, src_per_tile, dst_per_tile, dets,
+      counts, overflow);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }

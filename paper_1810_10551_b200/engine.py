@@ -16,6 +16,7 @@ Results equal the reference's run_sequence (pipeline.py:442-457) frame by frame.
 
 from __future__ import annotations
 
+import threading
 from contextlib import nullcontext
 
 import numpy as np
@@ -31,10 +32,11 @@ from .yolo import COCO_NAMES, DEFAULT_PRECISION, YoloNet
 MAX_BOXES = 256        # attention boxes per frame (conf >= min_conf)
 MAX_MERGED = 512       # merged window boxes per frame
 MAX_PER_FRAME = 2048   # raw stage-2 detections per frame (postprocess capacity)
+EXCHANGE_CAP = 128     # raw stage-2 records per tile in the crop-parallel exchange
 
 
 def _dist_exchange(local_dets, local_counts, all_dets, all_counts):
-    """Default crop_shard exchange: all-gather every rank's padded stage-2 slice in rank
+    """Default crop_shard exchange: all-gather every rank's compact stage-2 slice in rank
     order over the default process group (NCCL on GPUs: records and counts in one fused
     launch through tp_nccl_gather_dets; gloo on CPU)."""
     import torch.distributed as dist
@@ -52,11 +54,18 @@ class AttentionPipelineB200:
                  policy: MergePolicy | None = None, resample: str = "nearest",
                  head: str = "calibrated", net: YoloNet | None = None,
                  precision: str = DEFAULT_PRECISION,
-                 crop_shard: tuple[int, int] | None = None, exchange=None):
+                 crop_shard: tuple[int, int] | None = None, exchange=None,
+                 exchange_cap: int = EXCHANGE_CAP):
         """crop_shard=(rank, world): crop-parallel stage 2 — every rank runs
         stage 1 + selection for the same frames and evaluates its contiguous slice of the
         active crops; `exchange(local_dets, local_counts, all_dets, all_counts)` all-gathers
-        the padded slices in rank order (default: torch.distributed, NCCL on GPUs)."""
+        the compact slices (exchange_cap records per tile + true counts) in rank order
+        (default: torch.distributed, NCCL on GPUs).
+
+        Stage 1 and stage 2 run on two YoloNets sharing one set of device weights, so the
+        stage 1 of batch k+1 may run on another stream while batch k finishes
+        (stage1()/finish(), used by stream.run_stream); a caller-supplied `net` serves
+        both stages (no overlap)."""
         torch = native.require_cuda()
         if resample not in native.RESAMPLE:
             raise ValueError(f"resample must be one of {tuple(native.RESAMPLE)}")
@@ -74,13 +83,16 @@ class AttentionPipelineB200:
         if self.F > 1024 or fin.rows * fin.cols > 256:
             raise ValueError("final grid too large for the selection/merge kernels")
         mf = self.max_frames
-        self.max_tiles = mf * max(self.A, self.F)
         if net is None:  # precision "fp32" = the hi/lo fp16 activation-pair plan
-            net = YoloNet(self.max_tiles, seed=seed, head=head, dtype=precision)
-        self.net = net
+            net = YoloNet(mf * self.F, seed=seed, head=head, dtype=precision)
+            net1 = YoloNet(mf * self.A, share=net)
+        else:
+            if net.max_tiles < mf * max(self.A, self.F):
+                raise ValueError("shared YoloNet too small for this batch size")
+            net1 = net
+        self.net, self.net1 = net, net1
         self.dtype = self.net.dtype
-        if self.net.max_tiles < self.max_tiles:
-            raise ValueError("shared YoloNet too small for this batch size")
+        self.lock = threading.RLock()  # one batch at a time on the shared buffers
 
         dev = "cuda"
         self.frames = torch.empty((mf, self.H, self.W, 3), dtype=torch.uint8, device=dev)
@@ -95,9 +107,15 @@ class AttentionPipelineB200:
             [[int(c.global_rect.x), int(c.global_rect.y), int(c.global_rect.w),
               c.row * fin.cols + c.col] for c in fin.crops], dtype=torch.int32, device=dev)
         self.dets1, self.counts1 = kernels.alloc_dets(mf * self.A)
+        # attention box banks: slots 0..K-2 = history, K-1.. = the batch's own frames.
+        # Batch k uses bank k % 2, so stage 1 of batch k+1 never touches the bank batch k's
+        # selection reads; finish() carries its batch's last K-1 lists into the other bank.
         slots = (self.K - 1) + mf
-        self.boxes = torch.zeros((slots, MAX_BOXES, 4), dtype=torch.float64, device=dev)
-        self.box_counts = torch.zeros(slots, dtype=torch.int32, device=dev)
+        self._banks = [torch.zeros((slots, MAX_BOXES, 4), dtype=torch.float64, device=dev)
+                       for _ in range(2)]
+        self._bank_counts = [torch.zeros(slots, dtype=torch.int32, device=dev) for _ in range(2)]
+        self._next = 0  # bank of the next batch
+        self._bank = 0  # bank of the last finished batch (results read it)
         self.words = (self.F + 31) // 32
         self.mask = torch.zeros((mf, self.words), dtype=torch.int32, device=dev)
         self.active_ids = torch.zeros((mf, self.F), dtype=torch.int32, device=dev)
@@ -109,17 +127,22 @@ class AttentionPipelineB200:
         self.frame_job_start = torch.zeros(mf + 1, dtype=torch.int32, device=dev)
         self.n_jobs2 = torch.zeros(1, dtype=torch.int32, device=dev)
         self.dets2, self.counts2 = kernels.alloc_dets(mf * self.F)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=dev)
         self.crop_shard = None
         if crop_shard is not None:
             rank, world = (int(v) for v in crop_shard)
             if not (world >= 1 and 0 <= rank < world):
                 raise ValueError(f"bad crop_shard {crop_shard}")
+            if not (1 <= exchange_cap <= kernels.MAX_PER_TILE):
+                raise ValueError(f"exchange_cap must be 1..{kernels.MAX_PER_TILE}")
             self.crop_shard = (rank, world)
+            self.exchange_cap = int(exchange_cap)
             self.max_slice = -(-mf * self.F // world)
-            det_b = kernels.MAX_PER_TILE * native.DET_DTYPE.itemsize
+            det_b = self.exchange_cap * native.DET_DTYPE.itemsize
             self.jobs_local = torch.zeros(self.max_slice * native.JOB_DTYPE.itemsize,
                                           dtype=torch.uint8, device=dev)
             self.n_local = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.send_dets = torch.zeros(self.max_slice * det_b, dtype=torch.uint8, device=dev)
             self.all_dets = torch.zeros(world * self.max_slice * det_b, dtype=torch.uint8,
                                         device=dev)
             self.all_counts = torch.zeros(world * self.max_slice, dtype=torch.int32, device=dev)
@@ -140,19 +163,49 @@ class AttentionPipelineB200:
         self.last_n_tiles = (0, 0)
 
     # ------------------------------------------------------------------ state
+    @property
+    def boxes(self):
+        """Attention box slots of the last finished batch (history + its frames)."""
+        return self._banks[self._bank]
+
+    @property
+    def box_counts(self):
+        return self._bank_counts[self._bank]
+
     def reset_history(self, history=()):
-        """Seed the K-1 history slots from host AttentionModels (oldest first)."""
-        self.box_counts[: self.K - 1].zero_()
-        hist = list(history)[-(self.K - 1):] if self.K > 1 else []
-        off = (self.K - 1) - len(hist)
+        """Seed the K-1 history slots of the next batch from host AttentionModels
+        (oldest first)."""
+        b = self._next
+        K1 = self.K - 1
+        self._bank_counts[b][:K1].zero_()
+        hist = list(history)[-K1:] if K1 > 0 else []
+        off = K1 - len(hist)
         for i, m in enumerate(hist):
             n = len(m.boxes)
             if n > MAX_BOXES:
                 raise ValueError(f"history model has {n} boxes (> {MAX_BOXES})")
             if n:
-                self.boxes[off + i, :n] = self.torch.tensor(
-                    [[b.x, b.y, b.w, b.h] for b in m.boxes], dtype=self.torch.float64)
-            self.box_counts[off + i] = n
+                self._banks[b][off + i, :n] = self.torch.tensor(
+                    [[r.x, r.y, r.w, r.h] for r in m.boxes], dtype=self.torch.float64)
+            self._bank_counts[b][off + i] = n
+
+    def prime_history(self, frames, n: int, stream=None) -> None:
+        """Seed the K-1 history slots of the next batch by running stage 1 on the n <= K-1
+        frames (device uint8 [n,H,W,3]) that precede it — the boundary of a frame-parallel
+        shard (distributed.history_frames): no attention exchange between ranks."""
+        b = self._next
+        K1 = self.K - 1
+        cnt = self._bank_counts[b]
+        cnt[:K1].zero_()
+        if K1 == 0 or n == 0:
+            return
+        if n > K1:
+            raise ValueError(f"at most {K1} history frames")
+        self.stage1(n, frames, stream=stream, bank=b)
+        bank = self._banks[b]
+        with self.torch.cuda.stream(stream) if stream is not None else nullcontext():
+            bank[K1 - n:K1].copy_(bank[K1:K1 + n].clone())
+            cnt[K1 - n:K1].copy_(cnt[K1:K1 + n].clone())
 
     def upload(self, frames_host, n: int, non_blocking: bool = True):
         """Host uint8 [n,H,W,3] (ideally pinned) -> the device frame batch."""
@@ -175,8 +228,8 @@ class AttentionPipelineB200:
             cnt[f] = len(bl)
             for k, b in enumerate(bl):
                 arr[f, k] = b
-        self.boxes[K1:K1 + n].copy_(torch.from_numpy(arr))
-        self.box_counts[K1:K1 + n].copy_(torch.from_numpy(cnt))
+        self._banks[self._next][K1:K1 + n].copy_(torch.from_numpy(arr))
+        self._bank_counts[self._next][K1:K1 + n].copy_(torch.from_numpy(cnt))
 
     def run_device(self, n: int, frames=None, stream=None, timed: bool = False,
                    attention: str = "yolo") -> None:
@@ -188,70 +241,95 @@ class AttentionPipelineB200:
             raise ValueError(f"batch of {n} frames (max {self.max_frames})")
         if attention not in ("yolo", "inject", "all"):
             raise ValueError("attention must be 'yolo', 'inject' or 'all'")
-        fr = self.frames if frames is None else frames
-        st = native.stream_handle(stream)
-        ev = self.events
+        b = self._next
         K1 = self.K - 1
         if timed:
-            ev[0].record(stream)
+            self.events[0].record(stream)
         if attention == "all":
-            self.boxes[K1:K1 + n, 0] = self.full_box
-            self.box_counts[K1:K1 + n] = 1
+            self._banks[b][K1:K1 + n, 0] = self.full_box
+            self._bank_counts[b][K1:K1 + n] = 1
         elif attention == "yolo":
-            self._stage1(fr, n, stream, st)
-        self._finish(fr, n, stream, st, timed)
+            self.stage1(n, frames, stream=stream, bank=b)
+        self.finish(n, frames, stream=stream, bank=b, timed=timed)
 
     def capture(self, n: int, frames, attention: str = "yolo"):
         """CUDA-graph the whole device step for a fixed batch size and frame buffer (no host
         work between kernels: worth ~10% per frame at batch 1, nothing at batch >= 4).
         Returns a replay() callable; each replay is one run_device(n, frames) (history
-        advances as in eager mode) and results()/snapshot() read it as usual."""
+        advances as in eager mode) and results()/snapshot() read it as usual. The graph
+        captures both box banks' roles, so it is captured twice (even / odd batches)."""
         torch = self.torch
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
-        graph = torch.cuda.CUDAGraph()
+        graphs = []
         with torch.cuda.stream(side):
             self.run_device(n, frames=frames, attention=attention)  # warm-up on the stream
             side.synchronize()
-            with torch.cuda.graph(graph, stream=side):
-                self.run_device(n, frames=frames, attention=attention)
+            for _ in range(2):
+                g = torch.cuda.CUDAGraph()
+                bank = self._next
+                with torch.cuda.graph(g, stream=side):
+                    self.run_device(n, frames=frames, attention=attention)
+                graphs.append((bank, g))
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
+        by_bank = dict(graphs)
 
         def replay():
-            graph.replay()
-            self._n = n
-        replay.graph = graph
+            b = self._next
+            by_bank[b].replay()
+            self._bank, self._next, self._n = b, 1 - b, n
+        replay.graph = by_bank
         return replay
 
-    def _gather(self, fr, jobs, n_tiles, n_jobs_dev, stream):
-        """Crop gather into the net's layer-0 input slots."""
+    def _gather(self, net, fr, jobs, n_tiles, n_jobs_dev, stream):
+        """Crop gather into a net's layer-0 input slots."""
         kernels.gather(fr, self.frame_stride, self.H, self.W, jobs, n_tiles, self.resample,
-                       out_act_ptr=self.net.input_ptr, n_jobs_dev=n_jobs_dev, stream=stream,
+                       out_act_ptr=net.input_ptr, n_jobs_dev=n_jobs_dev, stream=stream,
                        dtype=self.dtype)
 
-    def _stage1(self, fr, n, stream, st):
+    def stage1(self, n: int, frames=None, stream=None, bank: int | None = None,
+               events=None) -> None:
+        """Stage 1 of a batch (attention_pass, reference pipeline.py:297-316): gather the
+        A attention tiles per frame, YOLO on net1, decode + to_global, conf >= min_conf
+        boxes into box bank `bank` (default: the next batch's) slots K-1... events:
+        optional (start, end) CUDA events recorded on `stream` around it."""
+        fr = self.frames if frames is None else frames
+        b = self._next if bank is None else bank
+        st = native.stream_handle(stream)
         K1 = self.K - 1
+        if events is not None:
+            events[0].record(stream)
         try:
             nt1 = n * self.A
-            self._gather(fr, self.att_jobs, nt1, None, stream)
-            self.net.forward(nt1, stream=stream)
-            kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
+            self._gather(self.net1, fr, self.att_jobs, nt1, None, stream)
+            self.net1.forward(nt1, stream=stream)
+            kernels.decode(self.net1, nt1, self.att_jobs, self.W, self.H, self.threshold,
                            self.dets1, self.counts1, stream=stream)
             native.call("tp_attention_boxes", native.ptr(self.dets1), native.ptr(self.counts1),
                         kernels.MAX_PER_TILE, n, self.A, float(self.settings.min_confidence),
-                        native.ptr(self.boxes) + K1 * MAX_BOXES * 32,
-                        native.ptr(self.box_counts) + K1 * 4, MAX_BOXES, st)
+                        native.ptr(self._banks[b]) + K1 * MAX_BOXES * 32,
+                        native.ptr(self._bank_counts[b]) + K1 * 4, MAX_BOXES, st)
         except native.NativeError as exc:
             raise StageFailure("attention", -1) from exc
+        if events is not None:
+            events[1].record(stream)
 
-    def _finish(self, fr, n, stream, st, timed):
+    def finish(self, n: int, frames=None, stream=None, bank: int | None = None,
+               timed: bool = False) -> None:
+        """Selection + stage 2 + postprocess of the batch whose attention boxes are in
+        `bank` (merge_temporal/select_active/final_pass/finish_detections, reference
+        pipeline.py:319-385), then carry its last K-1 attention lists into the other
+        bank's history slots. timed: events[1..4] around select / stage 2 / post."""
+        fr = self.frames if frames is None else frames
+        b = self._next if bank is None else bank
+        st = native.stream_handle(stream)
         ev = self.events
-        K1 = self.K - 1
+        boxes, counts = self._banks[b], self._bank_counts[b]
         try:
             if timed:
                 ev[1].record(stream)
-            native.call("tp_select_active", native.ptr(self.boxes), native.ptr(self.box_counts),
+            native.call("tp_select_active", native.ptr(boxes), native.ptr(counts),
                         MAX_BOXES, n, self.K, native.ptr(self.fin_rects), self.F, self.A,
                         float(self.settings.attention_margin_px), float(self.W), float(self.H),
                         native.ptr(self.mask), self.words, native.ptr(self.active_ids),
@@ -263,12 +341,13 @@ class AttentionPipelineB200:
                         native.ptr(self.n_jobs2), st)
         except native.NativeError as exc:
             raise StageFailure("select", -1) from exc
+        self._bank = b
         try:
             if timed:
                 ev[2].record(stream)
             nt2 = n * self.F  # upper bound; kernels read the real count from n_jobs2
             if self.crop_shard is None:
-                self._gather(fr, self.jobs2, nt2, self.n_jobs2, stream)
+                self._gather(self.net, fr, self.jobs2, nt2, self.n_jobs2, stream)
                 self.net.forward(nt2, n_tiles_dev=self.n_jobs2, stream=stream)
                 kernels.decode(self.net, nt2, self.jobs2, self.W, self.H, self.threshold,
                                self.dets2, self.counts2, n_tiles_dev=self.n_jobs2, stream=stream)
@@ -293,21 +372,29 @@ class AttentionPipelineB200:
                     world, native.ptr(self.jobs_local), native.ptr(self.n_local), self.max_slice,
                     st)
         ntl = min(-(-nt2 // world), self.max_slice)  # host upper bound of the slice
-        self._gather(fr, self.jobs_local, ntl, self.n_local, stream)
+        self._gather(self.net, fr, self.jobs_local, ntl, self.n_local, stream)
         self.net.forward(ntl, n_tiles_dev=self.n_local, stream=stream)
         kernels.decode(self.net, ntl, self.jobs_local, self.W, self.H, self.threshold,
                        self.dets2, self.counts2, n_tiles_dev=self.n_local, stream=stream)
+        # compact slice for the exchange: the first exchange_cap records of every tile
+        # (the counts stay true, so the receiver detects a clipped tile)
+        rec = native.DET_DTYPE.itemsize
+        src = self.dets2[: self.max_slice * kernels.MAX_PER_TILE * rec].view(
+            self.max_slice, kernels.MAX_PER_TILE * rec)[:, : self.exchange_cap * rec]
+        with self.torch.cuda.stream(stream) if stream is not None else nullcontext():
+            self.send_dets.view(self.max_slice, self.exchange_cap * rec).copy_(src)
 
     def _unslice(self, nt2, st):
         rank, world = self.crop_shard
         native.call("tp_unslice_dets", native.ptr(self.all_dets), native.ptr(self.all_counts),
-                    self.max_slice, native.ptr(self.n_jobs2), world, nt2, kernels.MAX_PER_TILE,
-                    native.ptr(self.dets2), native.ptr(self.counts2), st)
+                    self.max_slice, native.ptr(self.n_jobs2), world, nt2, self.exchange_cap,
+                    kernels.MAX_PER_TILE, native.ptr(self.dets2), native.ptr(self.counts2),
+                    native.ptr(self.overflow), st)
 
     def local_results(self):
-        """This rank's padded stage-2 slice: (dets bytes, counts) device tensors."""
-        det_b = kernels.MAX_PER_TILE * native.DET_DTYPE.itemsize
-        return self.dets2[: self.max_slice * det_b], self.counts2[: self.max_slice]
+        """This rank's compact stage-2 slice: (dets bytes, true counts) device tensors —
+        [max_slice][exchange_cap] records, [max_slice] counts."""
+        return self.send_dets, self.counts2[: self.max_slice]
 
     def run_local(self, n: int, frames=None, stream=None, timed: bool = False):
         """crop_shard phase 1: stages 1 + selection + this rank's stage-2 slice; then
@@ -333,6 +420,7 @@ class AttentionPipelineB200:
     def _post(self, n, stream, st, timed):
         ev = self.events
         K1 = self.K - 1
+        b = self._bank
         try:
             native.call("tp_collect_final", native.ptr(self.dets2), native.ptr(self.counts2),
                         kernels.MAX_PER_TILE, native.ptr(self.jobs2),
@@ -350,10 +438,12 @@ class AttentionPipelineB200:
                 ev[4].record(stream)
         except native.NativeError as exc:
             raise StageFailure("postprocess", -1) from exc
-        # carry the last K-1 frames' attention boxes to the history slots (device copy)
+        # carry the batch's last K-1 attention lists into the other bank's history slots
         if K1 > 0:
-            self.boxes[:K1].copy_(self.boxes[n:n + K1].clone())
-            self.box_counts[:K1].copy_(self.box_counts[n:n + K1].clone())
+            with self.torch.cuda.stream(stream) if stream is not None else nullcontext():
+                self._banks[1 - b][:K1].copy_(self._banks[b][n:n + K1])
+                self._bank_counts[1 - b][:K1].copy_(self._bank_counts[b][n:n + K1])
+        self._next = 1 - b
         self._n = n
 
     # ------------------------------------------------------------------ API helpers
@@ -371,34 +461,29 @@ class AttentionPipelineB200:
         """Frames (host pixels) -> [(FrameResult, AttentionModel)]. history=None keeps the
         device-carried attention of the previous call (clip mode)."""
         n = len(frames)
-        if history is not None:
-            self.reset_history(history)
-        self._upload_frames(frames)
-        self.run_device(n, timed=True)
-        t = [v / n for v in self.stage_times_ms()]
-        timing = TimingProfile(attention_wait_ms=t[0], client_processing_ms=t[1],
-                               final_eval_ms=t[2], postprocess_ms=t[3])
-        return self.results([f.frame_id for f in frames], timing)
+        with self.lock:
+            if history is not None:
+                self.reset_history(history)
+            self._upload_frames(frames)
+            self.run_device(n, timed=True)
+            t = [v / n for v in self.stage_times_ms()]
+            timing = TimingProfile(attention_wait_ms=t[0], client_processing_ms=t[1],
+                                   final_eval_ms=t[2], postprocess_ms=t[3])
+            return self.results([f.frame_id for f in frames], timing)
 
     def attention_only(self, frame):
         """attention_pass for one frame: stage 1 + box extraction, no selection."""
-        self._upload_frames([frame])
-        nt1 = self.A
-        K1 = self.K - 1
-        try:
-            self._gather(self.frames, self.att_jobs, nt1, None, None)
-            self.net.forward(nt1)
-            kernels.decode(self.net, nt1, self.att_jobs, self.W, self.H, self.threshold,
-                           self.dets1, self.counts1)
-            native.call("tp_attention_boxes", native.ptr(self.dets1), native.ptr(self.counts1),
-                        kernels.MAX_PER_TILE, 1, self.A, float(self.settings.min_confidence),
-                        native.ptr(self.boxes) + K1 * MAX_BOXES * 32,
-                        native.ptr(self.box_counts) + K1 * 4, MAX_BOXES, native.stream_handle())
-        except native.NativeError as exc:
-            raise StageFailure("attention", frame.frame_id) from exc
-        (bx,) = self.box_counts_snapshot(1)
-        boxes = tuple(Rect(int(b[0]), int(b[1]), int(b[2]), int(b[3])) for b in bx)
-        return AttentionModel(frame.frame_id, boxes, (frame.frame_id,))
+        with self.lock:
+            self._upload_frames([frame])
+            K1 = self.K - 1
+            b = self._next
+            self.stage1(1, self.frames, bank=b)
+            cnt = self._bank_counts[b][K1:K1 + 1].cpu().numpy()
+            if (cnt > MAX_BOXES).any():
+                raise StageFailure("attention", frame.frame_id)
+            bx = self._banks[b][K1, : int(cnt[0])].cpu().numpy()
+            boxes = tuple(Rect(int(v[0]), int(v[1]), int(v[2]), int(v[3])) for v in bx)
+            return AttentionModel(frame.frame_id, boxes, (frame.frame_id,))
 
     # ------------------------------------------------------------------ host views
     def stage_times_ms(self):
@@ -411,7 +496,7 @@ class AttentionPipelineB200:
         """Download and convert the last batch to (FrameResult, AttentionModel) pairs."""
         return self.results_from(self.snapshot(), frame_ids, timing)
 
-    def snapshot(self, slot: int = 0):
+    def snapshot(self, slot: int = 0, stream=None):
         """Queue stream-ordered D2H copies of the last batch's results into pinned host
         buffers (slot 0/1 double-buffers them), so the next batch may be launched before
         the host reads these: returns a handle for results_from()."""
@@ -426,31 +511,43 @@ class AttentionPipelineB200:
                           "pc": torch.empty(mf, dtype=torch.int32, **pin),
                           "ac": torch.empty(mf, dtype=torch.int32, **pin),
                           "bc": torch.empty(mf, dtype=torch.int32, **pin),
+                          "mc": torch.empty(mf, dtype=torch.int32, **pin),
+                          "of": torch.empty(1, dtype=torch.int32, **pin),
                           "boxes": torch.empty((mf, MAX_BOXES, 4), dtype=torch.float64, **pin),
                           "rec": torch.empty(mf * MAX_PER_FRAME * rec, dtype=torch.uint8, **pin),
                           "event": torch.cuda.Event()}
         s = bufs[slot]
         rb = n * MAX_PER_FRAME * native.PDET_DTYPE.itemsize
-        s["oc"][:n].copy_(self.ocounts[:n], non_blocking=True)
-        s["pc"][:n].copy_(self.pcounts[:n], non_blocking=True)
-        s["ac"][:n].copy_(self.active_counts[:n], non_blocking=True)
-        # after run_device the batch's own box slots are K1..K1+n-1
-        s["bc"][:n].copy_(self.box_counts[K1:K1 + n], non_blocking=True)
-        s["boxes"][:n].copy_(self.boxes[K1:K1 + n], non_blocking=True)
-        s["rec"][:rb].copy_(self.outp.view(-1)[:rb], non_blocking=True)
-        s["event"].record()
+        boxes, counts = self._banks[self._bank], self._bank_counts[self._bank]
+        with torch.cuda.stream(stream) if stream is not None else nullcontext():
+            s["oc"][:n].copy_(self.ocounts[:n], non_blocking=True)
+            s["pc"][:n].copy_(self.pcounts[:n], non_blocking=True)
+            s["ac"][:n].copy_(self.active_counts[:n], non_blocking=True)
+            s["mc"][:n].copy_(self.merged_counts[:n], non_blocking=True)
+            s["of"].copy_(self.overflow, non_blocking=True)
+            # the batch's own box slots are K1..K1+n-1 of its bank
+            s["bc"][:n].copy_(counts[K1:K1 + n], non_blocking=True)
+            s["boxes"][:n].copy_(boxes[K1:K1 + n], non_blocking=True)
+            s["rec"][:rb].copy_(self.outp.view(-1)[:rb], non_blocking=True)
+            s["event"].record(stream)
         return (n, s)
 
     def results_from(self, snap, frame_ids, timing: TimingProfile | None = None):
-        """(FrameResult, AttentionModel) pairs from a snapshot (waits for its copies)."""
+        """(FrameResult, AttentionModel) pairs from a snapshot (waits for its copies).
+        Capacity overflows raise StageFailure — results are never silently truncated."""
         n, s = snap
         s["event"].synchronize()
         oc, pc, ac = s["oc"][:n].numpy(), s["pc"][:n].numpy(), s["ac"][:n].numpy()
         if (pc > MAX_PER_FRAME).any():
             raise StageFailure("final", int(frame_ids[int(np.argmax(pc))]))
+        mc = s["mc"][:n].numpy()
+        if (mc > MAX_MERGED).any():  # temporal window above the selection kernel's capacity
+            raise StageFailure("select", int(frame_ids[int(np.argmax(mc))]))
+        if int(s["of"][0]) != 0:  # a tile clipped by the crop-parallel exchange cap
+            raise StageFailure("final", int(frame_ids[0]))
         cnt = s["bc"][:n].numpy()
         if (cnt > MAX_BOXES).any():
-            raise StageFailure("attention", -1)
+            raise StageFailure("attention", int(frame_ids[int(np.argmax(cnt))]))
         bx = s["boxes"][:n].numpy()
         rec = s["rec"][: n * MAX_PER_FRAME * native.PDET_DTYPE.itemsize].numpy()
         rec = rec.view(native.PDET_DTYPE).reshape(n, MAX_PER_FRAME)
@@ -470,8 +567,6 @@ class AttentionPipelineB200:
     def box_counts_snapshot(self, n):
         """Attention boxes per frame of the last batch (host lists)."""
         K1 = self.K - 1
-        # after run_device the batch's own slots are K1..K1+n-1 (the history copy only
-        # overwrote slots 0..K1-1)
         cnt = self.box_counts[K1:K1 + n].cpu().numpy()
         if (cnt > MAX_BOXES).any():
             raise StageFailure("attention", -1)

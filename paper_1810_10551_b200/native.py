@@ -16,7 +16,11 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libtilepipe_b200.so")
+# TP_LIB_VARIANT=debug selects the debug build (make debug): bounded, trapping mbarrier
+# waits (TP_MBAR_TIMEOUT_CYCLES) — same kernels and ABI otherwise
+_VARIANT = "_debug" if os.environ.get("TP_LIB_VARIANT") == "debug" else ""
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                        f"libtilepipe_b200{_VARIANT}.so")
 
 JOB_DTYPE = np.dtype(
     [("frame", "<i4"), ("crop_id", "<i4"), ("x", "<i4"), ("y", "<i4"), ("side", "<i4"),
@@ -99,7 +103,7 @@ SIGNATURES = {
     "tp_maxpool2": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "tp_debug_conv_counters": (_I, [_P, _I, _I]),
     "tp_slice_jobs": (_I, [_P, _P, _I, _I, _P, _P, _I, _P]),
-    "tp_unslice_dets": (_I, [_P, _P, _I, _P, _I, _I, _I, _P, _P, _P]),
+    "tp_unslice_dets": (_I, [_P, _P, _I, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "tp_render_frames": (_I, [_P, _P, _P, _I, _I, _I, _I, ctypes.c_uint32, _P, _P]),
     "tp_nccl_available": (_I, []),
     "tp_nccl_gather_dets": (_I, [_P, _P, _I64, _P, _I64, _P, _P, _P]),

@@ -229,23 +229,31 @@ def run_sequence(frames: Iterable[Frame], settings: PipelineSettings, det: Detec
 
 
 def _run_sequence_batched(frames, settings, det, policy):
-    """Clip mode: frames go through the device engine in batches, attention history
-    carried on the GPU (identical results to the per-frame loop)."""
+    """Clip mode: frames go through the device engine in batches. The generator keeps its
+    own attention history (the last K-1 AttentionModels, as the reference's run_sequence
+    does, pipeline.py:442-457) and hands it to every batch, so interleaved generators and
+    other callers sharing the cached engine cannot disturb each other; each batch holds
+    the engine's lock (identical results to the per-frame loop)."""
     eng = None
+    keep = settings.temporal_window - 1
+    history: list[AttentionModel] = []
     batch: list[Frame] = []
-    first = True
+
+    def flush():
+        nonlocal history
+        out = eng.evaluate_frames(batch, history)
+        history = [*history, *(att for _, att in out)][-keep:] if keep > 0 else []
+        return [res for res, _ in out]
+
     for fr in frames:
         if eng is None:
             eng = _engine_for(det, settings, fr.width, fr.height, policy)
         batch.append(fr)
         if len(batch) == eng.max_frames:
-            for res, _ in eng.evaluate_frames(batch, () if first else None):
-                yield res
-            first = False
+            yield from flush()
             batch = []
     if batch:
-        for res, _ in eng.evaluate_frames(batch, () if first else None):
-            yield res
+        yield from flush()
 
 
 def run_downscale_baseline(frame: Frame, det: Detector, settings: PipelineSettings | None = None,

@@ -160,11 +160,15 @@ class YoloNet:
     """Device-resident YOLO v2-608 plan over a persistent workspace (max_tiles tiles)."""
 
     def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated",
-                 dtype: str = DEFAULT_PRECISION):
+                 dtype: str = DEFAULT_PRECISION, share: "YoloNet | None" = None):
         """dtype "fp16" / "bf16": 16-bit activations; "fp32": the fp32-parity plan
-        (TP_DTYPE_F16X2 — exact hi/lo fp16 activation pairs, same kernels, 2x K)."""
+        (TP_DTYPE_F16X2 — exact hi/lo fp16 activation pairs, same kernels, 2x K).
+        share: another YoloNet whose device weights this one reuses (own workspace, so
+        the two can run concurrently on different streams)."""
         torch = native.require_cuda()
         lib = native.load()
+        if share is not None:
+            dtype = share.dtype
         if dtype not in native.DTYPES:
             raise ValueError(f"dtype must be one of {tuple(native.DTYPES)}")
         self.dtype = dtype
@@ -172,12 +176,15 @@ class YoloNet:
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float16
         wdtype = "fp16" if self.split else dtype
         self.weight_dtype = wdtype  # value grid of the weights (make_weights dtype)
-        wpacks, biases = weights if weights is not None else make_weights(seed, head, wdtype)
-        if self.split:
-            wpacks = [split_weight(li, w) for li, w in enumerate(wpacks)]
         self.max_tiles = int(max_tiles)
-        self.w_dev = [torch.from_numpy(w).to(self.tdtype).cuda() for w in wpacks]
-        self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
+        if share is not None:
+            self.w_dev, self.b_dev = share.w_dev, share.b_dev
+        else:
+            wpacks, biases = weights if weights is not None else make_weights(seed, head, wdtype)
+            if self.split:
+                wpacks = [split_weight(li, w) for li, w in enumerate(wpacks)]
+            self.w_dev = [torch.from_numpy(w).to(self.tdtype).cuda() for w in wpacks]
+            self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
         nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles, native.DTYPES[dtype]))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
         wptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.w_dev])
