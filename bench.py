@@ -2,27 +2,35 @@
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Workload (BASELINE.json configs[1]): a 300-frame synthetic 3840x2160 clip (frames
-0-99 sparse, 100-199 dense, 200-299 mixed scenes, seed 0, the reference generator's
-semantics), preset "1 att, 3 fin, 20 over", random-init YOLO v2-608 (seed 0). One
-step = one batch of --batch frames through the full two-stage pipeline (stage-1 YOLO
-on 2 attention tiles/frame, selection, stage-2 YOLO on the active crops, NMS+merge).
+Workload (BASELINE.json configs[1]): the 300-frame synthetic 3840x2160 clip of
+synthetic.bench_clip (frames 0-99 sparse, 100-199 dense, 200-299 mixed scenes, seed 0;
+the reference generator's semantics), preset "1 att, 3 fin, 20 over", random-init
+YOLO v2-608 (seed 0). One step = one batch of --batch frames through the full two-stage
+pipeline (stage-1 YOLO on 2 attention tiles/frame, selection, stage-2 YOLO on the active
+crops, NMS + merge). With N GPUs the clip is N x 300 frames (segment r = bench_clip with
+seed r) sharded contiguously over the ranks (frame-DP; rank r > 0 seeds its temporal
+window by recomputing stage 1 on the frame before its shard); weak scaling.
 
 * value: frames/sec with the clip resident in HBM (each batch's input is 30 4K frames,
-  746 MB > 126 MB L2, so no flush is needed between steps).
-* e2e: the same through the public engine API from pinned HOST frames: per step the
-  H2D copy of the batch and the D2H of the results are inside the timed region
-  (copy of batch i+1 overlaps compute of batch i on a second stream).
+  746 MB > 126 MB L2, so no flush is needed between steps); stage 1 of batch k+1 runs on
+  a second stream while batch k finishes (the run_stream schedule); at N > 1 every batch's
+  results are all-gathered over NCCL (the fused C-ABI gather) inside the timed region.
+* e2e: the same metric through the drop-in API — stream.run_stream (N = 1) /
+  distributed.run_stream_sharded (N > 1) — with HOST frames in pinned memory: per step
+  the H2D copy of the batch, the D2H of its results and the construction of every
+  FrameResult / Detection object are inside the timed region.
 * precision (default "fp32"): the fp32-parity plan — activations as exact fp16 hi/lo
-  pairs, fp32 accumulation — the mode inside the north-star 1e-3 score tolerance;
-  --precision fp16 runs the ~2x faster 16-bit-activation mode.
-* roofline: the dominant kernel is the tcgen05 implicit-GEMM conv (23 launches per
-  YOLO forward + 1 maxpool): achieved = 62.938 GFLOP x tiles / measured forward time
-  (algorithmic FLOPs; `executed_tflops` counts the parity plan's doubled K).
-* cpu_baseline: the CPU oracle port (oracle/: reference pipeline restatement + torch
-  CPU fp32 YOLO) on one frame of the same clip, all host threads.
-Multi-GPU (torchrun): frames shard across ranks (each rank streams its own 300-frame
-clip: weak scaling); the only collective is the NCCL gather of per-frame results.
+  pairs, fp32 accumulation — the mode inside the north-star 1e-3 score tolerance
+  (tests/test_gpu_e2e_parity.py); --precision fp16 runs the ~2x faster 16-bit mode.
+* roofline: the dominant kernel family is the tcgen05 implicit-GEMM conv (23 launches per
+  YOLO forward + 1 maxpool): achieved = 62.938 GFLOP x tiles / the union of the measured
+  forward intervals (algorithmic FLOPs; `executed_tflops` counts the parity plan's K).
+* cpu_baseline / --impl reference: the reference pipeline (oracle/pipeline_ref, pinned to
+  reference goldens) with the fp32 CPU YOLO (oracle/yolo_ref) on the box's host cores, on
+  frames spread over the same sparse/dense/mixed clip; the GPU arm's cpu_baseline also
+  checks those frames' results against the GPU's.
+* sub_results (N = 1): BASELINE configs[2] (all-crops), [3] (8K), [4] (density 0.5,
+  injected stage 1) and the fp16 mode, each a short timed run with its own clock record.
 """
 
 from __future__ import annotations
@@ -30,6 +38,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -41,17 +50,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PRESET = "1 att, 3 fin, 20 over"
-W, H = 3840, 2160
 FRAMES = {"4k": (3840, 2160), "8k": (7680, 4320)}
-CLIP = [("sparse", 100), ("dense", 100), ("mixed", 100)]
 METRIC = "frames/sec, synthetic 4K & 8K video, 1/2/4/8 B200; crops/sec; % roofline"
+LAUNCHES_PER_STEP = (1 + 24 + 1 + 1) + (2 + 1 + 24 + 1 + 1 + 1)  # stage 1 + finish
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=30)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--resample", default="nearest", choices=["nearest", "bilinear"])
@@ -60,8 +68,11 @@ def parse():
                     help="activation precision: fp32 = hi/lo fp16 pairs, the parity plan "
                          "(default); fp16/bf16 = 16-bit activations, ~2x faster")
     ap.add_argument("--profile", action="store_true",
-                    help="torch.profiler kernel table of the timed steps to stderr (not a bench run)")
+                    help="CUPTI kernel table of the timed steps to stderr (not a bench run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the sub_results runs")
+    ap.add_argument("--no-lookahead", action="store_true",
+                    help="stage 1 and 2 of a batch back to back on one stream")
     ap.add_argument("--frame", default="4k", choices=sorted(FRAMES))
     ap.add_argument("--preset", default=PRESET)
     ap.add_argument("--mode", default="pipeline", choices=["pipeline", "allcrops"],
@@ -70,37 +81,60 @@ def parse():
                     help="inject stage-1 boxes activating this fraction of the final grid "
                          "(config 5 density sweep; stage 1 is skipped)")
     ap.add_argument("--clip-frames", type=int, default=300)
-    args = ap.parse_args()
-    global W, H
-    W, H = FRAMES[args.frame]
-    return args
+    return ap.parse_args(argv)
 
 
-def kernel_table(prof, ms: float, steps: int) -> None:
-    """Per-kernel device time over the timed steps (warm, real overlap), to stderr."""
-    agg: dict[str, list] = {}
-    for ev in prof.events():
-        if ev.device_type != torch_device_type_cuda():
-            continue
-        name = ev.name.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0]
-        a = agg.setdefault(name, [0.0, 0])
-        a[0] += ev.time_range.elapsed_us() / 1e3
-        a[1] += 1
-    busy = sum(v[0] for v in agg.values())
-    print(f"# kernel table: {steps} steps, {ms:.3f} ms wall (device), {busy:.3f} ms kernel busy", file=sys.stderr)
-    for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
-        print(f"{100 * t / ms:6.2f}% {t / steps:9.3f} ms/step {n // steps:5d}/step  {k}", file=sys.stderr)
+# --------------------------------------------------------------------------- launch
 
 
-def torch_device_type_cuda():
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_launch_ranks(args) -> bool:
+    """`--gpus N` outside torchrun: launch N ranks (one per GPU) through
+    torch.distributed.run and return True (this process only waits). Fails loudly when
+    the box has fewer GPUs than asked."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
     import torch
-    return torch.autograd.DeviceType.CUDA
+
+    have = torch.cuda.device_count()
+    if have < args.gpus and os.environ.get("TP_BENCH_SHARED_GPU") != "1":
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
-def clip_objects(rank: int = 0, n_frames: int = 300):
-    from paper_1810_10551_b200 import synthetic
+def arm_config(args, world: int) -> dict:
+    """Workload description, identical for the B200 arm and the reference arm."""
+    W, H = FRAMES[args.frame]
+    kind = "all-crops baseline" if args.mode == "allcrops" else "attention pipeline"
+    dens = "" if args.density is None else f" (injected stage 1, density {args.density})"
+    return {"workload": f"{args.frame.upper()} {kind}{dens} on the synthetic bench clip "
+                        f"({args.clip_frames} frames per GPU: sparse/dense/mixed thirds, "
+                        f"segment r = seed r), preset '{args.preset}', random-init YOLO "
+                        "v2-608 (seed 0, calibrated head)",
+            "frame": [W, H], "frames_per_step": args.batch, "per_gpu_frames": args.clip_frames,
+            "resample": args.resample, "parallelism": f"frame-dp{world}",
+            "precision": args.precision}
 
-    return synthetic.bench_clip(W, H, n_frames, seed=rank)
+
+def lscpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------------------- clocks
 
 
 class ClockSampler:
@@ -110,7 +144,6 @@ class ClockSampler:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
-    # NVML clocks-event reason bits
     REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
                    "hw_thermal_slowdown": 0x40}
 
@@ -176,95 +209,267 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
-def cpu_baseline_frames_per_sec(objs, n_frames=1):
-    """Oracle port of the reference pipeline + CPU YOLO, all host threads, bounded sample."""
+# --------------------------------------------------------------------------- CPU arm
+
+
+def sample_frames(n_clip: int, k: int) -> list[int]:
+    """k frame indices spread evenly over the clip (sparse / dense / mixed thirds)."""
+    return [min(n_clip - 1, int((i + 0.5) * n_clip / k)) for i in range(k)]
+
+
+def cpu_reference_frames(args, fids, objs, threads=None):
+    """The reference pipeline + fp32 CPU YOLO on the given clip frames (each with its
+    K=2 history: the previous frame's attention, computed outside the timing — in a
+    sequential run it belongs to the previous frame's step). Returns per-frame seconds,
+    results and tiles."""
     import torch
 
-    from oracle import pipeline_ref as R, yolo_ref
+    from oracle import e2e as E
+    from oracle import pipeline_ref as R
     from paper_1810_10551_b200 import synthetic, yolo
 
-    threads = os.cpu_count() or 1
+    W, H = FRAMES[args.frame]
+    threads = threads or os.cpu_count() or 1
     torch.set_num_threads(threads)
-    wpacks, biases = yolo.make_weights(0, dtype="fp16")
+    cache = {}
+
+    def pixels_of(f):
+        if f not in cache:
+            cache[f] = synthetic.render_frame(W, H, objs[f])
+        return cache[f]
+    det = E.CpuYolo(pixels_of, yolo.COCO_NAMES, threads=threads)
     plan = R.Plan(W, H, 1, 3, 20)
-    frames = [synthetic.render_frame(W, H, objs[i]) for i in range(n_frames)]
-
-    def detect(fid, crop):
-        tile = R.cut_tile_nearest(frames[fid], crop)
-        head = yolo_ref.forward(tile[None], wpacks, biases, mode="fp32")  # the reference: fp32
-        return [(r, yolo.COCO_NAMES[c], conf) for r, c, conf, _ in
-                yolo_ref.region_decode(head, 0.25)[0]]
-
-    t0 = time.perf_counter()
-    R.run_sequence(plan, range(n_frames), detect)
-    dt = time.perf_counter() - t0
-    return n_frames / dt, threads, dt
-
-
-def arm_config(args, n_clip: int, world: int) -> dict:
-    """Workload description shared by the B200 arm and the reference arm."""
-    return {"workload": f"{args.frame.upper()} "
-                        f"{'all-crops baseline' if args.mode == 'allcrops' else 'attention pipeline'}"
-                        f"{'' if args.density is None else f' (injected stage-1, density {args.density})'}"
-                        f" on a {n_clip}-frame synthetic clip "
-                        f"(sparse/dense/mixed, seed=rank), preset '{args.preset}', "
-                        "random-init YOLO v2-608 (seed 0, calibrated head)",
-            "frame": [W, H], "frames_per_step": args.batch, "per_gpu_frames": n_clip,
-            "resample": args.resample, "parallelism": f"frame-dp{world}"}
+    out = []
+    for f in fids:
+        hist = []
+        if f > 0:
+            det.prefetch(f - 1, plan.att[3])
+            hist = [R.attention_pass(plan, f - 1, det, 0.3)]
+        t0 = time.perf_counter()
+        dets, active, att = E.reference_frame(plan, f, det, hist)
+        dt = time.perf_counter() - t0
+        out.append({"frame": f, "seconds": dt, "dets": dets, "active": active, "att": att,
+                    "tiles": len(plan.att[3]) + len(active)})
+        for k in [k for k in det.raw if k[0] < f - 1]:  # bounded memory
+            det.raw.pop(k, None)
+            det.tiles.pop(k, None)
+    return out, threads
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference pipeline on the host cores, one clip frame per
+    step, frames spread over the sparse/dense/mixed clip (same config as the GPU arm)."""
     if rank != 0:
         return
-    objs = clip_objects(0, args.clip_frames)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        fps, threads, dt = cpu_baseline_frames_per_sec(objs[i % len(objs):], 1)
-        if i >= args.warmup:
-            vals.append(dt)
-    total = sum(vals)
+    from paper_1810_10551_b200 import synthetic
+
+    W, H = FRAMES[args.frame]
+    objs = synthetic.bench_clip(W, H, args.clip_frames, seed=0)
+    n = args.warmup + args.steps
+    fids = sample_frames(len(objs), n)
+    res, threads = cpu_reference_frames(args, fids, objs)
+    timed = res[args.warmup:]
+    total = sum(r["seconds"] for r in timed)
     v = args.steps / total
+    tiles = sum(r["tiles"] for r in timed) / len(timed)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {**arm_config(args, len(objs), world),
-                       "step": "1 frame of the clip per step (bounded CPU sample of the workload)"},
-            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
-                             "sample": "1 frame per step: oracle run_sequence + torch-CPU fp32 YOLO"},
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": arm_config(args, world),
+            "step": "one clip frame per step (bounded CPU sample of the workload): frames "
+                    f"{[r['frame'] for r in timed]} spread over the sparse/dense/mixed clip",
+            "workload_stats": {"tiles_per_frame": tiles},
+            "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads,
+                             "kind": "port", "cpu": lscpu_model(),
+                             "sample": f"{args.steps} frames spread over the clip: oracle "
+                                       "reference pipeline + torch-CPU fp32 YOLO v2-608"},
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = parse()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
+def cpu_baseline_with_parity(args, objs):
+    """GPU arm's cpu_baseline: 3 frames (one per scene kind), timed on the host cores,
+    and their results compared with the GPU's (oracle.e2e contract)."""
+    from oracle import e2e as E
+    from paper_1810_10551_b200 import pipeline as P, synthetic, yolo
 
+    W, H = FRAMES[args.frame]
+    n = len(objs)
+    fids = [n // 6, n // 2, 5 * n // 6]
+    res, threads = cpu_reference_frames(args, fids, objs)
+    total = sum(r["seconds"] for r in res)
+    settings = P.PipelineSettings.from_preset(args.preset)
+    gdet = yolo.YoloB200Detector(precision=args.precision)
+    exact = 0
+    notes = []
+    for r in res:
+        f = r["frame"]
+        fr = [P.Frame(i, W, H, synthetic.render_frame(W, H, objs[i]))
+              for i in ([f - 1] if f else []) + [f]]
+        g = list(P.run_sequence(fr, settings, gdet))[-1]
+        got = [((d.rect.x, d.rect.y, d.rect.w, d.rect.h), d.class_label, d.confidence)
+               for d in g.detections]
+        cmp = E.compare_dets(r["dets"], got)
+        ok = cmp["ok"] and g.active_count == len(r["active"])
+        exact += ok
+        notes.append({"frame": f, "match": bool(ok), "dets": cmp["n"],
+                      "score_rel": cmp["score_rel"], "order_flips": cmp["order_flips"],
+                      "rounding_1px": cmp["n_1px"]})
+    return {"value": len(res) / total, "unit": "frames/s", "cores": threads, "kind": "port",
+            "cpu": lscpu_model(),
+            "sample": f"frames {fids} (sparse, dense, mixed), {total:.1f} s: oracle reference "
+                      "pipeline + torch-CPU fp32 YOLO v2-608, all host threads",
+            "parity": {"frames": len(res), "match": exact, "detail": notes}}
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+
+class DeviceLoop:
+    """The device-resident step loop: batch k's stage 1 on `att` (look-ahead) while batch
+    k-1 finishes on the main stream; at world > 1 the batch's results are all-gathered
+    (distributed.BatchGather, fused NCCL) after its finish. Conv forwards are bracketed
+    by events on their own streams for the roofline."""
+
+    def __init__(self, eng, clip, B, mode, density, lookahead, world, group=None):
+        import torch
+
+        self.torch, self.eng, self.clip, self.B = torch, eng, clip, B
+        self.mode, self.lookahead = mode, lookahead and eng.net1 is not eng.net
+        self.att = torch.cuda.Stream() if self.lookahead else None
+        self.att_done = [torch.cuda.Event() for _ in range(2)]
+        self.fin_done = [torch.cuda.Event() for _ in range(2)]
+        self.gather = None
+        if world > 1:
+            from paper_1810_10551_b200.distributed import BatchGather
+            self.gather = BatchGather(B, world, group)
+        self.fwd = []  # (start, end, tiles or None=device count, step)
+        self.n2 = []   # per step: device tensor holding the stage-2 tile count
+        self.injected = []
+        if density is not None:  # boxes at the centres of round(d*F) crops per frame
+            import random as _random
+
+            from paper_1810_10551_b200.engine import exclusive_boxes
+            fin = eng.plan.final_grid.crops
+            k = int(round(density * len(fin)))
+            rng = _random.Random(1234)
+            for _ in range(4):  # 4 batches of injected boxes, uploaded once
+                boxes = [exclusive_boxes(
+                    eng.plan.final_grid, [fin[c].crop_id for c in sorted(rng.sample(range(len(fin)), k))],
+                    eng.settings.attention_margin_px) for _ in range(B)]
+                arr = np.zeros((B, 256, 4))
+                cnt = np.zeros(B, dtype=np.int32)
+                for f, bl in enumerate(boxes):
+                    cnt[f] = len(bl)
+                    arr[f, : len(bl)] = bl
+                self.injected.append((torch.from_numpy(arr).cuda(), torch.from_numpy(cnt).cuda()))
+        self.density = density
+        self._wrap(eng.net)
+        if eng.net1 is not eng.net:
+            self._wrap(eng.net1)
+        self.record = False
+
+    def _wrap(self, net):
+        orig = net.forward
+        torch = self.torch
+
+        def timed(n, n_tiles_dev=None, stream=None):
+            if not self.record:
+                return orig(n, n_tiles_dev=n_tiles_dev, stream=stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            orig(n, n_tiles_dev=n_tiles_dev, stream=stream)
+            b.record(stream)
+            self.fwd.append((a, b, None if n_tiles_dev is not None else n))
+        net.forward = timed
+
+    def frames(self, i):
+        s = (i * self.B) % self.clip.shape[0]
+        return self.clip[s:s + self.B]
+
+    def stage1(self, i):
+        torch, eng = self.torch, self.eng
+        bank = (self.base + i) % 2
+        if self.mode != "pipeline" or self.density is not None:
+            K1 = eng.K - 1
+            if self.density is not None:
+                arr, cnt = self.injected[i % len(self.injected)]
+                eng._banks[bank][K1:K1 + self.B].copy_(arr)
+                eng._bank_counts[bank][K1:K1 + self.B].copy_(cnt)
+            else:  # all-crops: one full-frame box per frame
+                eng._banks[bank][K1:K1 + self.B, 0] = eng.full_box
+                eng._bank_counts[bank][K1:K1 + self.B] = 1
+            self.att_done[i % 2].record()
+            return
+        st = self.att if self.lookahead else torch.cuda.current_stream()
+        if self.lookahead and i >= 2:
+            st.wait_event(self.fin_done[i % 2])  # bank reuse: batch i-2's selection read it
+        with torch.cuda.stream(st):
+            eng.stage1(self.B, self.frames(i), stream=st, bank=bank)
+            self.att_done[i % 2].record(st)
+
+    def finish(self, i):
+        torch, eng = self.torch, self.eng
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self.att_done[i % 2])
+        eng.finish(self.B, self.frames(i), bank=(self.base + i) % 2)
+        if self.record:
+            n2 = torch.empty(1, dtype=torch.int32, device="cuda")
+            n2.copy_(eng.n_jobs2)
+            self.n2.append(n2)
+        if self.gather is not None:
+            self.gather.launch(eng, i, self.B, False, want_records=False)
+        self.fin_done[i % 2].record()
+
+    def run(self, first, last):
+        """Steps first..last-1 (stage 1 of `first` must not have been launched)."""
+        self.base = self.eng._next - first  # bank of step i = (base + i) % 2
+        self.stage1(first)
+        for i in range(first, last):
+            if self.lookahead and i + 1 < last:
+                self.stage1(i + 1)
+                self.finish(i)
+            else:
+                self.finish(i)
+                if i + 1 < last:
+                    self.stage1(i + 1)
+
+    def conv_stats(self, t0):
+        """(union of forward intervals in ms, algorithmic FLOPs) over the recorded steps."""
+        from paper_1810_10551_b200 import yolo
+
+        n2 = [int(t.item()) for t in self.n2]
+        iv, flops, k2 = [], 0.0, 0
+        for a, b, n in self.fwd:
+            if n is None:  # stage-2 forward: device-side tile count, in step order
+                n = n2[k2] if k2 < len(n2) else 0
+                k2 += 1
+            iv.append((t0.elapsed_time(a), t0.elapsed_time(b)))
+            flops += n * yolo.GFLOP_PER_TILE * 1e9
+        iv.sort()
+        busy, end = 0.0, -1e30
+        for s, e in iv:
+            if e <= end:
+                continue
+            busy += e - max(s, end)
+            end = e
+        return busy, flops, sum(n2)
+
+
+def gpu_run(args, rank, world, local, shared_gpu, group, sub=False):
+    """One GPU-arm measurement: (line fields, eng, clip objects) — the device-resident
+    timed loop; the caller adds e2e / cpu_baseline / sub_results."""
     import torch
     import torch.distributed as dist
 
-    from paper_1810_10551_b200 import distributed as D, native, pipeline as P, synthetic, yolo
+    from paper_1810_10551_b200 import pipeline as P, synthetic, yolo
     from paper_1810_10551_b200.engine import AttentionPipelineB200
 
-    # TP_BENCH_SHARED_GPU=1: logic check of the multi-rank path on a one-GPU box (every
-    # rank on cuda:0, gloo collectives, ranks never wait on each other's kernels); such a
-    # run is flagged in its config and is not a scaling measurement
-    shared_gpu = os.environ.get("TP_BENCH_SHARED_GPU") == "1"
-    dev_idx = 0 if shared_gpu else local
-    torch.cuda.set_device(dev_idx)
-    if world > 1:
-        if shared_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W, H = FRAMES[args.frame]
     B = args.batch
-    objs = clip_objects(rank, args.clip_frames)
-    # every step takes B consecutive clip frames: pad the clip cyclically to a multiple of B
+    objs = synthetic.bench_clip(W, H, args.clip_frames, seed=rank)
     objs = [objs[k % len(objs)] for k in range(-(-len(objs) // B) * B)]
     n_clip = len(objs)
     settings = P.PipelineSettings.from_preset(args.preset)
@@ -273,76 +478,32 @@ def main():
     clip = torch.empty((n_clip, H, W, 3), dtype=torch.uint8, device="cuda")
     for i in range(0, n_clip, 10):
         synthetic.render_frames_device(W, H, objs[i:i + 10], out=clip[i:i + 10])
-    stream = torch.cuda.current_stream()
-    n_steps = args.warmup + args.steps
-    tiles2 = torch.zeros(n_steps, dtype=torch.int32, device="cuda")
-    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(2 * n_steps)]
-
-    # instrument the two YOLO forwards of each step (conv roofline)
-    fwd_calls = {"i": 0}
-    orig_forward = eng.net.forward
-
-    def timed_forward(n, n_tiles_dev=None, stream=None):
-        k = fwd_calls["i"]
-        fwd_calls["i"] += 1
-        if k < len(fwd_ev):
-            fwd_ev[k][0].record()
-        orig_forward(n, n_tiles_dev=n_tiles_dev, stream=stream)
-        if k < len(fwd_ev):
-            fwd_ev[k][1].record()
-
-    eng.net.forward = timed_forward
-
-    def step(i):
-        s = (i * B) % n_clip
-        frames = clip[s:s + B]
-        if args.density is not None:
-            eng.set_attention(injected[i % len(injected)])
-            eng.run_device(B, frames=frames, attention="inject")
-        else:
-            eng.run_device(B, frames=frames, attention=attention)
-        tiles2[i:i + 1].copy_(eng.n_jobs2)
-        if world > 1:  # result gather (NCCL): per-frame counts + first 64 final records
-            recs = eng.outp.view(B, -1)[:, : 64 * native.PDET_DTYPE.itemsize]
-            D.gather_records(eng.ocounts[:B], recs, [B] * world, to_host=False)
-
-    attention = "all" if args.mode == "allcrops" else "yolo"
-    injected = []
-    if args.density is not None:  # boxes at the centres of round(d*F) crops per frame
-        import random as _random
-
-        fin = eng.plan.final_grid.crops
-        k = int(round(args.density * len(fin)))
-        rng = _random.Random(1234)
-        from paper_1810_10551_b200.engine import exclusive_boxes
-
-        for _ in range(4):
-            batch = []
-            for _f in range(B):
-                chosen = sorted(rng.sample(range(len(fin)), k))
-                batch.append(exclusive_boxes(eng.plan.final_grid,
-                                             [fin[c].crop_id for c in chosen],
-                                             settings.attention_margin_px))
-            injected.append(batch)
     eng.reset_history(())
-    for i in range(args.warmup):
-        step(i)
+    if rank > 0 and args.mode == "pipeline" and args.density is None:
+        # frame-DP boundary: the frame before this shard is the last of segment r-1
+        prev = synthetic.bench_clip(W, H, args.clip_frames, seed=rank - 1)[-1]
+        pf = synthetic.render_frames_device(W, H, [prev])
+        eng.prime_history(pf, 1)
+    mode = "allcrops" if args.mode == "allcrops" else "pipeline"
+    loop = DeviceLoop(eng, clip, B, mode, args.density, not args.no_lookahead, world, group)
+    n_steps = args.warmup + args.steps
+    loop.run(0, args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prof = None
-    if args.profile:  # CUPTI kernel table to stderr; the JSON value of such a run is not a bench number
+    if args.profile:
         prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
         prof.__enter__()
-    with ClockSampler(dev_idx) as clocks:
+    loop.record = True
+    with ClockSampler(0 if shared_gpu else local) as clocks:
         torch.cuda.synchronize()
-        t0.record(stream)
-        for i in range(args.warmup, n_steps):
-            step(i)
-        t1.record(stream)
+        t0.record()
+        loop.run(args.warmup, n_steps)
+        t1.record()
         torch.cuda.synchronize()
+    loop.record = False
     ms = t0.elapsed_time(t1)
     if prof is not None:
         prof.__exit__(None, None, None)
@@ -351,21 +512,20 @@ def main():
         mt = torch.tensor([ms], device="cuda")
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
         ms = float(mt.item())
-        dist.barrier()
-    frames_total = args.steps * B * world
-    value = frames_total / (ms / 1e3)
+    value = args.steps * B * world / (ms / 1e3)
+    busy, flops, tiles2 = loop.conv_stats(t0)
+    conv_tflops = flops / (busy / 1e3) / 1e12
+    stage1 = eng.A * B * args.steps if mode == "pipeline" and args.density is None else 0
+    tiles_per_frame = (stage1 + tiles2) / (args.steps * B)
+    fields = {"value": value, "ms_per_step": ms / args.steps, "clocks": clocks.summary(),
+              "conv_tflops": conv_tflops, "conv_busy_ms": busy, "tiles_per_frame": tiles_per_frame,
+              "kernels": eng.net.kernel_summary()}
+    return fields, eng, objs, clip
 
-    # conv roofline over the timed steps
-    t2 = tiles2.cpu().numpy()
-    fwd_ms, flops = 0.0, 0.0
-    per_step = 2 if attention == "yolo" and args.density is None else 1
-    for i in range(args.warmup, n_steps):
-        pairs = ((per_step * i, B * eng.A), (per_step * i + 1, int(t2[i]))) if per_step == 2 \
-            else ((i, int(t2[i])),)
-        for k, nt in pairs:
-            fwd_ms += fwd_ev[k][0].elapsed_time(fwd_ev[k][1])
-            flops += nt * yolo.GFLOP_PER_TILE * 1e9
-    conv_tflops = flops / (fwd_ms / 1e3) / 1e12
+
+def roofline(args, f):
+    from paper_1810_10551_b200 import yolo
+
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -380,157 +540,221 @@ def main():
         pass
     exec_scale = (yolo.EXEC_GFLOP_PER_TILE_FP32 / yolo.GFLOP_PER_TILE
                   if args.precision == "fp32" else 1.0)
-    stage1 = eng.A * B * args.steps if per_step == 2 else 0
-    tiles_per_frame = (stage1 + float(t2[args.warmup:].sum())) / (args.steps * B)
-    launches_per_step = (1 + 24 + 1 + 1) + 2 + (1 + 24 + 1 + 1) + 1
-
-    # e2e through the public engine API with pinned host frames
-    e2e = None
-    if not args.no_e2e:
-        def launch(i, frames):
-            if args.density is not None:
-                eng.set_attention(injected[i % len(injected)])
-                eng.run_device(B, frames=frames, attention="inject")
-            else:
-                eng.run_device(B, frames=frames, attention=attention)
-
-        e2e = run_e2e(eng, clip, B, args, world, dist if world > 1 else None, launch)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        fps, threads, dt = cpu_baseline_frames_per_sec(objs, 1)
-        cpu = {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"1 frame (frame 0 of the clip, {dt:.1f}s): oracle run_sequence + "
-                         "torch-CPU fp32 YOLO v2, all host threads"}
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": args.precision, "data": "synthetic",
-            "precision": (f"{args.precision} operands/activations, fp32 accumulation (tcgen05 kind::f16)"
-                          if args.precision != "fp32" else
-                          "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
-                          "accumulation and epilogue"),
-            "config": {**arm_config(args, n_clip, world),
-                       **({"shared_gpu_logic_check": "all ranks on cuda:0 over gloo: not a "
-                                                     "scaling measurement"} if shared_gpu else {}),
-                       "l2": "inputs exceed L2 (746 MB per step)",
-                       "tiles_per_frame": tiles_per_frame,
-                       "crops_per_sec": value * tiles_per_frame},
-            "roofline": {"bound": "tensor", "kernel": "YOLO v2 conv stack: 23 tcgen05 launches per "
-                         f"forward ({eng.net.kernel_summary()}) + 1 maxpool",
-                         "achieved": conv_tflops, "peak": peak,
-                         "unit": "TFLOP/s", "frac": conv_tflops / peak,
-                         "traffic": traffic.get("dram_MB_per_tile", 0) * 1e6 if traffic else None,
-                         "traffic_unit": "DRAM bytes per 608^2 tile, ncu --set full capture "
-                                         f"(profiles/{tfile})",
-                         "algorithmic_bytes_per_tile": traffic.get("algorithmic_MB_per_tile", 0) * 1e6
-                         if traffic else None,
-                         "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
-                         "algorithmic": f"{yolo.GFLOP_PER_TILE:.3f} GFLOP per 608^2 tile",
-                         "executed_tflops": conv_tflops * exec_scale,
-                         "executed_frac": conv_tflops * exec_scale / peak,
-                         "executed": ("tensor-core FLOPs issued: hi/lo activations double K on "
-                                      f"every layer but layer 0 ({yolo.EXEC_GFLOP_PER_TILE_FP32:.1f} "
-                                      "GFLOP per tile)") if args.precision == "fp32"
-                         else "same as algorithmic",
-                         "conv_share_of_step": fwd_ms / ms},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks.summary(),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    a = f["conv_tflops"]
+    return {"bound": "tensor", "kernel": "YOLO v2 conv stack: 23 tcgen05 launches per forward "
+                                         f"({f['kernels']}) + 1 maxpool",
+            "achieved": a, "peak": peak, "unit": "TFLOP/s", "frac": a / peak,
+            "traffic": traffic.get("dram_MB_per_tile", 0) * 1e6 if traffic else None,
+            "traffic_unit": f"DRAM bytes per 608^2 tile, ncu --set full (profiles/{tfile})",
+            "algorithmic_bytes_per_tile": traffic.get("algorithmic_MB_per_tile", 0) * 1e6
+            if traffic else None,
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else
+                           "B200_PROFILING.md fallback",
+            "algorithmic": f"{yolo.GFLOP_PER_TILE:.3f} GFLOP per 608^2 tile",
+            "timing": "union of the CUDA-event intervals of every YOLO forward in the timed "
+                      "steps (stage 1 and stage 2 overlap on two streams)",
+            "executed_tflops": a * exec_scale, "executed_frac": a * exec_scale / peak,
+            "executed": (f"tensor-core FLOPs issued: hi/lo activations double K on every layer "
+                         f"but layer 0 ({yolo.EXEC_GFLOP_PER_TILE_FP32:.1f} GFLOP per tile)")
+            if args.precision == "fp32" else "same as algorithmic",
+            "conv_share_of_step": f["conv_busy_ms"] / (f["ms_per_step"] * args.steps)}
 
 
-def run_e2e(eng, clip, B, args, world, dist, launch):
-    """Public engine API with HOST frames: pinned staging, H2D of batch i+1 overlapped on a
-    copy stream, and every step's results (per-frame counts + the final record buffer)
-    copied to pinned host memory and read by the host while the next step runs."""
+def run_e2e(args, eng, objs, clip, rank, world, group):
+    """The same metric through the drop-in API with pinned HOST frames: run_stream
+    (N = 1) / run_stream_sharded (N > 1) over steps x batch frames per rank, FrameResults
+    built on the host. Wall clock around the call, max over ranks."""
     import torch
+    import torch.distributed as dist
 
-    from paper_1810_10551_b200 import native
+    from paper_1810_10551_b200 import distributed as D, native, pipeline as P, synthetic
     from paper_1810_10551_b200.engine import MAX_PER_FRAME
+    from paper_1810_10551_b200.stream import run_stream
 
-    # pinned host source = the clip (same frames as the device-resident run), capped at
-    # 16 GB per rank (binds only at 8K, where e2e is bound by the H2D copy itself)
-    frame_bytes = int(np.prod(clip.shape[1:]))
-    cap = max(B, (16 << 30) // frame_bytes // B * B)
-    n_clip = min(clip.shape[0], cap)
-    host = torch.empty((n_clip,) + tuple(clip.shape[1:]), dtype=torch.uint8, pin_memory=True)
-    host.copy_(clip[:n_clip].cpu())
-    dev = [torch.empty((B, H, W, 3), dtype=torch.uint8, device="cuda") for _ in range(2)]
-    copy_stream = torch.cuda.Stream()
-    done_copy = [torch.cuda.Event() for _ in range(2)]
-    done_use = [torch.cuda.Event() for _ in range(2)]
-    res_ready = [torch.cuda.Event() for _ in range(2)]
-    rec = native.PDET_DTYPE.itemsize
-    rec_bytes = B * MAX_PER_FRAME * rec
-    host_counts = [torch.empty(2 * B, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-    host_recs = [torch.empty(rec_bytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-    d2h = 2 * B * 4 + rec_bytes
-    n_steps = args.warmup + args.steps
-    seen = []
+    W, H = FRAMES[args.frame]
+    B = args.batch
+    settings = P.PipelineSettings.from_preset(args.preset)
+    frame_bytes = W * H * 3
+    n_host = min(clip.shape[0], max(B, (16 << 30) // frame_bytes // B * B))
+    host = torch.empty((n_host, H, W, 3), dtype=torch.uint8, pin_memory=True)
+    host.copy_(clip[:n_host].cpu())
+    prev = None
+    if rank > 0:
+        p = synthetic.bench_clip(W, H, args.clip_frames, seed=rank - 1)[-1]
+        prev = torch.empty((H, W, 3), dtype=torch.uint8, pin_memory=True)
+        prev.copy_(synthetic.render_frames_device(W, H, [p])[0].cpu())
 
-    def issue_copy(i):
-        s = (i * B) % n_clip
-        slot = i % 2
-        with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(done_use[slot])
-            dev[slot].copy_(host[s:s + B], non_blocking=True)
-            done_copy[slot].record(copy_stream)
+    def frames_for(n_per_rank, base_id):
+        """Global clip of world x n_per_rank frames; only this rank's shard (and the
+        frame before it) carries pixels."""
+        out = []
+        for r in range(world):
+            for j in range(n_per_rank):
+                fid = base_id + r * n_per_rank + j
+                px = None
+                if r == rank:
+                    px = host[j % n_host].numpy()
+                elif r == rank - 1 and j == n_per_rank - 1:
+                    px = prev.numpy()
+                out.append(P.Frame(fid, W, H, px))
+        return out
 
-    def consume(i):  # host read of step i's results (detection records of every frame)
-        if seen and seen[-1][0] >= i:
-            return
-        slot = i % 2
-        res_ready[slot].synchronize()
-        counts = host_counts[slot][:B]
-        m = int(counts.max().item())
-        det = host_recs[slot].view(B, -1)[:, : max(m, 1) * rec]
-        seen.append((i, int(counts.sum().item()), int(det.sum().item())))
+    def call(frames):
+        if world == 1:
+            return run_stream(frames, settings, engine=eng)
+        return D.run_stream_sharded(frames, settings, engine=eng, group=group)
 
-    def run(i):
-        slot = i % 2
-        cur = torch.cuda.current_stream()
-        cur.wait_event(done_copy[slot])
-        if i + 1 < n_steps:
-            issue_copy(i + 1)
-        launch(i, dev[slot])
-        done_use[slot].record()
-        # results -> pinned host slot, ordered before step i+1 overwrites them
-        host_counts[slot][:B].copy_(eng.ocounts[:B], non_blocking=True)
-        host_counts[slot][B:].copy_(eng.active_counts[:B], non_blocking=True)
-        host_recs[slot].copy_(eng.outp.view(-1)[:rec_bytes], non_blocking=True)
-        res_ready[slot].record()
-        if i > 0:
-            consume(i - 1)  # overlaps step i on the device
-
-    eng.reset_history(())
-    issue_copy(0)
-    for i in range(args.warmup):
-        run(i)
-    consume(args.warmup - 1)
+    call(frames_for(args.warmup * B, 10 ** 6))
     torch.cuda.synchronize()
-    if dist is not None:
+    if world > 1:
         dist.barrier()
+    frames = frames_for(args.steps * B, 0)
     t0 = time.perf_counter()
-    for i in range(args.warmup, n_steps):
-        run(i)
-    consume(n_steps - 1)
+    res = call(frames)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    if dist is not None:
+    if world > 1:
         mt = torch.tensor([dt], device="cuda")
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
         dt = float(mt.item())
+    n_dets = sum(len(r.detections) for r in res)
+    rec = native.PDET_DTYPE.itemsize
+    d2h = B * (MAX_PER_FRAME * rec + 5 * 4) + 256 * 32 * B  # records, counts, box lists
+    if world > 1:
+        d2h = world * (B * D.GATHER_CAP * rec + 4 * (4 + 2 * B)) if rank == 0 else 0
     return {"value": args.steps * B * world / dt, "unit": "frames/s",
-            "h2d_bytes_per_step": B * H * W * 3, "d2h_bytes_per_step": int(d2h),
-            "timing": "host wall clock around the loop; results of step i are read on the "
-                      "host while step i+1 runs"}
+            "h2d_bytes_per_step": B * frame_bytes, "d2h_bytes_per_step": int(d2h),
+            "api": "stream.run_stream" if world == 1 else "distributed.run_stream_sharded",
+            "frame_results": len(res), "detections": n_dets,
+            "timing": "host wall clock around the API call (pinned host frames in, "
+                      "FrameResults out; H2D, D2H and result objects inside), max over ranks"}
+
+
+def sub_results(args, rank, world, local, shared_gpu, group):
+    """BASELINE configs[2], [3], [4] and the fp16 mode as short timed runs (N = 1)."""
+    import gc
+
+    import torch
+
+    runs = [
+        ("configs[2]: all-crops baseline, 4K", ["--mode", "allcrops"]),
+        ("configs[3]: attention pipeline, 8K (60-frame clip)", ["--frame", "8k", "--clip-frames", "60"]),
+        ("configs[4]: density 0.5 (injected stage 1), 4K", ["--density", "0.5"]),
+        ("configs[4]: density 0.5 (injected stage 1), 8K", ["--density", "0.5", "--frame", "8k",
+                                                            "--clip-frames", "60"]),
+        ("fp16 fast mode (scores within ~5e-3), 4K", ["--precision", "fp16"]),
+    ]
+    out = []
+    for name, extra in runs:
+        sa = parse(["--steps", "5", "--warmup", "2", "--batch", str(args.batch)] + extra)
+        try:
+            f, eng, _, clip = gpu_run(sa, rank, world, local, shared_gpu, group, sub=True)
+        except Exception as exc:  # a sub-run must never sink the headline line
+            out.append({"config": name, "error": str(exc)[:300]})
+            continue
+        out.append({"config": name, "args": " ".join(extra), "value": f["value"],
+                    "unit": "frames/s", "ms_per_step": f["ms_per_step"], "steps": sa.steps,
+                    "warmup": sa.warmup, "tiles_per_frame": f["tiles_per_frame"],
+                    "crops_per_sec": f["value"] * f["tiles_per_frame"],
+                    "roofline_frac": f["conv_tflops"] / 1391.0,
+                    "conv_tflops": f["conv_tflops"], "clocks": f["clocks"]})
+        del eng, clip
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
+
+
+def kernel_table(prof, ms: float, steps: int) -> None:
+    """Per-kernel device time over the timed steps (warm, real overlap), to stderr."""
+    import torch
+
+    agg: dict[str, list] = {}
+    for ev in prof.events():
+        if ev.device_type != torch.autograd.DeviceType.CUDA:
+            continue
+        name = ev.name.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0]
+        a = agg.setdefault(name, [0.0, 0])
+        a[0] += ev.time_range.elapsed_us() / 1e3
+        a[1] += 1
+    busy = sum(v[0] for v in agg.values())
+    print(f"# kernel table: {steps} steps, {ms:.3f} ms wall (device), {busy:.3f} ms kernel busy",
+          file=sys.stderr)
+    for k, (t, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        print(f"{100 * t / ms:6.2f}% {t / steps:9.3f} ms/step {n // steps:5d}/step  {k}",
+              file=sys.stderr)
+
+
+def main():
+    args = parse()
+    if maybe_launch_ranks(args):
+        return
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+
+    import torch
+    import torch.distributed as dist
+
+    # TP_BENCH_SHARED_GPU=1: logic check of the multi-rank path on a one-GPU box (every
+    # rank on cuda:0, gloo collectives, ranks never wait on each other's kernels); such a
+    # run is flagged in its line and is not a scaling measurement
+    shared_gpu = os.environ.get("TP_BENCH_SHARED_GPU") == "1"
+    if not shared_gpu and torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: {world} ranks but {torch.cuda.device_count()} GPUs")
+    dev_idx = 0 if shared_gpu else local
+    torch.cuda.set_device(dev_idx)
+    group = None
+    if world > 1:
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    f, eng, objs, clip = gpu_run(args, rank, world, local, shared_gpu, group)
+    e2e = None if args.no_e2e else run_e2e(args, eng, objs, clip, rank, world, group)
+    cpu = None
+    subs = None
+    if rank == 0 and world == 1:
+        del clip
+        if not args.no_cpu_baseline:
+            cpu = cpu_baseline_with_parity(args, objs[: args.clip_frames])
+    if world == 1 and not args.no_sub and args.mode == "pipeline" and args.density is None \
+            and args.frame == "4k" and args.precision == "fp32":
+        del eng
+        subs = sub_results(args, rank, world, local, shared_gpu, group)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": f["value"], "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": f["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic",
+            "precision": (f"{args.precision} operands/activations, fp32 accumulation (tcgen05 "
+                          "kind::f16)" if args.precision != "fp32" else
+                          "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
+                          "accumulation and epilogue"),
+            "config": arm_config(args, world),
+            "workload_stats": {"tiles_per_frame": f["tiles_per_frame"],
+                               "crops_per_sec": f["value"] * f["tiles_per_frame"],
+                               "l2": f"inputs exceed L2 ({args.batch * FRAMES[args.frame][0] * FRAMES[args.frame][1] * 3 / 1e6:.0f} MB per step)",
+                               "schedule": "stage-1 look-ahead on a second stream"
+                               if not args.no_lookahead else "sequential stages",
+                               **({"shared_gpu_logic_check": "all ranks on cuda:0 over gloo: "
+                                   "not a scaling measurement"} if shared_gpu else {})},
+            "roofline": roofline(args, f),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": f["clocks"],
+        }
+        if subs is not None:
+            line["sub_results"] = subs
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
