@@ -160,11 +160,14 @@ class YoloNet:
     """Device-resident YOLO v2-608 plan over a persistent workspace (max_tiles tiles)."""
 
     def __init__(self, max_tiles: int, seed: int = 0, weights=None, head: str = "calibrated",
-                 dtype: str = DEFAULT_PRECISION, share: "YoloNet | None" = None):
+                 dtype: str = DEFAULT_PRECISION, share: "YoloNet | None" = None,
+                 guard_bytes: int = 0):
         """dtype "fp16" / "bf16": 16-bit activations; "fp32": the fp32-parity plan
         (TP_DTYPE_F16X2 — exact hi/lo fp16 activation pairs, same kernels, 2x K).
         share: another YoloNet whose device weights this one reuses (own workspace, so
-        the two can run concurrently on different streams)."""
+        the two can run concurrently on different streams).
+        guard_bytes: a canary region after the workspace (0xA5 bytes; guard_ok() checks
+        that no kernel wrote past the workspace) — for the robustness tests."""
         torch = native.require_cuda()
         lib = native.load()
         if share is not None:
@@ -186,7 +189,10 @@ class YoloNet:
             self.w_dev = [torch.from_numpy(w).to(self.tdtype).cuda() for w in wpacks]
             self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
         nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles, native.DTYPES[dtype]))
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self._alloc = torch.empty(nbytes + int(guard_bytes), dtype=torch.uint8, device="cuda")
+        self.workspace = self._alloc[:nbytes]
+        self.guard = self._alloc[nbytes:]
+        self.guard.fill_(0xA5)
         wptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.w_dev])
         bptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.b_dev])
         handle = ctypes.c_void_p()
@@ -196,6 +202,10 @@ class YoloNet:
         self.input_ptr = int(lib.tp_yolo_input(handle))
         self.head_ptr = int(lib.tp_yolo_head(handle))
         self.head_cstride = int(lib.tp_yolo_head_cstride())
+
+    def guard_ok(self) -> bool:
+        """True when the canary region after the workspace is intact."""
+        return bool((self.guard == 0xA5).all().item()) if self.guard.numel() else True
 
     def forward(self, n_tiles: int, n_tiles_dev=None, stream=None) -> None:
         native.call("tp_yolo_forward", self.handle, int(n_tiles), native.ptr(n_tiles_dev),
