@@ -104,15 +104,26 @@ def test_library_loads_and_exports_every_header_symbol():
 
 
 def test_product_never_imports_oracle():
+    """No module of the package or its subpackages imports oracle/ (nor loads it by name
+    through importlib / __import__)."""
     pkg = os.path.join(ROOT, "paper_1810_10551_b200")
-    for fn in os.listdir(pkg):
-        if fn.endswith(".py"):
-            tree = ast.parse(open(os.path.join(pkg, fn)).read())
+    n = 0
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if not fn.endswith(".py"):
+                continue
+            path = os.path.join(dirpath, fn)
+            src = open(path).read()
+            tree = ast.parse(src)
+            n += 1
             for node in ast.walk(tree):
                 if isinstance(node, ast.Import):
-                    assert not any(a.name.split(".")[0] == "oracle" for a in node.names), fn
+                    assert not any(a.name.split(".")[0] == "oracle" for a in node.names), path
                 if isinstance(node, ast.ImportFrom):
-                    assert (node.module or "").split(".")[0] != "oracle", fn
+                    assert (node.module or "").split(".")[0] != "oracle", path
+                if isinstance(node, ast.Constant) and isinstance(node.value, str):
+                    assert not node.value.startswith("oracle."), path
+    assert n >= 15  # walked the subpackages too (distribution/)
 
 
 def test_ops_fail_loudly_without_gpu():
