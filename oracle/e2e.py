@@ -165,3 +165,36 @@ def compare_dets(ref_dets, gpu_dets):
                 res["first_diff"] = ("order", i, (ra, la, ca), gpu_dets[i])
                 return res
     return res
+
+
+def synthetic_raw_detections(plan, n, seed=0, labels=("person", "car")):
+    """n raw stage-2 detections for one frame of `plan` shaped like the detector's output:
+    clusters of jittered boxes around objects (so NMS suppresses and the split-merge rule
+    fires across crop borders), each tagged with a final crop that contains its centre.
+    Returns [(crop_id, (rect int tuple, label, conf))] in crop order — final_pass order."""
+    rng = np.random.default_rng(seed)
+    fw, fh = plan.fw, plan.fh
+    fin = plan.fin[3]
+    n_obj = max(1, n // 8)
+    objs = []
+    for _ in range(n_obj):
+        w = int(rng.integers(40, 260))
+        h = int(rng.integers(40, 360))
+        objs.append((int(rng.integers(0, fw - w)), int(rng.integers(0, fh - h)), w, h,
+                     labels[int(rng.integers(0, len(labels)))]))
+    out = []
+    for k in range(n):
+        x, y, w, h, lab = objs[k % n_obj]
+        jx, jy = rng.normal(0, 0.06 * w), rng.normal(0, 0.06 * h)
+        sw, sh = rng.uniform(0.8, 1.2), rng.uniform(0.8, 1.2)
+        x1 = int(min(max(0, x + jx), fw - 2))
+        y1 = int(min(max(0, y + jy), fh - 2))
+        ww = int(max(1, min(fw - x1, w * sw)))
+        hh = int(max(1, min(fh - y1, h * sh)))
+        cx, cy = x1 + ww / 2, y1 + hh / 2
+        crops = [c for c in fin if c[3] <= cx < c[3] + c[5] and c[4] <= cy < c[4] + c[5]]
+        crop = crops[int(rng.integers(0, len(crops)))]
+        conf = float(np.float32(rng.uniform(0.25, 1.0)))
+        out.append((crop[0], ((x1, y1, ww, hh), lab, conf)))
+    out.sort(key=lambda t: t[0])  # final_pass: ascending crop id, detector order inside
+    return out
