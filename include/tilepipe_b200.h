@@ -108,9 +108,10 @@ TP_API int tp_device_sm_count(int* out);
 
 /* K1/K2: crop gather + resample (+ normalise). frames: u8 [n][H][W][3] with
  * frame_stride bytes between frames. out_u8: optional [n_jobs][608][608][3].
- * out_act: optional 16-bit (act_dtype) [n_jobs][610][610][8] layer-0 input (halo rows and
- * slot 609 must be pre-zeroed): padded row v+1, slot X in [0, 608] = [q(X-1) rgb0 | q(X) rgb0]
- * with q(u) = tile pixel u / 255 (0 outside [0, 608)).
+ * out_act: optional 16-bit (act_dtype) [n_jobs][610][614][4] layer-0 input: tile pixel
+ * (v, u) at [v+1][u+2] as (r, g, b, 0) with values / 255 (the integer values for
+ * TP_DTYPE_F16X2); the halo (rows 0 / 609, columns 0, 1, 610..613) must be pre-zeroed and
+ * is never written.
  * n_jobs_dev: optional device count overriding n_jobs (n_jobs is then the max). */
 TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
                     const tp_tile_job_t* jobs, int n_jobs, const int32_t* n_jobs_dev,
@@ -118,7 +119,7 @@ TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, i
 
 /* K3/K4: YOLO v2-608 forward plan (23 tcgen05 implicit-GEMM conv layers,
  * maxpools, route/reorg). Weights are 16-bit [cout_pad][taps*cin] K-major with
- * BN folded in (layer 0: [32][144], 3 kernel rows x 3 window variants x 16 — see
+ * BN folded in (layer 0: [32][144], 3 kernel rows x 3 window variants x 4 pixels x rgb0 — see
  * paper_1810_10551_b200/yolo.py L0_VARIANTS); biases fp32 [cout_pad]. */
 typedef struct tp_yolo_net tp_yolo_net;
 TP_API size_t tp_yolo_workspace_bytes(int max_tiles, int dtype);
@@ -141,7 +142,7 @@ TP_API int tp_yolo_destroy(tp_yolo_net* net);
 /* Generic implicit-GEMM conv (one layer), for tests. Activations are compact NHWC 16-bit
  * [n][res][res][cstride]; the zero padding of 3x3 convs is implicit (TMA out-of-bounds
  * fill). cin_stride == 16 is the layer-0 mode (K = 16 per kernel row): input is the
- * gather's padded slot image [n][res+2][res+2][8] and the conv must pool. pool != 0 fuses a 2x2/2 max pool
+ * gather's padded pixel image [n][res+2][res+6][4] and the conv must pool. pool != 0 fuses a 2x2/2 max pool
  * (out is then [n][res/2][res/2][out_cstride]). */
 TP_API int tp_conv(const void* in, int n_img, int res, int cin_stride, const void* weight,
                    const float* bias, int cout, int cout_pad, int ksize, int leaky, void* out,

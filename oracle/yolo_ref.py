@@ -10,7 +10,8 @@ pinned by the repo's own golden vectors (seeded weights, rendered synthetic tile
 
 Weight format (shared with the GPU path, built by paper_1810_10551_b200/yolo.py):
   per conv (in LAYERS order) a bf16-valued matrix [cout_pad][K], K index = tap*cin + c,
-  tap = ky*3 + kx (layer 0: K = 48 = ky x [kx 0..2, pad] x [rgb, pad]), BN folded,
+  tap = ky*3 + kx (layer 0: [32][144] = ky x 3 window variants x 4 pixel slots x rgb0,
+  variant 0 slots 1..3 = kx 0..2 — see paper_1810_10551_b200/yolo.py), BN folded,
   and a fp32 bias [cout_pad].
 Activation precision: mode "bf16"/"fp16" rounds every stored activation to that 16-bit
 type exactly like the GPU buffers (fp32 accumulation in between); "fp32" keeps fp32.
@@ -57,8 +58,8 @@ def unpack_weight(wpack, li):
 
     _, cin, cout, k, _ = LAYERS[li]
     w = torch.as_tensor(np.asarray(wpack, dtype=np.float32))
-    if li == 0:  # K = dy(3) x variant(3) x slot(4) x [rgb+pad]; variant 0 slots 0,1,3 = dx -1,0,1
-        w = w[:cout, :144].reshape(cout, 3, 3, 4, 4)[:, :, 0, [0, 1, 3], :cin].reshape(cout, 9, cin)
+    if li == 0:  # K = dy(3) x variant(3) x slot(4) x [rgb+pad]; variant 0 slots 1,2,3 = dx -1,0,1
+        w = w[:cout, :144].reshape(cout, 3, 3, 4, 4)[:, :, 0, [1, 2, 3], :cin].reshape(cout, 9, cin)
     else:
         w = w[:cout, : k * k * cin].reshape(cout, k * k, cin)
     return w.reshape(cout, k, k, cin).permute(0, 3, 1, 2).contiguous()

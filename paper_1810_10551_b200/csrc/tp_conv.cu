@@ -14,9 +14,9 @@
 //     rectangle loaded as a 4-D box {C, 16, 8, 1}; the epilogue pools in registers.
 //   * box tiles (conv_box_kernel: 3x3 with cin 32/64 and resident weights): one box
 //     {C, 10, 18} per 8x16 tile, the nine taps are descriptor row offsets into it.
-//   * layer 0 (conv_l0_kernel): reads the gather's padded 16-byte slots
-//     E(X) = [q(X-1) rgb0 | q(X) rgb0] as 32-byte-aligned windows of two slots; even
-//     columns take one MMA per kernel row, odd columns two (see the kernel comment).
+//   * layer 0 (conv_l0_kernel): reads the gather's padded 8-byte rgb0 pixels as
+//     overlapping 64-byte rows of 8 pixels starting at every even column; even columns
+//     take one MMA per kernel row, odd columns two (see the kernel comment).
 //
 // Kernels are persistent and warp-specialised, one CTA per SM (320 threads): warps 0-7
 // epilogue (two warpgroups on alternate accumulators, one TMEM lane quadrant per warp:
@@ -1580,15 +1580,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Layer 0 (3x3, 3->32, leaky, 2x2 maxpool) has K = 48 but 608^2 outputs per tile, so it
 // is bound by epilogue instructions, not math. Here each M row is one POOLED output
 // pixel: the four pool positions (py,px) accumulate into four TMEM accumulators.
-// Input: 16-byte slots E(X) = [q(X-1) | q(X)]; windows W(k) = E(2k) E(2k+1) =
-// [q(2k-1) q(2k) q(2k) q(2k+1)] are 32-byte aligned. Even conv columns x = 2k use W(k)
-// with weights [w-1 w0 0 w+1]; odd columns x = 2k+1 use W(k) with [0 w-1 0 w0] plus
-// W(k+1) with [0 w+1 0 0], so no window straddles a 32-byte sector. Both column phases of
-// window index k share one 64-byte A row [W(k) | W(k+1)] (SW64, K = 32): TMA loads one box
+// Input: 8-byte pixels P(u) = rgb0 of tile column u (zero halo: 1 row above / below, 2
+// columns left, 4 right). A row R(k) = P(2k-2) .. P(2k+5) is 64 bytes at a 16-byte
+// aligned offset, so one overlapping TMA view (k 16 B apart) serves every k. Even conv
+// columns x = 2k use the first 32 bytes [P(2k-2) P(2k-1) P(2k) P(2k+1)] with weights
+// [0 w-1 w0 w+1]; odd columns x = 2k+1 use the same 32 bytes with [0 0 w-1 w0] plus the
+// second 32 bytes [P(2k+2) ..] with [w+1 0 0 0] — no MMA operand straddles a 32-byte
+// K chunk. Both column phases of index k share R(k) (SW64, K = 32): TMA loads one box
 // {32 halves, 16 k, 9 rows (stride 2)} per input row phase — 288 box rows per tile, the
 // TMA row rate was this kernel's limit at 32-byte rows. Per tile (16x8 pooled = 32x16
 // conv pixels): 12 MMAs (K=16: per pool row and kernel row one N=64 MMA for both column
-// phases' W(k) term + one N=32 for the odd phase's W(k+1) term at +32 B); the epilogue
+// phases' first-chunk term + one N=32 for the odd phase's second chunk at +32 B); the epilogue
 // reads 4 x 32 columns per row and does max + bias + leaky + pack.
 constexpr int L0_BOX_ROWS = 9;                       // strided rows per box
 constexpr int L0_BOX_BYTES = L0_BOX_ROWS * 16 * 64;  // 9216: 9 rows x 16 windows x 64 B
@@ -1683,7 +1685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     {
       if (n_tiles > 0) tp::mbar_wait(bres_bar, 0);  // weights load only if this CTA has tiles
-      // A: SW64 rows of 64 B = [W(k) | W(k+1)]; B: SW32 rows of 32 B (K = 16)
+      // A: SW64 rows of 64 B = R(k); B: SW32 rows of 32 B (K = 16)
       const uint64_t a_desc0 = tp::umma_desc(tp::smem_u32(smA), 16, 512, 4);
       const uint64_t b_desc0 = tp::umma_desc(tp::smem_u32(smB), 16, 256, 6);
       const uint32_t idesc64 = tp::idesc_f16kind(128, 64, p.f16 == 0);
@@ -1705,8 +1707,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t ad0 = a_desc0 + (uint64_t)(s * (L0_STAGE >> 4));
         if (tp::elect_one()) {
           // pool row py: accumulators (py, px=0) and (py, px=1) are adjacent TMEM column
-          // blocks and both read window W(k) first, with adjacent weight chunks (even,
-          // odd-A) — one N=64 MMA; the odd column's W(k+1) term is one N=32 MMA
+          // blocks and both read R(k)'s first 32 bytes, with adjacent weight chunks (even,
+          // odd-A) — one N=64 MMA; the odd column's second-chunk term is one N=32 MMA
 #pragma unroll
           for (int py = 0; py < 2; ++py) {
             const uint32_t d = tmem_base + (uint32_t)(acc * 128 + py * 64);
@@ -1714,10 +1716,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int dy = 0; dy < 3; ++dy) {
               const int o = py + dy;  // input row offset + 1, in 0..3
               const int f = o & 1, start = o >> 1;
-              const uint32_t w0 = (f * L0_BOX_BYTES + start * 16 * 64) >> 4;  // W(k): K 0..15
+              const uint32_t w0 = (f * L0_BOX_BYTES + start * 16 * 64) >> 4;  // R(k) bytes 0..31: K 0..15
               const uint64_t bw = b_desc0 + (uint64_t)(dy * 3 * 64);
               tp::mma_bf16(d, ad0 + w0, bw, idesc64, dy != 0);
-              tp::mma_bf16(d + 32, ad0 + w0 + 2, bw + 128, p.idesc, 1);  // W(k+1): +32 B
+              tp::mma_bf16(d + 32, ad0 + w0 + 2, bw + 128, p.idesc, 1);  // R(k) bytes 32..63
             }
           }
           tp::mma_commit(&empty[s]);
@@ -2615,20 +2617,21 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
                    "side %% 32 == 0");
       return TP_ERR_UNSUPPORTED;
     }
-    const int wp = res + 2;
+    const int hp = res + 2, xp = res + 6;
     {
-      // 16-byte slots E(X) = [q(X-1) | q(X)]; the kernel reads 64-byte rows [W(k) | W(k+1)]
-      // (W(k) = E(2k) E(2k+1)) through a {32 halves, k (32 B apart: rows overlap), row} view
-      // with the SW64 swizzle (tools/tma_overlap_probe.cu)
-      const uint64_t dims[3] = {32, (uint64_t)(wp / 2 - 1), (uint64_t)max_img * wp};
-      const cuuint64_t strides[2] = {32, (cuuint64_t)wp * 16};
+      // 8-byte pixels P(c) = rgb0 of tile column c - 2 (rows padded by 1, columns by 2|4);
+      // the kernel reads 64-byte rows [P(2k) .. P(2k+7)] = tile columns 2k-2 .. 2k+5
+      // through a {32 halves, k (16 B apart: rows overlap), row} view with the SW64
+      // swizzle (tools/tma_overlap_probe.cu)
+      const uint64_t dims[3] = {32, (uint64_t)((xp - 8) / 2 + 1), (uint64_t)max_img * hp};
+      const cuuint64_t strides[2] = {16, (cuuint64_t)xp * 8};
       const uint32_t box[3] = {32, 16, 18};
       const uint32_t estr[3] = {1, 1, 2};
       rc = make_tmap(&L->tmA, in, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_64B, f16, 2, estr,
                      strides);
       if (rc) return rc;
     }
-    {  // weights [32][144]: per kernel row dy, variants (even, odd W(k), odd W(k+1)) x K 16
+    {  // weights [32][144]: per kernel row dy, variants (even, odd first, odd second) x K 16
       const uint64_t dims[2] = {144, 32};
       const uint32_t box[2] = {16, 32};
       rc = make_tmap(&L->tmB, weight, 2, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16);
@@ -3162,7 +3165,7 @@ enum Buf {
 struct BufDef {
   int res, ch, bytes_per;  // bytes per element
 };
-const BufDef kBufs[NBUF] = {{608, 8, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
+const BufDef kBufs[NBUF] = {{608, 4, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
                             {152, 64, 2},  {76, 128, 2},  {76, 256, 2},   {76, 128, 2},
                             {38, 256, 2},  {38, 512, 2},  {38, 256, 2},   {38, 512, 2},
                             {19, 512, 2},  {19, 1024, 2}, {19, 512, 2},   {19, 1024, 2},
@@ -3194,7 +3197,11 @@ int buf_ch(int b, int dtype) {
 
 size_t buf_bytes(int b, int max_tiles, int dtype) {
   // compact NHWC, except the layer-0 input (padded, written by the gather)
-  const size_t side = kBufs[b].res + (b == I608 ? 2 : 0);
+  // the layer-0 input is [610 rows][614 columns][rgb0] (tp_gather.cu): a 1-pixel zero halo
+  // above / below, 2 | 4 columns left / right for the 64-byte 8-pixel windows
+  if (b == I608)
+    return (size_t)max_tiles * (kBufs[b].res + 2) * (kBufs[b].res + 6) * 4 * 2;
+  const size_t side = kBufs[b].res;
   return (size_t)max_tiles * side * side * buf_ch(b, dtype) * kBufs[b].bytes_per;
 }
 

@@ -84,11 +84,13 @@ def round_to(a: np.ndarray, dtype: str) -> np.ndarray:
     return _bf16_round(a)
 
 
-# Layer 0 reads 32-byte windows W(k) = [q(2k-1) q(2k) q(2k) q(2k+1)] (4 pixel slots of
-# rgb0) of its 16-byte-slot input; per kernel row it has 3 weight variants over those
-# slots (csrc/tp_conv.cu conv_l0_kernel): even column x = 2k from W(k), odd column
-# x = 2k+1 from W(k) and W(k+1). Entry [variant][slot] = kernel column dx (-1/0/+1) or None.
-L0_VARIANTS = [(-1, 0, None, 1), (None, -1, None, 0), (None, 1, None, None)]
+# Layer 0 reads 64-byte rows R(k) = 8 pixels (rgb0, 8 bytes each) starting at tile column
+# 2k-2 of its input (csrc/tp_conv.cu conv_l0_kernel): per kernel row it has 3 weight
+# variants over the 4 pixel slots of a 32-byte K chunk: even column x = 2k from R(k)'s
+# first chunk (columns 2k-2 .. 2k+1), odd column x = 2k+1 from the first chunk and the
+# second (2k+2 .. 2k+5). Entry [variant][slot] = kernel column dx (-1/0/+1) or None.
+L0_VARIANTS = [(None, -1, 0, 1), (None, None, -1, 0), (1, None, None, None)]
+L0_SLOTS = [1, 2, 3]  # variant 0's slots of dx = -1, 0, +1 (inverse packing)
 
 
 def pack_weight(li: int, w: np.ndarray, dtype: str = "bf16") -> np.ndarray:
@@ -248,11 +250,11 @@ class YoloNet:
             n_tiles, 19, 19, self.head_cstride)
 
     def input_tensor(self, n_tiles: int):
-        """16-bit layer-0 input view [n, 610, 610, 8]: padded rows of 16-byte slots,
-        slot X = [q(X-1) rgb0 | q(X) rgb0] for tile pixels q (zero outside the tile);
+        """16-bit layer-0 input view [n, 610, 614, 4]: pixel (v, u) of a tile at [v+1][u+2]
+        as rgb0 (zero halo: one row above / below, two columns left, four right);
         q = value/255, or the integer value itself in the fp32-parity plan."""
-        nb = n_tiles * 610 * 610 * 8 * 2
-        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 610, 8)
+        nb = n_tiles * 610 * 614 * 4 * 2
+        return self._view(self.input_ptr, nb).view(self.tdtype).view(n_tiles, 610, 614, 4)
 
     def step_tensor(self, step: int, n_tiles: int):
         """16-bit view of a step's output buffer [n, R, R, C] (compact NHWC; in the
@@ -298,7 +300,7 @@ def _unpack(wpack: np.ndarray, li: int) -> np.ndarray:
     _, cin, cout, k, _ = LAYERS[li]
     w = np.asarray(wpack, dtype=np.float32)
     if li == 0:
-        w = w[:cout, :144].reshape(cout, 3, 3, 4, 4)[:, :, 0][:, :, [0, 1, 3], :cin]
+        w = w[:cout, :144].reshape(cout, 3, 3, 4, 4)[:, :, 0][:, :, L0_SLOTS, :cin]
         return np.ascontiguousarray(np.transpose(w, (0, 3, 1, 2)))  # cout, cin, ky, kx
     w = w[:cout, : k * k * cin].reshape(cout, k, k, cin)
     return np.ascontiguousarray(np.transpose(w, (0, 3, 1, 2)))

@@ -123,17 +123,14 @@ def test_conv_fused_pool_rect_tiles(cuda, cin, cout, res, n, dtype):
 
 
 def test_conv_layer0_expanded_input(cuda):
-    """Layer-0 mode: padded rows of 16-byte slots, slot X = [q(X-1) rgb0 | q(X) rgb0]
-    (TMA pairs slots x and x+2 into the 32-byte A row); compact pooled output."""
+    """Layer-0 mode: the gather's [res+2][res+6][rgb0] pixels (pixel (v, u) at [v+1][u+2],
+    zero halo), read as overlapping 64-byte 8-pixel rows; compact pooled output."""
     torch = cuda
     n, res = 2, 64
     g = torch.Generator(device="cpu").manual_seed(4)
     img = torch.rand(n, res, res, 3, generator=g).half().float()
-    qpad = torch.zeros(n, res, res + 2, 3)
-    qpad[:, :, 1:-1] = img
-    ex = torch.zeros(n, res + 2, res + 2, 8)
-    ex[:, 1:-1, 0:res + 1, 0:3] = qpad[:, :, 0:res + 1]
-    ex[:, 1:-1, 0:res + 1, 4:7] = qpad[:, :, 1:res + 2]
+    ex = torch.zeros(n, res + 2, res + 6, 4)
+    ex[:, 1:-1, 2:res + 2, 0:3] = img
     ex = ex.half().cuda()
     w = torch.randn(32, 3, 3, 3, generator=g) * 0.3  # cout, ky, kx, cin
     wpack = torch.from_numpy(yolo.pack_weight(0, w.permute(0, 3, 1, 2).numpy(), "fp16")).half().cuda()

@@ -53,14 +53,13 @@ def _run(cuda, net, tiles):
 def test_input_normalisation_matches_oracle(cuda, net, tiles):
     torch = cuda
     n = _run(cuda, net, tiles)
-    x = net.input_tensor(n)[:, 1:-1].float().cpu()  # interior rows, slots 0..609
+    x = net.input_tensor(n)[:, 1:-1].float().cpu()  # interior rows; column u at u + 2
     ref = yolo_ref.tiles_to_input(tiles, net.dtype).permute(0, 2, 3, 1)
-    if net.dtype == "fp32":  # the parity plan's slots hold the integer pixel values
+    if net.dtype == "fp32":  # the parity plan's input holds the integer pixel values
         ref = torch.from_numpy(tiles.astype(np.float32))
-    assert torch.equal(x[:, :, 1:609, 0:3], ref)            # slot X: q(X-1)
-    assert torch.equal(x[:, :, 0:608, 4:7], ref)            # slot X: q(X)
-    assert x[:, :, 0, 0:3].abs().max().item() == 0 and x[:, :, 608, 4:7].abs().max().item() == 0
-    assert x[..., [3, 7]].abs().max().item() == 0 and x[:, :, 609].abs().max().item() == 0
+    assert torch.equal(x[:, :, 2:610, 0:3], ref)
+    assert x[..., 3].abs().max().item() == 0
+    assert x[:, :, :2].abs().max().item() == 0 and x[:, :, 610:].abs().max().item() == 0
 
 
 def _check_layers(cuda, net, tiles):
@@ -84,7 +83,7 @@ def _check_layers(cuda, net, tiles):
         src_step = conv_inputs[step]
         _, cin, cout, k, res = yolo.LAYERS[li]
         if src_step < 0:
-            xin = net.input_tensor(n)[:, 1:-1, 0:608, 4:7].float()
+            xin = net.input_tensor(n)[:, 1:-1, 2:610, 0:3].float()
             if net.dtype == "fp32":
                 xin = xin / 255.0
         else:

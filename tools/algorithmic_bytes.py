@@ -1,7 +1,7 @@
 """Compulsory HBM bytes per 608^2 tile of one YOLO v2 forward (the roofline's
 `algorithmic_bytes_per_tile`): every activation buffer read once by its consumer and
 written once by its producer, in the stored layout of each plan (csrc/tp_conv.cu kBufs /
-kSteps): compact NHWC 16-bit, the layer-0 input as [610][610][8] slots, the head fp32
+kSteps): compact NHWC 16-bit, the layer-0 input as [610][614][4] rgb0 pixels, the head fp32
 [19][19][448]; the fp32-parity plan doubles every activation but the input and head.
 Weights are amortised over the batch and reported separately.
 
@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1810_10551_b200 import yolo  # noqa: E402
 
 # buffer: (stored side, channels, bytes per element)
-BUFS = {"I608": (610, 8, 2), "P304": (304, 32, 2), "P152": (152, 64, 2), "A152": (152, 128, 2),
+BUFS = {"I608": (610, 4, 2), "P304": (304, 32, 2), "P152": (152, 64, 2), "A152": (152, 128, 2),
         "B152": (152, 64, 2), "P76": (76, 128, 2), "A76": (76, 256, 2), "B76": (76, 128, 2),
         "P38": (38, 256, 2), "A38": (38, 512, 2), "B38": (38, 256, 2), "E38": (38, 512, 2),
         "P19": (19, 512, 2), "A19": (19, 1024, 2), "B19": (19, 512, 2), "C19": (19, 1024, 2),
@@ -38,7 +38,7 @@ def activation_mb(split: bool) -> float:
     total = 0
     for src, dst, och in STEPS:
         s, c, e = BUFS[src]
-        total += s * s * c * e * mult(src)
+        total += (610 * 614 * 4 * 2 if src == "I608" else s * s * c * e * mult(src))
         s, _, e = BUFS[dst]
         total += s * s * och * e * mult(dst)
     return total / 1e6

@@ -2,11 +2,14 @@
 
     python tools/gather_bench.py [--frames 30] [--mode nearest] [--dtype fp32]
 
-Cuts every final-grid crop of `--frames` synthetic 4K frames (P1 preset: 18 crops per
-frame, ~1280-px squares) into the YOLO input slots, back to back, timed with CUDA events.
-Bytes = slots written (608 rows x 610 slots x 16 B per tile) + the source rows' bytes at
-32-byte sector granularity (what DRAM must deliver); printed as GB/s and as a fraction of
-MEASURED_PEAKS.json hbm_gbs.
+Cuts every final-grid crop (736-px squares at 4K P1; --grid attention: the 2160-px
+stage-1 squares) of `--frames` synthetic 4K frames into the YOLO input, back to back,
+timed with CUDA events. Two byte counts per launch:
+  * algorithmic: read 3*min(side,608)^2 (nearest) or 3*min(side,1216)^2
+    (bilinear) + write 608^2 * 3 * 2 B (16-bit rgb) per tile;
+  * delivered: the 8-byte rgb0 pixels actually written (608^2 * 8 B per tile) + the
+    source rows' bytes at 32-byte sector granularity (what DRAM must deliver);
+each printed as GB/s and as a fraction of MEASURED_PEAKS.json hbm_gbs.
 """
 
 import argparse
@@ -78,13 +81,18 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.reps
-    wr = n * 608 * 610 * 16
+    wr = n * 608 * 608 * 8
     rd = read_bytes(jobs, W, H, a.mode == "nearest")
+    lim = 608 if a.mode == "nearest" else 1216
+    alg = sum(3 * min(j[4], lim) ** 2 + 608 * 608 * 6 for j in jobs)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     gbs = (wr + rd) / ms / 1e6
-    print(json.dumps({"tiles": n, "grid": a.grid, "side": jobs[0][4], "mode": a.mode, "ms": ms, "write_MB": wr / 1e6,
-                      "read_MB": rd / 1e6, "GB_per_s": gbs, "hbm_peak_GB_per_s": peak,
-                      "frac": gbs / peak}))
+    alg_gbs = alg / ms / 1e6
+    print(json.dumps({"tiles": n, "grid": a.grid, "side": jobs[0][4], "mode": a.mode, "ms": ms,
+                      "write_MB": wr / 1e6, "read_MB": rd / 1e6, "GB_per_s": gbs,
+                      "frac": gbs / peak, "algorithmic_MB": alg / 1e6,
+                      "algorithmic_GB_per_s": alg_gbs, "algorithmic_frac": alg_gbs / peak,
+                      "hbm_peak_GB_per_s": peak}))
 
 
 if __name__ == "__main__":
