@@ -575,9 +575,15 @@ def run_e2e(args, eng, objs, clip, rank, world, group):
     B = args.batch
     settings = P.PipelineSettings.from_preset(args.preset)
     frame_bytes = W * H * 3
-    n_host = min(clip.shape[0], max(B, (16 << 30) // frame_bytes // B * B))
+    # pinned host copy of the rank's clip: all of it up to 16 GB (4 GB per rank when
+    # several ranks share the host); a capped copy takes evenly spaced frames so the
+    # sparse / dense / mixed mix is kept
+    cap_bytes = (16 << 30) if world == 1 else (4 << 30)
+    n_host = min(clip.shape[0], max(B, cap_bytes // frame_bytes))
+    pick = np.linspace(0, clip.shape[0] - 1, n_host).round().astype(np.int64)
     host = torch.empty((n_host, H, W, 3), dtype=torch.uint8, pin_memory=True)
-    host.copy_(clip[:n_host].cpu())
+    for i in range(0, n_host, 16):
+        host[i:i + 16].copy_(clip[torch.from_numpy(pick[i:i + 16]).cuda()].cpu())
     prev = None
     if rank > 0:
         p = synthetic.bench_clip(W, H, args.clip_frames, seed=rank - 1)[-1]

@@ -265,8 +265,7 @@ class ShardSink:
         self.gather.launch(self.engine, k, n, failed is not None, want_records=self.rank == 0)
 
     def emit(self, k, n, chunk, timing):
-        from .detector import Detection
-        from .geometry import Rect
+        from .engine import records_to_detections
 
         hdr, recs = self.gather.read(k)
         B, H = self.B, BatchGather.HDR
@@ -280,12 +279,8 @@ class ShardSink:
                 if oc > self.cap and self.overflow is None:
                     self.overflow = (g, oc)
                 if self.rank == 0 and oc <= self.cap:
-                    names = self.engine.labels.names
-                    dets = tuple(
-                        Detection(Rect(int(x["x"]), int(x["y"]), int(x["w"]), int(x["h"])),
-                                  names[int(x["cls"])], float(x["conf"]))
-                        for x in recs[r, j, :oc])
-                    self.records[g] = (dets, ac)
+                    self.records[g] = (records_to_detections(recs[r, j, :oc],
+                                                             self.engine.labels.names), ac)
         if n and timing is not None:
             for j in range(n):
                 self.timings[self.ranges[self.rank][0] + k * B + j] = timing
