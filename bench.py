@@ -64,9 +64,10 @@ def parse(argv=None):
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--resample", default="nearest", choices=["nearest", "bilinear"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp16", "bf16"],
-                    help="activation precision: fp32 = hi/lo fp16 pairs, the parity plan "
-                         "(default); fp16/bf16 = 16-bit activations, ~2x faster")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp32x2", "fp16", "bf16"],
+                    help="activation precision: fp32 = the parity plan (default: fp16 hi/lo "
+                         "pairs up to 152^2, then fp16 hi + e4m3 lo planes); fp32x2 = hi/lo "
+                         "fp16 pairs on every layer; fp16/bf16 = 16-bit activations")
     ap.add_argument("--profile", action="store_true",
                     help="CUPTI kernel table of the timed steps to stderr (not a bench run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -523,6 +524,22 @@ def gpu_run(args, rank, world, local, shared_gpu, group, sub=False):
     return fields, eng, objs, clip
 
 
+PRECISION_NOTE = {
+    "fp32": "fp32-parity: activations as exact fp16 hi/lo pairs up to 152^2, then an fp16 hi "
+            "plane + an e4m3 lo plane (x - hi) * 2^11 (kind::f16 + kind::f8f6f4 into one fp32 "
+            "accumulator); fp32 accumulation and epilogue",
+    "fp32x2": "fp32-parity: activations as fp16 hi/lo pairs on every layer (2x K), fp32 "
+              "accumulation and epilogue",
+}
+EXECUTED_NOTE = {
+    "fp32": "tensor-core work issued, in kind::f16-rate GFLOP: hi/lo fp16 pairs double K on "
+            "layers 2-6, fp16 hi + e4m3 lo (f8f6f4 at 2x rate) make 1.5x K from layer 8 on "
+            "({:.1f} GFLOP per tile)",
+    "fp32x2": "tensor-core FLOPs issued: hi/lo activations double K on every layer but "
+              "layer 0 ({:.1f} GFLOP per tile)",
+}
+
+
 def roofline(args, f):
     from paper_1810_10551_b200 import yolo
 
@@ -538,8 +555,8 @@ def roofline(args, f):
         traffic = json.load(open(os.path.join(ROOT, "profiles", tfile)))
     except Exception:
         pass
-    exec_scale = (yolo.EXEC_GFLOP_PER_TILE_FP32 / yolo.GFLOP_PER_TILE
-                  if args.precision == "fp32" else 1.0)
+    exec_gf = yolo.exec_gflop_per_tile(args.precision)
+    exec_scale = exec_gf / yolo.GFLOP_PER_TILE
     a = f["conv_tflops"]
     return {"bound": "tensor", "kernel": "YOLO v2 conv stack: 23 tcgen05 launches per forward "
                                          f"({f['kernels']}) + 1 maxpool",
@@ -554,9 +571,7 @@ def roofline(args, f):
             "timing": "union of the CUDA-event intervals of every YOLO forward in the timed "
                       "steps (stage 1 and stage 2 overlap on two streams)",
             "executed_tflops": a * exec_scale, "executed_frac": a * exec_scale / peak,
-            "executed": (f"tensor-core FLOPs issued: hi/lo activations double K on every layer "
-                         f"but layer 0 ({yolo.EXEC_GFLOP_PER_TILE_FP32:.1f} GFLOP per tile)")
-            if args.precision == "fp32" else "same as algorithmic",
+            "executed": EXECUTED_NOTE.get(args.precision, "same as algorithmic").format(exec_gf),
             "conv_share_of_step": f["conv_busy_ms"] / (f["ms_per_step"] * args.steps)}
 
 
@@ -737,10 +752,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": f["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic",
-            "precision": (f"{args.precision} operands/activations, fp32 accumulation (tcgen05 "
-                          "kind::f16)" if args.precision != "fp32" else
-                          "fp32-parity: activations as fp16 hi/lo pairs (2x K), fp32 "
-                          "accumulation and epilogue"),
+            "precision": PRECISION_NOTE.get(
+                args.precision, f"{args.precision} operands/activations, fp32 accumulation "
+                                "(tcgen05 kind::f16)"),
             "config": arm_config(args, world),
             "workload_stats": {"tiles_per_frame": f["tiles_per_frame"],
                                "crops_per_sec": f["value"] * f["tiles_per_frame"],

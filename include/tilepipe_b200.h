@@ -53,8 +53,15 @@ enum { TP_RESAMPLE_NEAREST = 0, TP_RESAMPLE_BILINEAR = 1 };
  * channel c at stored channel 32*(c/16) + c%16, its lo part 16 further), so a C-channel
  * tensor has 2C stored channels and K spans both parts (weights duplicated per 16-channel
  * group); products are exact and accumulate in fp32, so activations carry ~22 bits. The
- * gather writes integer pixel values (exact in fp16) and layer 0 scales by 1/255 in fp32. */
-enum { TP_DTYPE_BF16 = 0, TP_DTYPE_F16 = 1, TP_DTYPE_F16X2 = 2 };
+ * gather writes integer pixel values (exact in fp16) and layer 0 scales by 1/255 in fp32.
+ * TP_DTYPE_F16F8 is the same parity contract at 3/4 of the tensor work: from the 76^2 stage
+ * on (layer 8's input) an activation is two planes, hi = fp16(x) [pix][C] and
+ * lo = e4m3((x - hi) * 2^TP_LO_EXP) [pix][C] bytes ("HL8"); a consumer runs K over hi with
+ * fp16 weights w * 2^c (kind::f16) and over lo with e4m3 weights w * 2^(c - TP_LO_EXP)
+ * (kind::f8f6f4, twice the rate) into one fp32 accumulator and scales it by 2^-c. Earlier
+ * layers keep the F16X2 pairs. tp_yolo_create_ex takes the extra weights and scales. */
+enum { TP_DTYPE_BF16 = 0, TP_DTYPE_F16 = 1, TP_DTYPE_F16X2 = 2, TP_DTYPE_F16F8 = 3 };
+#define TP_LO_EXP 11
 
 /* One 608x608 tile to produce: crop square (x, y, side) of batch frame `frame`. */
 typedef struct tp_tile_job {
@@ -125,6 +132,16 @@ typedef struct tp_yolo_net tp_yolo_net;
 TP_API size_t tp_yolo_workspace_bytes(int max_tiles, int dtype);
 TP_API int tp_yolo_create(int max_tiles, const void* const* weights, const float* const* biases,
                    void* workspace, size_t workspace_bytes, int dtype, tp_yolo_net** out);
+/* TP_DTYPE_F16F8 plan: weights_lo[l] = e4m3 [cout_pad][taps*cin] lo-pass weights of every
+ * layer with an HL8 input (NULL for the others), alphas[l] = accumulator scale 2^-c of
+ * those layers (1 elsewhere; ignored for layer 0). Other dtypes: weights_lo and alphas may
+ * be NULL (tp_yolo_create). */
+TP_API int tp_yolo_create_ex(int max_tiles, const void* const* weights,
+                             const void* const* weights_lo, const float* const* biases,
+                             const float* alphas, void* workspace, size_t workspace_bytes,
+                             int dtype, tp_yolo_net** out);
+/* Which conv slots read an HL8 input in the TP_DTYPE_F16F8 plan: bit l of the mask. */
+TP_API uint32_t tp_yolo_hl8_inputs(void);
 TP_API void* tp_yolo_input(tp_yolo_net* net);        /* 16-bit [max_tiles][610][610][8] slots */
 TP_API int tp_yolo_num_steps(void);
 TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][19][19][448] */
@@ -134,6 +151,9 @@ TP_API int tp_yolo_forward(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles
 TP_API int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_t* n_tiles_dev,
                           int first, int last, void* stream);
 TP_API int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int* res, int* cstride);
+/* lo plane (e4m3 bytes, same [pixel][channel] index as the hi plane) of an HL8 step output;
+ * *ptr = NULL for other outputs. */
+TP_API int tp_yolo_layer_output_lo(tp_yolo_net* net, int layer, void** ptr);
 /* Kernel the plan chose for conv slot 0..22: 0 conv_tc, 1 conv_pair (cta_group::2),
  * 2 conv_l0, 3 conv_box, 4 conv_pair_rect (cta_group::2, pooled); -1 on a bad argument. */
 TP_API int tp_yolo_layer_kernel(tp_yolo_net* net, int conv);

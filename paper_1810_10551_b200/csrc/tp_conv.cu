@@ -75,7 +75,16 @@ struct ConvParams {
   // lo = fp16(v - hi), interleaved per 16 channels ([hi 16 | lo 16], stored channel of real
   // channel c = 32 (c / 16) + c % 16, its lo part +16); out_coff is in stored channels.
   int split;
-  float alpha;  // layer 0: accumulator scale (1/255 when the input holds integer pixels)
+  float alpha;  // accumulator scale: 1/255 for layer 0's integer pixels, 2^-c for HL8 inputs
+  // HL8 activations (TP_DTYPE_F16F8, the fp32-parity plan): a hi plane fp16(x) [pix][C]
+  // plus a lo plane e4m3((x - hi) * 2^TP_LO_EXP) [pix][C] bytes. Input side: each tap's K
+  // runs kb_hi hi blocks (64 channels, kind::f16 against fp16 weights w * 2^c) then the
+  // lo blocks (128 channels, kind::f8f6f4 against e4m3 weights w * 2^(c - TP_LO_EXP)) into
+  // the same fp32 accumulator; both stage kinds are 128 rows x 128 bytes. Output side:
+  // out_lo (!= nullptr) receives the lo plane at the hi plane's [pixel][channel] index.
+  int lo_in;
+  int kb_hi;
+  void* out_lo;
   // profiling only (TP_CONV_DEBUG bits): 1 skip epilogue, 2 skip MMAs, 4 skip stores,
   // 8 skip TMEM loads, 16 no TMA (stale operands), 32 role cycle counters (g_conv_prof),
   // 64 unmerged pool-in-M MMAs (box kernel A/B)
@@ -175,7 +184,8 @@ __device__ unsigned long long g_conv_prof[8];
   if (p.dbg & 32) acc += clock64() - (t0)
 
 // Epilogue variants, chosen at compile time (EPI_SPLIT: TMA-stored hi/lo fp16 pairs).
-enum Epi { EPI_PLAIN = 0, EPI_POOL = 1, EPI_REORG = 2, EPI_F32 = 3, EPI_SPLIT = 4 };
+// EPI_HL8: TMA-stored fp16 hi plane (as EPI_PLAIN) + directly stored e4m3 lo plane.
+enum Epi { EPI_PLAIN = 0, EPI_POOL = 1, EPI_REORG = 2, EPI_F32 = 3, EPI_SPLIT = 4, EPI_HL8 = 5 };
 
 // 2*NP fp32 values -> NP packed fp16 pairs hi = fp16(v) and NP packed lo = fp16(v - hi)
 template <int NP>
@@ -197,6 +207,57 @@ __device__ __forceinline__ void store_split16(__nv_bfloat16* o, const float* f) 
   *reinterpret_cast<uint4*>(o + 8) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
   *reinterpret_cast<uint4*>(o + 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   *reinterpret_cast<uint4*>(o + 24) = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+}
+// HL8 lo plane: 16 fp32 values -> hi (8 packed fp16 pairs, as __floats2half2_rn) and the
+// residuals (v - hi) * 2^TP_LO_EXP as 16 e4m3 bytes (4 words, byte j = channel j; RN,
+// saturating at +-448 — only for |v| beyond ~448, where the hi part alone carries 2^-12)
+constexpr float kLoScale = 2048.0f;  // 2^TP_LO_EXP
+static_assert(TP_LO_EXP == 11, "kLoScale");
+__device__ __forceinline__ uint32_t e4m3x4(float a, float b, float c, float d) {
+  uint16_t lo, hi;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+  return (uint32_t)lo | ((uint32_t)hi << 16);
+}
+__device__ __forceinline__ void split_hl8(const float* f, uint32_t* hi, uint32_t* lo) {
+  float r[16];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    __half2 h = __floats2half2_rn(f[2 * j], f[2 * j + 1]);
+    const float2 hf = __half22float2(h);
+    r[2 * j] = (f[2 * j] - hf.x) * kLoScale;
+    r[2 * j + 1] = (f[2 * j + 1] - hf.y) * kLoScale;
+    hi[j] = *reinterpret_cast<uint32_t*>(&h);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) lo[j] = e4m3x4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+}
+// 16 HL8 values to the hi plane (fp16, 32 B at oh) and the lo plane (16 B at ol)
+__device__ __forceinline__ void store_hl8(__half* oh, uint8_t* ol, const float* f) {
+  uint32_t hi[8], lo[4];
+  split_hl8(f, hi, lo);
+  *reinterpret_cast<uint4*>(oh) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(oh + 8) = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+  *reinterpret_cast<uint4*>(ol) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+// one scalar HL8 value (hi fp16 + lo e4m3 byte)
+__device__ __forceinline__ void store_hl8_1(__half* oh, uint8_t* ol, float v) {
+  const __half h = __float2half_rn(v);
+  uint16_t pr;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(pr) : "f"(0.0f), "f"((v - __half2float(h)) * kLoScale));
+  *oh = h;
+  *ol = (uint8_t)(pr & 0xFF);
+}
+// tcgen05 MMA with e4m3 A/B (kind::f8f6f4, K = 32 per instruction: 32 bytes per row, the
+// same operand bytes per instruction as kind::f16's K = 16), fp32 accumulate
+__device__ __forceinline__ void mma_f8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 constexpr int kMaxBias = 1024;
 
@@ -231,11 +292,12 @@ struct TileIter {
 template <int MODE, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+                   const __grid_constant__ CUtensorMap tmB2, const ConvParams p) {
   constexpr int BK = MODE == MODE_SW128 ? 64 : 32;
   constexpr bool RECT = EPI == EPI_POOL;
   // FLAT plain / fp32 / split outputs leave through per-warp swizzled smem slabs + TMA stores
-  constexpr bool TSTORE = EPI == EPI_PLAIN || EPI == EPI_F32 || EPI == EPI_SPLIT;
+  constexpr bool TSTORE = EPI == EPI_PLAIN || EPI == EPI_F32 || EPI == EPI_SPLIT || EPI == EPI_HL8;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -334,6 +396,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_4d(a_dst, &tmA, &full[s], cb * BK, rx + dx, ry + dy, it.img);
             } else {  // im2col: 128 consecutive compact pixels, window shifted by the tap
               const int ox = p.ksize == 3 ? tap % 3 : 0, oy = p.ksize == 3 ? tap / 3 : 0;
+              if (cb >= p.kb_hi) {  // HL8 lo block: 128 e4m3 channels (same stage bytes)
+                const int cl = cb - p.kb_hi;
+                tma_load_im2col(a_dst, &tmA2, &full[s], cl * 128, f0.x + lo, f0.y + lo, f0.n,
+                                (uint16_t)ox, (uint16_t)oy);
+                tp::tma_load_2d(b_dst, &tmB2, &full[s], tap * p.cin + cl * 128, n0);
+                if (++s == S) {
+                  s = 0;
+                  ph ^= 1;
+                }
+                continue;
+              }
               tma_load_im2col(a_dst, &tmA, &full[s], cb * BK, f0.x + lo, f0.y + lo, f0.n,
                               (uint16_t)ox, (uint16_t)oy);
             }
@@ -381,7 +454,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         aph[acc] ^= 1;
         tp::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.sub * p.bn);
+        int cbk = 0;  // K block within the tap (>= kb_hi: an HL8 lo block)
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          const bool lo_blk = cbk >= p.kb_hi;
+          if (++cbk == p.kb_per_tap) cbk = 0;
           PROF_T0(t2);
           tp::mbar_wait(&full[s], ph);
           PROF_ADD(w_fu, t2);
@@ -409,6 +485,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                   tp::mma_bf16(dj, aw + 2 * k, bw + 2 * k, idesc, (kb | dy | k) != 0);
               }
             }
+          } else if (lo_blk) {  // 128 e4m3 channels = 4 x K32, 32 bytes per step as below
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_f8(d_tmem, ad0 + 2 * k, bd0 + 2 * k, idesc, 1);
           } else {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
@@ -435,6 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // group g takes the CTA's local tiles i with i % 2 == g; its 4 warps cover the 4
     // TMEM lane quadrants, all BN columns.
     const int g = (int)warp >> 2;
+    const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
@@ -503,10 +584,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float4 bb = b4[j];
-          f[4 * j + 0] += bb.x;
-          f[4 * j + 1] += bb.y;
-          f[4 * j + 2] += bb.z;
-          f[4 * j + 3] += bb.w;
+          f[4 * j + 0] = fmaf(f[4 * j + 0], alpha, bb.x);
+          f[4 * j + 1] = fmaf(f[4 * j + 1], alpha, bb.y);
+          f[4 * j + 2] = fmaf(f[4 * j + 2], alpha, bb.z);
+          f[4 * j + 3] = fmaf(f[4 * j + 3], alpha, bb.w);
         }
         if (leaky) {  // leaky(x) = max(x, 0.1x), identical to x > 0 ? x : 0.1x
 #pragma unroll
@@ -568,6 +649,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             st_shared_v4(rbase + (((2 * cs) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
             st_shared_v4(rbase + (((2 * cs + 1) ^ swz) << 4), pk[4], pk[5], pk[6], pk[7]);
+            if (EPI == EPI_HL8 && valid && !(p.dbg & 4)) {  // lo plane: 16 bytes per pixel
+              uint32_t hh[8], ll[4];
+              split_hl8(f, hh, ll);
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out_lo) +
+                                        (size_t)out_px * p.out_cstride + p.out_coff + ch0) =
+                  make_uint4(ll[0], ll[1], ll[2], ll[3]);
+            }
           }
           if (cs == CPS - 1) {
             fence_proxy_async_smem();
@@ -583,7 +671,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (!valid || !writer || ch0 >= p.cout || (p.dbg & 4)) continue;
-        if (p.split) {
+        if (p.out_lo != nullptr) {  // HL8 planes (reorg / pooled direct stores)
+          const size_t o = (size_t)out_px * p.out_cstride + p.out_coff +
+                           (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
+          store_hl8(reinterpret_cast<__half*>(p.out) + o, reinterpret_cast<uint8_t*>(p.out_lo) + o, f);
+        } else if (p.split) {
           const int creal = (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
           store_split16(reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride +
                             p.out_coff + 2 * creal,
@@ -679,6 +771,15 @@ __device__ __forceinline__ void mma_pair(uint32_t d, uint64_t a, uint64_t b, uin
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_pair_f8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void commit_pair_mc(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -691,7 +792,9 @@ template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_pair_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+                     const __grid_constant__ CUtensorMap tmC,
+                     const __grid_constant__ CUtensorMap tmA2,
+                     const __grid_constant__ CUtensorMap tmB2, const ConvParams p) {
   constexpr int BK = 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -784,10 +887,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int tap = kb / p.kb_per_tap;
           const int cb = kb - tap * p.kb_per_tap;
           const int ox = p.ksize == 3 ? tap % 3 : 0, oy = p.ksize == 3 ? tap / 3 : 0;
-          tma_load_im2col_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK, f0.x + lo,
-                               f0.y + lo, f0.n, (uint16_t)ox, (uint16_t)oy);
-          tma_load_2d_pair(smB + (size_t)s * p.b_stage_bytes, &tmB, lbar, tap * p.cin + cb * BK,
-                           n0 + (int)rank * half_bn);
+          if (cb < p.kb_hi) {
+            tma_load_im2col_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK,
+                                 f0.x + lo, f0.y + lo, f0.n, (uint16_t)ox, (uint16_t)oy);
+            tma_load_2d_pair(smB + (size_t)s * p.b_stage_bytes, &tmB, lbar, tap * p.cin + cb * BK,
+                             n0 + (int)rank * half_bn);
+          } else {  // HL8 lo block: 128 e4m3 channels, same stage bytes
+            const int cl = cb - p.kb_hi;
+            tma_load_im2col_pair(smA + (size_t)s * p.a_stage_bytes, &tmA2, lbar, cl * 128,
+                                 f0.x + lo, f0.y + lo, f0.n, (uint16_t)ox, (uint16_t)oy);
+            tma_load_2d_pair(smB + (size_t)s * p.b_stage_bytes, &tmB2, lbar,
+                             tap * p.cin + cl * 128, n0 + (int)rank * half_bn);
+          }
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -819,18 +930,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         aph[acc] ^= 1;
         tp::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn);
+        int cbk = 0;  // K block within the tap (>= kb_hi: an HL8 lo block)
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          const bool lo_blk = cbk >= p.kb_hi;
+          if (++cbk == p.kb_per_tap) cbk = 0;
           PROF_T0(t2);
           tp::mbar_wait(&full[s], ph);
           PROF_ADD(w_fu, t2);
           tp::tc_fence_after();
           const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
           const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
-#pragma unroll
           if (tp::elect_one()) {
+            if (lo_blk) {  // 128 e4m3 channels: 4 x K32 (32 bytes per row per step)
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_pair(d_tmem, ad0 + 2 * k, bd0 + 2 * k, p.idesc, (kb | k) != 0);
+              for (int k = 0; k < 4; ++k) mma_pair_f8(d_tmem, ad0 + 2 * k, bd0 + 2 * k, p.idesc, 1);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_pair(d_tmem, ad0 + 2 * k, bd0 + 2 * k, p.idesc, (kb | k) != 0);
+            }
             commit_pair_mc(&empty[s]);  // frees the stage in both CTAs
           }
           __syncwarp();
@@ -851,6 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ============ epilogue: both CTAs, own 128 rows; groups alternate accumulators ============
     const int g = (int)warp >> 2;
+    const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const bool f16 = p.f16 != 0;
     const bool leaky = p.leaky != 0;
@@ -887,10 +1006,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float4 bb = b4[j];
-          f[4 * j + 0] += bb.x;
-          f[4 * j + 1] += bb.y;
-          f[4 * j + 2] += bb.z;
-          f[4 * j + 3] += bb.w;
+          f[4 * j + 0] = fmaf(f[4 * j + 0], alpha, bb.x);
+          f[4 * j + 1] = fmaf(f[4 * j + 1], alpha, bb.y);
+          f[4 * j + 2] = fmaf(f[4 * j + 2], alpha, bb.z);
+          f[4 * j + 3] = fmaf(f[4 * j + 3], alpha, bb.w);
         }
         if (leaky) {
 #pragma unroll
@@ -938,6 +1057,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           st_shared_v4(rowa + (((2 * cs) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
           st_shared_v4(rowa + (((2 * cs + 1) ^ swz) << 4), pk[4], pk[5], pk[6], pk[7]);
+          if (EPI == EPI_HL8 && valid) {  // lo plane: 16 bytes per pixel and chunk
+            uint32_t hh[8], ll[4];
+            split_hl8(f, hh, ll);
+            *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out_lo) +
+                                      (size_t)(rbase + (int)lane) * p.out_cstride + p.out_coff +
+                                      ch0) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+          }
         }
         if (cs == CPS - 1) {
           fence_proxy_async_smem();
@@ -1000,7 +1126,9 @@ constexpr int PR_W = 16, PR_H = 8;  // one M = 128 block: 16 x 8 output pixels
 template <int MH, bool POOL>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_pair_rect_kernel(const __grid_constant__ CUtensorMap tmA,
-                          const __grid_constant__ CUtensorMap tmB, const ConvParams p) {
+                          const __grid_constant__ CUtensorMap tmB,
+                          const __grid_constant__ CUtensorMap tmA2,
+                          const __grid_constant__ CUtensorMap tmB2, const ConvParams p) {
   constexpr int BK = 64;
   constexpr int CH = PR_H * MH;  // output rows per CTA
   extern __shared__ uint8_t smem_raw[];
@@ -1087,13 +1215,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t lbar = mapa_rank(&full[s], 0);
           const int dx = kb / p.kb_per_tap - 1;
           const int cb = kb - (dx + 1) * p.kb_per_tap;
-          tma_load_4d_pair(smA + (size_t)s * p.a_stage_bytes, &tmA, lbar, cb * BK, x0 + dx,
-                           y0 - 1, img);
+          // HL8 lo block (cb >= kb_hi): 128 e4m3 channels of the lo plane, same box bytes
+          const bool lo_blk = cb >= p.kb_hi;
+          const int cc = lo_blk ? (cb - p.kb_hi) * 128 : cb * BK;
+          tma_load_4d_pair(smA + (size_t)s * p.a_stage_bytes, lo_blk ? &tmA2 : &tmA, lbar, cc,
+                           x0 + dx, y0 - 1, img);
           uint8_t* bdst = smB + (size_t)s * p.b_stage_bytes;
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy)
-            tma_load_2d_pair(bdst + dy * b_slice, &tmB, lbar,
-                             (dy * 3 + dx + 1) * p.cin + cb * BK, n0 + (int)rank * half_bn);
+            tma_load_2d_pair(bdst + dy * b_slice, lo_blk ? &tmB2 : &tmB, lbar,
+                             (dy * 3 + dx + 1) * p.cin + cc, n0 + (int)rank * half_bn);
           if (++s == S) {
             s = 0;
             ph ^= 1;
@@ -1118,20 +1249,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         aph[acc] ^= 1;
         tp::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * MH * p.bn);
+        int cbk = 0;  // K block within the kernel column (>= kb_hi: an HL8 lo block)
         for (int kb = 0; kb < p.num_kb; ++kb) {
+          const bool lo_blk = cbk >= p.kb_hi;
+          if (++cbk == p.kb_per_tap) cbk = 0;
           tp::mbar_wait(&full[s], ph);
           tp::tc_fence_after();
           const uint64_t ad0 = a_desc0 + (uint64_t)(s * a_step);
           const uint64_t bd0 = b_desc0 + (uint64_t)(s * b_step);
           if (tp::elect_one()) {
+            if (lo_blk) {
 #pragma unroll
-            for (int dy = 0; dy < 3; ++dy)
+              for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-              for (int h = 0; h < MH; ++h)  // M block h: output rows 8h .. 8h+7 of the CTA
+                for (int h = 0; h < MH; ++h)
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  mma_pair(d_tmem + (uint32_t)(h * p.bn), ad0 + (dy + PR_H * h) * a_row16 + 2 * k,
-                           bd0 + dy * b_slice16 + 2 * k, p.idesc, (kb | dy | k) != 0);
+                  for (int k = 0; k < 4; ++k)
+                    mma_pair_f8(d_tmem + (uint32_t)(h * p.bn),
+                                ad0 + (dy + PR_H * h) * a_row16 + 2 * k,
+                                bd0 + dy * b_slice16 + 2 * k, p.idesc, 1);
+            } else {
+#pragma unroll
+              for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                for (int h = 0; h < MH; ++h)  // M block h: output rows 8h .. 8h+7 of the CTA
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)
+                    mma_pair(d_tmem + (uint32_t)(h * p.bn), ad0 + (dy + PR_H * h) * a_row16 + 2 * k,
+                             bd0 + dy * b_slice16 + 2 * k, p.idesc, (kb | dy | k) != 0);
+            }
             commit_pair_mc(&empty[s]);
           }
           __syncwarp();
@@ -1147,6 +1293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===== epilogue: both CTAs, own rows; groups alternate accumulators =====
     const int g = (int)warp >> 2;
+    const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0, leaky = p.leaky != 0, spl = p.split != 0;
@@ -1191,16 +1338,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const float4 bb = b4[j];
-            f[4 * j + 0] += bb.x;
-            f[4 * j + 1] += bb.y;
-            f[4 * j + 2] += bb.z;
-            f[4 * j + 3] += bb.w;
+            f[4 * j + 0] = fmaf(f[4 * j + 0], alpha, bb.x);
+            f[4 * j + 1] = fmaf(f[4 * j + 1], alpha, bb.y);
+            f[4 * j + 2] = fmaf(f[4 * j + 2], alpha, bb.z);
+            f[4 * j + 3] = fmaf(f[4 * j + 3], alpha, bb.w);
           }
           if (leaky) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) f[j] = fmaxf(f[j], 0.1f * f[j]);
           }
           if (!store || ch0 >= p.cout || (p.dbg & 4)) continue;
+          if (p.out_lo != nullptr) {
+            const size_t oo = (size_t)(img * oimg + oy * ores + ox) * p.out_cstride + p.out_coff + ch0;
+            store_hl8(reinterpret_cast<__half*>(p.out) + oo, reinterpret_cast<uint8_t*>(p.out_lo) + oo, f);
+            continue;
+          }
           if (spl) {
             store_split16(o + 2 * ch0, f);
             continue;
@@ -1443,6 +1595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // epilogue: group g takes tiles i % 2 == g; warp q owns output channels q*32 .. q*32+31
     const int g = (int)warp >> 2;
+    const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const bool f16 = p.f16 != 0, leaky = p.leaky != 0, spl = p.split != 0;
     const int ores = POOL ? p.res >> 1 : p.res;
@@ -1465,9 +1618,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto put = [&](int y, int x, float v) {
         v += bco;
         if (leaky) v = fmaxf(v, 0.1f * v);
-        __half* o = reinterpret_cast<__half*>(p.out) +
-                    ((size_t)(img * ores + y) * ores + x) * p.out_cstride + sc;
-        if (spl) {
+        const size_t oi = ((size_t)(img * ores + y) * ores + x) * p.out_cstride + sc;
+        __half* o = reinterpret_cast<__half*>(p.out) + oi;
+        if (p.out_lo != nullptr) {  // HL8 planes (sc is the real channel)
+          store_hl8_1(o, reinterpret_cast<uint8_t*>(p.out_lo) + oi, v);
+        } else if (spl) {
           const __half h = __float2half_rn(v);
           o[0] = h;
           o[16] = __float2half_rn(v - __half2float(h));
@@ -1739,6 +1894,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int g = (int)warp >> 2;
+    const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const bool f16 = p.f16 != 0;
     uint32_t ph = 0, nslab = 0;
@@ -2077,6 +2233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ================= epilogue: two warpgroups alternate accumulators =================
     const int g = (int)warp >> 2;
+    const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const int row = (int)(q * 32 + lane);
     const bool f16 = p.f16 != 0;
@@ -2215,10 +2372,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float4 bb = b4[j];
-          f[4 * j + 0] += bb.x;
-          f[4 * j + 1] += bb.y;
-          f[4 * j + 2] += bb.z;
-          f[4 * j + 3] += bb.w;
+          f[4 * j + 0] = fmaf(f[4 * j + 0], alpha, bb.x);
+          f[4 * j + 1] = fmaf(f[4 * j + 1], alpha, bb.y);
+          f[4 * j + 2] = fmaf(f[4 * j + 2], alpha, bb.z);
+          f[4 * j + 3] = fmaf(f[4 * j + 3], alpha, bb.w);
         }
         if (leaky) {
 #pragma unroll
@@ -2402,6 +2559,73 @@ __global__ void maxpool2_split_kernel(const __half* __restrict__ in, int n_img, 
   }
 }
 
+// 2x2/2 max pool of an HL8 tensor (hi fp16 plane + e4m3 lo plane, same indexing): each
+// thread pools 8 channels by their values hi + lo * 2^-TP_LO_EXP and copies the winning
+// pixel's hi and lo codes (ties keep the first: the values are equal).
+__device__ __forceinline__ float2 e4m3x2_to_float2(uint16_t v) {
+  uint32_t h2;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(v));
+  return __half22float2(*reinterpret_cast<__half2*>(&h2));
+}
+__global__ void maxpool2_hl8_kernel(const __half* __restrict__ in, const uint8_t* __restrict__ in_lo,
+                                    int n_img, int res, int cstride, __half* __restrict__ out,
+                                    uint8_t* __restrict__ out_lo,
+                                    const int32_t* __restrict__ n_img_dev) {
+  if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
+  const int ores = res >> 1;
+  const int cg = cstride >> 3;
+  const long long total = (long long)n_img * ores * ores * cg;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % cg);
+    long long r = i / cg;
+    const int x = (int)(r % ores);
+    r /= ores;
+    const int y = (int)(r % ores);
+    const int img = (int)(r / ores);
+    float best[8];
+    uint16_t bh[8];
+    uint8_t bl[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const long long e = (((long long)img * res + 2 * y + (k >> 1)) * res + 2 * x + (k & 1)) *
+                              cstride + g * 8;
+      const uint4 h = *reinterpret_cast<const uint4*>(in + e);
+      const uint2 l = *reinterpret_cast<const uint2*>(in_lo + e);
+      const uint16_t* hs = reinterpret_cast<const uint16_t*>(&h);
+      const uint8_t* ls = reinterpret_cast<const uint8_t*>(&l);
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(hs + j));
+        const float2 lf = e4m3x2_to_float2((uint16_t)(ls[j] | (ls[j + 1] << 8)));
+        const float v0 = hf.x + lf.x * (1.0f / kLoScale), v1 = hf.y + lf.y * (1.0f / kLoScale);
+        if (k == 0 || v0 > best[j]) {
+          best[j] = v0;
+          bh[j] = hs[j];
+          bl[j] = ls[j];
+        }
+        if (k == 0 || v1 > best[j + 1]) {
+          best[j + 1] = v1;
+          bh[j + 1] = hs[j + 1];
+          bl[j + 1] = ls[j + 1];
+        }
+      }
+    }
+    const long long o = (((long long)img * ores + y) * ores + x) * cstride + g * 8;
+    uint4 ho;
+    uint2 lo;
+    uint16_t* hp = reinterpret_cast<uint16_t*>(&ho);
+    uint8_t* lp = reinterpret_cast<uint8_t*>(&lo);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      hp[j] = bh[j];
+      lp[j] = bl[j];
+    }
+    *reinterpret_cast<uint4*>(out + o) = ho;
+    *reinterpret_cast<uint2*>(out_lo + o) = lo;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -2444,7 +2668,7 @@ EncodeIm2colFn get_im2col_fn() {
 // output pixels x `bk` channels per load; window corner `lo` (-1 = 3x3 with zero padding,
 // 0 = 1x1). Out-of-bounds taps are zero-filled.
 int make_tmap_im2col(CUtensorMap* tm, const void* base, int cstride, int res, int n, int bk,
-                     int pixels, int lo, CUtensorMapSwizzle swz, bool f16) {
+                     int pixels, int lo, CUtensorMapSwizzle swz, bool f16, int esize = 2) {
   EncodeIm2colFn enc = get_im2col_fn();
   if (enc == nullptr) {
     tp_set_error("cuTensorMapEncodeIm2col unavailable (no CUDA driver?)");
@@ -2452,11 +2676,14 @@ int make_tmap_im2col(CUtensorMap* tm, const void* base, int cstride, int res, in
   }
   const cuuint64_t dims[4] = {(cuuint64_t)cstride, (cuuint64_t)res, (cuuint64_t)res,
                               (cuuint64_t)n};
-  const cuuint64_t strides[3] = {(cuuint64_t)cstride * 2, (cuuint64_t)cstride * 2 * res,
-                                 (cuuint64_t)cstride * 2 * res * res};
+  const cuuint64_t strides[3] = {(cuuint64_t)cstride * esize, (cuuint64_t)cstride * esize * res,
+                                 (cuuint64_t)cstride * esize * res * res};
   const int lower[2] = {lo, lo}, upper[2] = {lo, lo};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(tm, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+  const CUtensorMapDataType dt = esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : f16      ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                            : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = enc(tm, dt, 4,
                    const_cast<void*>(base), dims, strides, lower, upper, (cuuint32_t)bk,
                    (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2492,6 +2719,7 @@ int make_tmap(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
     }
   }
   const CUtensorMapDataType dt = esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : f16       ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUresult r = enc(tm, dt,
@@ -2551,6 +2779,7 @@ struct ConvLaunch {
   int swap;  // swapped-operand 3x3 kernel for 128 output channels (conv_swap_kernel)
   int box_bk;
   CUtensorMap tmA, tmB, tmC;
+  CUtensorMap tmA2, tmB2;  // HL8 input: lo-plane activations and e4m3 weights
   ConvParams p;
   size_t smem;
 };
@@ -2562,8 +2791,13 @@ struct ConvLaunch {
 int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_stride, int cin_used,
                  const void* weight, const float* bias, int cout, int cout_pad, int ksize,
                  int leaky, void* out, int out_cstride, int out_coff, int out_fp32, int reorg,
-                 int dtype, int pool, float alpha = 1.0f) {
+                 int dtype, int pool, float alpha = 1.0f, const void* in_lo = nullptr,
+                 const void* weight_lo = nullptr, void* out_lo = nullptr) {
   memset(L, 0, sizeof(*L));
+  if (out_lo != nullptr && (dtype != TP_DTYPE_F16 || out_fp32)) {
+    tp_set_error("conv: an HL8 output is an fp16 hi plane (dtype F16) + lo plane");
+    return TP_ERR_ARG;
+  }
   const bool f16 = dtype != TP_DTYPE_BF16;
   // TP_DTYPE_F16X2: split (hi/lo) 16-bit outputs; the fp32 head output stays fp32
   const int split = dtype == TP_DTYPE_F16X2 && !out_fp32 ? 1 : 0;
@@ -2606,6 +2840,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   p.reorg = reorg;
   p.split = split;
   p.alpha = alpha;
+  p.out_lo = out_lo;
   p.dbg = getenv("TP_CONV_DEBUG") ? atoi(getenv("TP_CONV_DEBUG")) : 0;
   // everything else in smem: 1 KB alignment slack, bias, barriers (<= 12 stages), TMEM slot
   const int fixed = 1024 + cout_pad * 4 + (2 * 12 + 6) * 8 + 16;
@@ -2952,6 +3187,37 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       L->smem = 1024 + (size_t)st * stage + bres + staging + (2 * st + 10) * 8 + cout_pad * 4 + 16;
     }
   }
+  p.kb_hi = p.kb_per_tap;
+  if (in_lo != nullptr) {
+    // HL8 input: after each tap's kb_hi fp16 blocks come cin/128 e4m3 lo blocks of the
+    // same stage bytes (128 rows x 128 B); FLAT im2col (tc / pair) and pair-rect only
+    const bool flat_tc = !L->pair && !L->prect && !L->box && !L->swap && !L->l0 && !p.rect;
+    if (!(L->pair || L->prect || flat_tc) || cin_used % 128 != 0 || weight_lo == nullptr ||
+        mode != MODE_SW128) {
+      tp_set_error("conv: HL8 input needs a FLAT or pair-rect SW128 layer with cin %% 128 == 0");
+      return TP_ERR_UNSUPPORTED;
+    }
+    p.lo_in = 1;
+    p.kb_hi = cin_used / 64;
+    p.kb_per_tap = p.kb_hi + cin_used / 128;
+    p.num_kb = (L->prect ? 3 : taps) * p.kb_per_tap;
+    if (L->prect) {
+      const uint64_t adims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
+      const uint32_t abox[4] = {128, PR_W, (uint32_t)(PR_H * p.sub + 2), 1};
+      rc = make_tmap(&L->tmA2, in_lo, 4, adims, abox, CU_TENSOR_MAP_SWIZZLE_128B, f16, 1);
+    } else {
+      rc = make_tmap_im2col(&L->tmA2, in_lo, cin_stride, res, max_img, 128, 128,
+                            ksize == 3 ? -1 : 0, CU_TENSOR_MAP_SWIZZLE_128B, f16, 1);
+    }
+    if (rc) return rc;
+    const uint64_t wdims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+    const uint32_t wbox[2] = {128, (uint32_t)(L->pair || L->prect ? p.bn / 2 : p.bn)};
+    rc = make_tmap(&L->tmB2, weight_lo, 2, wdims, wbox, CU_TENSOR_MAP_SWIZZLE_128B, f16, 1);
+    if (rc) return rc;
+  } else {
+    L->tmA2 = L->tmA;  // unused
+    L->tmB2 = L->tmB;
+  }
   return TP_OK;
 }
 
@@ -2980,7 +3246,7 @@ int launch_mode(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   const long long tiles = m_blocks * p.n_blocks_n;
   if (tiles == 0) return TP_OK;
   int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_tc_kernel<MODE, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
+  conv_tc_kernel<MODE, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, L.tmA2, L.tmB2, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
@@ -3007,7 +3273,7 @@ int launch_pair(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_kernel<EPI>, L.tmA, L.tmB, L.tmC, p));
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_kernel<EPI>, L.tmA, L.tmB, L.tmC, L.tmA2, L.tmB2, p));
   return TP_OK;
 }
 
@@ -3033,7 +3299,7 @@ int launch_pair_rect(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_rect_kernel<MH, POOL>, L.tmA, L.tmB, p));
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_pair_rect_kernel<MH, POOL>, L.tmA, L.tmB, L.tmA2, L.tmB2, p));
   return TP_OK;
 }
 
@@ -3093,6 +3359,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
   if (L.pair)
     return L.p.out_fp32 ? launch_pair<EPI_F32>(L, n_img, n_img_dev, st)
            : L.p.split  ? launch_pair<EPI_SPLIT>(L, n_img, n_img_dev, st)
+           : L.p.out_lo ? launch_pair<EPI_HL8>(L, n_img, n_img_dev, st)
                         : launch_pair<EPI_PLAIN>(L, n_img, n_img_dev, st);
   if (L.l0) {
     if (int rc = ensure_smem_optin(conv_l0_kernel)) return rc;
@@ -3107,13 +3374,14 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
     return TP_OK;
   }
   const int epi = L.p.rect ? EPI_POOL : L.p.reorg ? EPI_REORG : L.p.out_fp32 ? EPI_F32
-                : L.p.split ? EPI_SPLIT : EPI_PLAIN;
+                : L.p.split ? EPI_SPLIT : L.p.out_lo ? EPI_HL8 : EPI_PLAIN;
 #define TP_EPI_SWITCH(M)                                                  \
   switch (epi) {                                                          \
     case EPI_POOL: return launch_mode<M, EPI_POOL>(L, n_img, n_img_dev, st);   \
     case EPI_REORG: return launch_mode<M, EPI_REORG>(L, n_img, n_img_dev, st); \
     case EPI_F32: return launch_mode<M, EPI_F32>(L, n_img, n_img_dev, st);     \
     case EPI_SPLIT: return launch_mode<M, EPI_SPLIT>(L, n_img, n_img_dev, st); \
+    case EPI_HL8: return launch_mode<M, EPI_HL8>(L, n_img, n_img_dev, st);     \
     default: return launch_mode<M, EPI_PLAIN>(L, n_img, n_img_dev, st);        \
   }
   if (L.mode == MODE_SW128) {
@@ -3124,11 +3392,19 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
 }
 
 int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStream_t st,
-             const int32_t* n_img_dev, int f16, int split = 0) {
+             const int32_t* n_img_dev, int f16, int split = 0, const void* in_lo = nullptr,
+             void* out_lo = nullptr) {
   const long long total = (long long)n_img * (res / 2) * (res / 2) * (cstride / (split ? 16 : 8));
   if (total == 0) return TP_OK;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  if (in_lo != nullptr) {
+    maxpool2_hl8_kernel<<<(int)blocks, 256, 0, st>>>((const __half*)in, (const uint8_t*)in_lo,
+                                                     n_img, res, cstride, (__half*)out,
+                                                     (uint8_t*)out_lo, n_img_dev);
+    TP_LAUNCH_CHECK();
+    return TP_OK;
+  }
   if (split) {
     maxpool2_split_kernel<<<(int)blocks, 256, 0, st>>>((const __half*)in, n_img, res, cstride,
                                                       (__half*)out, n_img_dev);
@@ -3189,10 +3465,22 @@ const Step kSteps[] = {
     {0, 20, E38, CAT19, 0, 1, 0}, {0, 21, CAT19, A19, 0, 0, 0}, {0, 22, A19, HEAD, 0, 0, 0}};
 constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
 
-// channels stored per pixel: the split plan doubles every activation except the layer-0
-// slots (integer pixel values, exact in fp16) and the fp32 head
-int buf_ch(int b, int dtype) {
-  return kBufs[b].ch * (dtype == TP_DTYPE_F16X2 && b != I608 && b != HEAD ? 2 : 1);
+// Storage format of a buffer: the F16X2 plan pairs every activation but the layer-0 slots
+// (integer pixel values, exact in fp16) and the fp32 head; the F16F8 plan keeps F16X2 up to
+// the 152^2 stage and stores the 76^2 .. 19^2 activations as HL8 planes (TP_DTYPE_F16F8).
+enum BufFmt { FMT_PLAIN = 0, FMT_X2 = 1, FMT_HL8 = 2 };
+int buf_fmt(int b, int dtype) {
+  if (b == I608 || b == HEAD) return FMT_PLAIN;
+  if (dtype == TP_DTYPE_F16X2) return FMT_X2;
+  if (dtype == TP_DTYPE_F16F8) return b >= P76 ? FMT_HL8 : FMT_X2;
+  return FMT_PLAIN;
+}
+// channels stored per pixel (hi plane for HL8)
+int buf_ch(int b, int dtype) { return kBufs[b].ch * (buf_fmt(b, dtype) == FMT_X2 ? 2 : 1); }
+// bytes of an HL8 buffer's e4m3 lo plane (0 for other formats)
+size_t buf_lo_bytes(int b, int max_tiles, int dtype) {
+  if (buf_fmt(b, dtype) != FMT_HL8) return 0;
+  return (size_t)max_tiles * kBufs[b].res * kBufs[b].res * kBufs[b].ch;
 }
 
 size_t buf_bytes(int b, int max_tiles, int dtype) {
@@ -3211,25 +3499,50 @@ struct tp_yolo_net {
   int max_tiles;
   int dtype;
   void* bufs[NBUF];
+  void* lo[NBUF];  // HL8 lo planes (nullptr for other formats)
   ConvLaunch convs[23];
 };
 
 extern "C" size_t tp_yolo_workspace_bytes(int max_tiles, int dtype) {
   size_t total = 0;
-  for (int b = 0; b < NBUF; ++b) total += (buf_bytes(b, max_tiles, dtype) + 1023) & ~size_t(1023);
+  for (int b = 0; b < NBUF; ++b) {
+    total += (buf_bytes(b, max_tiles, dtype) + 1023) & ~size_t(1023);
+    total += (buf_lo_bytes(b, max_tiles, dtype) + 1023) & ~size_t(1023);
+  }
   return total;
+}
+
+extern "C" uint32_t tp_yolo_hl8_inputs(void) {
+  uint32_t m = 0;
+  for (int s = 0; s < kNumSteps; ++s)
+    if (!kSteps[s].is_pool && buf_fmt(kSteps[s].in, TP_DTYPE_F16F8) == FMT_HL8)
+      m |= 1u << kSteps[s].conv;
+  return m;
 }
 
 extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
                               const float* const* biases, void* workspace,
                               size_t workspace_bytes, int dtype, tp_yolo_net** out) {
+  return tp_yolo_create_ex(max_tiles, weights, nullptr, biases, nullptr, workspace,
+                           workspace_bytes, dtype, out);
+}
+
+extern "C" int tp_yolo_create_ex(int max_tiles, const void* const* weights,
+                                 const void* const* weights_lo, const float* const* biases,
+                                 const float* alphas, void* workspace, size_t workspace_bytes,
+                                 int dtype, tp_yolo_net** out) {
   if (max_tiles < 1 || weights == nullptr || biases == nullptr || workspace == nullptr ||
       out == nullptr) {
     tp_set_error("tp_yolo_create: bad argument");
     return TP_ERR_ARG;
   }
-  if (dtype != TP_DTYPE_BF16 && dtype != TP_DTYPE_F16 && dtype != TP_DTYPE_F16X2) {
+  if (dtype != TP_DTYPE_BF16 && dtype != TP_DTYPE_F16 && dtype != TP_DTYPE_F16X2 &&
+      dtype != TP_DTYPE_F16F8) {
     tp_set_error("tp_yolo_create: bad dtype %d", dtype);
+    return TP_ERR_ARG;
+  }
+  if (dtype == TP_DTYPE_F16F8 && (weights_lo == nullptr || alphas == nullptr)) {
+    tp_set_error("tp_yolo_create: the F16F8 plan needs lo weights and accumulator scales");
     return TP_ERR_ARG;
   }
   if (workspace_bytes < tp_yolo_workspace_bytes(max_tiles, dtype)) {
@@ -3243,6 +3556,9 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
   for (int b = 0; b < NBUF; ++b) {
     net->bufs[b] = w;
     w += (buf_bytes(b, max_tiles, dtype) + 1023) & ~size_t(1023);
+    const size_t lb = buf_lo_bytes(b, max_tiles, dtype);
+    net->lo[b] = lb ? w : nullptr;
+    w += (lb + 1023) & ~size_t(1023);
   }
   // halos (and every never-written byte) must be zero
   cudaError_t e = cudaMemset(workspace, 0, tp_yolo_workspace_bytes(max_tiles, dtype));
@@ -3257,16 +3573,23 @@ extern "C" int tp_yolo_create(int max_tiles, const void* const* weights,
     const LayerDef& L = kConvs[st.conv];
     const int cout_pad = L.cout == 425 ? kHeadCstride : L.cout;
     const bool head = (st.out == HEAD);
-    // split plan: K covers the interleaved hi/lo input (duplicated weights); layer 0 reads
-    // integer pixels and scales its accumulators by 1/255
-    const bool split = dtype == TP_DTYPE_F16X2;
-    const int cin = split && st.conv != 0 ? 2 * L.cin : L.cin;
-    const int coff = split ? 2 * st.coff : st.coff;
+    // X2 input: K covers the interleaved hi/lo pairs (duplicated weights); HL8 input: hi
+    // blocks + e4m3 lo blocks, accumulator scaled by alphas[conv]; layer 0 reads integer
+    // pixels in both parity plans and scales its accumulators by 1/255
+    const int fin = buf_fmt(st.in, dtype), fout = buf_fmt(st.out, dtype);
+    const bool parity = dtype == TP_DTYPE_F16X2 || dtype == TP_DTYPE_F16F8;
+    const int cin = fin == FMT_X2 && st.conv != 0 ? 2 * L.cin : L.cin;
+    const int coff = fout == FMT_X2 ? 2 * st.coff : st.coff;
+    const int ldt = dtype == TP_DTYPE_F16F8 ? (fout == FMT_X2 ? TP_DTYPE_F16X2 : TP_DTYPE_F16)
+                                            : dtype;
+    const float alpha = parity && st.conv == 0 ? 1.0f / 255.0f
+                        : fin == FMT_HL8       ? alphas[st.conv]
+                                               : 1.0f;
     int rc = prepare_conv(&net->convs[st.conv], net->bufs[st.in], max_tiles, L.res,
                           buf_ch(st.in, dtype), cin, weights[st.conv], biases[st.conv], L.cout,
                           cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], buf_ch(st.out, dtype),
-                          coff, head ? 1 : 0, st.reorg, dtype, st.fpool,
-                          split && st.conv == 0 ? 1.0f / 255.0f : 1.0f);
+                          coff, head ? 1 : 0, st.reorg, ldt, st.fpool, alpha, net->lo[st.in],
+                          fin == FMT_HL8 ? weights_lo[st.conv] : nullptr, net->lo[st.out]);
     if (rc) {
       delete net;
       return rc;
@@ -3296,7 +3619,7 @@ extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_
     if (sp.is_pool) {
       rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, buf_ch(sp.in, net->dtype),
                     net->bufs[sp.out], st, n_tiles_dev, net->dtype != TP_DTYPE_BF16,
-                    net->dtype == TP_DTYPE_F16X2);
+                    buf_fmt(sp.in, net->dtype) == FMT_X2, net->lo[sp.in], net->lo[sp.out]);
     } else {
       rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
     }
@@ -3321,6 +3644,15 @@ extern "C" int tp_yolo_layer_output(tp_yolo_net* net, int layer, void** ptr, int
   *ptr = net->bufs[b];
   *res = kBufs[b].res;
   *cstride = buf_ch(b, net->dtype);
+  return TP_OK;
+}
+
+extern "C" int tp_yolo_layer_output_lo(tp_yolo_net* net, int layer, void** ptr) {
+  if (net == nullptr || layer < 0 || layer >= kNumSteps || ptr == nullptr) {
+    tp_set_error("tp_yolo_layer_output_lo: bad step %d", layer);
+    return TP_ERR_ARG;
+  }
+  *ptr = net->lo[kSteps[layer].out];
   return TP_OK;
 }
 

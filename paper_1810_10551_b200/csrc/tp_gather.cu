@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
 
   // Per-CTA tables, shared by all ROWS rows of this tile:
   //   lut: exact value/255 in the activation type (bit-identical to dividing); the
-  //   integer value itself for TP_DTYPE_F16X2 (layer 0 then scales by 1/255 in fp32)
+  //   integer value itself for the parity plans (layer 0 then scales by 1/255 in fp32)
   //   cx0/cx1: byte offset 3*x of the column's source tap(s) in a frame row, -1 outside
   //   the frame (or outside the tile for u = 608); cf: bilinear weight of tap 1
   __shared__ uint16_t lut[256];
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
   __shared__ __align__(16) uint8_t tabmem[(S + 1) * (nearest ? 4 : 16)];
   int* cx0 = reinterpret_cast<int*>(tabmem);
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    if (act_dtype == TP_DTYPE_F16X2) {  // fp32-parity plan: the integer value (exact)
+    if (act_dtype == TP_DTYPE_F16X2 || act_dtype == TP_DTYPE_F16F8) {  // parity plans: the integer value (exact)
       __half h = __float2half_rn((float)i);
       lut[i] = *reinterpret_cast<uint16_t*>(&h);
     } else if (act_dtype == TP_DTYPE_F16) {
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
       reinterpret_cast<int4*>(tabmem)[u] = make_int4(o0, in_tile && x1 >= 0 && x1 < W ? 3 * x1 : -1, f, 0);
   }
   __syncthreads();
-  const bool exact_int = act_dtype == TP_DTYPE_F16X2;
+  const bool exact_int = act_dtype == TP_DTYPE_F16X2 || act_dtype == TP_DTYPE_F16F8;
   // pixel -> (r,g | b,0) packed in the activation type. The parity plan stores the integer
   // value itself: fp16(1024 + n) has bits 0x6400 + n, so one packed half2 subtraction of
   // 1024 turns two bytes into two exact fp16 integers.

@@ -38,7 +38,10 @@ PDET_DTYPE = np.dtype(
 assert JOB_DTYPE.itemsize == 32 and DET_DTYPE.itemsize == 48 and PDET_DTYPE.itemsize == 56
 
 RESAMPLE = {"nearest": 0, "bilinear": 1}
-DTYPES = {"bf16": 0, "fp16": 1, "fp32": 2}  # "fp32" = TP_DTYPE_F16X2 (hi/lo pair plan)
+# "fp32" = TP_DTYPE_F16F8 (the fp32-parity plan: F16X2 pairs up to 152^2, then fp16 hi + e4m3
+# lo planes), "fp32x2" = TP_DTYPE_F16X2 (hi/lo fp16 pairs everywhere)
+DTYPES = {"bf16": 0, "fp16": 1, "fp32x2": 2, "fp32": 3}
+PARITY_DTYPES = ("fp32", "fp32x2")
 TP_MAX_CLASSES = 128
 RULES = {"vertical": 1, "horizontal": 2, "both": 3}
 
@@ -83,6 +86,9 @@ SIGNATURES = {
     "tp_yolo_workspace_bytes": (_SZ, [_I, _I]),
     "tp_yolo_layer_kernel": (_I, [_P, _I]),
     "tp_yolo_create": (_I, [_I, _P, _P, _P, _SZ, _I, _P]),
+    "tp_yolo_create_ex": (_I, [_I, _P, _P, _P, _P, _P, _SZ, _I, _P]),
+    "tp_yolo_hl8_inputs": (ctypes.c_uint32, []),
+    "tp_yolo_layer_output_lo": (_I, [_P, _I, _P]),
     "tp_yolo_input": (_P, [_P]),
     "tp_yolo_head": (_P, [_P]),
     "tp_yolo_head_cstride": (_I, []),

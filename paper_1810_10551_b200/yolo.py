@@ -64,10 +64,13 @@ def head_path(seed: int) -> str:
     return os.path.join(DATA_DIR, f"yolo_head_seed{seed}.npz")
 
 
-# "fp32": the fp32-parity plan (hi/lo fp16 activation pairs, TP_DTYPE_F16X2) — the mode
-# that meets the north-star 1e-3 score tolerance against the fp32 reference; "fp16" is
-# the 2x faster 16-bit-activation mode (scores within ~5e-3)
+# "fp32": the fp32-parity plan (TP_DTYPE_F16F8: hi/lo fp16 activation pairs up to the
+# 152^2 stage, then an fp16 hi plane + an e4m3 lo plane run as kind::f16 + kind::f8f6f4
+# MMAs into one fp32 accumulator) — meets the north-star 1e-3 score tolerance against the
+# fp32 reference; "fp32x2": the hi/lo fp16 pairs on every layer (TP_DTYPE_F16X2, 2x K);
+# "fp16": the 2x faster 16-bit-activation mode (scores within ~5e-3)
 DEFAULT_PRECISION = "fp32"
+LO_EXP = 11  # TP_LO_EXP: lo plane = e4m3((x - fp16(x)) * 2^LO_EXP)
 
 
 def _bf16_round(a: np.ndarray) -> np.ndarray:
@@ -121,7 +124,7 @@ def make_weights(seed: int = 0, head: str = "calibrated", dtype: str = "fp16"):
     head="calibrated" uses the committed probe head for this seed when present,
     head="random" always uses a random head.
     """
-    if dtype == "fp32":
+    if dtype in native.PARITY_DTYPES:
         dtype = "fp16"
     key = (seed, head, dtype)
     if key in _CACHE:
@@ -165,7 +168,8 @@ class YoloNet:
                  dtype: str = DEFAULT_PRECISION, share: "YoloNet | None" = None,
                  guard_bytes: int = 0):
         """dtype "fp16" / "bf16": 16-bit activations; "fp32": the fp32-parity plan
-        (TP_DTYPE_F16X2 — exact hi/lo fp16 activation pairs, same kernels, 2x K).
+        (TP_DTYPE_F16F8, see DEFAULT_PRECISION); "fp32x2": exact hi/lo fp16 activation
+        pairs on every layer (TP_DTYPE_F16X2, same kernels, 2x K).
         share: another YoloNet whose device weights this one reuses (own workspace, so
         the two can run concurrently on different streams).
         guard_bytes: a canary region after the workspace (0xA5 bytes; guard_ok() checks
@@ -177,18 +181,29 @@ class YoloNet:
         if dtype not in native.DTYPES:
             raise ValueError(f"dtype must be one of {tuple(native.DTYPES)}")
         self.dtype = dtype
-        self.split = dtype == "fp32"
+        self.split = dtype in native.PARITY_DTYPES  # exact pairs / integer layer-0 input
         self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float16
         wdtype = "fp16" if self.split else dtype
         self.weight_dtype = wdtype  # value grid of the weights (make_weights dtype)
         self.max_tiles = int(max_tiles)
+        # conv slots reading an HL8 input (fp16 hi weights * 2^c + e4m3 lo weights)
+        self.hl8_inputs = hl8_input_slots() if dtype == "fp32" else frozenset()
         if share is not None:
             self.w_dev, self.b_dev = share.w_dev, share.b_dev
+            self.wlo_dev, self.alphas = share.wlo_dev, share.alphas
         else:
             wpacks, biases = weights if weights is not None else make_weights(seed, head, wdtype)
-            if self.split:
-                wpacks = [split_weight(li, w) for li, w in enumerate(wpacks)]
-            self.w_dev = [torch.from_numpy(w).to(self.tdtype).cuda() for w in wpacks]
+            self.w_dev, self.wlo_dev, alphas = [], [], []
+            for li, w in enumerate(wpacks):
+                wlo, alpha = None, 1.0
+                if li in self.hl8_inputs:
+                    w, wlo, alpha = hl8_weights(w)
+                elif self.split:
+                    w = split_weight(li, w)
+                self.w_dev.append(torch.from_numpy(w).to(self.tdtype).cuda())
+                self.wlo_dev.append(None if wlo is None else torch.from_numpy(wlo).cuda())
+                alphas.append(alpha)
+            self.alphas = np.asarray(alphas, dtype=np.float32)
             self.b_dev = [torch.from_numpy(b).cuda() for b in biases]
         nbytes = int(lib.tp_yolo_workspace_bytes(self.max_tiles, native.DTYPES[dtype]))
         self._alloc = torch.empty(nbytes + int(guard_bytes), dtype=torch.uint8, device="cuda")
@@ -196,10 +211,13 @@ class YoloNet:
         self.guard = self._alloc[nbytes:]
         self.guard.fill_(0xA5)
         wptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.w_dev])
+        wlptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.wlo_dev])
         bptrs = (ctypes.c_void_p * len(LAYERS))(*[native.ptr(t) for t in self.b_dev])
+        aptr = self.alphas.ctypes.data_as(ctypes.c_void_p)
         handle = ctypes.c_void_p()
-        native.call("tp_yolo_create", self.max_tiles, wptrs, bptrs, native.ptr(self.workspace),
-                    nbytes, native.DTYPES[dtype], ctypes.byref(handle))
+        native.call("tp_yolo_create_ex", self.max_tiles, wptrs, wlptrs, bptrs, aptr,
+                    native.ptr(self.workspace), nbytes, native.DTYPES[dtype],
+                    ctypes.byref(handle))
         self.handle = handle
         self.input_ptr = int(lib.tp_yolo_input(handle))
         self.head_ptr = int(lib.tp_yolo_head(handle))
@@ -266,11 +284,25 @@ class YoloNet:
         nb = n_tiles * res * res * cs * 2
         return self._view(addr, nb).view(self.tdtype).view(n_tiles, res, res, cs)
 
+    def step_lo_tensor(self, step: int, n_tiles: int):
+        """uint8 view of an HL8 step output's e4m3 lo plane [n, R, R, C], or None."""
+        lo = ctypes.c_void_p()
+        native.call("tp_yolo_layer_output_lo", self.handle, step, ctypes.byref(lo))
+        if not lo.value:
+            return None
+        _, res, cs = self.layer_output(step)
+        return self._view(int(lo.value), n_tiles * res * res * cs).view(n_tiles, res, res, cs)
+
     def step_values(self, step: int, n_tiles: int):
-        """A step's output as fp32 [n, R, R, C] real channels (hi + lo in the parity plan)."""
+        """A step's output as fp32 [n, R, R, C] real channels (hi + lo in the parity plans)."""
+        import torch
+
         t = self.step_tensor(step, n_tiles)
         if not self.split or step == len(STEPS) - 1:
             return t.float()
+        lo = self.step_lo_tensor(step, n_tiles)
+        if lo is not None:  # HL8: hi + e4m3(lo) * 2^-LO_EXP
+            return t.float() + lo.view(torch.float8_e4m3fn).float() * (2.0 ** -LO_EXP)
         n, r, _, cs = t.shape
         g = t.view(n, r, r, cs // 32, 2, 16).float()
         return (g[:, :, :, :, 0] + g[:, :, :, :, 1]).reshape(n, r, r, cs // 2)
@@ -280,6 +312,59 @@ class YoloNet:
         if h is not None and native._lib is not None:
             native._lib.tp_yolo_destroy(h)
             self.handle = None
+
+
+def exec_gflop_per_tile(dtype: str) -> float:
+    """Tensor-core work a plan issues per tile, in kind::f16-rate-equivalent GFLOP: the
+    16-bit plans issue the algorithmic FLOPs; fp32x2 doubles K on every layer but layer 0;
+    fp32 doubles it on the F16X2-input layers and adds half of K (the e4m3 lo pass runs at
+    twice the f16 rate) on the HL8-input layers."""
+    g = [2.0 * s * s * cout * cin * k * k / 1e9 for _, cin, cout, k, s in LAYERS]
+    if dtype not in native.PARITY_DTYPES:
+        return sum(g)
+    hl8 = hl8_input_slots() if dtype == "fp32" else frozenset()
+    return g[0] + sum(x * (1.5 if li in hl8 else 2.0) for li, x in enumerate(g) if li)
+
+
+def hl8_input_slots() -> frozenset:
+    """Conv slots whose input is an HL8 tensor in the "fp32" (TP_DTYPE_F16F8) plan."""
+    m = int(native.load().tp_yolo_hl8_inputs())
+    return frozenset(li for li in range(len(LAYERS)) if m >> li & 1)
+
+
+def hl8_scales(wpack: np.ndarray) -> tuple[int, int]:
+    """(c, b) for a layer read from HL8 planes: the fp16 hi-pass weights are w * 2^c (the
+    largest power keeping them finite in fp16 while the e4m3 lo-pass weights w * 2^b,
+    b = c - LO_EXP, stay <= 240 of e4m3's 448), and the accumulator is scaled by 2^-c."""
+    wmax = float(np.abs(np.asarray(wpack, dtype=np.float32)).max())
+    b = min(int(np.floor(np.log2(240.0 / wmax))), int(np.floor(np.log2(65504.0 / wmax))) - LO_EXP)
+    return b + LO_EXP, b
+
+
+def e4m3_bytes(a: np.ndarray) -> np.ndarray:
+    """fp32 -> e4m3 (RNE, values within +-448) as uint8 codes."""
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    return t.to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+
+
+def hl8_weights(wpack: np.ndarray):
+    """Packed fp16-grid weights of a layer with an HL8 input -> (hi-pass weights w * 2^c as
+    fp32 holding fp16 values, lo-pass e4m3 codes of w * 2^(c - LO_EXP), alpha = 2^-c)."""
+    c, b = hl8_scales(wpack)
+    w = np.asarray(wpack, dtype=np.float32)
+    return (w * np.float32(2.0 ** c)).astype(np.float32), e4m3_bytes(w * np.float32(2.0 ** b)), \
+        float(2.0 ** -c)
+
+
+def hl8_lo_weight_values(wpack: np.ndarray) -> np.ndarray:
+    """What the lo pass multiplies by, in real scale: e4m3(w * 2^b) * 2^-b (packed layout)."""
+    import torch
+
+    _, b = hl8_scales(wpack)
+    codes = torch.from_numpy(e4m3_bytes(np.asarray(wpack, dtype=np.float32) * np.float32(2.0 ** b)))
+    return codes.view(torch.float8_e4m3fn).float().numpy() * np.float32(2.0 ** -b)
 
 
 def split_weight(li: int, wpack: np.ndarray) -> np.ndarray:

@@ -34,7 +34,10 @@ def tiles():
     return np.stack(out)
 
 
-@pytest.fixture(scope="module", params=["fp16", "bf16", "fp32"])
+PARITY = ("fp32", "fp32x2")
+
+
+@pytest.fixture(scope="module", params=["fp16", "bf16", "fp32", "fp32x2"])
 def net(cuda, request):
     return yolo.YoloNet(4, seed=0, dtype=request.param)
 
@@ -54,12 +57,16 @@ def test_input_normalisation_matches_oracle(cuda, net, tiles):
     torch = cuda
     n = _run(cuda, net, tiles)
     x = net.input_tensor(n)[:, 1:-1].float().cpu()  # interior rows; column u at u + 2
-    ref = yolo_ref.tiles_to_input(tiles, net.dtype).permute(0, 2, 3, 1)
-    if net.dtype == "fp32":  # the parity plan's input holds the integer pixel values
+    ref = yolo_ref.tiles_to_input(tiles, _oracle_mode(net)).permute(0, 2, 3, 1)
+    if net.dtype in PARITY:  # the parity plan's input holds the integer pixel values
         ref = torch.from_numpy(tiles.astype(np.float32))
     assert torch.equal(x[:, :, 2:610, 0:3], ref)
     assert x[..., 3].abs().max().item() == 0
     assert x[:, :, :2].abs().max().item() == 0 and x[:, :, 610:].abs().max().item() == 0
+
+
+def _oracle_mode(net):
+    return "fp32" if net.dtype in PARITY else net.dtype
 
 
 def _check_layers(cuda, net, tiles):
@@ -84,14 +91,23 @@ def _check_layers(cuda, net, tiles):
         _, cin, cout, k, res = yolo.LAYERS[li]
         if src_step < 0:
             xin = net.input_tensor(n)[:, 1:-1, 2:610, 0:3].float()
-            if net.dtype == "fp32":
+            if net.dtype in PARITY:
                 xin = xin / 255.0
         else:
             xin = net.step_values(src_step, n)
         xin = xin.float().permute(0, 3, 1, 2)
         w = yolo_ref.unpack_weight(wpacks[li], li).cuda()
         b = torch.from_numpy(biases[li][:cout]).cuda()
-        ref = torch.nn.functional.conv2d(xin, w, b, padding=k // 2)
+        if li in net.hl8_inputs:
+            # HL8 input: fp16 hi plane x w (kind::f16) + e4m3 lo plane x e4m3(w) (kind::f8f6f4)
+            hi = net.step_tensor(src_step, n).float().permute(0, 3, 1, 2)
+            wlo = yolo_ref.unpack_weight(yolo.hl8_lo_weight_values(wpacks[li]), li).cuda()
+            lo = net.step_lo_tensor(src_step, n).view(torch.float8_e4m3fn).float()
+            lo = lo.permute(0, 3, 1, 2) * 2.0 ** -yolo.LO_EXP
+            ref = (torch.nn.functional.conv2d(hi, w, b, padding=k // 2)
+                   + torch.nn.functional.conv2d(lo, wlo, None, padding=k // 2))
+        else:
+            ref = torch.nn.functional.conv2d(xin, w, b, padding=k // 2)
         if li != yolo.HEAD:
             ref = torch.where(ref > 0, ref, 0.1 * ref)
         if li in yolo.POOLED:
@@ -108,9 +124,10 @@ def _check_layers(cuda, net, tiles):
         scale = ref.abs().max().item() + 1e-6
         err = (out - ref).abs().max().item() / scale
         worst = max(worst, err)
-        # 16-bit output rounding; the fp32 plan's hi/lo pair carries ~22 bits, so what is
-        # left is fp32 accumulation order over K up to 23040 (measured <= 2.3e-5)
-        tol = 5e-5 if net.dtype == "fp32" else 1e-2
+        # 16-bit output rounding; the fp32x2 plan's hi/lo pair carries ~22 bits, so what is
+        # left is fp32 accumulation order over K up to 23040 (measured <= 2.3e-5); an HL8
+        # output's e4m3 lo adds up to 2^-15 relative of its stored value
+        tol = {"fp32": 8e-5, "fp32x2": 5e-5}.get(net.dtype, 1e-2)
         assert err < tol, f"layer {yolo.LAYERS[li][0]}: rel err {err}"
     return worst
 
@@ -119,7 +136,7 @@ def test_each_conv_layer_matches_torch_fp32(cuda, net, tiles):
     print("worst per-layer rel err", _check_layers(cuda, net, tiles))
 
 
-@pytest.mark.parametrize("dtype", ["fp32", "fp16"])
+@pytest.mark.parametrize("dtype", ["fp32", "fp32x2", "fp16"])
 def test_each_conv_layer_many_tiles(cuda, dtype):
     """40 tiles: every persistent CTA / CTA pair runs several tiles on each TMEM
     accumulator buffer and reuses its epilogue staging slabs (the 3-tile test gives the
@@ -137,13 +154,13 @@ def test_head_matches_cpu_oracle(cuda, net, tiles):
     torch.cuda.synchronize()
     got = net.head_tensor(n)[..., :425].cpu().numpy()
     wpacks, biases = yolo.make_weights(0, dtype=net.weight_dtype)
-    ref = yolo_ref.forward(tiles, wpacks, biases, mode=net.dtype)
+    ref = yolo_ref.forward(tiles, wpacks, biases, mode=_oracle_mode(net))
     scale = np.abs(ref).max()
     rel = np.abs(got - ref).max() / scale
     # 16-bit activation storage through 23 layers: isolated rounding flips propagate;
     # fp32 plan vs the fp32 oracle (no activation rounding): the lo half of small
     # activations is fp16-subnormal (6e-8 absolute spacing) and K reaches 11520 in fp32
-    assert rel < {"bf16": 5e-2, "fp16": 1e-2, "fp32": 1e-4}[net.dtype], rel
+    assert rel < {"bf16": 5e-2, "fp16": 1e-2, "fp32": 1e-4, "fp32x2": 1e-4}[net.dtype], rel
     print("head max rel err vs oracle", rel, "mean abs", np.abs(got - ref).mean())
 
 
@@ -156,5 +173,5 @@ def test_plan_kernel_choice(net):
     print(net.dtype, net.kernel_summary())
     assert ks[0] == "conv_l0_kernel"
     assert all(ks[i] == "conv_pair_kernel" for i in (5, 8, 10, 12, 13, 15, 17, 18, 19, 21))
-    if net.dtype != "fp32":
+    if net.dtype not in PARITY:
         assert ks[1] == ks[2] == ks[4] == "conv_box_kernel"
