@@ -1449,10 +1449,102 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, const void* smem_
       : "memory");
 }
 
+// Unpooled swap epilogue with HL8 output (layer 4 of the F16F8 plan): per output row the
+// warp's 32 channels x 16 pixels leave as an fp16 hi slab (16 px x 64 B, SW64, stmatrix
+// .trans as in the pair path) and an e4m3 lo slab (16 px x 32 B): thread t holds channels
+// t/4 and t/4 + 8 of each 16-channel half for pixels 2(t%4), +1 (+8), so 4 shuffles per
+// (half, pixel group) gather channel pair (2k, 2k+1), k = t/4, into one b16 per pixel and
+// a second stmatrix .trans writes each pixel's 32 lo bytes in channel order. Both slabs of
+// a row are one bulk group; two rows alternate (wait_group.read 1), as the pair path.
+__device__ __forceinline__ void swap_epilogue_hl8(const ConvParams& p, const CUtensorMap& tmC,
+                                                  const CUtensorMap& tmC2, uint8_t* smC,
+                                                  uint32_t slab0, uint32_t t_row, bool live,
+                                                  int y0, int x0, int img, int nb, uint32_t q,
+                                                  uint32_t lane, int ores, float alpha,
+                                                  bool leaky) {
+  const int m = (int)lane >> 3, j = (int)lane & 7;
+  const int cq = (int)lane >> 2, tq = (int)lane & 3;
+  const float* bias = p.bias;
+  float bq[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    bq[h][0] = bias[nb * 128 + (int)q * 32 + 16 * h + cq];
+    bq[h][1] = bias[nb * 128 + (int)q * 32 + 16 * h + cq + 8];
+  }
+  // destination channel pair k = cq of each half: sources = lanes holding channels 2k, 2k+1
+  const int src_a = 4 * ((2 * cq) & 7) + tq, src_b = src_a + 4;
+  const bool hi_e = cq >= 4;  // channels 2k >= 8 are those lanes' e = 1 values
+#pragma unroll 1
+  for (int r = 0; r < SW_H; ++r) {
+    if (!live || y0 + r >= ores) break;
+    const uint32_t slab = slab0 + (uint32_t)(r & 1) * 2048;  // hi: [0, 1024), lo: [1024, 1536)
+    uint32_t hs[2][2][2], lw[2][2];  // hi pairs [h][cg][e]; lo stmatrix words [h][cg]
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t v[8];
+      tmem_ld_16x256b_x2(t_row + ((uint32_t)(16 * h) << 16) + (uint32_t)(r * 16), v);
+      tp::tmem_ld_wait_regs(v);
+#pragma unroll
+      for (int cg = 0; cg < 2; ++cg) {
+        uint32_t l2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          float a = fmaf(__uint_as_float(v[4 * cg + 2 * e]), alpha, bq[h][e]);
+          float b = fmaf(__uint_as_float(v[4 * cg + 2 * e + 1]), alpha, bq[h][e]);
+          if (leaky) {
+            a = fmaxf(a, 0.1f * a);
+            b = fmaxf(b, 0.1f * b);
+          }
+          const __half2 hh = __floats2half2_rn(a, b);
+          hs[h][cg][e] = *reinterpret_cast<const uint32_t*>(&hh);
+          const float2 hf = __half22float2(hh);
+          uint16_t pr;  // byte 0 = pixel 2tq, byte 1 = pixel 2tq + 1
+          asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;"
+              : "=h"(pr)
+              : "f"((b - hf.y) * kLoScale), "f"((a - hf.x) * kLoScale));
+          l2[e] = pr;
+        }
+        const uint32_t a0 = __shfl_sync(0xffffffffu, l2[0], src_a);
+        const uint32_t a1 = __shfl_sync(0xffffffffu, l2[1], src_a);
+        const uint32_t b0 = __shfl_sync(0xffffffffu, l2[0], src_b);
+        const uint32_t b1 = __shfl_sync(0xffffffffu, l2[1], src_b);
+        // (ch 2k, px) (ch 2k+1, px) (ch 2k, px+1) (ch 2k+1, px+1)
+        lw[h][cg] = __byte_perm(hi_e ? a1 : a0, hi_e ? b1 : b0, 0x5140);
+      }
+    }
+    if (lane == 0) bulk_wait_read1();  // the stores two rows back have read this slab
+    __syncwarp();
+    {
+      // hi: matrices (h, channels 0-7 | 8-15) -> 16-byte chunk 2h + (m & 1) of the pixel's
+      // 64-byte row (SW64: chunk ^ ((pixel >> 1) & 3)); one x4 per pixel group cg
+#pragma unroll
+      for (int cg = 0; cg < 2; ++cg) {
+        const int pix = 8 * cg + j;
+        const uint32_t addr = slab + (uint32_t)(pix * 64) + (uint32_t)(((m ^ (pix >> 1)) & 3) * 16);
+        stmatrix_x4_trans(addr, hs[0][cg][0], hs[0][cg][1], hs[1][cg][0], hs[1][cg][1]);
+      }
+      // lo: matrix m = (h = m >> 1, cg = m & 1): pixel 8cg + j, bytes 16h .. 16h + 15
+      const int lpix = 8 * (m & 1) + j;
+      stmatrix_x4_trans(slab + 1024 + (uint32_t)(lpix * 32 + 16 * (m >> 1)), lw[0][0], lw[0][1],
+                        lw[1][0], lw[1][1]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      const int c0 = p.out_coff + nb * 128 + (int)q * 32;
+      tma_store_4d(&tmC, smC + (slab - tp::smem_u32(smC)), c0, x0, y0 + r, img);
+      tma_store_4d(&tmC2, smC + (slab + 1024 - tp::smem_u32(smC)), c0, x0, y0 + r, img);
+      bulk_commit();
+    }
+  }
+}
+
 template <bool POOL>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+                     const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC2,
+                     const ConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1525,14 +1617,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           tp::mbar_arrive_expect_tx(&full[s], p.a_stage_bytes + p.b_stage_bytes);
           const int dx = kb / p.kb_per_tap - 1;
           const int cb = kb - (dx + 1) * p.kb_per_tap;
-          tma_load_4d(smX + (size_t)s * p.a_stage_bytes, &tmA, &full[s], cb * SW_BK, x0 + dx,
-                      y0 - 1, img);
+          // HL8 lo block (cb >= kb_hi): 64 e4m3 channels (64-byte rows, same box bytes)
+          const bool lo_blk = cb >= p.kb_hi;
+          const int cc = lo_blk ? (cb - p.kb_hi) * 64 : cb * SW_BK;
+          tma_load_4d(smX + (size_t)s * p.a_stage_bytes, lo_blk ? &tmA2 : &tmA, &full[s], cc,
+                      x0 + dx, y0 - 1, img);
           // this CTA's 128 / SW_CL output channels of each tap's slice, to every CTA
           uint8_t* wdst = smW + (size_t)s * p.b_stage_bytes + rank * (w_slice / SW_CL);
 #pragma unroll
           for (int dy = 0; dy < 3; ++dy)
-            tma_load_2d_mc(wdst + dy * w_slice, &tmB, &full[s],
-                           (dy * 3 + dx + 1) * p.cin + cb * SW_BK,
+            tma_load_2d_mc(wdst + dy * w_slice, lo_blk ? &tmB2 : &tmB, &full[s],
+                           (dy * 3 + dx + 1) * p.cin + cc,
                            nb * 128 + (128 / SW_CL) * (int)rank, (uint16_t)((1 << SW_CL) - 1));
           if (++s == S) {
             s = 0;
@@ -1561,7 +1656,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       aph[acc] ^= 1;
       tp::tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * 256);
+      int cbk = 0;  // K block within the kernel column (>= kb_hi: an HL8 lo block)
       for (int kb = 0; kb < p.num_kb; ++kb) {
+        const bool lo_blk = cbk >= p.kb_hi;
+        if (++cbk == p.kb_per_tap) cbk = 0;
         PROF_T0(t2);
         tp::mbar_wait(&full[s], ph);
         PROF_ADD(w_fu, t2);
@@ -1569,12 +1667,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t xd = x_desc0 + (uint64_t)(s * x_step);
         const uint64_t wd = w_desc0 + (uint64_t)(s * w_step);
         if (tp::elect_one()) {
+          if (lo_blk) {  // 64 e4m3 channels per row: 2 x K32 (32 bytes each, as below)
 #pragma unroll
-          for (int dy = 0; dy < 3; ++dy)
+            for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-            for (int k = 0; k < SW_BK / 16; ++k)
-              tp::mma_bf16(d_tmem, wd + dy * w_slice16 + 2 * k, xd + dy * x_row16 + 2 * k, p.idesc,
-                           (kb | dy | k) != 0);
+              for (int k = 0; k < 2; ++k)
+                mma_f8(d_tmem, wd + dy * w_slice16 + 2 * k, xd + dy * x_row16 + 2 * k, p.idesc, 1);
+          } else {
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+              for (int k = 0; k < SW_BK / 16; ++k)
+                tp::mma_bf16(d_tmem, wd + dy * w_slice16 + 2 * k, xd + dy * x_row16 + 2 * k,
+                             p.idesc, (kb | dy | k) != 0);
+          }
           commit_mc(&empty[s], (uint16_t)((1 << SW_CL) - 1));  // frees it for every producer
         }
         __syncwarp();
@@ -1616,7 +1722,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 256);
       // a warp writes one pixel's 32 channels per instruction (64 B, or 2 x 32 B hi/lo runs)
       auto put = [&](int y, int x, float v) {
-        v += bco;
+        v = fmaf(v, alpha, bco);
         if (leaky) v = fmaxf(v, 0.1f * v);
         const size_t oi = ((size_t)(img * ores + y) * ores + x) * p.out_cstride + sc;
         __half* o = reinterpret_cast<__half*>(p.out) + oi;
@@ -1657,6 +1763,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // pixel's [hi 16 | lo 16] channel groups contiguously.
         const uint32_t slab0 = tp::smem_u32(smC) + warp * 4096;
         const int m = (int)lane >> 3, j = (int)lane & 7;  // stmatrix: matrix m, row j
+        if (p.out_lo != nullptr) {
+          swap_epilogue_hl8(p, tmC, tmC2, smC, slab0, t_row, live, y0, x0, img, nb, q, lane,
+                            ores, alpha, leaky);
+          tp::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tp::mbar_arrive(&tempty[g]);
+          continue;
+        }
         const int cq = (int)lane >> 2;                     // fragment row (channel) of this thread
         float bq[2][2];
 #pragma unroll
@@ -1683,8 +1797,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int cg = 0; cg < 2; ++cg)  // pixels 8cg .. 8cg+7
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                float a = __uint_as_float(v[4 * cg + 2 * e]) + bq[h][e];
-                float b = __uint_as_float(v[4 * cg + 2 * e + 1]) + bq[h][e];
+                float a = fmaf(__uint_as_float(v[4 * cg + 2 * e]), alpha, bq[h][e]);
+                float b = fmaf(__uint_as_float(v[4 * cg + 2 * e + 1]), alpha, bq[h][e]);
                 if (leaky) {
                   a = fmaxf(a, 0.1f * a);
                   b = fmaxf(b, 0.1f * b);
@@ -2436,6 +2550,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (!store || c * 16 >= p.cout || (p.dbg & 4)) continue;
+        if (p.out_lo != nullptr) {  // HL8 planes
+          const size_t oo = (size_t)opx * p.out_cstride + p.out_coff + c * 16;
+          store_hl8(reinterpret_cast<__half*>(p.out) + oo, reinterpret_cast<uint8_t*>(p.out_lo) + oo, f);
+          continue;
+        }
         if (p.split) {
           store_split16(o + 2 * c * 16, f);
           continue;
@@ -2780,6 +2899,7 @@ struct ConvLaunch {
   int box_bk;
   CUtensorMap tmA, tmB, tmC;
   CUtensorMap tmA2, tmB2;  // HL8 input: lo-plane activations and e4m3 weights
+  CUtensorMap tmC2;        // swap kernel HL8 output: lo-plane store map
   ConvParams p;
   size_t smem;
 };
@@ -3063,7 +3183,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   // still wins where it applies.
   const char* sw = getenv("TP_SWAP");
   if (ksize == 3 && cout_pad == 128 && cout == 128 && cin_used % SW_BK == 0 && !halo &&
-      !out_fp32 && !reorg && (pool || split) && (sw == nullptr || atoi(sw) != 0)) {
+      !out_fp32 && !reorg && (pool || split || out_lo != nullptr) &&
+      (sw == nullptr || atoi(sw) != 0)) {
     ConvLaunch P = *L;
     const uint64_t xdims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
     const uint32_t xbox[4] = {SW_BK, SW_W, SW_H + 2, 1};
@@ -3085,7 +3206,15 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     q.halo = 0;
     q.sub = 1;
     q.rect = pool ? 1 : 0;
-    if (!pool) {  // store map {stored channels, x, y, image}, box = 16 px x 128 B of one row
+    if (!pool && out_lo != nullptr) {  // HL8: hi 16 px x 64 B (SW64) + lo 16 px x 32 B
+      const uint64_t cdims[4] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)res,
+                                 (uint64_t)max_img};
+      const uint32_t cbox[4] = {32, SW_W, 1, 1};
+      rc = make_tmap(&P.tmC, out, 4, cdims, cbox, CU_TENSOR_MAP_SWIZZLE_64B, f16);
+      if (rc) return rc;
+      rc = make_tmap(&P.tmC2, out_lo, 4, cdims, cbox, CU_TENSOR_MAP_SWIZZLE_NONE, f16, 1);
+      if (rc) return rc;
+    } else if (!pool) {  // store map {stored channels, x, y, image}, box = 16 px x 128 B of one row
       const uint64_t cdims[4] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)res,
                                  (uint64_t)max_img};
       const uint32_t cbox[4] = {64, SW_W, 1, 1};
@@ -3111,7 +3240,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   // full-halo box kernel (TP_BOX=0 disables it): 3x3, one K block, resident weights
   const char* be = getenv("TP_BOX");
   const bool box_ok = ksize == 3 && (cin_used == 32 || cin_used == 64) && cout_pad <= 256 &&
-                      cout == cout_pad && !reorg && !out_fp32 && res % 8 == 0 &&
+                      cout == cout_pad && !reorg && !out_fp32 && res % 8 == 0 && in_lo == nullptr &&
                       bres <= 160 * 1024 && (be == nullptr || atoi(be) != 0);
   // pool-in-M first (4 pool accumulators x 2 buffers must fit TMEM; pooled side in 8-px
   // tiles), then the shuffle-pool / plain box if its four parity planes do not fit smem
@@ -3191,7 +3320,25 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   if (in_lo != nullptr) {
     // HL8 input: after each tap's kb_hi fp16 blocks come cin/128 e4m3 lo blocks of the
     // same stage bytes (128 rows x 128 B); FLAT im2col (tc / pair) and pair-rect only
+    // (swap kernel: 32-channel fp16 blocks + 64-channel e4m3 blocks, 64-byte rows)
     const bool flat_tc = !L->pair && !L->prect && !L->box && !L->swap && !L->l0 && !p.rect;
+    if (L->swap) {
+      if (cin_used % 64 != 0 || weight_lo == nullptr) {
+        tp_set_error("conv: HL8 input of the swap kernel needs cin %% 64 == 0");
+        return TP_ERR_UNSUPPORTED;
+      }
+      p.lo_in = 1;
+      p.kb_hi = cin_used / SW_BK;
+      p.kb_per_tap = p.kb_hi + cin_used / 64;
+      p.num_kb = 3 * p.kb_per_tap;
+      const uint64_t xdims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
+      const uint32_t xbox[4] = {64, SW_W, SW_H + 2, 1};
+      rc = make_tmap(&L->tmA2, in_lo, 4, xdims, xbox, CU_TENSOR_MAP_SWIZZLE_64B, f16, 1);
+      if (rc) return rc;
+      const uint64_t wdims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+      const uint32_t wbox[2] = {64, 128 / SW_CL};
+      return make_tmap(&L->tmB2, weight_lo, 2, wdims, wbox, CU_TENSOR_MAP_SWIZZLE_64B, f16, 1);
+    }
     if (!(L->pair || L->prect || flat_tc) || cin_used % 128 != 0 || weight_lo == nullptr ||
         mode != MODE_SW128) {
       tp_set_error("conv: HL8 input needs a FLAT or pair-rect SW128 layer with cin %% 128 == 0");
@@ -3326,7 +3473,8 @@ int launch_swap(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaSt
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_swap_kernel<POOL>, L.tmA, L.tmB, L.tmC, p));
+  TP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, conv_swap_kernel<POOL>, L.tmA, L.tmB, L.tmC, L.tmA2, L.tmB2,
+                                   L.tmC2, p));
   return TP_OK;
 }
 
@@ -3466,13 +3614,14 @@ const Step kSteps[] = {
 constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
 
 // Storage format of a buffer: the F16X2 plan pairs every activation but the layer-0 slots
-// (integer pixel values, exact in fp16) and the fp32 head; the F16F8 plan keeps F16X2 up to
-// the 152^2 stage and stores the 76^2 .. 19^2 activations as HL8 planes (TP_DTYPE_F16F8).
+// (integer pixel values, exact in fp16) and the fp32 head; the F16F8 plan stores the inputs
+// of every layer from 4 on as HL8 planes (TP_DTYPE_F16F8) and keeps F16X2 for layer 2's
+// input (the pool-in-M box kernel reads it).
 enum BufFmt { FMT_PLAIN = 0, FMT_X2 = 1, FMT_HL8 = 2 };
 int buf_fmt(int b, int dtype) {
   if (b == I608 || b == HEAD) return FMT_PLAIN;
   if (dtype == TP_DTYPE_F16X2) return FMT_X2;
-  if (dtype == TP_DTYPE_F16F8) return b >= P76 ? FMT_HL8 : FMT_X2;
+  if (dtype == TP_DTYPE_F16F8) return b >= P152 ? FMT_HL8 : FMT_X2;
   return FMT_PLAIN;
 }
 // channels stored per pixel (hi plane for HL8)
