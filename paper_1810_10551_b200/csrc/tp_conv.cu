@@ -1868,7 +1868,8 @@ constexpr int L0_STAGING = 8 * 2 * 4096;             // epilogue store slabs
 
 __global__ void __launch_bounds__(kThreads, 1)
     conv_l0_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+                   const ConvParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -2029,7 +2030,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // 16-byte stores at a 128-byte pixel pitch were LSU-bound (0.86 -> 0.44 ms per 120
       // tiles). Plain 64-byte pixels are stored directly (staging measured 13% slower).
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 128);
-      const bool spl = p.split != 0;
+      const bool spl = p.split != 0 || p.out_lo != nullptr;  // staged TMA-store outputs
       const uint32_t slab = tp::smem_u32(smC) + warp * 8192 + (nslab & 1) * 4096;
       const int X = bx * 16 + (int)(lane & 15), Y = by * 8 + 2 * (int)q + (int)(lane >> 4);
       __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) +
@@ -2038,24 +2039,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) bulk_wait_read1();
         __syncwarp();
       }
+      // TMEM loads software-pipelined: chunk 1's four loads are in flight while chunk 0 is
+      // pooled, converted and staged
+      uint32_t v0[16], v1[16], v2[16], v3[16];
+      tp::tmem_ld16(t_row, v0);
+      tp::tmem_ld16(t_row + 32, v1);
+      tp::tmem_ld16(t_row + 64, v2);
+      tp::tmem_ld16(t_row + 96, v3);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t v0[16], v1[16], v2[16], v3[16];
-        tp::tmem_ld16(t_row + c * 16, v0);
-        tp::tmem_ld16(t_row + 32 + c * 16, v1);
-        tp::tmem_ld16(t_row + 64 + c * 16, v2);
-        tp::tmem_ld16(t_row + 96 + c * 16, v3);
         tp::tmem_ld_wait();
         float fv[16];
 #pragma unroll
+        for (int j = 0; j < 16; ++j)
+          fv[j] = fmaxf(fmaxf(__uint_as_float(v0[j]), __uint_as_float(v1[j])),
+                        fmaxf(__uint_as_float(v2[j]), __uint_as_float(v3[j])));
+        if (c == 0) {
+          tp::tmem_ld16(t_row + 16, v0);
+          tp::tmem_ld16(t_row + 48, v1);
+          tp::tmem_ld16(t_row + 80, v2);
+          tp::tmem_ld16(t_row + 112, v3);
+        }
+#pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float m = fmaxf(fmaxf(__uint_as_float(v0[j]), __uint_as_float(v1[j])),
-                                fmaxf(__uint_as_float(v2[j]), __uint_as_float(v3[j])));
           // scale (alpha > 0), bias and leaky are monotonic: pooling first is the same value
-          const float a = fmaf(m, p.alpha, bias_s[c * 16 + j]);
+          const float a = fmaf(fv[j], p.alpha, bias_s[c * 16 + j]);
           fv[j] = fmaxf(a, 0.1f * a);
         }
-        if (spl) {  // SW128 rows: 16-byte unit u at u ^ (row & 7)
+        if (p.split) {  // SW128 rows: 16-byte unit u at u ^ (row & 7)
           uint32_t hi[8], lo[8];
           split_pairs<8>(fv, hi, lo);
           const uint32_t rb = slab + lane * 128, sw = lane & 7;
@@ -2063,6 +2074,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_shared_v4(rb + (((4 * c + 1) ^ sw) << 4), hi[4], hi[5], hi[6], hi[7]);
           st_shared_v4(rb + (((4 * c + 2) ^ sw) << 4), lo[0], lo[1], lo[2], lo[3]);
           st_shared_v4(rb + (((4 * c + 3) ^ sw) << 4), lo[4], lo[5], lo[6], lo[7]);
+          continue;
+        }
+        if (p.out_lo != nullptr) {  // HL8: staged hi rows (64 B, SW64) + lo rows (32 B, SW32)
+          uint32_t hi[8], lo[4];
+          split_hl8(fv, hi, lo);
+          const uint32_t rh = slab + lane * 64, sh = (lane >> 1) & 3;
+          st_shared_v4(rh + (((2 * c) ^ sh) << 4), hi[0], hi[1], hi[2], hi[3]);
+          st_shared_v4(rh + (((2 * c + 1) ^ sh) << 4), hi[4], hi[5], hi[6], hi[7]);
+          st_shared_v4(slab + 2048 + lane * 32 + ((c ^ ((lane >> 2) & 1)) << 4), lo[0], lo[1],
+                       lo[2], lo[3]);
           continue;
         }
         uint32_t pk[8];
@@ -2086,6 +2107,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && (p.dbg & 4) == 0) {
           tma_store_3d(&tmC, smC + (slab - tp::smem_u32(smC)), 0, bx * 16,
                        img * ores + by * 8 + 2 * (int)q);
+          if (p.out_lo != nullptr)
+            tma_store_3d(&tmC2, smC + (slab + 2048 - tp::smem_u32(smC)), 0, bx * 16,
+                         img * ores + by * 8 + 2 * (int)q);
           bulk_commit();
         }
         ++nslab;
@@ -2128,7 +2152,8 @@ constexpr int PLANE_W = BOX_TW + 1, PLANE_H = BOX_TH + 1;  // 9 x 17 parity-plan
 template <int BK, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_box_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, const ConvParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+                    const __grid_constant__ CUtensorMap tmB2, const ConvParams p) {
   constexpr uint32_t RB = BK * 2;  // bytes per pixel row in smem (one swizzle row)
   constexpr uint32_t LAY = BK == 64 ? 2 : 4;
   constexpr bool PM = EPI == BOX_POOLM;
@@ -2191,7 +2216,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::mbar_arrive_expect_tx(bres_bar, p.bres_bytes);
         for (int j = 0; j < p.n_bchunks; ++j) {  // chunk j = (K block j / 9, tap j % 9)
           const int cb = j / 9, tap = j - cb * 9;
-          tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, tap * p.cin + cb * BK, 0);
+          if (PM && p.lo_in && cb >= p.kb_hi)  // HL8: e4m3 lo chunks after the fp16 ones
+            tp::tma_load_2d(smB + (size_t)9 * p.kb_hi * p.bchunk_bytes +
+                                (size_t)(j - 9 * p.kb_hi) * (p.bchunk_bytes >> 1),
+                            &tmB2, bres_bar, tap * p.cin, 0);
+          else
+            tp::tma_load_2d(smB + (size_t)j * p.bchunk_bytes, &tmB, bres_bar, tap * p.cin + cb * BK, 0);
         }
       }
       int s = 0;
@@ -2207,16 +2237,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tp::mbar_wait(&empty[s], ph ^ 1);
         PROF_ADD(pr_wait, tw);
         uint8_t* dst = smA + (size_t)s * p.a_stage_bytes;
-        // exact box bytes (stages / planes are padded to 1 KB in smem)
+        // exact box bytes (stages / planes are padded to 1 KB in smem); an HL8 lo block
+        // (PM, cb >= kb_hi) has BK e4m3 channels: half the row bytes (SW32)
+        const bool lo_blk = PM && p.lo_in && cb >= p.kb_hi;
         constexpr uint32_t tx = PM ? 4 * PLANE_W * PLANE_H * RB : (BOX_TW + 2) * (BOX_TH + 2) * RB;
-        tp::mbar_arrive_expect_tx(&full[s], tx);
+        tp::mbar_arrive_expect_tx(&full[s], lo_blk ? tx / 2 : tx);
         if (PM) {
           // plane (ey, ex) holds input (2*X0 - ex + 2i, 2*Y0 - ey + 2j); -1 reads as 0
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int ey = b >> 1, ex = b & 1;
-            tma_load_4d(dst + b * (p.a_stage_bytes >> 2), &tmA, &full[s], cb * BK,
-                        2 * BOX_TW * bx - ex, 2 * BOX_TH * by - ey, img);
+            tma_load_4d(dst + b * (p.a_stage_bytes >> 2), lo_blk ? &tmA2 : &tmA, &full[s],
+                        lo_blk ? (cb - p.kb_hi) * BK : cb * BK, 2 * BOX_TW * bx - ex,
+                        2 * BOX_TH * by - ey, img);
           }
         } else {  // tile + one-pixel halo; the halo outside the image reads as 0
           tma_load_4d(dst, &tmA, &full[s], 0, BOX_TW * bx - 1, BOX_TH * by - 1, img);
@@ -2269,7 +2302,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t ad = a_desc0 + (uint64_t)(s * a_step);
       const uint32_t d0 = tmem_base + (uint32_t)(acc * NACC * N);
       const uint64_t b_desc0 = b_desc_base + (uint64_t)(cb * 9 * bch);  // this K block's taps
-      if (tp::elect_one() && (p.dbg & 2) == 0) {
+      const bool lo_blk = PM && p.lo_in && cb >= p.kb_hi;
+      if (lo_blk) {
+        // HL8 lo block: BK e4m3 channels = one K = 32 MMA per (tap, accumulator) from
+        // BK-byte rows (SW32); weights = the e4m3 chunks after the 9 * kb_hi fp16 ones
+        if (BK == 32 && tp::elect_one() && (p.dbg & 2) == 0) {
+          constexpr uint32_t RBL = BK;
+          const uint64_t adl = tp::umma_desc(tp::smem_u32(smA), 16, PLANE_W * RBL, 6) +
+                               (uint64_t)(s * a_step);
+          const uint32_t bchl = bch >> 1;
+          const uint64_t bdl = tp::umma_desc(tp::smem_u32(smB), 16, 8 * RBL, 6) +
+                               (uint64_t)(9 * p.kb_hi * bch + (cb - p.kb_hi) * 9 * bchl);
+          const uint32_t idesc2 = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(2 * N) >> 3 << 17);
+#pragma unroll
+          for (int py = 0; py < 2; ++py) {
+            const uint32_t dpair = d0 + (uint32_t)(2 * py * N);
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy) {
+              const int sy = py + dy;
+#pragma unroll
+              for (int o = 0; o < 4; ++o) {
+                const int sx = o == 0 ? 1 : o == 1 ? 2 : o == 2 ? 0 : 3;
+                const int plane = ((sy + 1) & 1) * 2 + ((sx + 1) & 1);
+                const uint32_t off = plane * plane16 + (((sy >> 1) * PLANE_W + (sx >> 1)) * RBL >> 4);
+                const int chunk = 3 * dy + (o < 2 ? sx - 1 : o == 2 ? 0 : 2);
+                mma_f8(o == 2 ? dpair + (uint32_t)N : dpair, adl + off, bdl + chunk * bchl,
+                       o < 2 ? idesc2 : idesc, 1);
+              }
+            }
+          }
+        }
+      } else if (tp::elect_one() && (p.dbg & 2) == 0) {
         if (PM && (p.dbg & 64)) {  // profiling: unmerged pool-in-M (6 N-wide MMAs per row)
 #pragma unroll
           for (int pp = 0; pp < NACC; ++pp) {
@@ -3003,6 +3066,10 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
       rc = make_tmap(&L->tmC, out, 3, dims, box,
                      split ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, f16);
       if (rc) return rc;
+      if (out_lo != nullptr) {  // HL8 lo plane: 32-byte rows
+        rc = make_tmap(&L->tmC2, out_lo, 3, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 1);
+        if (rc) return rc;
+      }
     }
     L->l0 = 1;
     int st = (int)((227 * 1024 - fixed - 9 * 1024 - L0_STAGING) / L0_STAGE);
@@ -3240,8 +3307,11 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   // full-halo box kernel (TP_BOX=0 disables it): 3x3, one K block, resident weights
   const char* be = getenv("TP_BOX");
   const bool box_ok = ksize == 3 && (cin_used == 32 || cin_used == 64) && cout_pad <= 256 &&
-                      cout == cout_pad && !reorg && !out_fp32 && res % 8 == 0 && in_lo == nullptr &&
+                      cout == cout_pad && !reorg && !out_fp32 && res % 8 == 0 &&
+                      (in_lo == nullptr || (pool && cin_used == 32 && cout_pad <= 64)) &&
                       bres <= 160 * 1024 && (be == nullptr || atoi(be) != 0);
+  // HL8 input (pool-in-M only): + 9 resident e4m3 lo chunks (half the fp16 chunk bytes)
+  const size_t bres_box = in_lo != nullptr ? bres + bres / 2 : bres;
   // pool-in-M first (4 pool accumulators x 2 buffers must fit TMEM; pooled side in 8-px
   // tiles), then the shuffle-pool / plain box if its four parity planes do not fit smem
   for (int try_pm = 1; box_ok && try_pm >= 0 && !L->box; --try_pm) {
@@ -3260,7 +3330,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
                               : ((BOX_TW + 2) * (BOX_TH + 2) * rb + 1023) & ~1023u;
     const uint32_t staging = (!pool && res % 4 == 0) ? 8 * 4096 : 0;  // 2 slabs per warp
     const int bfixed = 1024 + cout_pad * 4 + (2 * 8 + 10) * 8 + 16 + (int)staging;
-    int st = (int)((227 * 1024 - bfixed - (int)bres) / (int)stage);
+    int st = (int)((227 * 1024 - bfixed - (int)bres_box) / (int)stage);
     if (st > 8) st = 8;
     const uint32_t per_tile = (pm ? 4u : 1u) * (uint32_t)cout_pad;  // TMEM columns per tile
     const int nbuf = per_tile <= 128 ? 4 : 2;
@@ -3317,6 +3387,28 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     }
   }
   p.kb_hi = p.kb_per_tap;
+  if (in_lo != nullptr && L->box) {
+    // pool-in-M box with an HL8 input (cin 32): K block 0 = the fp16 hi planes (SW64),
+    // K block 1 = the e4m3 lo planes (32-byte rows, SW32) against 9 resident e4m3 chunks
+    if (L->box - 1 != BOX_POOLM || L->box_bk != 32 || weight_lo == nullptr) {
+      tp_set_error("conv: HL8 input of the box kernel needs pool-in-M with 32 channels");
+      return TP_ERR_UNSUPPORTED;
+    }
+    p.lo_in = 1;
+    p.kb_hi = 1;
+    p.num_kb = 2;
+    p.n_bchunks = 18;
+    p.bres_bytes += p.bres_bytes / 2;
+    L->smem += bres / 2;
+    const uint64_t dims[4] = {(uint64_t)cin_stride, (uint64_t)res, (uint64_t)res, (uint64_t)max_img};
+    const uint32_t box[4] = {32, 2 * PLANE_W, 2 * PLANE_H, 1};
+    const uint32_t estr[4] = {1, 2, 2, 1};
+    rc = make_tmap(&L->tmA2, in_lo, 4, dims, box, CU_TENSOR_MAP_SWIZZLE_32B, f16, 1, estr);
+    if (rc) return rc;
+    const uint64_t wdims[2] = {(uint64_t)ktotal, (uint64_t)cout_pad};
+    const uint32_t wbox[2] = {32, (uint32_t)cout_pad};
+    return make_tmap(&L->tmB2, weight_lo, 2, wdims, wbox, CU_TENSOR_MAP_SWIZZLE_32B, f16, 1);
+  }
   if (in_lo != nullptr) {
     // HL8 input: after each tap's kb_hi fp16 blocks come cin/128 e4m3 lo blocks of the
     // same stage bytes (128 rows x 128 B); FLAT im2col (tc / pair) and pair-rect only
@@ -3377,7 +3469,7 @@ int launch_box(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStr
   const long long tiles = (long long)n_img * p.tiles_x * p.tiles_y;
   if (tiles == 0) return TP_OK;
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  conv_box_kernel<BK, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
+  conv_box_kernel<BK, EPI><<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, L.tmA2, L.tmB2, p);
   TP_LAUNCH_CHECK();
   return TP_OK;
 }
@@ -3517,7 +3609,7 @@ int run_conv(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStrea
     const long long tiles = (long long)n_img * (p.res / 32) * (p.res / 16);
     if (tiles == 0) return TP_OK;
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-    conv_l0_kernel<<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, p);
+    conv_l0_kernel<<<grid, kThreads, L.smem, st>>>(L.tmA, L.tmB, L.tmC, L.tmC2, p);
     TP_LAUNCH_CHECK();
     return TP_OK;
   }
@@ -3614,14 +3706,13 @@ const Step kSteps[] = {
 constexpr int kNumSteps = sizeof(kSteps) / sizeof(kSteps[0]);
 
 // Storage format of a buffer: the F16X2 plan pairs every activation but the layer-0 slots
-// (integer pixel values, exact in fp16) and the fp32 head; the F16F8 plan stores the inputs
-// of every layer from 4 on as HL8 planes (TP_DTYPE_F16F8) and keeps F16X2 for layer 2's
-// input (the pool-in-M box kernel reads it).
+// (integer pixel values, exact in fp16) and the fp32 head; the F16F8 plan stores those same
+// activations as HL8 planes (TP_DTYPE_F16F8).
 enum BufFmt { FMT_PLAIN = 0, FMT_X2 = 1, FMT_HL8 = 2 };
 int buf_fmt(int b, int dtype) {
   if (b == I608 || b == HEAD) return FMT_PLAIN;
   if (dtype == TP_DTYPE_F16X2) return FMT_X2;
-  if (dtype == TP_DTYPE_F16F8) return b >= P152 ? FMT_HL8 : FMT_X2;
+  if (dtype == TP_DTYPE_F16F8) return FMT_HL8;
   return FMT_PLAIN;
 }
 // channels stored per pixel (hi plane for HL8)
