@@ -540,15 +540,24 @@ EXECUTED_NOTE = {
 }
 
 
+def measured_peaks() -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def peak_tflops() -> float:
+    """Dense bf16 (= fp16) TFLOP/s sustained, MEASURED_PEAKS.json (driver-written), else the
+    profiling recipe's fallback."""
+    return float(measured_peaks().get("bf16_tflops_sustained", 1391.0))
+
+
 def roofline(args, f):
     from paper_1810_10551_b200 import yolo
 
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    peak = float(peaks.get("bf16_tflops_sustained", 1391.0))
+    peaks = measured_peaks()
+    peak = peak_tflops()
     traffic = {}
     tfile = "r01_conv_traffic.json" if args.precision != "fp32" else "r01_conv_traffic_fp32.json"
     try:
@@ -677,7 +686,7 @@ def sub_results(args, rank, world, local, shared_gpu, group):
                     "unit": "frames/s", "ms_per_step": f["ms_per_step"], "steps": sa.steps,
                     "warmup": sa.warmup, "tiles_per_frame": f["tiles_per_frame"],
                     "crops_per_sec": f["value"] * f["tiles_per_frame"],
-                    "roofline_frac": f["conv_tflops"] / 1391.0,
+                    "roofline_frac": f["conv_tflops"] / peak_tflops(),
                     "conv_tflops": f["conv_tflops"], "clocks": f["clocks"]})
         del eng, clip
         gc.collect()

@@ -74,10 +74,26 @@ def tiles_to_input(tiles_u8, mode="bf16"):
 
 
 def reorg(x):
-    """[n,64,38,38] -> [n,256,19,19]; channel (dy*2+dx)*64 + c <- pixel (2y+dy, 2x+dx)."""
+    """[n,64,38,38] -> [n,256,19,19] exactly as darknet's yolov2-608 [reorg] stride=2 layer:
+    forward_reorg_layer calls reorg_cpu(input, w, h, c, batch, stride, forward=0, output)
+    (darknet src/reorg_layer.c, src/blas.c), whose loop over the input's (k, j, i) sets
+    out[i + w*(j + h*k)] = in[w2 + 2w*(h2 + 2h*c2)] with c2 = k % (c/4), off = k / (c/4),
+    w2 = 2i + off % 2, h2 = 2j + off / 2 — i.e. it reads the C x H x W input as
+    C/4 x 2H x 2W memory; not a clean space-to-depth. Restated on flat NCHW indices."""
     n, c, h, w = x.shape
-    x = x.reshape(n, c, h // 2, 2, w // 2, 2)  # n c y dy x dx
-    return x.permute(0, 3, 5, 1, 2, 4).reshape(n, 4 * c, h // 2, w // 2)
+    k, j, i = np.meshgrid(np.arange(c), np.arange(h), np.arange(w), indexing="ij")
+    out_c = c // 4
+    c2, off = k % out_c, k // out_c
+    w2, h2 = i * 2 + off % 2, j * 2 + off // 2
+    src = (w2 + w * 2 * (h2 + h * 2 * c2)).reshape(-1)  # out[in_index] = x[out_index]
+    flat = x.reshape(n, -1)[:, torch_index(src)]
+    return flat.reshape(n, 4 * c, h // 2, w // 2)
+
+
+def torch_index(a):
+    import torch
+
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.long)
 
 
 def forward(tiles_u8, weights, biases, mode="bf16", threads=None, return_features=False):

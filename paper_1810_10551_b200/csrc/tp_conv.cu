@@ -259,6 +259,23 @@ __device__ __forceinline__ void mma_f8(uint32_t d, uint64_t a, uint64_t b, uint3
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Darknet's reorg (yolov2-608 [reorg] stride=2: forward_reorg_layer -> reorg_cpu(...,
+// forward = 0), darknet src/blas.c): it reads the C x R x R input as C/4 x 2R x 2R memory and
+// writes a 4C x R/2 x R/2 output, which is not a clean space-to-depth. Input element
+// (c, y, x) lands at output (C, Y, X): with a = c % 4, h2 = (R/2) a + y/2, w2 = R (y % 2) + x,
+// k = (2 (h2 % 2) + w2 % 2) (C/4) + c / 4 and P = w2/2 + R (h2/2) + R^2 k (NCHW flat),
+// C = P / (R/2)^2, Y, X = the rest (oracle/yolo_ref.py reorg is the same map).
+__device__ __forceinline__ void reorg_dest(int c, int y, int x, int R, int cin, int& Y, int& X,
+                                           int& C) {
+  const int hr = R >> 1;
+  const int h2 = hr * (c & 3) + (y >> 1), w2 = R * (y & 1) + x;
+  const int k = (2 * (h2 & 1) + (w2 & 1)) * (cin >> 2) + (c >> 2);
+  const int P = (w2 >> 1) + R * (h2 >> 1) + R * R * k;
+  C = P / (hr * hr);
+  const int r = P - C * hr * hr;
+  Y = r / hr;
+  X = r - Y * hr;
+}
 constexpr int kMaxBias = 1024;
 
 // Walks a CTA's contiguous tile range: t = mt * n_blocks_n + nb, and for RECT tiles
@@ -557,10 +574,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pix = it.mt * 128 + row;
         valid = pix < total_px;
         out_px = pix;
-        if (valid && EPI == EPI_REORG) {
+        if (valid && EPI == EPI_REORG) {  // (image, y, x) of the input pixel for reorg_dest
           const PixPos q0 = pix_pos(pix, p.res, p.img_px);
-          sub = (q0.y & 1) * 2 + (q0.x & 1);
-          out_px = q0.n * oimg + (q0.y >> 1) * ores + (q0.x >> 1);
+          sub = q0.y * p.res + q0.x;
+          out_px = q0.n;
         }
       }
       const uint32_t t_row =
@@ -671,14 +688,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (!valid || !writer || ch0 >= p.cout || (p.dbg & 4)) continue;
-        if (p.out_lo != nullptr) {  // HL8 planes (reorg / pooled direct stores)
-          const size_t o = (size_t)out_px * p.out_cstride + p.out_coff +
-                           (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
+        if (EPI == EPI_REORG) {  // darknet reorg: every element to its own (Y, X, C)
+          const int y = sub / p.res, x = sub - y * p.res;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            int Y, X, C;
+            reorg_dest(ch0 + j, y, x, p.res, p.cout, Y, X, C);
+            const size_t px = ((size_t)out_px * ores + Y) * ores + X;
+            const float v = f[j];
+            if (p.out_lo != nullptr) {
+              const size_t o = px * p.out_cstride + p.out_coff + C;
+              store_hl8_1(reinterpret_cast<__half*>(p.out) + o,
+                          reinterpret_cast<uint8_t*>(p.out_lo) + o, v);
+            } else if (p.split) {
+              __half* o = reinterpret_cast<__half*>(p.out) + px * p.out_cstride + p.out_coff +
+                          32 * (C >> 4) + (C & 15);
+              const __half h = __float2half_rn(v);
+              o[0] = h;
+              o[16] = __float2half_rn(v - __half2float(h));
+            } else {
+              __half* o = reinterpret_cast<__half*>(p.out) + px * p.out_cstride + p.out_coff + C;
+              if (f16)
+                *o = __float2half_rn(v);
+              else
+                *reinterpret_cast<__nv_bfloat16*>(o) = __float2bfloat16_rn(v);
+            }
+          }
+        } else if (p.out_lo != nullptr) {  // HL8 planes (pooled direct stores)
+          const size_t o = (size_t)out_px * p.out_cstride + p.out_coff + ch0;
           store_hl8(reinterpret_cast<__half*>(p.out) + o, reinterpret_cast<uint8_t*>(p.out_lo) + o, f);
         } else if (p.split) {
-          const int creal = (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
           store_split16(reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride +
-                            p.out_coff + 2 * creal,
+                            p.out_coff + 2 * ch0,
                         f);
         } else {  // (fp32 outputs always take the TMA-store path above)
           uint32_t pk[8];
@@ -692,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               pk[j] = *reinterpret_cast<uint32_t*>(&h);
             }
           }
-          const int cofs = p.out_coff + (EPI == EPI_REORG ? sub * p.cout : 0) + ch0;
+          const int cofs = p.out_coff + ch0;
           __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)out_px * p.out_cstride + cofs;
           *reinterpret_cast<uint4*>(o) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           *reinterpret_cast<uint4*>(o + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);

@@ -10,6 +10,8 @@ relative) plus accumulation-order noise.
 import numpy as np
 import pytest
 
+from oracle import yolo_ref
+
 from paper_1810_10551_b200 import native, yolo
 
 pytestmark = pytest.mark.gpu
@@ -97,8 +99,8 @@ def test_conv_reorg_and_channel_offset(cuda):
     x = _input(torch, 2, 38, 64, seed=9)
     out, ref = _run_conv(torch, x, 38, 64, 64, 64, 1, leaky=True, reorg=True, out_cstride=1280,
                          out_coff=0)
-    # space-to-depth: out(y, x, (dy*2+dx)*64 + c) = in(2y+dy, 2x+dx, c)
-    r = ref.reshape(2, 19, 2, 19, 2, 64).permute(0, 1, 3, 2, 4, 5).reshape(2, 19, 19, 256)
+    # darknet reorg (reorg_cpu forward=0), restated in oracle/yolo_ref.reorg
+    r = yolo_ref.reorg(ref.permute(0, 3, 1, 2).cpu()).permute(0, 2, 3, 1).to(ref.device)
     _check(torch, out[..., :256], r)
     assert out[..., 256:].abs().max().item() == 0
     out2, ref2 = _run_conv(torch, _input(torch, 2, 19, 128, seed=3), 19, 128, 64, 64, 3,

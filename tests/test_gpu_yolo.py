@@ -115,7 +115,8 @@ def _check_layers(cuda, net, tiles):
         ref = ref.permute(0, 2, 3, 1)
         out = net.step_values(step, n)
         if li == 20:  # reorg into channels [0,256) of the concat buffer
-            ref = ref.reshape(n, 19, 2, 19, 2, 64).permute(0, 1, 3, 2, 4, 5).reshape(n, 19, 19, 256)
+            # darknet reorg order (oracle/yolo_ref.reorg, reorg_cpu forward=0)
+            ref = yolo_ref.reorg(ref.permute(0, 3, 1, 2).cpu()).permute(0, 2, 3, 1).cuda()
             out = out[..., :256]
         elif li == 19:  # layer 24 -> channels [256, 1280)
             out = out[..., 256:]

@@ -2,7 +2,8 @@
 `algorithmic_bytes_per_tile`): every activation buffer read once by its consumer and
 written once by its producer, in the stored layout of each plan (csrc/tp_conv.cu kBufs /
 kSteps): compact NHWC 16-bit, the layer-0 input as [610][614][4] rgb0 pixels, the head fp32
-[19][19][448]; the fp32-parity plan doubles every activation but the input and head.
+[19][19][448]; the fp32x2 plan doubles every activation but the input and head (hi/lo fp16
+pairs), the fp32 plan (HL8) stores them as 3 bytes per element (fp16 hi + e4m3 lo planes).
 Weights are amortised over the batch and reported separately.
 
     python tools/algorithmic_bytes.py
@@ -31,9 +32,12 @@ STEPS = [("I608", "P304", 32), ("P304", "P152", 64), ("P152", "A152", 128),
          ("CAT19", "A19", 1024), ("A19", "HEAD", 448)]
 
 
-def activation_mb(split: bool) -> float:
+MULT = {"fp16": 1.0, "fp32x2": 2.0, "fp32": 1.5}  # stored bytes per element / 2
+
+
+def activation_mb(plan: str) -> float:
     def mult(b):
-        return 2 if split and b not in ("I608", "HEAD") else 1
+        return MULT[plan] if b not in ("I608", "HEAD") else 1
 
     total = 0
     for src, dst, och in STEPS:
@@ -44,16 +48,16 @@ def activation_mb(split: bool) -> float:
     return total / 1e6
 
 
-def weights_mb(split: bool) -> float:
+def weights_mb(plan: str) -> float:
     total = 0
     for li, (_, cin, cout, k, _) in enumerate(yolo.LAYERS):
         cpad = yolo.HEAD_CPAD if li == yolo.HEAD else cout
-        kk = 144 if li == 0 else k * k * cin * (2 if split else 1)
-        total += cpad * kk * 2
+        kk = 144 * 2 if li == 0 else k * k * cin * 2 * MULT[plan]
+        total += cpad * kk
     return total / 1e6
 
 
 if __name__ == "__main__":
-    for name, split in (("fp16/bf16", False), ("fp32-parity", True)):
-        print(f"{name}: activations {activation_mb(split):.2f} MB per tile, "
-              f"weights {weights_mb(split):.1f} MB per forward")
+    for plan in ("fp16", "fp32", "fp32x2"):
+        print(f"{plan}: activations {activation_mb(plan):.2f} MB per tile, "
+              f"weights {weights_mb(plan):.1f} MB per forward")
