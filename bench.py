@@ -559,7 +559,8 @@ def roofline(args, f):
     peaks = measured_peaks()
     peak = peak_tflops()
     traffic = {}
-    tfile = "r01_conv_traffic.json" if args.precision != "fp32" else "r01_conv_traffic_fp32.json"
+    tfile = {"fp32": "r02_conv_traffic_fp32.json",
+             "fp32x2": "r01_conv_traffic_fp32.json"}.get(args.precision, "r01_conv_traffic.json")
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", tfile)))
     except Exception:

@@ -102,7 +102,7 @@ class StreamDriver:
         self.copy_start = [ev() for _ in range(N_DEV_SLOTS)]
         self.staged = [torch.cuda.Event() for _ in range(2)]  # H2D done reading stage slot
         self.used = [torch.cuda.Event() for _ in range(N_DEV_SLOTS)]
-        self.att_ev = [(ev(), ev()) for _ in range(2)]
+        self.att_ev = [(ev(), ev()) for _ in range(3)]  # k % 3: k+2 is queued before k emits
         self.fin_ev = [[ev() for _ in range(5)] for _ in range(2)]
         self.fin_end = [ev() for _ in range(3)]  # batch k -> k % 3 (read two batches later)
         self.pool = ThreadPoolExecutor(max_workers=max(1, io_threads))
@@ -145,14 +145,14 @@ class StreamDriver:
             st.wait_event(self.fin_end[(k - 2) % 3])
         with torch.cuda.stream(st):
             self.engine.stage1(n, self.dev[slot], stream=st, bank=bank,
-                               events=self.att_ev[k % 2])
+                               events=self.att_ev[k % 3])
 
     def finish(self, k: int, n: int) -> None:
         torch = self.torch
         slot, bank = k % N_DEV_SLOTS, (self.base + k) % 2
         cur = torch.cuda.current_stream()
         cur.wait_event(self.copied[slot])
-        cur.wait_event(self.att_ev[k % 2][1])
+        cur.wait_event(self.att_ev[k % 3][1])
         eng = self.engine
         eng.events = self.fin_ev[k % 2]
         eng.finish(n, self.dev[slot], bank=bank, timed=True)
@@ -163,7 +163,7 @@ class StreamDriver:
         """Per-frame TimingProfile of batch k (its events must have completed)."""
         slot = k % N_DEV_SLOTS
         e = self.fin_ev[k % 2]
-        a0, a1 = self.att_ev[k % 2]
+        a0, a1 = self.att_ev[k % 3]
         att = a0.elapsed_time(a1)
         if self.lookahead and k > 0:  # only the part not hidden behind batch k-1's finish
             wait = max(0.0, self.fin_end[(k - 1) % 3].elapsed_time(a1))
@@ -203,15 +203,18 @@ class StreamDriver:
                 except Exception as exc:
                     failed, n = exc, 0
             sink.after_finish(k, n, chunk, failed)
-            if pending is not None:  # batch k-1 finishes while batch k is queued
-                self._emit(sink, *pending)
-                pending = None
             if failed is None and k + 1 < len(chunks):
-                try:  # host packing + H2D of the next batch overlap batch k on the GPU
+                # host packing + H2D + stage 1 of batch k+1 are queued BEFORE batch k-1's
+                # results are built on the host, so the copy and the look-ahead never wait
+                # for Python result objects (slots and banks are guarded by events)
+                try:
                     self.load(k + 1, chunks[k + 1])
                     self.stage1(k + 1, len(chunks[k + 1]))
                 except Exception as exc:
                     failed = exc
+            if pending is not None:  # batch k-1 finishes while batch k is queued
+                self._emit(sink, *pending)
+                pending = None
             pending = (k, n, chunk)
             if failed is not None and not sink.collective:
                 self._emit(sink, *pending)  # keep the finished batch, then abort
