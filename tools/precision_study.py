@@ -7,8 +7,12 @@ hi + fp16(x - hi) as the GPU's parity buffers store it, "fp16" = one RNE fp16), 
 of the forward is fp32, and the decoded detections are compared with the all-fp32 run.
 
   python tools/precision_study.py [--tiles 8] [--greedy]
+  python tools/precision_study.py --lo8        # the HL8 plan (fp16 hi + e4m3 lo on every input)
 
 Prints per-slot sensitivity (only that slot fp16) and the executed-FLOP saving of a plan.
+--lo8 emulates the "fp32" plan exactly: every conv input x (but layer 0's) as
+hi = fp16(x) times the fp16 weights plus e4m3((x - hi) 2^a) 2^-a times e4m3(w 2^b) 2^-b,
+with b from yolo.hl8_scales (a = LO_EXP; also a = 9, 10, 12 for comparison).
 """
 
 from __future__ import annotations
@@ -106,6 +110,47 @@ def forward(tiles, wp, bs, rounds):
     return head.permute(0, 2, 3, 1).contiguous().numpy()
 
 
+def forward_lo8(tiles, wp, bs, a):
+    """The HL8 plan's forward (see module docstring), everything else fp32."""
+    import torch
+    import torch.nn.functional as F
+
+    def e4m3(t):
+        return t.clamp(-448, 448).to(torch.float8_e4m3fn).to(torch.float32)
+
+    with torch.no_grad():
+        x = yolo_ref.tiles_to_input(tiles, "fp32")
+
+        def conv(li, inp, linear=False):
+            _, cin, cout, k, _ = LAY[li]
+            w = yolo_ref.unpack_weight(wp[li], li)
+            b = torch.as_tensor(np.asarray(bs[li][:cout], dtype=np.float32))
+            if li == 0:
+                y = F.conv2d(inp, w, b, padding=k // 2)
+            else:
+                hi = inp.to(torch.float16).to(torch.float32)
+                lo = e4m3((inp - hi) * 2.0 ** a) / 2.0 ** a
+                wm = float(w.abs().max())
+                be = min(int(np.floor(np.log2(240.0 / wm))), int(np.floor(np.log2(65504.0 / wm))) - a)
+                wlo = e4m3(w * 2.0 ** be) / 2.0 ** be
+                y = F.conv2d(hi, w, b, padding=k // 2) + F.conv2d(lo, wlo, None, padding=k // 2)
+            if not linear:
+                y = torch.where(y > 0, y, 0.1 * y)
+            return y
+
+        route16 = None
+        for li in range(20):
+            x = conv(li, x)
+            if LAY[li][0] == 16:
+                route16 = x
+            if LAY[li][0] in yolo_ref.POOL_AFTER:
+                x = F.max_pool2d(x, 2)
+        x = torch.cat([yolo_ref.reorg(conv(20, route16)), x], dim=1)
+        x = conv(21, x)
+        head = conv(22, x, linear=True)
+    return head.permute(0, 2, 3, 1).contiguous().numpy()
+
+
 def compare(ref_head, head, thr=0.25):
     """max relative score error over detections present in both, max box err / 608,
     number of threshold flips (detection on one side only)."""
@@ -132,6 +177,7 @@ def main():
     ap.add_argument("--tiles", type=int, default=8)
     ap.add_argument("--greedy", action="store_true")
     ap.add_argument("--plan", default="", help="comma list of slots stored as single fp16")
+    ap.add_argument("--lo8", action="store_true", help="emulate the HL8 (fp32) plan")
     args = ap.parse_args()
     import torch
 
@@ -143,6 +189,11 @@ def main():
     print(f"fp32 reference: {time.time() - t0:.1f} s for {len(tiles)} tiles", flush=True)
     hilo = forward(tiles, wp, bs, ["hilo"] * 23)
     print("all hilo (parity plan):  score %.2e box %.2e flips %d n %d head %.2e" % compare(ref, hilo))
+    if args.lo8:
+        for a in (yolo.LO_EXP, 9, 10, 12):
+            print(f"HL8 lo exponent {a}:        score %.2e box %.2e flips %d n %d head %.2e"
+                  % compare(ref, forward_lo8(tiles, wp, bs, a)), flush=True)
+        return
     allf = forward(tiles, wp, bs, ["fp16"] * 23)
     print("all fp16 (fast plan):    score %.2e box %.2e flips %d n %d head %.2e" % compare(ref, allf))
     total = yolo.GFLOP_PER_TILE
