@@ -54,12 +54,12 @@ enum { TP_RESAMPLE_NEAREST = 0, TP_RESAMPLE_BILINEAR = 1 };
  * tensor has 2C stored channels and K spans both parts (weights duplicated per 16-channel
  * group); products are exact and accumulate in fp32, so activations carry ~22 bits. The
  * gather writes integer pixel values (exact in fp16) and layer 0 scales by 1/255 in fp32.
- * TP_DTYPE_F16F8 is the same parity contract at 3/4 of the tensor work: from the 76^2 stage
- * on (layer 8's input) an activation is two planes, hi = fp16(x) [pix][C] and
- * lo = e4m3((x - hi) * 2^TP_LO_EXP) [pix][C] bytes ("HL8"); a consumer runs K over hi with
- * fp16 weights w * 2^c (kind::f16) and over lo with e4m3 weights w * 2^(c - TP_LO_EXP)
- * (kind::f8f6f4, twice the rate) into one fp32 accumulator and scales it by 2^-c. Earlier
- * layers keep the F16X2 pairs. tp_yolo_create_ex takes the extra weights and scales. */
+ * TP_DTYPE_F16F8 (the default parity plan) keeps the same contract at 3/4 of the tensor
+ * work: every activation but the layer-0 input and the head is two planes, hi = fp16(x)
+ * [pix][C] and lo = e4m3((x - hi) * 2^TP_LO_EXP) [pix][C] bytes ("HL8"); a consumer runs K
+ * over hi with fp16 weights w * 2^c (kind::f16) and over lo with e4m3 weights
+ * w * 2^(c - TP_LO_EXP) (kind::f8f6f4, twice the rate) into one fp32 accumulator and scales
+ * it by 2^-c. tp_yolo_create_ex takes the extra weights and scales. */
 enum { TP_DTYPE_BF16 = 0, TP_DTYPE_F16 = 1, TP_DTYPE_F16X2 = 2, TP_DTYPE_F16F8 = 3 };
 #define TP_LO_EXP 11
 
@@ -116,8 +116,8 @@ TP_API int tp_device_sm_count(int* out);
 /* K1/K2: crop gather + resample (+ normalise). frames: u8 [n][H][W][3] with
  * frame_stride bytes between frames. out_u8: optional [n_jobs][608][608][3].
  * out_act: optional 16-bit (act_dtype) [n_jobs][610][614][4] layer-0 input: tile pixel
- * (v, u) at [v+1][u+2] as (r, g, b, 0) with values / 255 (the integer values for
- * TP_DTYPE_F16X2); the halo (rows 0 / 609, columns 0, 1, 610..613) must be pre-zeroed and
+ * (v, u) at [v+1][u+2] as (r, g, b, 0) with values / 255 (the integer values for the
+ * parity plans TP_DTYPE_F16X2 / TP_DTYPE_F16F8); the halo (rows 0 / 609, columns 0, 1, 610..613) must be pre-zeroed and
  * is never written.
  * n_jobs_dev: optional device count overriding n_jobs (n_jobs is then the max). */
 TP_API int tp_gather_tiles(const uint8_t* frames, int64_t frame_stride, int H, int W,
@@ -142,7 +142,7 @@ TP_API int tp_yolo_create_ex(int max_tiles, const void* const* weights,
                              int dtype, tp_yolo_net** out);
 /* Which conv slots read an HL8 input in the TP_DTYPE_F16F8 plan: bit l of the mask. */
 TP_API uint32_t tp_yolo_hl8_inputs(void);
-TP_API void* tp_yolo_input(tp_yolo_net* net);        /* 16-bit [max_tiles][610][610][8] slots */
+TP_API void* tp_yolo_input(tp_yolo_net* net);        /* 16-bit [max_tiles][610][614][4] pixels */
 TP_API int tp_yolo_num_steps(void);
 TP_API const float* tp_yolo_head(tp_yolo_net* net);  /* fp32 [max_tiles][19][19][448] */
 TP_API int tp_yolo_head_cstride(void);
