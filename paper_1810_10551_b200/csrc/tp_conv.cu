@@ -582,6 +582,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const uint32_t t_row =
           tmem_base + ((q * 32u) << 16) + (uint32_t)((g * p.sub + jt) * p.bn);
+      int rg_px[4] = {0, 0, 0, 0}, rg_cb[4] = {0, 0, 0, 0};  // reorg: per a = c % 4
+      if (EPI == EPI_REORG && valid) {
+        const int y = sub / p.res, x = sub - y * p.res;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          int Y, X, C;
+          reorg_dest(a, y, x, p.res, p.cout, Y, X, C);  // channel 4m + a -> C + 4m
+          rg_px[a] = (out_px * ores + Y) * ores + X;
+          rg_cb[a] = C;
+        }
+      }
       uint32_t v[16];
       const bool do_ld = (p.dbg & 8) == 0;
       if (do_ld) {
@@ -689,12 +700,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!valid || !writer || ch0 >= p.cout || (p.dbg & 4)) continue;
         if (EPI == EPI_REORG) {  // darknet reorg: every element to its own (Y, X, C)
-          const int y = sub / p.res, x = sub - y * p.res;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            int Y, X, C;
-            reorg_dest(ch0 + j, y, x, p.res, p.cout, Y, X, C);
-            const size_t px = ((size_t)out_px * ores + Y) * ores + X;
+            // channels c = 4m + a of one input pixel go to 4 output pixels (one per a),
+            // channel base + 4m there (reorg_dest; the bases are computed once per pixel)
+            const int a = j & 3, C = rg_cb[a] + 4 * ((ch0 + j) >> 2);
+            const size_t px = (size_t)rg_px[a];
             const float v = f[j];
             if (p.out_lo != nullptr) {
               const size_t o = px * p.out_cstride + p.out_coff + C;
@@ -1921,11 +1932,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smC + L0_STAGING);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
+  // 4 accumulator buffers (4 x 128 TMEM columns): epilogue group g takes tiles i % 2 == g
+  // and alternates buffers i % 4, so the MMAs of its next tile run while it drains one
   uint64_t* tfull = bars + 2 * S;
-  uint64_t* tempty = bars + 2 * S + 2;
-  uint64_t* bres_bar = bars + 2 * S + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 5);
-  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 6);
+  uint64_t* tempty = bars + 2 * S + 4;
+  uint64_t* bres_bar = bars + 2 * S + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
+  float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 10);
 
   const uint32_t warp = tp::warp_id();
   const uint32_t lane = tp::lane_id();
@@ -1936,14 +1949,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::mbar_init(&full[s], 1);
       tp::mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < 4; ++a) {
       tp::mbar_init(&tfull[a], 1);
       tp::mbar_init(&tempty[a], 4);
     }
     tp::mbar_init(bres_bar, 1);
     tp::fence_mbar_init();
   }
-  if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, 256);
+  if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, 512);
   for (int i = threadIdx.x; i < 32; i += blockDim.x) bias_s[i] = p.bias[i];
   tp::tc_fence_before();
   __syncthreads();
@@ -2002,15 +2015,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc64 = tp::idesc_f16kind(128, 64, p.f16 == 0);
       int s = 0;
       uint32_t ph = 0;
-      uint32_t aph[2] = {0, 0};
+      uint32_t aph = 0;  // phase bit per accumulator buffer
       long long w_te = 0, w_fu = 0;
       PROF_T0(m_start);
       for (int i = 0; i < n_tiles; ++i) {
-        const int acc = i & 1;
+        const int acc = i & 3;
         PROF_T0(t1);
-        tp::mbar_wait(&tempty[acc], aph[acc] ^ 1);
+        tp::mbar_wait(&tempty[acc], ((aph >> acc) & 1) ^ 1);
         PROF_ADD(w_te, t1);
-        aph[acc] ^= 1;
+        aph ^= 1u << acc;
         PROF_T0(t2);
         tp::mbar_wait(&full[s], ph);
         PROF_ADD(w_fu, t2);
@@ -2053,24 +2066,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float alpha = p.alpha;
     const uint32_t q = warp & 3;
     const bool f16 = p.f16 != 0;
-    uint32_t ph = 0, nslab = 0;
+    uint32_t ph = 0, nslab = 0;  // ph: phase bit per accumulator buffer
     long long e_wait = 0;
     PROF_T0(e_start);
     for (int i = 0; i < n_tiles; ++i) {
       if ((i & 1) != g) continue;
+      const int acc = i & 3;
       const int t = t_begin + i;
       const int img = t / per_img, r = t - img * per_img;
       const int by = r / txs, bx = r - by * txs;
       PROF_T0(t3);
-      tp::mbar_wait(&tfull[g], ph);
+      tp::mbar_wait(&tfull[acc], (ph >> acc) & 1);
       PROF_ADD(e_wait, t3);
-      ph ^= 1;
+      ph ^= 1u << acc;
       tp::tc_fence_after();
       // split outputs: this warp's 32 pooled pixels (2 output rows x 16) are staged as 32
       // SW128 smem rows [hi 16 | lo 16] x 2 and written by one TMA store — per-thread
       // 16-byte stores at a 128-byte pixel pitch were LSU-bound (0.86 -> 0.44 ms per 120
       // tiles). Plain 64-byte pixels are stored directly (staging measured 13% slower).
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 128);
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(acc * 128);
       const bool spl = p.split != 0 || p.out_lo != nullptr;  // staged TMA-store outputs
       const uint32_t slab = tp::smem_u32(smC) + warp * 8192 + (nslab & 1) * 4096;
       const int X = bx * 16 + (int)(lane & 15), Y = by * 8 + 2 * (int)q + (int)(lane >> 4);
@@ -2157,7 +2171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tp::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tp::mbar_arrive(&tempty[g]);
+      if (lane == 0) tp::mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) bulk_wait_all();
     if ((p.dbg & 32) && warp == 0 && lane == 0) {
@@ -2168,7 +2182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tp::tc_fence_before();
   __syncthreads();
   tp::tc_fence_after();
-  if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, 256);
+  if (warp == kMmaWarp) tp::tmem_dealloc(tmem_base, 512);
 }
 
 // ------------------------------------------------------------------ full-halo box kernel
@@ -2849,6 +2863,65 @@ __global__ void maxpool2_hl8_kernel(const __half* __restrict__ in, const uint8_t
   }
 }
 
+// Darknet reorg as a gather (the YOLO plan's layer 26): layer 26 writes its plain
+// [n][R][R][cin] output to a scratch buffer (TMA-store epilogue, L2-resident), then each
+// thread builds 8 consecutive channels of one output pixel of [n][R/2][R/2][4 cin] from their
+// sources (the inverse of reorg_dest: output (C, Y, X) at NCHW flat P reads input flat
+// Q = w2 + 2R h2 + 4R^2 c2 with i = P % R, j = (P / R) % R, k = P / R^2, c2 = k % (cin/4),
+// off = k / (cin/4), w2 = 2i + off % 2, h2 = 2j + off / 2) and stores them as one run —
+// the scatter epilogue's 2-byte stores to 4 pixels per source pixel were LSU-bound.
+// fmt: 0 plain 16-bit, 1 X2 (hi/lo interleaved per 16 channels), 2 HL8 (+ lo planes).
+template <int R, int cin>  // compile-time sides: the index math is multiply-shift only
+__global__ void reorg_gather_kernel(const uint16_t* __restrict__ in, const uint8_t* __restrict__ in_lo,
+                                    int n_img, const int32_t* __restrict__ n_img_dev,
+                                    int in_cstride, uint16_t* __restrict__ out,
+                                    uint8_t* __restrict__ out_lo, int out_cstride, int fmt) {
+  if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
+  constexpr int hr = R >> 1, cout = 4 * cin, groups = cout >> 3;
+  const long long total = (long long)n_img * hr * hr * groups;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(t % groups);
+    const long long px = t / groups;  // output pixel: img * hr^2 + Y * hr + X
+    const int img = (int)(px / (hr * hr));
+    const int yx = (int)(px - (long long)img * hr * hr);
+    uint32_t h[8], l[8];  // 16-bit codes (lo: e4m3 bytes for HL8)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int C = 8 * g + e;
+      const int P = yx + hr * hr * C;
+      const int i = P % R, j = (P / R) % R, k = P / (R * R);
+      constexpr int q4 = cin >> 2;
+      const int c2 = k % q4, off = k / q4;
+      const int Q = (2 * i + (off & 1)) + 2 * R * (2 * j + (off >> 1)) + 4 * R * R * c2;
+      const int ci = Q / (R * R), yi = (Q / R) % R, xi = Q % R;
+      const size_t src = ((size_t)img * R * R + (size_t)yi * R + xi) * in_cstride;
+      if (fmt == 1) {
+        h[e] = in[src + 32 * (ci >> 4) + (ci & 15)];
+        l[e] = in[src + 32 * (ci >> 4) + (ci & 15) + 16];
+      } else {
+        h[e] = in[src + ci];
+        l[e] = fmt == 2 ? in_lo[src + ci] : 0;
+      }
+    }
+    const size_t dst = (size_t)px * out_cstride;
+    if (fmt == 1) {  // hi and lo 8-runs of the interleaved group
+      const int c0 = 8 * g, so = 32 * (c0 >> 4) + (c0 & 15);
+      *reinterpret_cast<uint4*>(out + dst + so) =
+          make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+      *reinterpret_cast<uint4*>(out + dst + so + 16) =
+          make_uint4(l[0] | (l[1] << 16), l[2] | (l[3] << 16), l[4] | (l[5] << 16), l[6] | (l[7] << 16));
+    } else {
+      *reinterpret_cast<uint4*>(out + dst + 8 * g) =
+          make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+      if (fmt == 2)
+        *reinterpret_cast<uint2*>(out_lo + dst + 8 * g) =
+            make_uint2(l[0] | (l[1] << 8) | (l[2] << 16) | (l[3] << 24),
+                       l[4] | (l[5] << 8) | (l[6] << 16) | (l[7] << 24));
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -3119,7 +3192,7 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     p.bn = 32;
     p.n_blocks_n = 1;
     p.idesc = tp::idesc_f16kind(128, 32, !f16);
-    L->smem = 1024 + (size_t)st * L0_STAGE + 9 * 1024 + L0_STAGING + (2 * st + 6) * 8 + 32 * 4 + 16;
+    L->smem = 1024 + (size_t)st * L0_STAGE + 9 * 1024 + L0_STAGING + (2 * st + 10) * 8 + 32 * 4 + 16;
     return TP_OK;
   }
 
@@ -3715,18 +3788,19 @@ const LayerDef kConvs[23] = {
     {23, 1024, 1024, 3, 19}, {24, 1024, 1024, 3, 19}, {26, 512, 64, 1, 38},
     {29, 1280, 1024, 3, 19}, {30, 1024, 425, 1, 19}};
 
+// R38: layer 26's plain 38^2 x 64 output, gathered into CAT19 by reorg_gather_kernel
 enum Buf {
   I608, P304, P152, A152, B152, P76, A76, B76, P38, A38, B38, E38, P19, A19, B19, C19, CAT19,
-  HEAD, NBUF
+  HEAD, R38, NBUF
 };
 struct BufDef {
   int res, ch, bytes_per;  // bytes per element
 };
-const BufDef kBufs[NBUF] = {{608, 4, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
+constexpr BufDef kBufs[NBUF] = {{608, 4, 2},  {304, 32, 2},  {152, 64, 2},   {152, 128, 2},
                             {152, 64, 2},  {76, 128, 2},  {76, 256, 2},   {76, 128, 2},
                             {38, 256, 2},  {38, 512, 2},  {38, 256, 2},   {38, 512, 2},
                             {19, 512, 2},  {19, 1024, 2}, {19, 512, 2},   {19, 1024, 2},
-                            {19, 1280, 2}, {19, 448, 4}};
+                            {19, 1280, 2}, {19, 448, 4},  {38, 64, 2}};
 constexpr int kHeadCstride = 448;
 
 // Step list: conv (layer slot, in, out, channel offset, reorg, fused pool) or pool (in, out).
@@ -3866,11 +3940,15 @@ extern "C" int tp_yolo_create_ex(int max_tiles, const void* const* weights,
     const float alpha = parity && st.conv == 0 ? 1.0f / 255.0f
                         : fin == FMT_HL8       ? alphas[st.conv]
                                                : 1.0f;
+    // the reorg layer writes R38 (plain layout, TMA-store epilogue); tp_yolo_forward_range
+    // gathers it into the concat buffer (reorg_gather_kernel)
+    const int ob = st.reorg ? R38 : st.out;
     int rc = prepare_conv(&net->convs[st.conv], net->bufs[st.in], max_tiles, L.res,
                           buf_ch(st.in, dtype), cin, weights[st.conv], biases[st.conv], L.cout,
-                          cout_pad, L.k, head ? 0 : 1, net->bufs[st.out], buf_ch(st.out, dtype),
-                          coff, head ? 1 : 0, st.reorg, ldt, st.fpool, alpha, net->lo[st.in],
-                          fin == FMT_HL8 ? weights_lo[st.conv] : nullptr, net->lo[st.out]);
+                          cout_pad, L.k, head ? 0 : 1, net->bufs[ob], buf_ch(ob, dtype),
+                          st.reorg ? 0 : coff, head ? 1 : 0, 0, ldt, st.fpool, alpha,
+                          net->lo[st.in], fin == FMT_HL8 ? weights_lo[st.conv] : nullptr,
+                          net->lo[ob]);
     if (rc) {
       delete net;
       return rc;
@@ -3903,6 +3981,20 @@ extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_
                     buf_fmt(sp.in, net->dtype) == FMT_X2, net->lo[sp.in], net->lo[sp.out]);
     } else {
       rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
+      if (rc == TP_OK && sp.reorg) {  // layer 26 wrote R38: gather it into CAT19 [0, 256)
+        const int fmt = buf_fmt(R38, net->dtype) == FMT_X2 ? 1 : buf_fmt(R38, net->dtype) == FMT_HL8 ? 2 : 0;
+        const long long total = (long long)n_tiles * 19 * 19 * (4 * kBufs[R38].ch / 8);
+        long long blocks = (total + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        static_assert(kBufs[R38].res == 38 && kBufs[R38].ch == 64, "reorg_gather_kernel<38, 64>");
+        if (total > 0) {
+          reorg_gather_kernel<38, 64><<<(int)blocks, 256, 0, st>>>(
+              (const uint16_t*)net->bufs[R38], (const uint8_t*)net->lo[R38], n_tiles, n_tiles_dev,
+              buf_ch(R38, net->dtype), (uint16_t*)net->bufs[sp.out], (uint8_t*)net->lo[sp.out],
+              buf_ch(sp.out, net->dtype), fmt);
+          TP_LAUNCH_CHECK();
+        }
+      }
     }
     if (rc) return rc;
   }
