@@ -1526,23 +1526,29 @@ __device__ __forceinline__ void swap_epilogue_hl8(const ConvParams& p, const CUt
   // destination channel pair k = cq of each half: sources = lanes holding channels 2k, 2k+1
   const int src_a = 4 * ((2 * cq) & 7) + tq, src_b = src_a + 4;
   const bool hi_e = cq >= 4;  // channels 2k >= 8 are those lanes' e = 1 values
+  // TMEM loads are software-pipelined: row r+1's two 16x256b loads are in flight while row
+  // r's lo bytes are exchanged and both slabs are staged and stored
+  uint32_t v[16];  // [h = 0: v0..7 | h = 1: v8..15]
+  if (live && y0 < ores) {
+    tmem_ld_16x256b_x2(t_row, *reinterpret_cast<uint32_t(*)[8]>(v));
+    tmem_ld_16x256b_x2(t_row + (16u << 16), *reinterpret_cast<uint32_t(*)[8]>(v + 8));
+  }
 #pragma unroll 1
   for (int r = 0; r < SW_H; ++r) {
     if (!live || y0 + r >= ores) break;
     const uint32_t slab = slab0 + (uint32_t)(r & 1) * 2048;  // hi: [0, 1024), lo: [1024, 1536)
     uint32_t hs[2][2][2], lw[2][2];  // hi pairs [h][cg][e]; lo stmatrix words [h][cg]
+    uint32_t lp[2][2];               // lo byte pairs of channels cq (low 16) and cq + 8 (high)
+    tp::tmem_ld_wait_regs(v);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      uint32_t v[8];
-      tmem_ld_16x256b_x2(t_row + ((uint32_t)(16 * h) << 16) + (uint32_t)(r * 16), v);
-      tp::tmem_ld_wait_regs(v);
 #pragma unroll
       for (int cg = 0; cg < 2; ++cg) {
         uint32_t l2[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          float a = fmaf(__uint_as_float(v[4 * cg + 2 * e]), alpha, bq[h][e]);
-          float b = fmaf(__uint_as_float(v[4 * cg + 2 * e + 1]), alpha, bq[h][e]);
+          float a = fmaf(__uint_as_float(v[8 * h + 4 * cg + 2 * e]), alpha, bq[h][e]);
+          float b = fmaf(__uint_as_float(v[8 * h + 4 * cg + 2 * e + 1]), alpha, bq[h][e]);
           if (leaky) {
             a = fmaxf(a, 0.1f * a);
             b = fmaxf(b, 0.1f * b);
@@ -1556,14 +1562,25 @@ __device__ __forceinline__ void swap_epilogue_hl8(const ConvParams& p, const CUt
               : "f"((b - hf.y) * kLoScale), "f"((a - hf.x) * kLoScale));
           l2[e] = pr;
         }
-        const uint32_t a0 = __shfl_sync(0xffffffffu, l2[0], src_a);
-        const uint32_t a1 = __shfl_sync(0xffffffffu, l2[1], src_a);
-        const uint32_t b0 = __shfl_sync(0xffffffffu, l2[0], src_b);
-        const uint32_t b1 = __shfl_sync(0xffffffffu, l2[1], src_b);
-        // (ch 2k, px) (ch 2k+1, px) (ch 2k, px+1) (ch 2k+1, px+1)
-        lw[h][cg] = __byte_perm(hi_e ? a1 : a0, hi_e ? b1 : b0, 0x5140);
+        lp[h][cg] = l2[0] | (l2[1] << 16);
       }
     }
+    if (r + 1 < SW_H && y0 + r + 1 < ores) {
+      tmem_ld_16x256b_x2(t_row + (uint32_t)((r + 1) * 16), *reinterpret_cast<uint32_t(*)[8]>(v));
+      tmem_ld_16x256b_x2(t_row + (16u << 16) + (uint32_t)((r + 1) * 16),
+                         *reinterpret_cast<uint32_t(*)[8]>(v + 8));
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int cg = 0; cg < 2; ++cg) {
+        // one shuffle per source lane brings both of its channels (cq, cq + 8); the
+        // destination keeps the one its channel pair needs
+        const uint32_t A = __shfl_sync(0xffffffffu, lp[h][cg], src_a);
+        const uint32_t B = __shfl_sync(0xffffffffu, lp[h][cg], src_b);
+        // (ch 2k, px) (ch 2k+1, px) (ch 2k, px+1) (ch 2k+1, px+1)
+        lw[h][cg] = __byte_perm(hi_e ? A >> 16 : A, hi_e ? B >> 16 : B, 0x5140);
+      }
     if (lane == 0) bulk_wait_read1();  // the stores two rows back have read this slab
     __syncwarp();
     {
