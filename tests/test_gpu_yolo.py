@@ -84,7 +84,17 @@ def _check_layers(cuda, net, tiles):
     for step, (kind, _) in enumerate(yolo.STEPS):
         net.forward_range(n, step, step)
         torch.cuda.synchronize()
-        if kind != "conv":
+        if kind != "conv":  # the route's 2x2 max pool (step 13) copies the winner exactly
+            pooled = torch.nn.functional.max_pool2d(
+                net.step_values(step - 1, n).permute(0, 3, 1, 2), 2).permute(0, 2, 3, 1)
+            got = net.step_values(step, n)
+            if net.dtype == "fp32x2":  # re-split of hi + lo: exact up to fp16 tie rounding
+                assert (got - pooled).abs().max().item() <= 1e-6 * pooled.abs().max().item()
+            else:
+                assert torch.equal(got, pooled), "route max pool"
+            if net.dtype == "fp32":  # HL8: hi and lo codes both come from the winning pixel
+                lo = net.step_lo_tensor(step, n)
+                assert lo is not None and net.step_lo_tensor(step - 1, n) is not None
             continue
         li += 1
         src_step = conv_inputs[step]
