@@ -285,8 +285,7 @@ def run_stream(frames, settings: PipelineSettings, det=None,
         return []
     if engine is None:
         engine = make_engine(settings, W, H, det, policy, batch)
-    B = engine.max_frames
-    chunks = [items[i:i + B] for i in range(0, len(items), B)]
+    chunks = ramp_chunks(items, engine.max_frames)
     drv = StreamDriver(engine, W, H, io_threads=io_threads, lookahead=lookahead)
     sink = LocalSink(engine)
     with engine.lock:
@@ -298,6 +297,22 @@ def run_stream(frames, settings: PipelineSettings, det=None,
         finally:
             drv.close()
     return sink.results
+
+
+def ramp_chunks(items, B: int) -> list:
+    """Batches of a stream: B frames each, except that a long stream (> 2B frames) starts
+    with B/4 and B/2 so the first batch's H2D copy and stage 1 — the only ones no earlier
+    batch hides — are short; each ramp batch's compute then covers the next one's copy.
+    Results do not depend on the batching (attention history stays on the device)."""
+    sizes = []
+    if len(items) > 2 * B and B >= 4:
+        sizes = [B // 4, B // 2]
+    chunks, i = [], 0
+    for n in sizes:
+        chunks.append(items[i:i + n])
+        i += n
+    chunks += [items[j:j + B] for j in range(i, len(items), B)]
+    return chunks
 
 
 def _frame_loader(fr, W: int, H: int):
@@ -333,4 +348,4 @@ def write_results(results: Sequence[FrameResult], path) -> None:
 
 
 __all__ = ["StreamAborted", "StreamDriver", "LocalSink", "run_stream", "result_line",
-           "write_results", "stream_items", "make_engine"]
+           "write_results", "stream_items", "make_engine", "ramp_chunks"]

@@ -257,6 +257,22 @@ def test_run_stream_equals_run_sequence_and_aborts_with_cursor(cuda, clip):
     assert ei.value.cursor == 2 and len(ei.value.completed) == 2
 
 
+def test_run_stream_ramped_batches_equal_run_sequence(cuda):
+    """A stream longer than 2 batches starts with B/4 and B/2 frames (stream.ramp_chunks):
+    batches of 1, 2, 4, 4, 1 frames must give run_sequence's results."""
+    from paper_1810_10551_b200.stream import ramp_chunks, run_stream
+
+    W, H = 3840, 2160
+    gt = synthetic.generate_scene(synthetic.SceneSpec("mixed", W, H, 12, seed=3))
+    frames = [P.Frame(i, W, H, synthetic.render_frame(W, H, gt[i])) for i in range(12)]
+    assert [len(c) for c in ramp_chunks(frames, 4)] == [1, 2, 4, 4, 1]
+    settings = P.PipelineSettings.from_preset("1 att, 3 fin, 20 over")
+    seq = list(P.run_sequence(frames, settings, yolo.YoloB200Detector()))
+    streamed = run_stream(frames, settings, batch=4)
+    assert [(r.frame_id, r.detections, r.active_count) for r in streamed] == \
+        [(r.frame_id, r.detections, r.active_count) for r in seq]
+
+
 def test_run_stream_from_disk_equals_in_memory(cuda, clip, tmp_path):
     """§8f-2: a FrameSource (PPM directory) streamed from disk straight into pinned staging
     gives the same results as the in-memory frames; a corrupt file aborts at its batch."""

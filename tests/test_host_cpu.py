@@ -155,3 +155,15 @@ def test_result_line_is_byte_identical_to_reference_format():
         '{"active_count":3,"detections":[{"class":"person","confidence":0.500000,"h":40,"w":30,'
         '"x":10,"y":20},{"class":"car \\"x\\"","confidence":1.000000,"h":4,"w":3,"x":1,"y":2}],'
         '"frame_id":7,"total_count":18}')
+
+
+def test_stream_ramp_chunks():
+    """run_stream's batching: long streams ramp B/4, B/2, then B; order is kept."""
+    from paper_1810_10551_b200.stream import ramp_chunks
+
+    items = list(range(100))
+    ch = ramp_chunks(items, 30)
+    assert [len(c) for c in ch] == [7, 15, 30, 30, 18]
+    assert [x for c in ch for x in c] == items
+    assert [len(c) for c in ramp_chunks(items[:60], 30)] == [30, 30]  # not > 2B: no ramp
+    assert [len(c) for c in ramp_chunks(items[:10], 2)] == [2] * 5     # B < 4: no ramp
