@@ -2582,14 +2582,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ch = c * 16 + (odd ? 8 : 0);
           const float4 b0 = *reinterpret_cast<const float4*>(bias_s + ch);
           const float4 b1 = *reinterpret_cast<const float4*>(bias_s + ch + 4);
-          h8[0] += b0.x;
-          h8[1] += b0.y;
-          h8[2] += b0.z;
-          h8[3] += b0.w;
-          h8[4] += b1.x;
-          h8[5] += b1.y;
-          h8[6] += b1.z;
-          h8[7] += b1.w;
+          h8[0] = fmaf(h8[0], alpha, b0.x);
+          h8[1] = fmaf(h8[1], alpha, b0.y);
+          h8[2] = fmaf(h8[2], alpha, b0.z);
+          h8[3] = fmaf(h8[3], alpha, b0.w);
+          h8[4] = fmaf(h8[4], alpha, b1.x);
+          h8[5] = fmaf(h8[5], alpha, b1.y);
+          h8[6] = fmaf(h8[6], alpha, b1.z);
+          h8[7] = fmaf(h8[7], alpha, b1.w);
           if (leaky) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) h8[j] = fmaxf(h8[j], 0.1f * h8[j]);

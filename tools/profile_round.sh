@@ -5,7 +5,7 @@
 # Outputs land in gpurun_out/.
 set -u
 TAG=${1:-r01}
-CMD="python bench.py --steps 1 --warmup 1 --batch 30 --no-e2e --no-cpu-baseline"
+CMD="python bench.py --steps 1 --warmup 1 --batch 30 --no-e2e --no-cpu-baseline --no-sub"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/plain_$TAG.log; exit 1; }
 tail -1 gpurun_out/plain_$TAG.log | cut -c1-400
