@@ -4071,6 +4071,10 @@ extern "C" int tp_conv(const void* in, int n_img, int res, int cin_stride, const
     tp_set_error("tp_conv: bad argument");
     return TP_ERR_ARG;
   }
+  if (dtype == TP_DTYPE_F16F8) {  // HL8 lo planes exist only inside a tp_yolo_net plan
+    tp_set_error("tp_conv: TP_DTYPE_F16F8 is a plan format (tp_yolo_create_ex), not a layer dtype");
+    return TP_ERR_UNSUPPORTED;
+  }
   ConvLaunch L;
   const float alpha = dtype == TP_DTYPE_F16X2 && cin_stride == 16 ? 1.0f / 255.0f : 1.0f;
   int rc = prepare_conv(&L, in, n_img, res, cin_stride, cin_stride, weight, bias, cout, cout_pad,
@@ -4103,8 +4107,9 @@ extern "C" int tp_debug_conv_counters(uint64_t* out, int n, int reset) {
 extern "C" int tp_maxpool2(const void* in, int n_img, int res, int cstride, int dtype,
                            void* out, void* stream) {
   const int split = dtype == TP_DTYPE_F16X2;
-  if (in == nullptr || out == nullptr || (res & 1) || (cstride & (split ? 31 : 7))) {
-    tp_set_error("tp_maxpool2: bad argument");
+  if (in == nullptr || out == nullptr || (res & 1) || (cstride & (split ? 31 : 7)) ||
+      dtype == TP_DTYPE_F16F8) {
+    tp_set_error("tp_maxpool2: bad argument (TP_DTYPE_F16F8 pools run inside the YOLO plan)");
     return TP_ERR_ARG;
   }
   return run_pool(in, n_img, res, cstride, out, (cudaStream_t)stream, nullptr,
