@@ -2825,18 +2825,16 @@ __global__ void maxpool2_hl8_kernel(const __half* __restrict__ in, const uint8_t
                                     int n_img, int res, int cstride, __half* __restrict__ out,
                                     uint8_t* __restrict__ out_lo,
                                     const int32_t* __restrict__ n_img_dev) {
+  // one block row per output row (blockIdx.y = image * ores + y): 32-bit index math only
+  // (the 64-bit grid-stride divisions of a flat index cost more than the pool itself)
   if (n_img_dev != nullptr) n_img = min(n_img, *n_img_dev);
   const int ores = res >> 1;
   const int cg = cstride >> 3;
-  const long long total = (long long)n_img * ores * ores * cg;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i % cg);
-    long long r = i / cg;
-    const int x = (int)(r % ores);
-    r /= ores;
-    const int y = (int)(r % ores);
-    const int img = (int)(r / ores);
+  const int img = (int)blockIdx.y / ores, y = (int)blockIdx.y - img * ores;
+  const int t = (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (img >= n_img || t >= ores * cg) return;
+  {
+    const int x = t / cg, g = t - x * cg;
     float best[8];
     uint16_t bh[8];
     uint8_t bl[8];
@@ -3770,9 +3768,9 @@ int run_pool(const void* in, int n_img, int res, int cstride, void* out, cudaStr
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (in_lo != nullptr) {
-    maxpool2_hl8_kernel<<<(int)blocks, 256, 0, st>>>((const __half*)in, (const uint8_t*)in_lo,
-                                                     n_img, res, cstride, (__half*)out,
-                                                     (uint8_t*)out_lo, n_img_dev);
+    const dim3 grid((unsigned)(((res / 2) * (cstride / 8) + 255) / 256), (unsigned)(n_img * (res / 2)));
+    maxpool2_hl8_kernel<<<grid, 256, 0, st>>>((const __half*)in, (const uint8_t*)in_lo, n_img, res,
+                                              cstride, (__half*)out, (uint8_t*)out_lo, n_img_dev);
     TP_LAUNCH_CHECK();
     return TP_OK;
   }
