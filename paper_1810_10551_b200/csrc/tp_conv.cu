@@ -1458,6 +1458,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ~55 B/clk per SM unshared, held the MMA issuer on `full` 16-38% of the time).
 constexpr int SW_BK = 32, SW_W = 16, SW_H = 16, SW_CL = 2;  // 4-CTA clusters: not all co-resident (1.7x slower)
 constexpr int SW_STAGING = 8 * 2 * 2048;  // unpooled epilogue: 2 slabs of 16 px x 128 B per warp
+// HL8 unpooled epilogue: 2 slabs per warp of two rows (hi 2 x 1 KB + lo 2 x 512 B)
+constexpr int SW_SLAB_HL8 = 3072, SW_STAGING_HL8 = 8 * 2 * SW_SLAB_HL8;
 
 // 16 TMEM lanes x 16 columns in the mma-fragment layout: thread t holds lane t/4 (v0, v1;
 // v4, v5) and lane t/4 + 8 (v2, v3; v6, v7), columns 2(t%4), 2(t%4)+1 (+8 for v4..v7)
@@ -1533,10 +1535,14 @@ __device__ __forceinline__ void swap_epilogue_hl8(const ConvParams& p, const CUt
     tmem_ld_16x256b_x2(t_row, *reinterpret_cast<uint32_t(*)[8]>(v));
     tmem_ld_16x256b_x2(t_row + (16u << 16), *reinterpret_cast<uint32_t(*)[8]>(v + 8));
   }
+  // rows leave in pairs: a slab holds two rows (hi [0, 2048), lo [2048, 3072)) and one
+  // 2-row TMA store per plane drains it (half the store count of per-row slabs; a row
+  // below the image inside a pair is staged garbage that the tensor map clips)
 #pragma unroll 1
   for (int r = 0; r < SW_H; ++r) {
     if (!live || y0 + r >= ores) break;
-    const uint32_t slab = slab0 + (uint32_t)(r & 1) * 2048;  // hi: [0, 1024), lo: [1024, 1536)
+    const int rr = r & 1;
+    const uint32_t slab = slab0 + (uint32_t)((r >> 1) & 1) * SW_SLAB_HL8;
     uint32_t hs[2][2][2], lw[2][2];  // hi pairs [h][cg][e]; lo stmatrix words [h][cg]
     uint32_t lp[2][2];               // lo byte pairs of channels cq (low 16) and cq + 8 (high)
     tp::tmem_ld_wait_regs(v);
@@ -1581,29 +1587,33 @@ __device__ __forceinline__ void swap_epilogue_hl8(const ConvParams& p, const CUt
         // (ch 2k, px) (ch 2k+1, px) (ch 2k, px+1) (ch 2k+1, px+1)
         lw[h][cg] = __byte_perm(hi_e ? A >> 16 : A, hi_e ? B >> 16 : B, 0x5140);
       }
-    if (lane == 0) bulk_wait_read1();  // the stores two rows back have read this slab
-    __syncwarp();
+    if (rr == 0) {
+      if (lane == 0) bulk_wait_read1();  // the stores two pairs back have read this slab
+      __syncwarp();
+    }
     {
       // hi: matrices (h, channels 0-7 | 8-15) -> 16-byte chunk 2h + (m & 1) of the pixel's
       // 64-byte row (SW64: chunk ^ ((pixel >> 1) & 3)); one x4 per pixel group cg
 #pragma unroll
       for (int cg = 0; cg < 2; ++cg) {
-        const int pix = 8 * cg + j;
+        const int pix = 16 * rr + 8 * cg + j;
         const uint32_t addr = slab + (uint32_t)(pix * 64) + (uint32_t)(((m ^ (pix >> 1)) & 3) * 16);
         stmatrix_x4_trans(addr, hs[0][cg][0], hs[0][cg][1], hs[1][cg][0], hs[1][cg][1]);
       }
       // lo: matrix m = (h = m >> 1, cg = m & 1): pixel 8cg + j, bytes 16h .. 16h + 15
-      const int lpix = 8 * (m & 1) + j;
-      stmatrix_x4_trans(slab + 1024 + (uint32_t)(lpix * 32 + 16 * (m >> 1)), lw[0][0], lw[0][1],
+      const int lpix = 16 * rr + 8 * (m & 1) + j;
+      stmatrix_x4_trans(slab + 2048 + (uint32_t)(lpix * 32 + 16 * (m >> 1)), lw[0][0], lw[0][1],
                         lw[1][0], lw[1][1]);
     }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      const int c0 = p.out_coff + nb * 128 + (int)q * 32;
-      tma_store_4d(&tmC, smC + (slab - tp::smem_u32(smC)), c0, x0, y0 + r, img);
-      tma_store_4d(&tmC2, smC + (slab + 1024 - tp::smem_u32(smC)), c0, x0, y0 + r, img);
-      bulk_commit();
+    if (rr == 1 || r + 1 >= SW_H || y0 + r + 1 >= ores) {  // the pair is staged: store it
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int c0 = p.out_coff + nb * 128 + (int)q * 32;
+        tma_store_4d(&tmC, smC + (slab - tp::smem_u32(smC)), c0, x0, y0 + r - rr, img);
+        tma_store_4d(&tmC2, smC + (slab + 2048 - tp::smem_u32(smC)), c0, x0, y0 + r - rr, img);
+        bulk_commit();
+      }
     }
   }
 }
@@ -1833,8 +1843,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t slab0 = tp::smem_u32(smC) + warp * 4096;
         const int m = (int)lane >> 3, j = (int)lane & 7;  // stmatrix: matrix m, row j
         if (p.out_lo != nullptr) {
-          swap_epilogue_hl8(p, tmC, tmC2, smC, slab0, t_row, live, y0, x0, img, nb, q, lane,
-                            ores, alpha, leaky);
+          swap_epilogue_hl8(p, tmC, tmC2, smC, tp::smem_u32(smC) + warp * (2 * SW_SLAB_HL8), t_row,
+                            live, y0, x0, img, nb, q, lane, ores, alpha, leaky);
           tp::tc_fence_before();
           __syncwarp();
           if (lane == 0) tp::mbar_arrive(&tempty[g]);
@@ -3398,14 +3408,14 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     q.a_stage_bytes = SW_W * (SW_H + 2) * SW_BK * 2;  // pixel box (MMA B operand)
     q.b_stage_bytes = 3 * 128 * SW_BK * 2;              // three weight slices (MMA A operand)
     q.bres_bytes = 0;
-    q.stage_bytes = pool ? 0 : SW_STAGING;
+    q.stage_bytes = pool ? 0 : out_lo != nullptr ? SW_STAGING_HL8 : SW_STAGING;
     q.halo = 0;
     q.sub = 1;
     q.rect = pool ? 1 : 0;
     if (!pool && out_lo != nullptr) {  // HL8: hi 16 px x 64 B (SW64) + lo 16 px x 32 B
       const uint64_t cdims[4] = {(uint64_t)out_cstride, (uint64_t)res, (uint64_t)res,
                                  (uint64_t)max_img};
-      const uint32_t cbox[4] = {32, SW_W, 1, 1};
+      const uint32_t cbox[4] = {32, SW_W, 2, 1};  // two rows per store
       rc = make_tmap(&P.tmC, out, 4, cdims, cbox, CU_TENSOR_MAP_SWIZZLE_64B, f16);
       if (rc) return rc;
       rc = make_tmap(&P.tmC2, out_lo, 4, cdims, cbox, CU_TENSOR_MAP_SWIZZLE_NONE, f16, 1);
