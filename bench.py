@@ -52,7 +52,11 @@ sys.path.insert(0, ROOT)
 PRESET = "1 att, 3 fin, 20 over"
 FRAMES = {"4k": (3840, 2160), "8k": (7680, 4320)}
 METRIC = "frames/sec, synthetic 4K & 8K video, 1/2/4/8 B200; crops/sec; % roofline"
-LAUNCHES_PER_STEP = (1 + 24 + 1 + 1) + (2 + 1 + 24 + 1 + 1 + 1)  # stage 1 + finish
+# our kernels per step (CUPTI table, profiles/r02_step_kernel_table.txt): a YOLO forward is 25
+# launches (23 convs, the route max pool, the reorg gather); stage 1 = gather + forward +
+# decode + attention boxes; finish = select + build jobs + gather + forward + decode +
+# collect + postprocess
+LAUNCHES_PER_STEP = (1 + 25 + 1 + 1) + (1 + 1 + 1 + 25 + 1 + 1 + 1)
 
 
 def parse(argv=None):
