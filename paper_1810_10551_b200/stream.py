@@ -31,6 +31,9 @@ client.py:202). The multi-GPU version (frame shards, NCCL result gather) is
 from __future__ import annotations
 
 import json
+import os
+import sys
+import time
 from collections.abc import Sequence
 from concurrent.futures import ThreadPoolExecutor
 
@@ -107,6 +110,8 @@ class StreamDriver:
         self.fin_end = [ev() for _ in range(3)]  # batch k -> k % 3 (read two batches later)
         self.pool = ThreadPoolExecutor(max_workers=max(1, io_threads))
         self.dev_name = f"cuda:{torch.cuda.current_device()}"
+        # TP_STREAM_TRACE=1: host seconds per phase of run(), printed to stderr at the end
+        self.trace = {} if os.environ.get("TP_STREAM_TRACE") else None
 
     def close(self):
         self.pool.shutdown(wait=True)
@@ -197,12 +202,16 @@ class StreamDriver:
         for k in range(nb):
             chunk = chunks[k] if k < len(chunks) else []
             n = len(chunk) if failed is None else 0
+            t0 = time.perf_counter()
             if n:
                 try:
                     self.finish(k, n)
                 except Exception as exc:
                     failed, n = exc, 0
             sink.after_finish(k, n, chunk, failed)
+            t1 = time.perf_counter()
+            if self.trace is not None:
+                self._tr("finish_enqueue", t1 - t0)
             if failed is None and k + 1 < len(chunks):
                 # host packing + H2D + stage 1 of batch k+1 are queued BEFORE batch k-1's
                 # results are built on the host, so the copy and the look-ahead never wait
@@ -212,6 +221,8 @@ class StreamDriver:
                     self.stage1(k + 1, len(chunks[k + 1]))
                 except Exception as exc:
                     failed = exc
+                if self.trace is not None:
+                    self._tr("load_stage1_enqueue", time.perf_counter() - t1)
             if pending is not None:  # batch k-1 finishes while batch k is queued
                 self._emit(sink, *pending)
                 pending = None
@@ -225,11 +236,22 @@ class StreamDriver:
         if pending is not None:
             self._emit(sink, *pending)
         sink.check(nb, failed)
+        if self.trace is not None:
+            print("stream trace (host s): " + ", ".join(f"{k} {v:.4f}" for k, v in self.trace.items())
+                  + f", batches {nb}", file=sys.stderr)
 
     def _emit(self, sink, k, n, chunk):
+        t0 = time.perf_counter()
         if n:
             self.fin_end[k % 3].synchronize()
+        t1 = time.perf_counter()
         sink.emit(k, n, chunk, self.timing(k, n) if n else None)
+        if self.trace is not None:
+            self._tr("emit_wait", t1 - t0)
+            self._tr("emit_build", time.perf_counter() - t1)
+
+    def _tr(self, key, dt):
+        self.trace[key] = self.trace.get(key, 0.0) + dt
 
 
 class LocalSink:

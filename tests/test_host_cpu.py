@@ -167,3 +167,23 @@ def test_stream_ramp_chunks():
     assert [x for c in ch for x in c] == items
     assert [len(c) for c in ramp_chunks(items[:60], 30)] == [30, 30]  # not > 2B: no ramp
     assert [len(c) for c in ramp_chunks(items[:10], 2)] == [2] * 5     # B < 4: no ramp
+
+
+def test_hl8_plan_tables():
+    """The F16F8 (HL8) plan's host-side tables, without a GPU: every conv but layer 0 reads
+    HL8 planes; the weight scales keep the fp16 hi-pass weights finite and the e4m3 lo-pass
+    weights <= 240 with b = c - LO_EXP; the issued-work count is 1.5x K past layer 0."""
+    import numpy as np
+
+    from paper_1810_10551_b200 import yolo
+
+    assert yolo.hl8_input_slots() == frozenset(range(1, len(yolo.LAYERS)))
+    wpacks, _ = yolo.make_weights(0, dtype="fp16")
+    for li in range(1, len(yolo.LAYERS)):
+        c, b = yolo.hl8_scales(wpacks[li])
+        wmax = float(np.abs(wpacks[li]).max())
+        assert b == c - yolo.LO_EXP and wmax * 2.0 ** c <= 65504 and wmax * 2.0 ** b <= 240
+        assert wmax * 2.0 ** (b + 1) > 240 or wmax * 2.0 ** (c + 1) > 65504  # the largest
+    g = [2.0 * s * s * co * ci * k * k / 1e9 for _, ci, co, k, s in yolo.LAYERS]
+    assert abs(yolo.exec_gflop_per_tile("fp32") - (g[0] + 1.5 * sum(g[1:]))) < 1e-9
+    assert abs(yolo.exec_gflop_per_tile("fp32x2") - (g[0] + 2.0 * sum(g[1:]))) < 1e-9
