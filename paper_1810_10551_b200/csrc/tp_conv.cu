@@ -2016,12 +2016,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         PROF_T0(tw);
         tp::mbar_wait(&empty[s], ph ^ 1);
         PROF_ADD(pr_wait, tw);
-        tp::mbar_arrive_expect_tx(&full[s], L0_STAGE);
         uint8_t* dst = smA + (size_t)s * L0_STAGE;
+        if (p.dbg & 16) {  // profiling: no TMA, stale operands
+          tp::mbar_arrive(&full[s]);
+        } else {
+          tp::mbar_arrive_expect_tx(&full[s], L0_STAGE);
 #pragma unroll
-        for (int f = 0; f < 2; ++f)  // input row phase; both column phases share the rows
-          tma_load_3d(dst + f * L0_BOX_BYTES, &tmA, &full[s], 0, 16 * bx,
-                      img * hp + 1 + 16 * by + f - 1);
+          for (int f = 0; f < 2; ++f)  // input row phase; both column phases share the rows
+            tma_load_3d(dst + f * L0_BOX_BYTES, &tmA, &full[s], 0, 16 * bx,
+                        img * hp + 1 + 16 * by + f - 1);
+        }
         if (++s == S) {
           s = 0;
           ph ^= 1;
@@ -2056,7 +2060,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         PROF_ADD(w_fu, t2);
         tp::tc_fence_after();
         const uint64_t ad0 = a_desc0 + (uint64_t)(s * (L0_STAGE >> 4));
-        if (tp::elect_one()) {
+        const bool leader = tp::elect_one();
+        if (leader && (p.dbg & 2)) {  // profiling: no MMAs
+          tp::mma_commit(&empty[s]);
+          tp::mma_commit(&tfull[acc]);
+        } else if (leader) {
           // pool row py: accumulators (py, px=0) and (py, px=1) are adjacent TMEM column
           // blocks and both read R(k)'s first 32 bytes, with adjacent weight chunks (even,
           // odd-A) — one N=64 MMA; the odd column's second-chunk term is one N=32 MMA
@@ -2107,6 +2115,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       PROF_ADD(e_wait, t3);
       ph ^= 1u << acc;
       tp::tc_fence_after();
+      if (p.dbg & 1) {  // profiling: no epilogue work
+        tp::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tp::mbar_arrive(&tempty[acc]);
+        continue;
+      }
       // split outputs: this warp's 32 pooled pixels (2 output rows x 16) are staged as 32
       // SW128 smem rows [hi 16 | lo 16] x 2 and written by one TMA store — per-thread
       // 16-byte stores at a 128-byte pixel pitch were LSU-bound (0.86 -> 0.44 ms per 120
