@@ -99,6 +99,32 @@ def test_config0_dense_frame_matches_cpu_reference(cuda, cpu):
     assert len(ref[0]) > 0 and len(ref[1]) > 8  # a dense frame: many crops, detections
 
 
+def test_8k_frames_match_cpu_reference(cuda):
+    """BASELINE configs[3] (8K): frames 0 and 1 of a dense 7680x4320 scene (the K = 2 window:
+    frame 1 carries frame 0's attention) through the drop-in API vs the CPU reference."""
+    W8, H8 = 7680, 4320
+    gt = synthetic.generate_scene(synthetic.SceneSpec("dense", W8, H8, 2, seed=0))
+    pxs = {i: synthetic.render_frame(W8, H8, gt[i]) for i in range(2)}
+    plan = R.Plan(W8, H8, 1, 3, 20)
+    det = E.CpuYolo(lambda fid: pxs[fid], yolo.COCO_NAMES)
+    gdet = yolo.YoloB200Detector()
+    frames = [P.Frame(i, W8, H8, pxs[i]) for i in range(2)]
+    eng = P._engine_for(gdet, SETTINGS, W8, H8, None)
+    out = eng.evaluate_frames(frames, history=())
+    report, exact, hist = [], 0, []
+    for fid in range(2):
+        ref = E.reference_frame(plan, fid, det, hist)
+        res, att = out[fid]
+        n_act = int(eng.active_counts[fid])
+        gpu_active = eng.active_ids[fid, :n_act].cpu().tolist()
+        exact += _check_frame(plan, det, fid, ref, res, att, gpu_active, [0] if fid else [],
+                              report)
+        hist = [ref[2]]
+    print("\n".join(report))
+    print(f"8K: {exact}/2 frames exact; {len(det.raw)} CPU YOLO tiles")
+    assert exact == 2 and len(ref[0]) > 0
+
+
 def test_bench_clip_sample_matches_cpu_reference(cuda, cpu):
     """Stratified sample of the bench clip through the drop-in API (run_sequence on
     [f-1, f]: the K=2 window) vs the CPU reference with the same history."""
