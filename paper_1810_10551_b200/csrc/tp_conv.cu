@@ -1818,22 +1818,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       if (POOL) {
+        // TMEM loads software-pipelined: pooled row r+1's two loads are in flight while
+        // row r is pooled and stored
+        uint32_t a[16], b[16];
+        tp::tmem_ld16(t_row, a);
+        tp::tmem_ld16(t_row + 16u, b);
         for (int r = 0; r < SW_H / 2; ++r) {
-          uint32_t a[16], b[16];
-          tp::tmem_ld16(t_row + (uint32_t)(2 * r * 16), a);
-          tp::tmem_ld16(t_row + (uint32_t)((2 * r + 1) * 16), b);
-          tp::tmem_ld_wait();
+          tp::tmem_ld_wait_regs(a);
+          tp::tmem_ld_wait_regs(b);
+          float m[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)  // 2x2 max before bias + leaky (both monotonic)
+            m[j] = fmaxf(fmaxf(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1])),
+                         fmaxf(__uint_as_float(b[2 * j]), __uint_as_float(b[2 * j + 1])));
+          if (r + 1 < SW_H / 2) {
+            tp::tmem_ld16(t_row + (uint32_t)(2 * (r + 1) * 16), a);
+            tp::tmem_ld16(t_row + (uint32_t)((2 * (r + 1) + 1) * 16), b);
+          }
           const int oy = (y0 >> 1) + r;
           if (!live || oy >= ores) continue;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int ox = (x0 >> 1) + j;
-            // 2x2 max before bias + leaky (both monotonic)
-            const float m = fmaxf(fmaxf(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1])),
-                                  fmaxf(__uint_as_float(b[2 * j]), __uint_as_float(b[2 * j + 1])));
-            if (ox < ores) put(oy, ox, m);
+            if (ox < ores) put(oy, ox, m[j]);
           }
         }
+        tp::tmem_ld_wait();
       } else {
         // unpooled (parity plan): per output row, the warp's 32 channels x 16 pixels leave
         // through a 16 x 128 B smem slab (SW128) written transposed by stmatrix, then one TMA
