@@ -1458,6 +1458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ~55 B/clk per SM unshared, held the MMA issuer on `full` 16-38% of the time).
 constexpr int SW_BK = 32, SW_W = 16, SW_H = 16, SW_CL = 2;  // 4-CTA clusters: not all co-resident (1.7x slower)
 constexpr int SW_STAGING = 8 * 2 * 2048;  // unpooled epilogue: 2 slabs of 16 px x 128 B per warp
+constexpr int SW_POOL_SCRATCH = 1024;     // pooled HL8 epilogue: per-warp transpose tile
 // HL8 unpooled epilogue: 2 slabs per warp of two rows (hi 2 x 1 KB + lo 2 x 512 B)
 constexpr int SW_SLAB_HL8 = 3072, SW_STAGING_HL8 = 8 * 2 * SW_SLAB_HL8;
 
@@ -1837,6 +1838,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           const int oy = (y0 >> 1) + r;
           if (!live || oy >= ores) continue;
+          if (p.out_lo != nullptr) {
+            // HL8: the warp's 32 channels x 8 pooled pixels go through a per-warp smem tile
+            // (hi [8 px][32 ch] fp16, lo [8 px][32 ch] bytes) and leave as 16-byte vectors,
+            // one store per lane and plane instead of 8 scalar 2-byte / 1-byte stores per
+            // lane (the scalar stores held the epilogue at ~1.4x the MMA time)
+            uint8_t* scr = smC + warp * SW_POOL_SCRATCH;
+            __syncwarp();  // the previous row's vector reads are done
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float v = fmaf(m[j], alpha, bco);
+              if (leaky) v = fmaxf(v, 0.1f * v);
+              store_hl8_1(reinterpret_cast<__half*>(scr) + j * 32 + lane, scr + 512 + j * 32 + lane, v);
+            }
+            __syncwarp();
+            const int pj = (int)lane >> 2, c8 = (int)lane & 3;
+            const int ox = (x0 >> 1) + pj;
+            const size_t px = (size_t)(img * ores + oy) * ores + ox;
+            const int cb = p.out_coff + nb * 128 + (int)q * 32;
+            if (ox < ores) {
+              *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + px * p.out_cstride + cb + 8 * c8) =
+                  *reinterpret_cast<const uint4*>(scr + pj * 64 + c8 * 16);
+              if (c8 < 2)
+                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out_lo) + px * p.out_cstride + cb + 16 * c8) =
+                    *reinterpret_cast<const uint4*>(scr + 512 + pj * 32 + c8 * 16);
+            }
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int ox = (x0 >> 1) + j;
@@ -3432,7 +3460,8 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
     q.a_stage_bytes = SW_W * (SW_H + 2) * SW_BK * 2;  // pixel box (MMA B operand)
     q.b_stage_bytes = 3 * 128 * SW_BK * 2;              // three weight slices (MMA A operand)
     q.bres_bytes = 0;
-    q.stage_bytes = pool ? 0 : out_lo != nullptr ? SW_STAGING_HL8 : SW_STAGING;
+    q.stage_bytes = pool ? (out_lo != nullptr ? 8 * SW_POOL_SCRATCH : 0)
+                    : out_lo != nullptr ? SW_STAGING_HL8 : SW_STAGING;
     q.halo = 0;
     q.sub = 1;
     q.rect = pool ? 1 : 0;
