@@ -5,7 +5,7 @@
 * ``make_weights(seed)`` — deterministic random init shared with the CPU oracle:
   He-normal conv weights, BatchNorm statistics folded into weight+bias, weights rounded
   to bf16. The 1x1 head (layer 30) is a committed, deterministic linear probe
-  (tools/calibrate_head.py) so the random backbone emits boxes on the synthetic
+  (tests/tools/calibrate_head.py) so the random backbone emits boxes on the synthetic
   scenes; without it no score reaches the pipeline's 0.3 threshold.
 * ``YoloNet`` — the device plan (23 tcgen05 conv launches + pools + route/reorg) over
   a persistent workspace; ``YoloB200Detector`` — the plugin-compatible Detector.

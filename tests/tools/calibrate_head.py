@@ -1,7 +1,7 @@
 """Build the committed YOLO head for a seed: a deterministic linear probe on the random
 backbone's layer-29 features (dev tool; its output is data, not code on the hot path).
 
-    python tools/calibrate_head.py [--seed 0]
+    python tests/tools/calibrate_head.py [--seed 0]
 
 Why: a random-init YOLO v2 never reaches the pipeline's 0.3 score threshold (SURVEY
 §0.4), so stage 1 would select nothing. The probe keeps the backbone random (seeded,
@@ -20,7 +20,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 from oracle import pipeline_ref, yolo_ref  # noqa: E402

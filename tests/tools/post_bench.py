@@ -1,6 +1,6 @@
 """tp_postprocess (K7: per-class greedy NMS + split merge + min_conf) at stress sizes.
 
-    python tools/post_bench.py [--frames 30] [--n 400 1000 2000] [--reps 20]
+    python tests/tools/post_bench.py [--frames 30] [--n 400 1000 2000] [--reps 20]
 
 One launch handles --frames frames of n raw detections each (one CTA per frame, as in the
 engine's batched step). Reports the CUDA-event time per launch, per frame, the bytes the
@@ -19,7 +19,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 

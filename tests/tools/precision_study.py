@@ -6,8 +6,8 @@ the fp32 reference? Each conv slot's OUTPUT is rounded as chosen ("fp32" exact, 
 hi + fp16(x - hi) as the GPU's parity buffers store it, "fp16" = one RNE fp16), the rest
 of the forward is fp32, and the decoded detections are compared with the all-fp32 run.
 
-  python tools/precision_study.py [--tiles 8] [--greedy]
-  python tools/precision_study.py --lo8        # the HL8 plan (fp16 hi + e4m3 lo on every input)
+  python tests/tools/precision_study.py [--tiles 8] [--greedy]
+  python tests/tools/precision_study.py --lo8        # the HL8 plan (fp16 hi + e4m3 lo on every input)
 
 Prints per-slot sensitivity (only that slot fp16) and the executed-FLOP saving of a plan.
 --lo8 emulates the "fp32" plan exactly: every conv input x (but layer 0's) as
@@ -24,7 +24,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 
 from oracle import pipeline_ref as R  # noqa: E402
