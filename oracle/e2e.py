@@ -111,15 +111,30 @@ def rounding_edges(plan, det, fids):
 
 def compare_boxes(ref_boxes, gpu_boxes):
     """Attention box lists (int rects). Returns (exact, n_1px) — n_1px = boxes equal up
-    to a 1-px rounding flip; exact False if anything else differs."""
+    to a 1-px rounding flip; exact False if anything else differs. The list order is
+    crop-id order, then the detector's descending confidence (pipeline.py:297-316); two
+    boxes of near-equal confidence may swap places (a score-tolerance order flip, as in
+    compare_dets), which changes nothing downstream (merge_temporal dedups and
+    select_active tests every box), so a positional mismatch falls back to matching the
+    two lists as multisets."""
     if len(ref_boxes) != len(gpu_boxes):
         return False, 0
     n1 = 0
     for a, b in zip(ref_boxes, gpu_boxes):
         d = max(abs(p - q) for p, q in zip(a, b))
         if d > 1:
+            break
+        n1 += d == 1
+    else:
+        return True, n1
+    free, n1 = list(gpu_boxes), 0
+    for a in ref_boxes:
+        cand = [(max(abs(p - q) for p, q in zip(a, b)), k) for k, b in enumerate(free)]
+        d, k = min(cand)
+        if d > 1:
             return False, n1
         n1 += d == 1
+        free.pop(k)
     return True, n1
 
 

@@ -181,6 +181,34 @@ def test_bench_clip_sample_matches_cpu_reference(cuda, cpu):
     assert box_err <= 1e-3 and conf_err <= 1e-3
 
 
+@pytest.mark.skipif(not __import__("os").environ.get("TP_PARITY_SWEEP"),
+                    reason="opt-in (TP_PARITY_SWEEP=1): 30 frames, ~2 min of CPU YOLO")
+def test_parity_sweep_every_tenth_frame(cuda, cpu):
+    """Every 10th frame of the bench clip (30 frames over the sparse / dense / mixed
+    thirds), each with its predecessor for the K = 2 window, against the CPU reference."""
+    det, pixels_of = cpu
+    plan = R.Plan(W, H, 1, 3, 20)
+    gdet = yolo.YoloB200Detector()
+    report, exact = [], 0
+    for fid in range(0, 300, 10):
+        hist_fids = [fid - 1] if fid > 0 else []
+        hist = []
+        for h in hist_fids:
+            det.prefetch(h, plan.att[3])
+            hist.append(R.attention_pass(plan, h, det, 0.3))
+        ref = E.reference_frame(plan, fid, det, hist)
+        frames = [P.Frame(i, W, H, pixels_of(i)) for i in hist_fids + [fid]]
+        eng = P._engine_for(gdet, SETTINGS, W, H, None)
+        out = eng.evaluate_frames(frames, history=())
+        res, att = out[-1]
+        n_act = int(eng.active_counts[len(frames) - 1])
+        gpu_active = eng.active_ids[len(frames) - 1, :n_act].cpu().tolist()
+        exact += _check_frame(plan, det, fid, ref, res, att, gpu_active, hist_fids, report)
+    print("\n".join(report))
+    print(f"sweep: {exact}/30 frames exact; {len(det.raw)} CPU YOLO tiles evaluated")
+    assert exact == 30
+
+
 def test_bench_engine_run_equals_api_on_sample(cuda, cpu, clip):
     """The bench's own device path (whole clip in 30-frame batches, frames rendered on
     the GPU, history carried on device) gives the API's FrameResults at the sampled
