@@ -1843,25 +1843,42 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (hi [8 px][32 ch] fp16, lo [8 px][32 ch] bytes) and leave as 16-byte vectors,
             // one store per lane and plane instead of 8 scalar 2-byte / 1-byte stores per
             // lane (the scalar stores held the epilogue at ~1.4x the MMA time)
-            uint8_t* scr = smC + warp * SW_POOL_SCRATCH;
+            const uint32_t scr = tp::smem_u32(smC) + warp * SW_POOL_SCRATCH;  // explicit .shared
             __syncwarp();  // the previous row's vector reads are done
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               float v = fmaf(m[j], alpha, bco);
               if (leaky) v = fmaxf(v, 0.1f * v);
-              store_hl8_1(reinterpret_cast<__half*>(scr) + j * 32 + lane, scr + 512 + j * 32 + lane, v);
+              const __half h = __float2half_rn(v);
+              uint16_t pr;
+              asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;"
+                  : "=h"(pr)
+                  : "f"(0.0f), "f"((v - __half2float(h)) * kLoScale));
+              asm volatile("st.shared.b16 [%0], %1;" ::"r"(scr + (uint32_t)(j * 32 + lane) * 2),
+                           "h"(__half_as_ushort(h))
+                           : "memory");
+              asm volatile("st.shared.b8 [%0], %1;" ::"r"(scr + 512u + (uint32_t)(j * 32 + lane)),
+                           "h"(pr)
+                           : "memory");
             }
             __syncwarp();
             const int pj = (int)lane >> 2, c8 = (int)lane & 3;
             const int ox = (x0 >> 1) + pj;
             const size_t px = (size_t)(img * ores + oy) * ores + ox;
             const int cb = p.out_coff + nb * 128 + (int)q * 32;
+            uint4 hv, lv;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(hv.x), "=r"(hv.y), "=r"(hv.z), "=r"(hv.w)
+                         : "r"(scr + (uint32_t)(pj * 64 + c8 * 16))
+                         : "memory");
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(lv.x), "=r"(lv.y), "=r"(lv.z), "=r"(lv.w)
+                         : "r"(scr + 512u + (uint32_t)(pj * 32 + (c8 & 1) * 16))
+                         : "memory");
             if (ox < ores) {
-              *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + px * p.out_cstride + cb + 8 * c8) =
-                  *reinterpret_cast<const uint4*>(scr + pj * 64 + c8 * 16);
+              *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.out) + px * p.out_cstride + cb + 8 * c8) = hv;
               if (c8 < 2)
-                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out_lo) + px * p.out_cstride + cb + 16 * c8) =
-                    *reinterpret_cast<const uint4*>(scr + 512 + pj * 32 + c8 * 16);
+                *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out_lo) + px * p.out_cstride + cb + 16 * c8) = lv;
             }
             continue;
           }
