@@ -184,6 +184,17 @@ def test_hl8_plan_tables():
         wmax = float(np.abs(wpacks[li]).max())
         assert b == c - yolo.LO_EXP and wmax * 2.0 ** c <= 65504 and wmax * 2.0 ** b <= 240
         assert wmax * 2.0 ** (b + 1) > 240 or wmax * 2.0 ** (c + 1) > 65504  # the largest
+        # hi-pass weights are the model's fp16 values scaled exactly by 2^c; the e4m3
+        # lo-pass copy is within e4m3's 2^-4 relative rounding of w (normal range)
+        whi, wlo, alpha = yolo.hl8_weights(wpacks[li])
+        assert alpha == 2.0 ** -c
+        assert np.array_equal(whi.astype(np.float16).astype(np.float32), whi)
+        assert np.array_equal(whi * np.float32(alpha), np.asarray(wpacks[li], np.float32))
+        lov = yolo.hl8_lo_weight_values(wpacks[li])
+        w = np.asarray(wpacks[li], np.float32)
+        big = np.abs(w) * 2.0 ** b >= 2.0 ** -6  # e4m3 normal range
+        assert np.all(np.abs(lov - w)[big] <= np.abs(w)[big] * 2.0 ** -4 + 1e-12)
+        assert wlo.dtype == np.uint8 and wlo.shape == w.shape
     g = [2.0 * s * s * co * ci * k * k / 1e9 for _, ci, co, k, s in yolo.LAYERS]
     assert abs(yolo.exec_gflop_per_tile("fp32") - (g[0] + 1.5 * sum(g[1:]))) < 1e-9
     assert abs(yolo.exec_gflop_per_tile("fp32x2") - (g[0] + 2.0 * sum(g[1:]))) < 1e-9
