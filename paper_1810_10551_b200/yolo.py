@@ -39,9 +39,6 @@ HEAD_CPAD = 448
 ANCHORS = np.array([0.57273, 0.677385, 1.87446, 2.06253, 3.33843, 5.47434, 7.88282, 3.52778,
                     9.77052, 9.16828], dtype=np.float32)
 GFLOP_PER_TILE = sum(2.0 * (s * s) * cout * cin * k * k for _, cin, cout, k, s in LAYERS) / 1e9
-# tensor-core work actually issued per tile in the fp32-parity plan: K doubled (hi + lo)
-# on every layer but layer 0 (its K = 3 taps x 48 slot halves vs 27 algorithmic MACs)
-EXEC_GFLOP_PER_TILE_FP32 = (2 * GFLOP_PER_TILE - 2.0 * 608 * 608 * 32 * 3 * 9 / 1e9)
 
 COCO_NAMES = (
     "person", "bicycle", "car", "motorbike", "aeroplane", "bus", "train", "truck", "boat",
