@@ -118,3 +118,39 @@ def test_unframed_garbage_reports_malformed_and_closes():
             header, _ = wire.recv_message(sock)
             assert header["type"] == "ERROR" and header["code"] == "malformed"
             assert sock.recv(1) == b""  # the server closed the connection
+
+
+def test_message_parser_streamed_and_malformed():
+    """The I/O-free parser the client and the worker share: a request fed one byte at a
+    time round-trips, and each malformed form raises ProtocolError with the reference's
+    message (wire.py recv_message)."""
+    tiles = np.arange(2 * 3 * 3, dtype=np.uint8).tobytes()
+    msg = wire.eval_request(7, [{"crop_id": 1, "width": 3, "height": 2}], tiles)
+    stream = iter(msg)
+    header, payload = wire.drive(wire.message_steps(),
+                                 lambda n: bytes(next(stream) for _ in range(n)))
+    assert header == {"type": "EVAL_REQUEST", "frame_id": 7,
+                      "crops": [{"crop_id": 1, "width": 3, "height": 2}]}
+    assert payload == tiles and next(stream, None) is None
+
+    def parse(raw):
+        buf = memoryview(raw)
+        pos = [0]
+
+        def read(n):
+            chunk = bytes(buf[pos[0]:pos[0] + n])
+            pos[0] += n
+            return chunk
+        return wire.drive(wire.message_steps(), read)
+
+    def framed(body):
+        return struct.pack(">I", len(body)) + body
+
+    for raw, text in [(struct.pack(">I", wire.MAX_HEADER_BYTES + 1), "exceeds limit"),
+                      (framed(b"\xff\xfe"), "not valid JSON"),
+                      (framed(b"[1,2]"), "'type' field"),
+                      (framed(b'{"crops":[{"width":1}],"type":"EVAL_REQUEST"}'),
+                       "malformed crop list")]:
+        with pytest.raises(wire.ProtocolError, match=text):
+            parse(raw)
+    assert parse(framed(b'{"type":"HEALTH"}')) == ({"type": "HEALTH"}, b"")
