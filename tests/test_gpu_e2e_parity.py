@@ -125,6 +125,41 @@ def test_8k_frames_match_cpu_reference(cuda):
     assert exact == 2 and len(ref[0]) > 0
 
 
+@pytest.mark.parametrize("FW,FH,preset,kind", [
+    (1080, 1920, "1 att, 3 fin, 20 over", "dense"),    # portrait: attention square wider than the frame
+    (1920, 1080, "2 att, 4 fin, 50 over", "mixed"),    # 1080p, two attention rows, 50 px overlap
+    (800, 600, "1 att, 2 fin, 0 over", "straddle"),    # sub-608 crops (upsampling), no overlap
+])
+def test_other_shapes_and_presets_match_cpu_reference(cuda, FW, FH, preset, kind):
+    """Frame shapes and presets off the bench's 16:9 P1 path — crops that leave the frame,
+    other crop sides (up- and down-sampling), several attention rows, other overlaps —
+    through the drop-in API (engine on frames [0, 1], the K = 2 window) vs the CPU
+    reference with the same history."""
+    gt = synthetic.generate_scene(synthetic.SceneSpec(kind, FW, FH, 2, seed=3))
+    pxs = {i: synthetic.render_frame(FW, FH, gt[i]) for i in range(2)}
+    settings = P.PipelineSettings.from_preset(preset)
+    plan = R.Plan(FW, FH, settings.attention.rows, settings.final.rows,
+                  settings.attention.overlap_px)
+    det = E.CpuYolo(lambda fid: pxs[fid], yolo.COCO_NAMES)
+    gdet = yolo.YoloB200Detector()
+    eng = P._engine_for(gdet, settings, FW, FH, None)
+    out = eng.evaluate_frames([P.Frame(i, FW, FH, pxs[i]) for i in range(2)], history=())
+    report, exact, hist, n_att = [], 0, [], 0
+    for fid in range(2):
+        ref = E.reference_frame(plan, fid, det, hist)
+        res, att = out[fid]
+        n_act = int(eng.active_counts[fid])
+        gpu_active = eng.active_ids[fid, :n_act].cpu().tolist()
+        exact += _check_frame(plan, det, fid, ref, res, att, gpu_active, [0] if fid else [],
+                              report)
+        hist = [ref[2]]
+        n_att += len(ref[2])
+        assert res.total_count == len(plan.fin[3])
+    print("\n".join(report))
+    print(f"{FW}x{FH} {preset!r}: {exact}/2 frames exact; {len(det.raw)} CPU YOLO tiles")
+    assert n_att > 0  # the scenes give stage 1 something to select
+
+
 def test_bench_clip_sample_matches_cpu_reference(cuda, cpu):
     """Stratified sample of the bench clip through the drop-in API (run_sequence on
     [f-1, f]: the K=2 window) vs the CPU reference with the same history."""
