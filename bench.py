@@ -52,11 +52,15 @@ sys.path.insert(0, ROOT)
 PRESET = "1 att, 3 fin, 20 over"
 FRAMES = {"4k": (3840, 2160), "8k": (7680, 4320)}
 METRIC = "frames/sec, synthetic 4K & 8K video, 1/2/4/8 B200; crops/sec; % roofline"
-# our kernels per step (CUPTI table, profiles/r02_step_kernel_table.txt): a YOLO forward is 25
-# launches (23 convs, the route max pool, the reorg gather); stage 1 = gather + forward +
+# our kernels per step (CUPTI table, profiles/r02_step_kernel_table.txt): a YOLO forward is
+# 23 convs + the route max pool + the reorg gather, minus the convs fused into their
+# producer (fp32 plan: layer 5 inside layer 4's kernel -> 24); stage 1 = gather + forward +
 # decode + attention boxes; finish = select + build jobs + gather + forward + decode +
 # collect + postprocess
-LAUNCHES_PER_STEP = (1 + 25 + 1 + 1) + (1 + 1 + 1 + 25 + 1 + 1 + 1)
+
+
+def launches_per_step(fwd: int) -> int:
+    return (1 + fwd + 1 + 1) + (1 + 1 + 1 + fwd + 1 + 1 + 1)
 
 
 def parse(argv=None):
@@ -524,7 +528,8 @@ def gpu_run(args, rank, world, local, shared_gpu, group, sub=False):
     tiles_per_frame = (stage1 + tiles2) / (args.steps * B)
     fields = {"value": value, "ms_per_step": ms / args.steps, "clocks": clocks.summary(),
               "conv_tflops": conv_tflops, "conv_busy_ms": busy, "tiles_per_frame": tiles_per_frame,
-              "kernels": eng.net.kernel_summary()}
+              "kernels": eng.net.kernel_summary(),
+              "forward_launches": 25 - len(eng.net.fused_steps)}
     return fields, eng, objs, clip
 
 
@@ -780,7 +785,7 @@ def main():
             "roofline": roofline(args, f),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": launches_per_step(f["forward_launches"]) * args.steps,
             "clocks": f["clocks"],
         }
         if subs is not None:

@@ -157,6 +157,14 @@ TP_API int tp_yolo_layer_output_lo(tp_yolo_net* net, int layer, void** ptr);
 /* Kernel the plan chose for conv slot 0..22: 0 conv_tc, 1 conv_pair (cta_group::2),
  * 2 conv_l0, 3 conv_box, 4 conv_pair_rect (cta_group::2, pooled); -1 on a bad argument. */
 TP_API int tp_yolo_layer_kernel(tp_yolo_net* net, int conv);
+/* TP_DTYPE_F16F8 plan: layer 5 (1x1, step 3) runs inside layer 4's kernel (step 2) by
+ * default — layer 4's output stays on chip and its buffer is not written. fused = 0 keeps
+ * the two launches (every step output materialised, for per-layer checks); the results are
+ * bit-identical either way. TP_ERR_UNSUPPORTED when asked to fuse a plan that cannot. */
+TP_API int tp_yolo_set_fused(tp_yolo_net* net, int fused);
+/* 1 if `step` currently runs inside the previous step's kernel (its input buffer is not
+ * written by a forward), else 0. */
+TP_API int tp_yolo_step_fused(tp_yolo_net* net, int step);
 TP_API int tp_yolo_destroy(tp_yolo_net* net);
 
 /* Generic implicit-GEMM conv (one layer), for tests. Activations are compact NHWC 16-bit

@@ -85,6 +85,18 @@ struct ConvParams {
   int lo_in;
   int kb_hi;
   void* out_lo;
+  // conv_swap_kernel<false> with a fused 1x1 consumer (fuse != 0; the F16F8 plan's layer
+  // 4 -> layer 5, whose input buffer nothing else reads): the 1x1's fp16 / e4m3 weights
+  // [64][128], bias, accumulator scale and HL8 output planes (f5_cstride channels per pixel)
+  int fuse;
+  const void* f5_w;
+  const void* f5_wlo;
+  const float* f5_bias;
+  float f5_alpha;
+  int f5_leaky;
+  void* f5_out;
+  void* f5_out_lo;
+  int f5_cstride;
   // profiling only (TP_CONV_DEBUG bits): 1 skip epilogue, 2 skip MMAs, 4 skip stores,
   // 8 skip TMEM loads, 16 no TMA (stale operands), 32 role cycle counters (g_conv_prof),
   // 64 unmerged pool-in-M MMAs (box kernel A/B)
@@ -1619,6 +1631,234 @@ __device__ __forceinline__ void swap_epilogue_hl8(const ConvParams& p, const CUt
   }
 }
 
+// ---- fused 1x1 consumer of the unpooled HL8 swap epilogue (layer 4 -> layer 5)
+// Staging X (one buffer for both epilogue groups) + the resident 1x1 weights, in the
+// operand layouts the unfused 1x1 kernel reads: X hi = 4 K blocks (32 channels each, warp q
+// writes block q) of [128 px][64 B] SW64, X lo = 4 x [128 px][32 B] SW32; W likewise with
+// 64 rows (output channels).
+constexpr int FU_N = 64;                  // 1x1 output channels
+constexpr uint32_t FU_XL = 32768, FU_WH = 49152, FU_WL = 65536, FU_BYTES = 73728;
+constexpr int FU_SCRATCH = 3072;           // per epilogue warp: one tile row, hi 2 KB + lo 1 KB
+constexpr int FU_EXTRA = 4 * 8 + FU_N * 4 + 16 + kEpiWarps * FU_SCRATCH;  // x4bar, bias, scratch
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Per tile i and pixel half hf (tile rows 8hf .. 8hf+7 = 128 pixels = TMEM columns
+// [128hf, 128hf + 128) of the group's accumulator): the group's 4 warps turn layer 4's
+// accumulators into its HL8 values (the same ops as swap_epilogue_hl8) and stage them in X;
+// after a group barrier one thread issues the 1x1's MMAs (A = X, B = W, M = 128, N = 64)
+// into the half's drained accumulator columns [128hf, 128hf + 64), in the unfused 1x1
+// kernel's K order (hi channels in K16 steps, then lo channels in K32 steps: the same
+// products summed in the same order, so the results are the unfused ones bit for bit).
+// X use u = 2i + hf waits for use u - 1's MMAs (x4bar[(u - 1) % 4], arrived by their
+// commit); uses complete in order and a group has seen its own use u - 4 complete, so every
+// parity wait is within one phase. Then the 1x1's epilogue: warp q reads TMEM lanes 32q ..
+// 32q + 31 (pixels) x 64 columns and stores both HL8 planes of the 1x1's output.
+__device__ __forceinline__ void swap_fused_1x1(const ConvParams& p, uint32_t xs, uint32_t scr,
+                                               uint64_t* x4bar, const float* bias4,
+                                               const float* bias5,
+                                               uint32_t tmem_base, int i, int g, uint32_t q,
+                                               uint32_t lane, bool live, int y0, int x0, int img,
+                                               int ores, float alpha, bool leaky) {
+  const int m = (int)lane >> 3, j = (int)lane & 7;
+  const int cq = (int)lane >> 2, tq = (int)lane & 3;
+  float bq[2][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    bq[h][0] = bias4[(int)q * 32 + 16 * h + cq];
+    bq[h][1] = bias4[(int)q * 32 + 16 * h + cq + 8];
+  }
+  const int src_a = 4 * ((2 * cq) & 7) + tq, src_b = src_a + 4;
+  const bool hi_e = cq >= 4;
+  const uint32_t t_row = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 256);
+  const uint32_t xh = xs + q * 8192u, xl = xs + FU_XL + q * 4096u;
+  // TP_CONV_DEBUG bit 32: phase cycles of warp q = 0 (g_conv_prof 0: waiting for the staging
+  // buffer, 1: staging, 5: waiting for the 1x1's MMAs, 6: the 1x1's epilogue)
+  const bool prof = (p.dbg & 32) && q == 0 && lane == 0;
+  long long t_a = 0, t_b = 0, t_c = 0, t_d = 0, t0 = 0;
+#pragma unroll 1
+  for (int hf = 0; hf < 2; ++hf) {
+    const int u = 2 * i + hf;
+    if (prof) t0 = clock64();
+    if (u > 0) tp::mbar_wait(&x4bar[(u - 1) & 3], (uint32_t)(((u - 1) >> 2) & 1));
+    if (prof) {
+      const long long t1 = clock64();
+      t_a += t1 - t0;
+      t0 = t1;
+    }
+    const uint32_t c0 = t_row + (uint32_t)(hf * 128);
+    uint32_t v[16];
+    tmem_ld_16x256b_x2(c0, *reinterpret_cast<uint32_t(*)[8]>(v));
+    tmem_ld_16x256b_x2(c0 + (16u << 16), *reinterpret_cast<uint32_t(*)[8]>(v + 8));
+#pragma unroll 1
+    for (int r = 0; r < 8; ++r) {
+      uint32_t hs[2][2][2], lw[2][2], lp[2][2];
+      tp::tmem_ld_wait_regs(v);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int cg = 0; cg < 2; ++cg) {
+          uint32_t l2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            float a = fmaf(__uint_as_float(v[8 * h + 4 * cg + 2 * e]), alpha, bq[h][e]);
+            float b = fmaf(__uint_as_float(v[8 * h + 4 * cg + 2 * e + 1]), alpha, bq[h][e]);
+            if (leaky) {
+              a = fmaxf(a, 0.1f * a);
+              b = fmaxf(b, 0.1f * b);
+            }
+            const __half2 hh = __floats2half2_rn(a, b);
+            hs[h][cg][e] = *reinterpret_cast<const uint32_t*>(&hh);
+            const float2 hf2 = __half22float2(hh);
+            uint16_t pr;
+            asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;"
+                : "=h"(pr)
+                : "f"((b - hf2.y) * kLoScale), "f"((a - hf2.x) * kLoScale));
+            l2[e] = pr;
+          }
+          lp[h][cg] = l2[0] | (l2[1] << 16);
+        }
+      }
+      if (r + 1 < 8) {
+        tmem_ld_16x256b_x2(c0 + (uint32_t)((r + 1) * 16), *reinterpret_cast<uint32_t(*)[8]>(v));
+        tmem_ld_16x256b_x2(c0 + (16u << 16) + (uint32_t)((r + 1) * 16),
+                           *reinterpret_cast<uint32_t(*)[8]>(v + 8));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int cg = 0; cg < 2; ++cg) {
+          const uint32_t A = __shfl_sync(0xffffffffu, lp[h][cg], src_a);
+          const uint32_t B = __shfl_sync(0xffffffffu, lp[h][cg], src_b);
+          lw[h][cg] = __byte_perm(hi_e ? A >> 16 : A, hi_e ? B >> 16 : B, 0x5140);
+        }
+#pragma unroll
+      for (int cg = 0; cg < 2; ++cg) {
+        const int pl = 16 * r + 8 * cg + j;
+        stmatrix_x4_trans(xh + (uint32_t)(pl * 64) + (uint32_t)(((m ^ (pl >> 1)) & 3) * 16),
+                          hs[0][cg][0], hs[0][cg][1], hs[1][cg][0], hs[1][cg][1]);
+      }
+      const int lpl = 16 * r + 8 * (m & 1) + j;
+      stmatrix_x4_trans(xl + (uint32_t)(lpl * 32) + (uint32_t)((((m >> 1) ^ (lpl >> 2)) & 1) * 16),
+                        lw[0][0], lw[0][1], lw[1][0], lw[1][1]);
+    }
+    fence_proxy_async_smem();
+    tp::tc_fence_before();
+    named_bar_sync(1u + (uint32_t)g, 128);
+    tp::tc_fence_after();
+    if (prof) t_b += clock64() - t0;
+    if (q == 0) {
+      if (tp::elect_one()) {
+        const uint32_t d = tmem_base + (uint32_t)(g * 256 + hf * 128);
+        const uint32_t idesc = tp::idesc_f16kind(128, FU_N, false);
+        const uint64_t xhd = tp::umma_desc(xs, 16, 512, 4);
+        const uint64_t whd = tp::umma_desc(xs + FU_WH, 16, 512, 4);
+        const uint64_t xld = tp::umma_desc(xs + FU_XL, 16, 256, 6);
+        const uint64_t wld = tp::umma_desc(xs + FU_WL, 16, 256, 6);
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            tp::mma_bf16(d, xhd + (uint64_t)(kq * 512 + 2 * k), whd + (uint64_t)(kq * 256 + 2 * k),
+                         idesc, (kq | k) != 0);
+#pragma unroll
+        for (int kq = 0; kq < 4; ++kq)
+          mma_f8(d, xld + (uint64_t)(kq * 256), wld + (uint64_t)(kq * 128), idesc, 1);
+        tp::mma_commit(&x4bar[u & 3]);
+      }
+      __syncwarp();
+    }
+  }
+#pragma unroll 1
+  for (int hf = 0; hf < 2; ++hf) {
+    const int u = 2 * i + hf;
+    if (prof) t0 = clock64();
+    tp::mbar_wait(&x4bar[u & 3], (uint32_t)((u >> 2) & 1));
+    if (prof) {
+      const long long t1 = clock64();
+      t_c += t1 - t0;
+      t0 = t1;
+    }
+    tp::tc_fence_after();
+    const uint32_t ta = tmem_base + ((q * 32u) << 16) + (uint32_t)(g * 256 + hf * 128);
+    uint32_t a[4][16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tp::tmem_ld16(ta + (uint32_t)(16 * c), a[c]);
+    tp::tmem_ld_wait();
+    uint32_t hi[4][8], lo[4][4];  // this lane's pixel: 64 fp16 + 64 e4m3 channels
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float f[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        f[e] = fmaf(__uint_as_float(a[c][e]), p.f5_alpha, bias5[16 * c + e]);
+        if (p.f5_leaky) f[e] = fmaxf(f[e], 0.1f * f[e]);
+      }
+      split_hl8(f, hi[c], lo[c]);
+    }
+    // lanes 16k .. 16k+15 hold tile row 8hf + 2q + k: stage that row (hi 16 x 128 B SW128,
+    // lo 16 x 64 B SW64) in the warp's scratch, then store it with every lane writing 16
+    // consecutive bytes (4 pixels = 512 contiguous bytes per instruction; a lane-per-pixel
+    // store touched 32 lines per instruction and held the epilogue)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      __syncwarp();
+      if (((int)lane >> 4) == k) {
+        const uint32_t r = lane & 15;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          st_shared_v4(scr + r * 128 + (((uint32_t)cc ^ (r & 7)) << 4), hi[cc >> 1][4 * (cc & 1)],
+                       hi[cc >> 1][4 * (cc & 1) + 1], hi[cc >> 1][4 * (cc & 1) + 2],
+                       hi[cc >> 1][4 * (cc & 1) + 3]);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          st_shared_v4(scr + 2048 + r * 64 + (((uint32_t)cc ^ ((r >> 1) & 3)) << 4), lo[cc][0],
+                       lo[cc][1], lo[cc][2], lo[cc][3]);
+      }
+      __syncwarp();
+      const int y = y0 + 8 * hf + 2 * (int)q + k;
+      if (!live || y >= ores) {
+        if (prof && k == 1) t_d += clock64() - t0;
+        continue;
+      }
+      const size_t row0 = ((size_t)img * ores + y) * ores;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t pr = 4 * t + (lane >> 3), cc = lane & 7;
+        uint4 v;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(scr + pr * 128 + ((cc ^ (pr & 7)) << 4))
+                     : "memory");
+        if (x0 + (int)pr < ores)
+          *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.f5_out) +
+                                    (row0 + x0 + pr) * p.f5_cstride + 8 * cc) = v;
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint32_t pr = 8 * t + (lane >> 2), cc = lane & 3;
+        uint4 v;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(scr + 2048 + pr * 64 + ((cc ^ ((pr >> 1) & 3)) << 4))
+                     : "memory");
+        if (x0 + (int)pr < ores)
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.f5_out_lo) +
+                                    (row0 + x0 + pr) * p.f5_cstride + 16 * cc) = v;
+      }
+      if (prof && k == 1) t_d += clock64() - t0;
+    }
+  }
+  if (prof) {
+    atomicAdd(&g_conv_prof[0], (unsigned long long)t_a);
+    atomicAdd(&g_conv_prof[1], (unsigned long long)t_b);
+    atomicAdd(&g_conv_prof[5], (unsigned long long)t_c);
+    atomicAdd(&g_conv_prof[6], (unsigned long long)t_d);
+  }
+}
+
 template <bool POOL>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_swap_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1639,10 +1879,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = bars + 2 * S + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
   float* bias_s = reinterpret_cast<float*>(bars + 2 * S + 5);
+  uint64_t* x4bar = bars + 2 * S + 5 + 64;  // fused 1x1: staging-buffer uses (after 128 biases)
+  float* bias5_s = reinterpret_cast<float*>(x4bar + 4);
+  // fused 1x1: per-epilogue-warp store scratch (16-byte aligned, after the 1x1's bias)
+  const uint32_t fu_scr = (tp::smem_u32(bias5_s + FU_N) + 15u) & ~15u;
 
   const uint32_t warp = tp::warp_id();
   const uint32_t lane = tp::lane_id();
   const int cout_pad = 128 * p.n_blocks_n;
+  const bool fused = !POOL && p.fuse != 0;
   if (warp == kProdWarp && lane == 0) {
     tp::tma_prefetch(&tmA);
     tp::tma_prefetch(&tmB);
@@ -1654,10 +1899,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       tp::mbar_init(&tfull[a], 1);
       tp::mbar_init(&tempty[a], 4);
     }
+    if (fused)
+      for (int a = 0; a < 4; ++a) tp::mbar_init(&x4bar[a], 1);
     tp::fence_mbar_init();
   }
   if (warp == kMmaWarp) tp::tmem_alloc(tmem_slot, 512);
   for (int i = threadIdx.x; i < cout_pad; i += blockDim.x) bias_s[i] = p.bias[i];
+  if (fused) {
+    // the 1x1's weights, resident: hi [64][128] fp16 -> 4 SW64 K blocks, lo [64][128] e4m3
+    // -> 4 SW32 K blocks (16-byte chunks; chunk c of row n XORed as TMA would place it)
+    const uint32_t xs = tp::smem_u32(smC);
+    const uint4* wh = reinterpret_cast<const uint4*>(p.f5_w);
+    const uint4* wl = reinterpret_cast<const uint4*>(p.f5_wlo);
+    for (int t = threadIdx.x; t < FU_N * 16; t += blockDim.x) {
+      const int n = t >> 4, c = t & 15;
+      const uint4 w = wh[t];
+      st_shared_v4(xs + FU_WH + (uint32_t)((c >> 2) * 4096 + n * 64 + (((c & 3) ^ ((n >> 1) & 3)) << 4)),
+                   w.x, w.y, w.z, w.w);
+    }
+    for (int t = threadIdx.x; t < FU_N * 8; t += blockDim.x) {
+      const int n = t >> 3, c = t & 7;
+      const uint4 w = wl[t];
+      st_shared_v4(xs + FU_WL + (uint32_t)((c >> 1) * 2048 + n * 32 + (((c & 1) ^ ((n >> 2) & 1)) << 4)),
+                   w.x, w.y, w.z, w.w);
+    }
+    for (int t = threadIdx.x; t < FU_N; t += blockDim.x) bias5_s[t] = p.f5_bias[t];
+    fence_proxy_async_smem();  // generic-proxy writes -> the MMAs' async-proxy reads
+  }
   tp::tc_fence_before();
   cluster_sync_all();  // the peer's barriers are initialised before any multicast lands
   tp::tc_fence_after();
@@ -1897,6 +2165,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // pixel's [hi 16 | lo 16] channel groups contiguously.
         const uint32_t slab0 = tp::smem_u32(smC) + warp * 4096;
         const int m = (int)lane >> 3, j = (int)lane & 7;  // stmatrix: matrix m, row j
+        if (fused) {
+          swap_fused_1x1(p, tp::smem_u32(smC), fu_scr + warp * FU_SCRATCH, x4bar, bias_s, bias5_s,
+                         tmem_base, i, g, q, lane, live, y0, x0, img, ores, alpha, leaky);
+          tp::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tp::mbar_arrive(&tempty[g]);
+          continue;
+        }
         if (p.out_lo != nullptr) {
           swap_epilogue_hl8(p, tmC, tmC2, smC, tp::smem_u32(smC) + warp * (2 * SW_SLAB_HL8), t_row,
                             live, y0, x0, img, nb, q, lane, ores, alpha, leaky);
@@ -3669,6 +3945,36 @@ int prepare_conv(ConvLaunch* L, const void* in, int max_img, int res, int cin_st
   return TP_OK;
 }
 
+// Fuse a 1x1 HL8 consumer (128 -> 64 channels, leaky) into an unpooled HL8 swap launch:
+// the 3x3's HL8 output is staged in shared memory as the 1x1's A operand instead of being
+// written to HBM, and the 1x1's MMAs + epilogue run in the same kernel (swap_fused_1x1).
+int fuse_swap_1x1(ConvLaunch* L, const void* w, const void* wlo, const float* bias, float alpha,
+                  void* out, void* out_lo, int out_cstride) {
+  ConvParams& q = L->p;
+  if (!L->swap || q.rect || q.out_lo == nullptr || q.n_blocks_n != 1 || w == nullptr ||
+      wlo == nullptr || bias == nullptr || out == nullptr || out_lo == nullptr ||
+      out_cstride % 16 != 0)
+    return TP_ERR_UNSUPPORTED;
+  const int fixed = 1024 + 128 * 4 + (2 * 12 + 6) * 8 + 16 + FU_EXTRA;
+  const uint32_t sb = q.a_stage_bytes + q.b_stage_bytes;
+  int st = (int)((227 * 1024 - fixed - (int)FU_BYTES) / (int)sb);
+  if (st > 8) st = 8;
+  if (st < 2) return TP_ERR_UNSUPPORTED;
+  q.stages = st;
+  q.stage_bytes = FU_BYTES;
+  q.fuse = 1;
+  q.f5_w = w;
+  q.f5_wlo = wlo;
+  q.f5_bias = bias;
+  q.f5_alpha = alpha;
+  q.f5_leaky = 1;
+  q.f5_out = out;
+  q.f5_out_lo = out_lo;
+  q.f5_cstride = out_cstride;
+  L->smem = 1024 + (size_t)st * sb + FU_BYTES + (2 * st + 6) * 8 + 128 * 4 + 16 + FU_EXTRA;
+  return TP_OK;
+}
+
 template <int BK, int EPI>
 int launch_box(const ConvLaunch& L, int n_img, const int32_t* n_img_dev, cudaStream_t st) {
   if (int rc = ensure_smem_optin(conv_box_kernel<BK, EPI>)) return rc;
@@ -3904,7 +4210,7 @@ struct Step {
   int conv;  // index into kConvs
   int in, out, coff, reorg, fpool;
 };
-const Step kSteps[] = {
+constexpr Step kSteps[] = {
     {0, 0, I608, P304, 0, 0, 1},  {0, 1, P304, P152, 0, 0, 1},  {0, 2, P152, A152, 0, 0, 0},
     {0, 3, A152, B152, 0, 0, 0},  {0, 4, B152, P76, 0, 0, 1},   {0, 5, P76, A76, 0, 0, 0},
     {0, 6, A76, B76, 0, 0, 0},    {0, 7, B76, P38, 0, 0, 1},    {0, 8, P38, A38, 0, 0, 0},
@@ -3951,7 +4257,14 @@ struct tp_yolo_net {
   void* bufs[NBUF];
   void* lo[NBUF];  // HL8 lo planes (nullptr for other formats)
   ConvLaunch convs[23];
+  // F16F8 plan: step kFuseStep's 1x1 runs inside step kFuseStep - 1's swap kernel when
+  // fused != 0 (the default); unfused keeps the separate launches (tp_yolo_set_fused)
+  int fusable, fused;
+  ConvLaunch fused_launch, plain_launch;
 };
+// the F16F8 plan's fused pair: step 2 (layer 4, 3x3 64 -> 128 at 152^2, conv_swap_kernel)
+// feeds step 3 (layer 5, 1x1 128 -> 64), and nothing else reads step 2's output
+constexpr int kFuseStep = 3;
 
 extern "C" size_t tp_yolo_workspace_bytes(int max_tiles, int dtype) {
   size_t total = 0;
@@ -4049,8 +4362,40 @@ extern "C" int tp_yolo_create_ex(int max_tiles, const void* const* weights,
       return rc;
     }
   }
+  if (dtype == TP_DTYPE_F16F8) {
+    const Step& a = kSteps[kFuseStep - 1];
+    const Step& b = kSteps[kFuseStep];
+    const LayerDef& lb = kConvs[b.conv];
+    static_assert(kSteps[kFuseStep].in == kSteps[kFuseStep - 1].out, "fused pair");
+    if (!a.is_pool && !b.is_pool && lb.k == 1 && lb.cin == 128 && lb.cout == FU_N && b.coff == 0 &&
+        !b.reorg && !b.fpool) {
+      ConvLaunch f = net->convs[a.conv];
+      if (fuse_swap_1x1(&f, weights[b.conv], weights_lo[b.conv], biases[b.conv], alphas[b.conv],
+                        net->bufs[b.out], net->lo[b.out], buf_ch(b.out, dtype)) == TP_OK) {
+        net->plain_launch = net->convs[a.conv];
+        net->fused_launch = f;
+        net->convs[a.conv] = f;
+        net->fusable = net->fused = 1;
+      }
+    }
+  }
   *out = net;
   return TP_OK;
+}
+
+extern "C" int tp_yolo_set_fused(tp_yolo_net* net, int fused) {
+  if (net == nullptr) {
+    tp_set_error("tp_yolo_set_fused: null plan");
+    return TP_ERR_ARG;
+  }
+  if (!net->fusable) return fused ? TP_ERR_UNSUPPORTED : TP_OK;
+  net->fused = fused ? 1 : 0;
+  net->convs[kSteps[kFuseStep - 1].conv] = fused ? net->fused_launch : net->plain_launch;
+  return TP_OK;
+}
+
+extern "C" int tp_yolo_step_fused(tp_yolo_net* net, int step) {
+  return net != nullptr && net->fused && step == kFuseStep ? 1 : 0;
 }
 
 extern "C" void* tp_yolo_input(tp_yolo_net* net) { return net ? net->bufs[I608] : nullptr; }
@@ -4074,6 +4419,8 @@ extern "C" int tp_yolo_forward_range(tp_yolo_net* net, int n_tiles, const int32_
       rc = run_pool(net->bufs[sp.in], n_tiles, kBufs[sp.in].res, buf_ch(sp.in, net->dtype),
                     net->bufs[sp.out], st, n_tiles_dev, net->dtype != TP_DTYPE_BF16,
                     buf_fmt(sp.in, net->dtype) == FMT_X2, net->lo[sp.in], net->lo[sp.out]);
+    } else if (net->fused && s == kFuseStep) {
+      rc = TP_OK;  // ran inside step kFuseStep - 1's kernel
     } else {
       rc = run_conv(net->convs[sp.conv], n_tiles, n_tiles_dev, st);
       if (rc == TP_OK && sp.reorg) {  // layer 26 wrote R38: gather it into CAT19 [0, 256)

@@ -85,6 +85,8 @@ SIGNATURES = {
     "tp_gather_tiles": (_I, [_P, _I64, _I, _I, _P, _I, _P, _I, _P, _P, _I, _P]),
     "tp_yolo_workspace_bytes": (_SZ, [_I, _I]),
     "tp_yolo_layer_kernel": (_I, [_P, _I]),
+    "tp_yolo_set_fused": (_I, [_P, _I]),
+    "tp_yolo_step_fused": (_I, [_P, _I]),
     "tp_yolo_create": (_I, [_I, _P, _P, _P, _SZ, _I, _P]),
     "tp_yolo_create_ex": (_I, [_I, _P, _P, _P, _P, _P, _SZ, _I, _P]),
     "tp_yolo_hl8_inputs": (ctypes.c_uint32, []),

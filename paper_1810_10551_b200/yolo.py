@@ -228,6 +228,18 @@ class YoloNet:
         native.call("tp_yolo_forward", self.handle, int(n_tiles), native.ptr(n_tiles_dev),
                     native.stream_handle(stream))
 
+    def set_fused(self, fused: bool) -> None:
+        """F16F8 plan: run layer 5 inside layer 4's kernel (default) or as its own launch
+        (every step output materialised); bit-identical results (tp_yolo_set_fused)."""
+        native.call("tp_yolo_set_fused", self.handle, int(bool(fused)))
+
+    @property
+    def fused_steps(self) -> frozenset:
+        """Steps that currently run inside the previous step's kernel."""
+        lib = native.load()
+        return frozenset(s for s in range(len(STEPS))
+                         if lib.tp_yolo_step_fused(self.handle, s))
+
     def forward_range(self, n_tiles, first, last, stream=None):
         native.call("tp_yolo_forward_range", self.handle, int(n_tiles), None, first, last,
                     native.stream_handle(stream))

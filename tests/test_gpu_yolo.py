@@ -70,6 +70,16 @@ def _oracle_mode(net):
 
 
 def _check_layers(cuda, net, tiles):
+    # every step's output materialised: the fp32 plan's fused layer 4 -> 5 pair runs as two
+    # launches here (bit-identical to the fused kernel: test_fused_layer5_bit_identical)
+    net.set_fused(False)
+    try:
+        return _check_each_layer(cuda, net, tiles)
+    finally:
+        net.set_fused(net.dtype == "fp32")
+
+
+def _check_each_layer(cuda, net, tiles):
     torch = cuda
     torch.backends.cudnn.allow_tf32 = False
     n = _run(cuda, net, tiles)
@@ -156,6 +166,37 @@ def test_each_conv_layer_many_tiles(cuda, dtype):
     tiles = rng.integers(0, 256, (40, 608, 608, 3), np.uint8)
     net = yolo.YoloNet(40, seed=0, dtype=dtype)
     print("worst per-layer rel err (40 tiles)", _check_layers(cuda, net, tiles))
+
+
+@pytest.mark.parametrize("n_tiles", [3, 11])
+def test_fused_layer5_bit_identical(cuda, n_tiles):
+    """The fp32 (HL8) plan runs layer 5 (1x1, 128 -> 64) inside layer 4's swap kernel: layer
+    4's HL8 output is staged in shared memory as layer 5's operand and never reaches HBM.
+    Layer 5's hi / lo planes and the head must equal the two-launch plan's bit for bit
+    (same products, same K order), over partial edge tiles (152 = 9.5 x 16 pixels) and
+    uneven tile counts per CTA; layer 4's buffer must stay untouched when fused."""
+    torch = cuda
+    rng = np.random.default_rng(5)
+    tiles = rng.integers(0, 256, (n_tiles, 608, 608, 3), np.uint8)
+    net = yolo.YoloNet(n_tiles, seed=0, dtype="fp32")
+    assert net.fused_steps == {3}
+    n = _run(cuda, net, tiles)
+    l4 = net.step_tensor(2, n)
+    l4.view(torch.uint8).fill_(0x7B)  # sentinel: the fused kernel must not write layer 4's output
+    net.forward(n)
+    torch.cuda.synchronize()
+    assert bool((l4.view(torch.uint8) == 0x7B).all())
+    fused = [net.step_tensor(3, n).clone(), net.step_lo_tensor(3, n).clone(),
+             net.head_tensor(n).clone()]
+    net.set_fused(False)
+    assert not net.fused_steps
+    net.step_tensor(3, n).view(torch.uint8).fill_(0)
+    net.forward(n)
+    torch.cuda.synchronize()
+    plain = [net.step_tensor(3, n), net.step_lo_tensor(3, n), net.head_tensor(n)]
+    for a, b in zip(fused, plain):
+        assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    assert fused[0].float().abs().max().item() > 0
 
 
 def test_head_matches_cpu_oracle(cuda, net, tiles):

@@ -4,7 +4,9 @@ written once by its producer, in the stored layout of each plan (csrc/tp_conv.cu
 kSteps): compact NHWC 16-bit, the layer-0 input as [610][614][4] rgb0 pixels, the head fp32
 [19][19][448]; the fp32x2 plan doubles every activation but the input and head (hi/lo fp16
 pairs), the fp32 plan (HL8) stores them as 3 bytes per element (fp16 hi + e4m3 lo planes).
-Weights are amortised over the batch and reported separately.
+Weights are amortised over the batch and reported separately. The fp32 plan runs layer 5
+inside layer 4's kernel (csrc/tp_conv.cu swap_fused_1x1): layer 4's output never reaches
+HBM, so its write and read drop out ("fp32" = fused default, "fp32-unfused" = both kept).
 
     python tools/algorithmic_bytes.py
 """
@@ -32,7 +34,8 @@ STEPS = [("I608", "P304", 32), ("P304", "P152", 64), ("P152", "A152", 128),
          ("CAT19", "A19", 1024), ("A19", "HEAD", 448)]
 
 
-MULT = {"fp16": 1.0, "fp32x2": 2.0, "fp32": 1.5}  # stored bytes per element / 2
+MULT = {"fp16": 1.0, "fp32x2": 2.0, "fp32": 1.5, "fp32-unfused": 1.5}  # bytes per element / 2
+ON_CHIP = {"fp32": {"A152"}}  # buffers a plan keeps on chip (fused producer -> consumer)
 
 
 def activation_mb(plan: str) -> float:
@@ -41,6 +44,10 @@ def activation_mb(plan: str) -> float:
 
     total = 0
     for src, dst, och in STEPS:
+        if dst in ON_CHIP.get(plan, ()):  # the fused kernel reads src, writes the consumer's dst
+            continue
+        if src in ON_CHIP.get(plan, ()):
+            src = next(a for a, b, _ in STEPS if b == src)
         s, c, e = BUFS[src]
         total += (610 * 614 * 4 * 2 if src == "I608" else s * s * c * e * mult(src))
         s, _, e = BUFS[dst]
@@ -58,6 +65,6 @@ def weights_mb(plan: str) -> float:
 
 
 if __name__ == "__main__":
-    for plan in ("fp16", "fp32", "fp32x2"):
+    for plan in ("fp16", "fp32", "fp32-unfused", "fp32x2"):
         print(f"{plan}: activations {activation_mb(plan):.2f} MB per tile, "
               f"weights {weights_mb(plan):.1f} MB per forward")

@@ -23,8 +23,11 @@ def main():
     ap.add_argument("--tiles", type=int, default=120)
     ap.add_argument("--dtype", default=yolo.DEFAULT_PRECISION)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--unfused", action="store_true", help="layer 5 as its own launch")
     a = ap.parse_args()
     net = yolo.YoloNet(a.tiles, dtype=a.dtype)
+    if a.unfused:
+        net.set_fused(False)
     x = net.input_tensor(a.tiles)
     x[:, 1:-1, 1:-1, :] = torch.rand_like(x[:, 1:-1, 1:-1, :].float()).to(x.dtype)
     net.forward(a.tiles)
@@ -47,6 +50,9 @@ def main():
             li += 1
             d, cin, cout, k, side = yolo.LAYERS[li]
             fl = 2.0 * side * side * cout * cin * k * k * a.tiles
+            if s in net.fused_steps:  # ran inside the previous step's kernel
+                print(f"{s:4d} {d:5d}    fused into step {s - 1}")
+                continue
             print(f"{s:4d} {d:5d} {times[s]:8.3f} {100 * times[s] / total:5.1f}% "
                   f"{fl / times[s] / 1e9:8.1f}")
         else:

@@ -13,6 +13,8 @@ import subprocess
 import sys
 
 LAYERS = [0, 2, 4, 5, 6, 8, 9, 10, 12, 13, 14, 15, 16, 18, 19, 20, 21, 22, 23, 24, 26, 29, 30]
+# the fp32 (HL8) plan runs layer 5 inside layer 4's kernel: 22 launches
+LAYERS_FUSED = [0, 2, "4+5"] + LAYERS[4:]
 COLS = {
     "name": "Kernel Name",
     "ms": "gpu__time_duration.sum",
@@ -48,7 +50,8 @@ def main():
     print("layer,kernel,ms,share_pct,dram_read_MB,dram_write_MB,tensor_active_pct,sm_throughput_pct,grid")
     for i, r in enumerate(data):
         name = r[idx["name"]].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
-        layer = LAYERS[i] if len(data) == len(LAYERS) else i
+        layer = (LAYERS[i] if len(data) == len(LAYERS)
+                 else LAYERS_FUSED[i] if len(data) == len(LAYERS_FUSED) else i)
         print(f"{layer},{name.replace(',', ';')},{val(r, 'ms'):.3f},{100 * val(r, 'ms') / tot:.1f},"
               f"{val(r, 'rd'):.1f},{val(r, 'wr'):.1f},{val(r, 'tensor'):.1f},{val(r, 'sm'):.1f},"
               f"{int(val(r, 'grid'))}")
