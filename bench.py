@@ -534,16 +534,16 @@ def gpu_run(args, rank, world, local, shared_gpu, group, sub=False):
 
 
 PRECISION_NOTE = {
-    "fp32": "fp32-parity: activations as exact fp16 hi/lo pairs up to 152^2, then an fp16 hi "
-            "plane + an e4m3 lo plane (x - hi) * 2^11 (kind::f16 + kind::f8f6f4 into one fp32 "
-            "accumulator); fp32 accumulation and epilogue",
+    "fp32": "fp32-parity (HL8): every activation but the layer-0 pixels and the fp32 head is "
+            "an fp16 hi plane + an e4m3 lo plane e4m3((x - hi) * 2^11); each conv runs "
+            "kind::f16 MMAs on hi and kind::f8f6f4 MMAs on lo into one fp32 accumulator; fp32 "
+            "epilogue; layer 5 runs inside layer 4's kernel",
     "fp32x2": "fp32-parity: activations as fp16 hi/lo pairs on every layer (2x K), fp32 "
               "accumulation and epilogue",
 }
 EXECUTED_NOTE = {
-    "fp32": "tensor-core work issued, in kind::f16-rate GFLOP: hi/lo fp16 pairs double K on "
-            "layers 2-6, fp16 hi + e4m3 lo (f8f6f4 at 2x rate) make 1.5x K from layer 8 on "
-            "({:.1f} GFLOP per tile)",
+    "fp32": "tensor-core work issued, in kind::f16-rate GFLOP: fp16 hi + e4m3 lo (f8f6f4 at "
+            "2x rate) make 1.5x K on every layer but layer 0 ({:.1f} GFLOP per tile)",
     "fp32x2": "tensor-core FLOPs issued: hi/lo activations double K on every layer but "
               "layer 0 ({:.1f} GFLOP per tile)",
 }
@@ -568,7 +568,7 @@ def roofline(args, f):
     peaks = measured_peaks()
     peak = peak_tflops()
     traffic = {}
-    tfile = {"fp32": "r02_conv_traffic_fp32.json",
+    tfile = {"fp32": "r02h_conv_traffic_fp32.json",
              "fp32x2": "r01_conv_traffic_fp32.json"}.get(args.precision, "r01_conv_traffic.json")
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", tfile)))

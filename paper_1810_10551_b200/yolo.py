@@ -326,8 +326,8 @@ class YoloNet:
 def exec_gflop_per_tile(dtype: str) -> float:
     """Tensor-core work a plan issues per tile, in kind::f16-rate-equivalent GFLOP: the
     16-bit plans issue the algorithmic FLOPs; fp32x2 doubles K on every layer but layer 0;
-    fp32 doubles it on the F16X2-input layers and adds half of K (the e4m3 lo pass runs at
-    twice the f16 rate) on the HL8-input layers."""
+    fp32 adds half of K (the e4m3 lo pass runs at twice the f16 rate) on the HL8-input
+    layers — every layer but layer 0 (a layer with another paired input would count 2x)."""
     g = [2.0 * s * s * cout * cin * k * k / 1e9 for _, cin, cout, k, s in LAYERS]
     if dtype not in native.PARITY_DTYPES:
         return sum(g)
