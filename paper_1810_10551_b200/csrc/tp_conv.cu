@@ -945,6 +945,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           PROF_T0(tw);
           tp::mbar_wait(&empty[s], ph ^ 1);
           PROF_ADD(pr_wait, tw);
+          if (p.dbg & 16) {  // profiling: no TMA, stale operands (the leader's arrival only)
+            if (rank == 0) tp::mbar_arrive(&full[s]);
+            if (++s == S) {
+              s = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
           if (rank == 0)
             tp::mbar_arrive_expect_tx(&full[s], 2 * (p.a_stage_bytes + p.b_stage_bytes));
           const uint32_t lbar = mapa_rank(&full[s], 0);
