@@ -261,8 +261,11 @@ class YoloNet:
                 for i in range(len(LAYERS))]
 
     def kernel_summary(self) -> str:
-        ks = self.layer_kernels()
-        return ", ".join(f"{ks.count(k)}x {k}" for k in self.KERNEL_NAMES if k in ks)
+        """Launches per kernel of one forward's convs (a fused slot runs inside its producer)."""
+        fused = {slot for s, (kind, slot) in enumerate(STEPS) if s in self.fused_steps}
+        ks = [k for li, k in enumerate(self.layer_kernels()) if li not in fused]
+        out = ", ".join(f"{ks.count(k)}x {k}" for k in self.KERNEL_NAMES if k in ks)
+        return out + (f" ({len(fused)} 1x1 fused into its producer)" if fused else "")
 
     def _view(self, addr: int, nbytes: int):
         off = addr - self.workspace.data_ptr()
